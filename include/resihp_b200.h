@@ -1,0 +1,261 @@
+/*
+ * resihp_b200.h — C ABI of the B200-native ResiHP data-parallel core.
+ *
+ * The reference (arxiv 2605.06374, `resilsim`, /root/reference/pkg/src) is a
+ * pure-Python package with no FFI; its "interface" for this path is the set
+ * of Python functions exported from resilsim/__init__.py:5-60.  Every entry
+ * point below replaces one of those functions (cited per declaration) for a
+ * BATCH of inputs; the Python package paper_2605_06374_b200 binds them with
+ * ctypes and keeps the reference's Python signatures.
+ *
+ * Conventions
+ *   - plain C types only; all array pointers are DEVICE pointers unless the
+ *     function name ends in _host;
+ *   - every function returns RH_OK (0) or a negative RH_E_* code, with a
+ *     message in rh_last_error() (thread-local);
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default);
+ *     functions are asynchronous on that stream unless documented otherwise;
+ *   - arithmetic on every decision-carrying quantity is IEEE fp64 with the
+ *     reference's evaluation order and no FMA contraction.
+ */
+#ifndef RESIHP_B200_H
+#define RESIHP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RH_ABI_VERSION 1
+
+enum {
+  RH_OK = 0,
+  RH_E_INVALID = -1,   /* bad argument: Python shim raises ValueError        */
+  RH_E_CUDA = -2,      /* CUDA runtime failure                               */
+  RH_E_NOMEM = -3,     /* workspace allocation failed                        */
+  RH_E_SHAPE = -4      /* shape outside this kernel's envelope (documented)  */
+};
+
+/* Per-iteration status bits (rh_pipeline_batch / rh_detect_batch). */
+enum {
+  RH_IT_ESCALATE = 1,   /* filter_candidate(...) == ESCALATE  (detector.py:111-116) */
+  RH_IT_STAGE_FLAG = 2, /* validate: >=1 (replica,stage) flagged (detector.py:141-147) */
+  RH_IT_LINK_FLAG = 4,  /* validate: >=1 link flagged (detector.py:148-152)          */
+  RH_IT_STOPPED = 8,    /* chunk mapped to a stopped stage (pipeline.py:408-415)      */
+  RH_IT_CAPACITY = 16,  /* activation footprint > capacity (pipeline.py:516-539)      */
+  RH_IT_OVERFLOW = 32   /* a replica owns more than max_mb_per_replica micro-batches  */
+};
+
+enum { RH_SCHED_1F1B = 0, RH_SCHED_ZBH = 1 };  /* cluster.py SCHEDULES */
+
+/* CostModel (workload.py:29-49).  ratio(BW) = ratio_b + ratio_w. */
+typedef struct rh_cost_model {
+  double alpha;   /* seconds per token    */
+  double beta;    /* seconds per token^2  */
+  double ratio_f;
+  double ratio_b;
+  double ratio_w;
+} rh_cost_model;
+
+/* Fixed pipeline shape of a batch (ParallelismConfig, cluster.py:37-50). */
+typedef struct rh_pipe_shape {
+  int32_t pp;             /* P stages                                        */
+  int32_t dp;             /* D replicas                                      */
+  int32_t tp;             /* nominal TP degree T = device slots per group    */
+  int32_t schedule;       /* RH_SCHED_*                                      */
+  int32_t micro_batches;  /* M micro-batches per iteration                   */
+  int32_t token_budget;   /* N tokens per micro-batch                        */
+  int32_t capacity;       /* activation capacity; <= 0 = unchecked           */
+  int32_t has_allreduce;  /* terminal AR vertex per replica (pipeline.py:242) */
+  int32_t max_mb_per_replica; /* upper bound on dp_counts over all segments;
+                                 sizes shared memory (<= 0: use M)          */
+} rh_pipe_shape;
+
+/*
+ * Segment tables: a segment is a span of iterations with one layout / one
+ * view of device speeds.  All tables are per segment, row-major.
+ *   speed[d][s]   effective stage speed (ClusterState.effective_stage_speed,
+ *                 cluster.py:155-169); <= 0 marks a stopped stage
+ *   hop_fwd[d][s] seconds on the data edge F(j,s) -> F(j,s+1), s < P-1
+ *   hop_bwd[d][s] seconds on the data edge B(j,s+1) -> B(j,s), s < P-1
+ *                 (edge_cost_fn, pipeline.py:336-353)
+ *   allreduce[d]  terminal AR vertex cost (_allreduce_map, pipeline.py:356-372)
+ *   mb_start[d]   first micro-batch (index within the iteration) owned by
+ *                 replica d; mb_start[D] = M (split_micro_batches,
+ *                 cluster.py:309-328)
+ *   link_ratio    measured/expected ratios of the exercised inter-node links
+ *                 (_used_link_ratios, pipeline.py:491-513), CSR by link_off.
+ */
+typedef struct rh_segments {
+  int32_t n_seg;
+  const int32_t* layers;      /* [n_seg][P]                    */
+  const int32_t* mb_start;    /* [n_seg][D+1]                  */
+  const double* speed;        /* [n_seg][D][P]                 */
+  const double* hop_fwd;      /* [n_seg][D][P]                 */
+  const double* hop_bwd;      /* [n_seg][D][P]                 */
+  const double* allreduce;    /* [n_seg][D]; read iff has_allreduce */
+  const int32_t* link_off;    /* [n_seg+1] or NULL (no links)  */
+  const double* link_ratio;   /* [link_off[n_seg]]             */
+} rh_segments;
+
+/*
+ * A batch of iterations (the device x iteration trace).
+ *   mb_off[i*M + j] .. mb_off[i*M + j + 1] index the packed documents of
+ *   micro-batch j of iteration i in doc_len (padding document included,
+ *   workload.py:52-80).  Offsets are int32: a batch holds < 2^31 documents.
+ *   device_time[i][d][s][t]: measured stage seconds of member t of group
+ *   (d,s); 0 for an empty slot.  The group's measured stage time is the max
+ *   over its members (a TP group runs at its slowest member, cluster.py:155).
+ */
+typedef struct rh_trace {
+  int64_t n_iter;
+  const int32_t* seg;          /* [n_iter] segment id; NULL = segment 0 */
+  const int32_t* mb_off;       /* [n_iter*M + 1]                       */
+  const int32_t* doc_len;      /* [mb_off[n_iter*M]]                   */
+  const float* device_time;    /* [n_iter][D][P][T]  (detect only)     */
+  const double* observed;      /* [n_iter]           (detect only)     */
+} rh_trace;
+
+/* Outputs.  Optional arrays may be NULL. */
+typedef struct rh_pass_out {
+  double* makespan;     /* [n_iter] critical path (pipeline.py:259-292)     required */
+  uint8_t* status;      /* [n_iter] RH_IT_* bits                            required */
+  double* stage_cost;   /* [n_iter][D][P] sum of chunk costs (pipeline.py:446-453) */
+  uint8_t* stage_flag;  /* [n_iter][D][P] validate flag            (detect only)    */
+  float* severity;      /* [n_iter][D][P] expected/measured if flagged else 0       */
+} rh_pass_out;
+
+typedef struct rh_ctx rh_ctx;
+
+/* ---------------------------------------------------------------- context */
+int rh_abi_version(void);
+const char* rh_last_error(void);
+int rh_ctx_create(int device, rh_ctx** out);
+int rh_ctx_destroy(rh_ctx* ctx);
+/* number of kernel launches issued through this context (for bench.py) */
+int64_t rh_ctx_launches(const rh_ctx* ctx);
+
+/* ------------------------------------------------------- cost model rows */
+/* quad_load (workload.py:83-85) for n micro-batches given a CSR of docs. */
+int rh_quad_load(rh_ctx* ctx, int64_t n_mb, const int32_t* mb_off,
+                 const int32_t* doc_len, int64_t* quad_out, void* stream);
+
+/* predict_chunk_time (workload.py:88-98) for n chunks:
+ *   t[i] = ((ratio(kind[i]) * layers[i]) * (alpha*budget[i] + beta*quad[i])) / speed[i]
+ * kind: 0=F 1=B 2=W 3=BW.  speed <= 0 sets bad[i]=1 and t[i]=0 (ValueError). */
+int rh_chunk_time(rh_ctx* ctx, const rh_cost_model* model, int64_t n,
+                  const int64_t* quad, const int32_t* budget, const uint8_t* kind,
+                  const int32_t* layers, const double* speed, double* t_out,
+                  uint8_t* bad_out, void* stream);
+
+/* --------------------------------------------- pipeline predictor (Eq. 2) */
+/*
+ * Canonical (migration-free) chunk-DAG critical path for a batch of
+ * iterations: per iteration i, the makespan of build_dag(...) +
+ * critical_path(...) (pipeline.py:129-292) under the segment's speeds, the
+ * per-(replica,stage) stage cost sums and the activation check.  Replaces
+ * the two build_dag/critical_path calls inside simulate_iteration
+ * (pipeline.py:432-441) for every iteration of the batch at once.
+ * Envelope: 1 <= P <= 32, D*next_pow2(P) <= 1024.
+ */
+int rh_pipeline_batch(rh_ctx* ctx, const rh_pipe_shape* shape,
+                      const rh_cost_model* model, const rh_segments* segs,
+                      const rh_trace* trace, const rh_pass_out* out,
+                      void* stream);
+
+/*
+ * Fused Detector pass: rh_pipeline_batch on the KNOWN view (the predictor,
+ * harness.py:406-410) fused with filter_candidate (detector.py:111-116) and
+ * validate (detector.py:127-158) against the measured device trace.
+ * threshold = DetectorState.escalation_factor (1.25).
+ */
+int rh_detect_batch(rh_ctx* ctx, const rh_pipe_shape* shape,
+                    const rh_cost_model* model, const rh_segments* segs,
+                    const rh_trace* trace, double threshold,
+                    const rh_pass_out* out, void* stream);
+
+/*
+ * Same as rh_detect_batch but every pointer in segs/trace/out is a HOST
+ * pointer (pinned memory recommended).  Copies in, runs, copies out and
+ * synchronises `stream`.  This is the reference-facing end-to-end call.
+ */
+int rh_detect_batch_host(rh_ctx* ctx, const rh_pipe_shape* shape,
+                         const rh_cost_model* model, const rh_segments* segs,
+                         const rh_trace* trace, double threshold,
+                         const rh_pass_out* out, void* stream);
+
+/* ------------------------------------------------------ validate (batch) */
+/* validate (detector.py:127-158) on explicit arrays: flag[i] = measured[i] >
+ * thr*expected[i] (skipping non-positive entries), sev[i] = expected/measured
+ * when flagged else 0.  Used for standalone validate() and link ratios
+ * (pass expected=NULL to test ratio[i] > thr with sev = 1/ratio). */
+int rh_validate(rh_ctx* ctx, int64_t n, const double* measured,
+                const double* expected, double threshold, uint8_t* flag,
+                double* severity, void* stream);
+
+/* ------------------------------------------------ change-point screen */
+enum {
+  RH_SC_CANDIDATE = 1,  /* detect_change_point fired (detector.py:94-108)  */
+  RH_SC_FILTERED = 2,   /* filter ran (candidate or refill, detector.py:221) */
+  RH_SC_ESCALATED = 4,  /* escalated to validation                         */
+  RH_SC_CONFIRMED = 8,  /* validation confirmed                            */
+  RH_SC_POPPED = 16     /* observation removed from the series             */
+};
+
+typedef struct rh_screen_params {
+  int32_t window;          /* DetectorState.window (20)             */
+  int32_t filter_enabled;  /* DetectorState.filter_enabled          */
+  double kappa;            /* DetectorState.kappa (3.0)             */
+} rh_screen_params;
+
+/*
+ * DetectorState.observe state machine (detector.py:198-271) over n
+ * iterations.  The carried series state is (series_len, the last
+ * min(series_len, window) values in hist).  it_status are the RH_IT_* bits
+ * of rh_detect_batch; reset[i] != 0 clears the series before iteration i
+ * (harness.py:398); reset may be NULL.  outcome[i] gets RH_SC_* bits.
+ * series_len_out (device int64) receives the final series length.
+ */
+int rh_screen(rh_ctx* ctx, const rh_screen_params* params, int64_t series_len,
+              const double* hist, int64_t n, const double* observed,
+              const uint8_t* it_status, const uint8_t* reset, uint8_t* outcome,
+              int64_t* series_len_out, void* stream);
+
+/* ---------------------------------------------------- workload ingest */
+/*
+ * pack_sequences (workload.py:52-80), HOST function: first-fit-decreasing
+ * packing of n_docs lengths into bins of exactly `budget` tokens (residual
+ * appended as a padding document).  Keeps the first max_bins bins
+ * (max_bins < 0: all; harness.py:251-252 keeps packed[:M]).  With mb_off or
+ * doc_len NULL only *n_bins_out / *n_entries_out are computed (size query);
+ * otherwise mb_off[n_bins+1] and doc_len[n_entries] are filled (host memory).
+ */
+int rh_pack_sequences(int64_t n_docs, const int32_t* lengths, int32_t budget,
+                      int64_t max_bins, int32_t* mb_off, int32_t* doc_len,
+                      int64_t* n_bins_out, int64_t* n_entries_out);
+
+/* -------------------------------------------- general DAG critical path */
+/*
+ * critical_path (pipeline.py:259-292) on an arbitrary DAG given in CSR by
+ * source (succ_off[V+1], succ_dst[E], succ_w[E]); writes starts[V] and
+ * makespan[0].  Optionally (n_chains > 0) reduces resource chains — vertex
+ * ranges [chain_off[k], chain_off[k+1]) in creation order, as build_dag
+ * emits them per (replica, stage) — to chain_sum[k] (sequential sum,
+ * pipeline.py:446-453) and runs the activation check along each chain with
+ * kind[v] (0=F +1 at start, 1=B/3=BW -1 at finish; pipeline.py:516-539).
+ * flags[0] = 1 on a cycle (CycleError), flags[1] = 1 if capacity > 0 was
+ * exceeded.  flags is a device int32[2].  Level-synchronous, one CTA.
+ */
+int rh_dag_critical_path(rh_ctx* ctx, int32_t n_vertices, const double* cost,
+                         const int32_t* succ_off, const int32_t* succ_dst,
+                         const double* succ_w, int32_t n_chains,
+                         const int32_t* chain_off, const uint8_t* kind,
+                         int32_t capacity, double* starts, double* makespan,
+                         double* chain_sum, int32_t* flags, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RESIHP_B200_H */

@@ -1,0 +1,71 @@
+/*
+ * TEST INFRASTRUCTURE — NOT PRODUCT CODE.
+ *
+ * CPU restatement of the reference algorithm (arxiv 2605.06374 `resilsim`,
+ * /root/reference/pkg/src/resilsim) for the ResiHP data-parallel hot path.
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load liboracle.so, and only as the checker or
+ * the timed CPU baseline.  The product (paper_2605_06374_b200) never links it.
+ *
+ * Parity is PINNED: tests/test_oracle_golden.py checks every function here
+ * against golden vectors produced by importing the reference itself
+ * (tests/golden/make_golden.py, committed with its fixtures).
+ *
+ * The entry points take the same descriptor structs as the product ABI
+ * (include/resihp_b200.h) but HOST pointers.
+ */
+#ifndef RESIHP_ORACLE_H
+#define RESIHP_ORACLE_H
+
+#include <stdint.h>
+#include "../include/resihp_b200.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* workload.py:83-85 */
+int64_t orc_quad_load(int32_t n_docs, const int32_t* docs);
+/* workload.py:88-98; kind 0=F 1=B 2=W 3=BW.  Returns 0 and sets *bad when
+ * speed <= 0 (the reference raises ValueError). */
+double orc_chunk_time(const rh_cost_model* m, int kind, int64_t quad,
+                      int32_t budget, int32_t layers, double speed, int* bad);
+
+/* pipeline.py:92-118: writes kinds/ids of the stage sequence, returns length */
+int orc_stage_sequence(int schedule, int pp, int stage, int m, int first_id,
+                       int* kinds, int* ids);
+
+/* pipeline.py:259-292 on an edge list; returns 1 on a cycle (CycleError). */
+int orc_critical_path(int32_t nv, const double* cost, int32_t ne,
+                      const int32_t* src, const int32_t* dst, const double* w,
+                      double* starts, double* makespan);
+
+/* Canonical build_dag + critical_path + stage sums + activation check for a
+ * batch (pipeline.py:129-292,446-453,516-539).  n_threads <= 0: all cores. */
+int orc_pipeline_batch(const rh_pipe_shape* shape, const rh_cost_model* model,
+                       const rh_segments* segs, const rh_trace* trace,
+                       const rh_pass_out* out, int n_threads);
+
+/* Predictor on the known view fused with filter_candidate + validate
+ * (detector.py:111-158), same contract as rh_detect_batch. */
+int orc_detect_batch(const rh_pipe_shape* shape, const rh_cost_model* model,
+                     const rh_segments* segs, const rh_trace* trace,
+                     double threshold, const rh_pass_out* out, int n_threads);
+
+/* detector.py:127-158 on arrays (expected == NULL: link-ratio mode). */
+int orc_validate(int64_t n, const double* measured, const double* expected,
+                 double threshold, uint8_t* flag, double* severity);
+
+/* detector.py:94-108 */
+int orc_change_point(int64_t len, const double* series, int window, double kappa);
+
+/* DetectorState.observe state machine, detector.py:198-271 */
+int orc_screen(const rh_screen_params* params, int64_t series_len,
+               const double* hist, int64_t n, const double* observed,
+               const uint8_t* it_status, const uint8_t* reset, uint8_t* outcome,
+               int64_t* series_len_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,59 @@
+// Shared plumbing for the ResiHP B200 library: error state, context, launch
+// accounting.  Every translation unit of libresihp_b200.so includes this.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <atomic>
+#include <string>
+
+#include "../../include/resihp_b200.h"
+
+struct rh_ctx {
+  int device = 0;
+  int num_sms = 148;
+  size_t smem_optin = 0;
+  std::atomic<int64_t> launches{0};
+  // grow-only device workspace (host-buffer entry points, screen scratch)
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  // grow-only pinned host staging is NOT kept: callers pass pinned memory.
+};
+
+namespace rh {
+
+void set_error(const char* fmt, ...);
+
+inline int cuda_fail(cudaError_t e, const char* what) {
+  set_error("%s: %s", what, cudaGetErrorString(e));
+  return RH_E_CUDA;
+}
+
+#define RH_CUDA(call)                                   \
+  do {                                                  \
+    cudaError_t _e = (call);                            \
+    if (_e != cudaSuccess) return rh::cuda_fail(_e, #call); \
+  } while (0)
+
+#define RH_CHECK_LAUNCH(ctx)                                        \
+  do {                                                              \
+    cudaError_t _e = cudaGetLastError();                            \
+    if (_e != cudaSuccess) return rh::cuda_fail(_e, "kernel launch"); \
+    (ctx)->launches.fetch_add(1, std::memory_order_relaxed);        \
+  } while (0)
+
+// Grow the context workspace to at least `bytes` (stream-ordered free of the
+// old buffer is not needed: callers synchronise before growth).
+int workspace(rh_ctx* ctx, size_t bytes, void** out);
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Doubles that are >= 0 order like their bit patterns (used by atomicMax).
+__device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
+  atomicMax(reinterpret_cast<unsigned long long*>(addr),
+            static_cast<unsigned long long>(__double_as_longlong(v)));
+}
+
+}  // namespace rh

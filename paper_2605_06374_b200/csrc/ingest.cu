@@ -1,0 +1,75 @@
+// Workload ingest (host-side, native): first-fit-decreasing packing of
+// document lengths into token-budget micro-batches — pack_sequences,
+// workload.py:52-80 — in O(n log n) with a max-segment-tree over bin
+// residuals ("leftmost bin with room >= l" is a tree descent) instead of the
+// reference's O(n * bins) scan.  Output is identical: bins in creation
+// order, documents in insertion (descending) order, the residual appended as
+// a padding document when non-zero.
+#include <algorithm>
+#include <functional>
+#include <vector>
+
+#include "common.cuh"
+
+extern "C" int rh_pack_sequences(int64_t n_docs, const int32_t* lengths, int32_t budget,
+                                 int64_t max_bins, int32_t* mb_off, int32_t* doc_len,
+                                 int64_t* n_bins_out, int64_t* n_entries_out) {
+  if (n_docs < 0 || budget <= 0 || !n_bins_out || !n_entries_out ||
+      (n_docs && !lengths)) {
+    rh::set_error("rh_pack_sequences: invalid arguments");
+    return RH_E_INVALID;
+  }
+  std::vector<int32_t> v(lengths, lengths + n_docs);
+  for (int32_t l : v) {
+    if (l <= 0) {
+      rh::set_error("document length must be positive, got %d", l);
+      return RH_E_INVALID;
+    }
+    if (l > budget) {
+      rh::set_error("document of %d tokens exceeds budget %d", l, budget);
+      return RH_E_INVALID;
+    }
+  }
+  std::sort(v.begin(), v.end(), std::greater<int32_t>());
+  // at most n_docs bins; tree over bin slots, unopened slots hold `budget`
+  int64_t cap = 1;
+  while (cap < std::max<int64_t>(n_docs, 1)) cap <<= 1;
+  std::vector<int32_t> tree(2 * cap, budget);
+  std::vector<int64_t> bin_of(n_docs);
+  std::vector<int64_t> bin_count(n_docs + 1, 0);
+  int64_t opened = 0;
+  for (int64_t i = 0; i < n_docs; ++i) {
+    const int32_t l = v[i];
+    // leftmost slot with residual >= l: first-fit over opened bins, else the
+    // next fresh slot (index == opened, residual == budget >= l)
+    int64_t node = 1;
+    while (node < cap) node = tree[2 * node] >= l ? 2 * node : 2 * node + 1;
+    const int64_t b = node - cap;
+    if (b == opened) ++opened;
+    bin_of[i] = b;
+    bin_count[b]++;
+    tree[node] -= l;
+    for (node >>= 1; node; node >>= 1) tree[node] = std::max(tree[2 * node], tree[2 * node + 1]);
+  }
+  const int64_t keep = max_bins >= 0 ? std::min(opened, max_bins) : opened;
+  // CSR: docs of bin b in insertion order, then padding if residual > 0
+  std::vector<int64_t> start(keep + 1, 0);
+  for (int64_t b = 0; b < keep; ++b)
+    start[b + 1] = start[b] + bin_count[b] + (tree[cap + b] > 0 ? 1 : 0);
+  if (start[keep] >= INT32_MAX) {
+    rh::set_error("rh_pack_sequences: too many entries for int32 offsets");
+    return RH_E_SHAPE;
+  }
+  *n_bins_out = keep;
+  *n_entries_out = start[keep];
+  if (!mb_off || !doc_len) return RH_OK;  // size query
+  std::vector<int64_t> fill(start.begin(), start.end() - 1);
+  for (int64_t i = 0; i < n_docs; ++i)
+    if (bin_of[i] < keep) doc_len[fill[bin_of[i]]++] = v[i];
+  for (int64_t b = 0; b < keep; ++b) {
+    if (tree[cap + b] > 0) doc_len[fill[b]++] = tree[cap + b];
+    mb_off[b] = (int32_t)start[b];
+  }
+  mb_off[keep] = (int32_t)start[keep];
+  return RH_OK;
+}

@@ -1,0 +1,131 @@
+"""Batched Detector pass over a device x iteration trace (the product path).
+
+``DetectorPass(trace)`` moves a DetectorTrace into HBM once; ``run()`` is
+two launches on the current stream:
+
+  1. rh_detect_batch — per iteration: quad loads, chunk costs, the
+     canonical chunk-DAG critical path of the known view (Eq. 2), stage cost
+     sums, the workload-aware filter and per-(replica,stage)/link validation;
+  2. rh_screen — the DetectorState.observe state machine (median/MAD
+     change-point screen with benign/unconfirmed pops) for the whole trace.
+
+``pipeline(view)`` runs only the predictor (rh_pipeline_batch) on either
+view; trace synthesis uses it on the ACTUAL view to produce ground truth.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+from .tables import DeviceSegments, pipe_shape
+from .workload import cost_model_c
+
+
+class DetectorPass:
+    def __init__(self, trace, device=None, *, threshold: float = 1.25, window: int = 20,
+                 kappa: float = 3.0, filter_enabled: bool = True, keep_stage_cost=False):
+        import torch
+
+        self.trace = trace
+        self.dev = device or torch.device("cuda", torch.cuda.current_device())
+        self.threshold = float(threshold)
+        self.screen_params = _lib.ScreenParams(int(window), 1 if filter_enabled else 0,
+                                               float(kappa))
+        t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(self.dev)
+        self.seg = t(trace.seg, np.int32)
+        self.mb_off = t(trace.mb_off, np.int32)
+        self.doc_len = t(trace.doc_len if trace.doc_len.size else np.zeros(1), np.int32)
+        self.reset = t(trace.reset, np.uint8)
+        self.device_time = (t(trace.device_time, np.float32) if trace.device_time is not None
+                            else None)
+        self.observed = t(trace.observed, np.float64) if trace.observed is not None else None
+        self.known = DeviceSegments(trace.known, self.dev)
+        self.actual = DeviceSegments(trace.actual, self.dev)
+        n, G = trace.n_iter, trace.cfg.dp * trace.cfg.pp
+        self.makespan = torch.empty(n, dtype=torch.float64, device=self.dev)
+        self.status = torch.empty(n, dtype=torch.uint8, device=self.dev)
+        self.stage_flag = torch.empty(n * G, dtype=torch.uint8, device=self.dev)
+        self.severity = torch.empty(n * G, dtype=torch.float32, device=self.dev)
+        self.stage_cost = (torch.empty(n * G, dtype=torch.float64, device=self.dev)
+                           if keep_stage_cost else None)
+        self.outcome = torch.empty(max(n, 1), dtype=torch.uint8, device=self.dev)
+        self.series_len = torch.zeros(1, dtype=torch.int64, device=self.dev)
+        self.hist = torch.zeros(1, dtype=torch.float64, device=self.dev)
+        self.model_c = cost_model_c(trace.model)
+        self.lib = _lib.load_library()
+        self.ctx = _lib.context(self.dev.index)
+
+    def _shape(self, segs, capacity=None):
+        tr = self.trace
+        return pipe_shape(tr.cfg, tr.M, tr.N, capacity=capacity,
+                          has_allreduce=tr.has_allreduce, max_mb=segs.max_mb)
+
+    def _trace_c(self, with_measurements: bool):
+        return _lib.Trace(self.trace.n_iter, self.seg.data_ptr(), self.mb_off.data_ptr(),
+                          self.doc_len.data_ptr(),
+                          self.device_time.data_ptr() if with_measurements else None,
+                          self.observed.data_ptr() if with_measurements else None)
+
+    def pipeline(self, view: str = "known", capacity=None):
+        """rh_pipeline_batch -> (makespan, status, stage_cost[n, D*P]) as tensors."""
+        import torch
+
+        segs = self.known if view == "known" else self.actual
+        n, G = self.trace.n_iter, self.trace.cfg.dp * self.trace.cfg.pp
+        ms = torch.empty(n, dtype=torch.float64, device=self.dev)
+        st = torch.empty(n, dtype=torch.uint8, device=self.dev)
+        sc = torch.empty(n * G, dtype=torch.float64, device=self.dev)
+        out = _lib.PassOut(ms.data_ptr(), st.data_ptr(), sc.data_ptr(), None, None)
+        shape = self._shape(segs, capacity)
+        tr = self._trace_c(False)
+        _lib.check(self.lib.rh_pipeline_batch(self.ctx, _lib.C.byref(shape),
+                                              _lib.C.byref(self.model_c), _lib.C.byref(segs.c),
+                                              _lib.C.byref(tr), _lib.C.byref(out),
+                                              _lib.stream_handle()), "rh_pipeline_batch")
+        return ms, st, sc.view(n, G)
+
+    def detect(self, stream=None):
+        out = _lib.PassOut(self.makespan.data_ptr(), self.status.data_ptr(),
+                           self.stage_cost.data_ptr() if self.stage_cost is not None else None,
+                           self.stage_flag.data_ptr(), self.severity.data_ptr())
+        shape = self._shape(self.known)
+        tr = self._trace_c(True)
+        _lib.check(self.lib.rh_detect_batch(self.ctx, _lib.C.byref(shape),
+                                            _lib.C.byref(self.model_c),
+                                            _lib.C.byref(self.known.c), _lib.C.byref(tr),
+                                            self.threshold, _lib.C.byref(out),
+                                            _lib.stream_handle(stream)), "rh_detect_batch")
+
+    def screen(self, stream=None):
+        _lib.check(self.lib.rh_screen(self.ctx, _lib.C.byref(self.screen_params), 0,
+                                      self.hist.data_ptr(), self.trace.n_iter,
+                                      self.observed.data_ptr(), self.status.data_ptr(),
+                                      self.reset.data_ptr(), self.outcome.data_ptr(),
+                                      self.series_len.data_ptr(), _lib.stream_handle(stream)),
+                   "rh_screen")
+
+    def run(self, stream=None):
+        self.detect(stream)
+        self.screen(stream)
+
+    def results(self) -> dict:
+        n, G = self.trace.n_iter, self.trace.cfg.dp * self.trace.cfg.pp
+        out = {
+            "makespan": self.makespan.cpu().numpy(),
+            "status": self.status.cpu().numpy(),
+            "stage_flag": self.stage_flag.cpu().numpy().reshape(n, G),
+            "severity": self.severity.cpu().numpy().reshape(n, G),
+            "outcome": self.outcome.cpu().numpy()[:n],
+            "series_len": int(self.series_len.item()),
+        }
+        if self.stage_cost is not None:
+            out["stage_cost"] = self.stage_cost.cpu().numpy().reshape(n, G)
+        return out
+
+
+def synthesize_measurements(trace, noise: float = 0.01, seed: int = 1) -> None:
+    """Ground truth on the GPU (actual view) -> trace.device_time / observed."""
+    p = DetectorPass(trace)
+    ms, st, sc = p.pipeline("actual")
+    trace.attach_measurements(sc.cpu().numpy(), ms.cpu().numpy(), noise=noise, seed=seed)

@@ -1,0 +1,168 @@
+"""Micro-batch cost model (mirror of resilsim/workload.py).
+
+``quad_load`` and ``predict_chunk_time`` run on the GPU (rh_quad_load /
+rh_chunk_time); batch callers should use ``quad_loads`` / ``chunk_times``.
+``pack_sequences`` (first-fit decreasing) is host-side workload ingest.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .cluster import MicroBatch
+
+CHUNK_F = "F"
+CHUNK_B = "B"
+CHUNK_W = "W"
+CHUNK_BW = "BW"
+CHUNK_ALLREDUCE = "AR"
+
+KIND_CODE = {CHUNK_F: 0, CHUNK_B: 1, CHUNK_W: 2, CHUNK_BW: 3}
+DEFAULT_CHUNK_RATIOS = {CHUNK_F: 1.0, CHUNK_B: 1.0, CHUNK_W: 1.0}
+
+
+@dataclass
+class CostModel:
+    """workload.py:29-49: t = ratio * L * (alpha*N + beta*sum l^2) / speed."""
+
+    alpha: float
+    beta: float
+    chunk_ratios: dict[str, float] = field(default_factory=lambda: dict(DEFAULT_CHUNK_RATIOS))
+
+    def __post_init__(self):
+        if self.alpha < 0 or self.beta < 0:
+            raise ValueError("cost coefficients must be non-negative")
+        if self.alpha == 0 and self.beta == 0:
+            raise ValueError("cost model needs at least one non-zero coefficient")
+        for kind in (CHUNK_F, CHUNK_B, CHUNK_W):
+            if self.chunk_ratios.get(kind, 0.0) <= 0:
+                raise ValueError(f"chunk ratio for {kind} must be positive")
+
+    def ratio(self, kind: str) -> float:
+        if kind == CHUNK_BW:
+            return self.chunk_ratios[CHUNK_B] + self.chunk_ratios[CHUNK_W]
+        return self.chunk_ratios[kind]
+
+
+def cost_model_c(model):
+    """rh_cost_model struct of any CostModel-like object (duck-typed)."""
+    from . import _lib
+
+    r = model.chunk_ratios
+    return _lib.CostModelC(float(model.alpha), float(model.beta), float(r[CHUNK_F]),
+                           float(r[CHUNK_B]), float(r[CHUNK_W]))
+
+
+def pack_sequences(doc_lengths, token_budget: int) -> list[MicroBatch]:
+    """workload.py:52-80: first-fit decreasing into bins of exactly
+    ``token_budget`` tokens; each bin's residual becomes a padding document."""
+    lengths = [int(x) for x in doc_lengths]
+    for x in lengths:
+        if x <= 0:
+            raise ValueError(f"document length must be positive, got {x}")
+        if x > token_budget:
+            raise ValueError(f"document of {x} tokens exceeds budget {token_budget}")
+    contents: list[list[int]] = []
+    free: list[int] = []
+    for x in sorted(lengths, reverse=True):
+        slot = next((i for i, room in enumerate(free) if x <= room), None)
+        if slot is None:
+            contents.append([x])
+            free.append(token_budget - x)
+        else:
+            contents[slot].append(x)
+            free[slot] -= x
+    return [MicroBatch(id=i, doc_lengths=tuple(docs + ([room] if room > 0 else [])),
+                       token_budget=token_budget)
+            for i, (docs, room) in enumerate(zip(contents, free))]
+
+
+def csr_of(micro_batches) -> tuple[np.ndarray, np.ndarray]:
+    """(mb_off int32[M+1], doc_len int32[...]) of a list of micro-batches."""
+    counts = np.fromiter((len(mb.doc_lengths) for mb in micro_batches), dtype=np.int64,
+                         count=len(micro_batches))
+    off = np.zeros(len(micro_batches) + 1, dtype=np.int64)
+    np.cumsum(counts, out=off[1:])
+    if off[-1] >= 2**31:
+        raise ValueError("too many documents for int32 offsets")
+    docs = np.fromiter((x for mb in micro_batches for x in mb.doc_lengths), dtype=np.int64,
+                       count=int(off[-1]))
+    if docs.size and (docs.min() < 0 or docs.max() >= 2**31):
+        raise ValueError("document length outside int32")
+    return off.astype(np.int32), docs.astype(np.int32)
+
+
+def quad_loads(micro_batches) -> np.ndarray:
+    """quad_load of every micro-batch, computed by rh_quad_load on the GPU."""
+    import torch
+
+    from . import _lib
+
+    n = len(micro_batches)
+    if n == 0:
+        return np.zeros(0, dtype=np.int64)
+    off, docs = csr_of(micro_batches)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    t_off = torch.from_numpy(off).to(dev)
+    t_doc = torch.from_numpy(docs if docs.size else np.zeros(1, np.int32)).to(dev)
+    out = torch.empty(n, dtype=torch.int64, device=dev)
+    lib = _lib.load_library()
+    _lib.check(lib.rh_quad_load(_lib.context(), n, t_off.data_ptr(), t_doc.data_ptr(),
+                                out.data_ptr(), _lib.stream_handle()), "rh_quad_load")
+    return out.cpu().numpy()
+
+
+def quad_load(mb: MicroBatch) -> int:
+    """workload.py:83-85 — sum of squared document lengths, padding included."""
+    return int(quad_loads([mb])[0])
+
+
+def chunk_times(model, micro_batches, kinds, layers, speeds) -> np.ndarray:
+    """predict_chunk_time for n chunks at once (rh_chunk_time on the GPU).
+
+    ``micro_batches``, ``kinds``, ``layers`` and ``speeds`` are parallel
+    sequences.  Raises ValueError like the reference when a speed is <= 0.
+    """
+    import torch
+
+    from . import _lib
+
+    n = len(kinds)
+    if n == 0:
+        return np.zeros(0, dtype=np.float64)
+    sp = np.asarray(speeds, dtype=np.float64)
+    if (sp <= 0).any():
+        raise ValueError("cannot schedule onto a stopped device (speed <= 0)")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    uniq: dict[int, int] = {}
+    mbs = []
+    idx = np.empty(n, dtype=np.int64)
+    for i, mb in enumerate(micro_batches):
+        k = id(mb)
+        if k not in uniq:
+            uniq[k] = len(mbs)
+            mbs.append(mb)
+        idx[i] = uniq[k]
+    q = torch.from_numpy(quad_loads(mbs)[idx]).to(dev)
+    budget = torch.from_numpy(np.fromiter((mbs[j].token_budget for j in idx), np.int32, n)).to(dev)
+    kind = torch.from_numpy(np.fromiter((KIND_CODE[k] for k in kinds), np.uint8, n)).to(dev)
+    lay = torch.from_numpy(np.asarray(layers, dtype=np.int32)).to(dev)
+    spd = torch.from_numpy(sp).to(dev)
+    out = torch.empty(n, dtype=torch.float64, device=dev)
+    bad = torch.empty(n, dtype=torch.uint8, device=dev)
+    lib = _lib.load_library()
+    _lib.check(lib.rh_chunk_time(_lib.context(), _lib.C.byref(cost_model_c(model)), n,
+                                 q.data_ptr(), budget.data_ptr(), kind.data_ptr(),
+                                 lay.data_ptr(), spd.data_ptr(), out.data_ptr(),
+                                 bad.data_ptr(), _lib.stream_handle()), "rh_chunk_time")
+    return out.cpu().numpy()
+
+
+def predict_chunk_time(mb: MicroBatch, kind: str, model: CostModel, layers_on_stage: int,
+                       device_speed: float) -> float:
+    """workload.py:88-98"""
+    if device_speed <= 0:
+        raise ValueError("cannot schedule onto a stopped device (speed <= 0)")
+    return float(chunk_times(model, [mb], [kind], [layers_on_stage], [device_speed])[0])

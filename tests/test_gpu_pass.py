@@ -1,0 +1,86 @@
+"""GPU parity: the fused predictor / Detector pass vs the CPU oracle.
+
+Bit-exact comparisons (fp64 bit patterns, flags, status bits) on seeded
+random traces covering 1F1B and ZBH, 1..6 stages, 1..4 replicas, uneven and
+empty micro-batch ownership, slow and subgroup stages, hop and all-reduce
+weights, stopped stages and the activation-capacity check.
+"""
+
+import numpy as np
+import pytest
+
+from tests.helpers import random_trace, with_measurements
+
+pytestmark = pytest.mark.gpu
+
+
+def _bits(a):
+    return np.ascontiguousarray(a, dtype=np.float64).view(np.uint64)
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_pipeline_matches_oracle(seed, oracle, cuda_device):
+    from paper_2605_06374_b200.detect_pass import DetectorPass
+
+    tr = random_trace(seed, stop=(seed % 7 == 3))
+    p = DetectorPass(tr)
+    for view in ("known", "actual"):
+        ms, st, sc = p.pipeline(view)
+        oms, ost, osc = oracle.pipeline(tr, view=view)
+        np.testing.assert_array_equal(st.cpu().numpy(), ost)
+        np.testing.assert_array_equal(_bits(ms.cpu().numpy()), _bits(oms))
+        np.testing.assert_array_equal(_bits(sc.cpu().numpy()), _bits(osc))
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_pipeline_capacity_matches_oracle(seed, oracle, cuda_device):
+    from paper_2605_06374_b200.detect_pass import DetectorPass
+
+    tr = random_trace(100 + seed, pp=int(2 + seed % 5))
+    p = DetectorPass(tr)
+    for cap in (1, 2, 3, tr.cfg.pp + 2):
+        ms, st, _ = p.pipeline("actual", capacity=cap)
+        oms, ost, _ = oracle.pipeline(tr, view="actual", capacity=cap)
+        np.testing.assert_array_equal(st.cpu().numpy(), ost)
+        np.testing.assert_array_equal(_bits(ms.cpu().numpy()), _bits(oms))
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_detect_matches_oracle(seed, oracle, cuda_device):
+    from paper_2605_06374_b200.detect_pass import DetectorPass
+
+    tr = with_measurements(random_trace(200 + seed, n_iter=24), oracle, noise=0.02, seed=seed)
+    p = DetectorPass(tr, keep_stage_cost=True)
+    p.detect()
+    r = p.results()
+    oms, ost, osc, ofl, osv = oracle.detect(tr)
+    np.testing.assert_array_equal(r["status"], ost)
+    np.testing.assert_array_equal(_bits(r["makespan"]), _bits(oms))
+    np.testing.assert_array_equal(_bits(r["stage_cost"]), _bits(osc))
+    np.testing.assert_array_equal(r["stage_flag"], ofl)
+    np.testing.assert_array_equal(r["severity"].view(np.uint32), osv.view(np.uint32))
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_screen_matches_oracle(seed, oracle, cuda_device):
+    """rh_screen (Jacobi fixpoint) == the sequential state machine."""
+    from paper_2605_06374_b200.detector import _screen
+
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(1, 3000))
+    base = 10.0 + rng.standard_normal(n) * rng.choice([0.05, 0.5, 2.0])
+    spikes = rng.random(n) < rng.choice([0.02, 0.1, 0.3])
+    obs = np.where(spikes, base * rng.uniform(1.1, 3.0, n), base)
+    st = np.zeros(n, np.uint8)
+    st |= (rng.random(n) < 0.3).astype(np.uint8)  # escalate
+    st |= ((rng.random(n) < 0.2).astype(np.uint8) << 1)  # stage flag
+    reset = (rng.random(n) < 0.003).astype(np.uint8)
+    w = int(rng.choice([3, 5, 20, 21]))
+    fe = bool(rng.integers(0, 2))
+    L0 = int(rng.choice([0, 2, w, 50]))
+    hist = list(10.0 + rng.standard_normal(min(L0, w)))
+    oc, ln = _screen(L0, hist, obs, st, w, 3.0, fe, reset=reset)
+    ooc, oln = oracle.screen(obs, st, window=w, kappa=3.0, filter_enabled=fe, series_len=L0,
+                             hist=hist, reset=reset)
+    np.testing.assert_array_equal(oc, ooc)
+    assert ln == oln
