@@ -1,0 +1,357 @@
+"""Generate golden vectors by running the REFERENCE implementation.
+
+Run in the build container only (needs /root/reference, which does not
+exist on the GPU box):
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+It imports the unmodified reference package (resilsim, from
+/root/reference/pkg/src), evaluates it on seeded inputs and writes JSON
+fixtures next to this script.  Floats are stored with repr() (exact
+round-trip).  The fixtures are committed; tests read only the fixtures.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import random
+import sys
+from pathlib import Path
+
+import numpy as np
+
+REF = Path(os.environ.get("RESIHP_REFERENCE", "/root/reference/pkg/src"))
+sys.dont_write_bytecode = True
+sys.path.insert(0, str(REF))
+
+import resilsim  # noqa: E402
+from resilsim import cluster as rc  # noqa: E402
+from resilsim import detector as rd  # noqa: E402
+from resilsim import pipeline as rp  # noqa: E402
+from resilsim import policies as rpol  # noqa: E402
+from resilsim import scheduler as rs  # noqa: E402
+from resilsim import workload as rw  # noqa: E402
+from resilsim.comm import CommSpec  # noqa: E402
+
+OUT = Path(__file__).resolve().parent
+
+
+def dump(name, obj):
+    path = OUT / f"{name}.json"
+    path.write_text(json.dumps(obj, separators=(",", ":")) + "\n")
+    print(f"wrote {path} ({path.stat().st_size} bytes)")
+
+
+# ----------------------------------------------------------------- helpers
+def state_to_json(state):
+    return {
+        "devices": [[d.id, d.node_id, d.speed, d.status] for d in state.devices],
+        "devices_per_node": state.devices_per_node,
+        "tp_groups": [[k[0], k[1], list(v)] for k, v in state.tp_groups.items()],
+        "intra_bw": state.intra_bw,
+        "inter_bw": state.inter_bw,
+        "link_factors": [[k[0], k[1], v] for k, v in state.link_factors.items()],
+    }
+
+
+def cfg_to_json(cfg):
+    return {"tp": cfg.tp, "dp": cfg.dp, "pp": cfg.pp, "schedule": cfg.schedule,
+            "layer_partition": list(cfg.layer_partition)}
+
+
+def model_to_json(m):
+    return {"alpha": m.alpha, "beta": m.beta, "chunk_ratios": dict(m.chunk_ratios)}
+
+
+def mbs_to_json(mbs):
+    return [[mb.id, list(mb.doc_lengths), mb.token_budget] for mb in mbs]
+
+
+def keyed(d):
+    return [[k[0], k[1], v] for k, v in d.items()]
+
+
+def random_scenario(rng: random.Random, *, allow_fail_stop=False):
+    tp = rng.choice([1, 2, 4])
+    dp = rng.choice([1, 2, 3, 4])
+    pp = rng.choice([1, 2, 3, 4, 6])
+    schedule = rng.choice(["1f1b", "zbh"])
+    layers = [rng.randint(1, 5) for _ in range(pp)]
+    cfg = rc.ParallelismConfig(tp=tp, dp=dp, pp=pp, schedule=schedule, layer_partition=layers)
+    n_dev = tp * dp * pp
+    dpn = 8
+    nodes = max(1, -(-n_dev // dpn))
+    state = rc.build_cluster(nodes, dpn, cfg, rng.choice([300e9, 300.0 * 2**30]),
+                             rng.choice([25e9, 25.0 * 2**30]))
+    events = []
+    for _ in range(rng.randint(0, 3)):
+        events.append(rc.FailureEvent(kind="fail_slow_compute", start=0.0,
+                                      device=rng.randrange(n_dev),
+                                      severity=rng.choice([0.5, 0.3, 0.75, 0.62])))
+    if nodes > 1 and rng.random() < 0.4:
+        a, b = rng.sample(range(nodes), 2)
+        events.append(rc.FailureEvent(kind="fail_slow_comm", start=0.0, link=(a, b),
+                                      severity=rng.choice([0.5, 0.4])))
+    if allow_fail_stop and rng.random() < 0.3:
+        events.append(rc.FailureEvent(kind="fail_stop", start=0.0, device=rng.randrange(n_dev)))
+    if events:
+        state = rc.apply_failures(state, events, 0.0)
+    budget = rng.choice([1024, 2048, 4096])
+    M = dp * rng.randint(1, 5)
+    docs = [max(1, min(budget, int(rng.lognormvariate(6.8, 0.9)))) for _ in range(M * 6)]
+    mbs = rw.pack_sequences(docs, budget)[:M]
+    model = rw.CostModel(alpha=rng.uniform(1e-6, 4e-6), beta=rng.uniform(1e-10, 9e-10),
+                         chunk_ratios={"F": 1.0, "B": rng.choice([1.0, 0.5]),
+                                       "W": rng.choice([1.0, 0.75])})
+    comm = CommSpec(p2p_optimized=rng.random() < 0.7) if rng.random() < 0.7 else None
+    return state, cfg, mbs, model, comm
+
+
+# ----------------------------------------------------------------- workload
+def gen_workload():
+    rng = random.Random(1)
+    quad = [[[4096], 16777216], [[1024] * 4, 4194304], [[3000, 1000], 10000000]]
+    for _ in range(200):
+        docs = [rng.randint(1, 32768) for _ in range(rng.randint(1, 12))]
+        quad.append([docs, rw.quad_load(rc.MicroBatch(0, tuple(docs), sum(docs)))])
+    chunk = []
+    for _ in range(400):
+        docs = [rng.randint(1, 8192) for _ in range(rng.randint(1, 8))]
+        budget = sum(docs) + rng.choice([0, 0, rng.randint(1, 4096)])
+        if budget > sum(docs):
+            docs.append(budget - sum(docs))
+        mb = rc.MicroBatch(0, tuple(docs), budget)
+        m = rw.CostModel(alpha=rng.choice([0.0, rng.uniform(1e-7, 5e-6)]),
+                         beta=rng.uniform(1e-13, 1e-9),
+                         chunk_ratios={"F": rng.choice([1.0, 0.7]), "B": rng.choice([1.0, 1.3]),
+                                       "W": rng.choice([1.0, 0.4])})
+        kind = rng.choice(["F", "B", "W", "BW"])
+        layers = rng.randint(0, 12)
+        speed = rng.choice([1.0, 0.5, 0.25, rng.uniform(0.05, 1.0)])
+        chunk.append([docs, budget, model_to_json(m), kind, layers, speed,
+                      rw.predict_chunk_time(mb, kind, m, layers, speed)])
+    pack = []
+    for _ in range(120):
+        budget = rng.choice([512, 1024, 4096, 8192])
+        docs = [rng.randint(1, budget) for _ in range(rng.randint(0, 60))]
+        pack.append([docs, budget, [list(mb.doc_lengths) for mb in rw.pack_sequences(docs, budget)]])
+    pack.append([[3000, 2000, 1000], 4096, [[3000, 1000, 96], [2000, 2096]]])
+    dump("workload", {"quad_load": quad, "chunk_time": chunk, "pack": pack})
+
+
+# ----------------------------------------------------------------- pipeline
+def gen_pipeline():
+    rng = random.Random(2)
+    cases = []
+    while len(cases) < 160:
+        state, cfg, mbs, model, comm = random_scenario(rng, allow_fail_stop=True)
+        counts = None
+        if rng.random() < 0.4 and cfg.dp > 1:
+            cuts = sorted(rng.randint(0, len(mbs)) for _ in range(cfg.dp - 1))
+            counts = [b - a for a, b in zip([0] + cuts, cuts + [len(mbs)])]
+        plan = rs.AdaptationPlan(dp_assignment=counts) if counts else None
+        capacity = rng.choice([None, None, cfg.pp + 2, 2, 1])
+        case = {"state": state_to_json(state), "cfg": cfg_to_json(cfg), "mbs": mbs_to_json(mbs),
+                "model": model_to_json(model),
+                "comm": None if comm is None else [comm.hidden_bytes_per_token, comm.layer_bytes,
+                                                   comm.p2p_optimized],
+                "dp_counts": counts, "capacity": capacity}
+        try:
+            rec = rp.simulate_iteration(state, cfg, mbs, model, plan, comm=comm,
+                                        capacity=capacity)
+            case["result"] = {
+                "observed": rec.observed_time, "predicted": rec.predicted_healthy_time,
+                "stage_cost": keyed(rec.stage_cost),
+                "stage_cost_reference": keyed(rec.stage_cost_reference),
+                "busy": [[k, v] for k, v in rec.per_device_busy.items()],
+                "idle": [[k, v] for k, v in rec.per_device_idle.items()],
+                "link_ratio": keyed(rec.link_ratio),
+            }
+        except rp.SimulationError as exc:
+            case["error"] = str(exc)
+        cases.append(case)
+    # critical_path on the reference's DAGs, including migrated plans whose
+    # stage orders come from plan_migration (general DAGs)
+    dags = []
+    while len(dags) < 60:
+        state, cfg, mbs, model, comm = random_scenario(rng)
+        speeds = rp._stage_speed_maps(state, cfg)[0]
+        executors, orders = {}, None
+        if cfg.dp > 1 and rng.random() < 0.6:
+            res = rs.plan_migration(cfg, mbs, model, speeds, delta=rng.choice([0, 1]),
+                                    capacity=cfg.pp + 2)
+            executors = {(m.mb, m.stage): m.executor for m in res.migrations}
+            orders = res.stage_orders if res.migrations else None
+        dag = rp.build_dag(cfg, mbs, model, speeds, rng.choice([0.0, 1e-3]),
+                           executors=executors, stage_orders=orders,
+                           allreduce_seconds=rng.choice([None, 0.01]))
+        starts, ms = rp.critical_path(dag)
+        dags.append({"cost": [v.cost for v in dag.vertices],
+                     "kind": [v.kind for v in dag.vertices],
+                     "edges": [[e.src, e.dst, e.weight] for e in dag.edges],
+                     "starts": starts, "makespan": ms, "migrated": bool(executors)})
+    # unit-cost KATs from the reference tests (test_pipeline.py:125-149)
+    unit = rw.CostModel(alpha=1.0, beta=0.0, chunk_ratios={"F": 1.0, "B": 0.5, "W": 0.5})
+    ub = [rc.MicroBatch(i, (1,), 1) for i in range(2)]
+    d = rp.build_dag(rc.ParallelismConfig(1, 1, 2, layer_partition=[1, 1]), ub, unit, 1.0)
+    s, m = rp.critical_path(d)
+    dags.append({"cost": [v.cost for v in d.vertices], "kind": [v.kind for v in d.vertices],
+                 "edges": [[e.src, e.dst, e.weight] for e in d.edges], "starts": s,
+                 "makespan": m, "migrated": False})
+    dump("pipeline", {"simulate": cases, "dags": dags})
+
+
+# ----------------------------------------------------------------- detector
+def gen_detector():
+    rng = random.Random(3)
+    cp = []
+    for _ in range(300):
+        w = rng.choice([3, 5, 20])
+        n = rng.randint(w - 1, w + 5)
+        scale = rng.choice([0.0, 0.01, 0.3])
+        series = [10.0 + rng.choice([0.0, scale * rng.gauss(0, 1)]) for _ in range(n)]
+        if rng.random() < 0.5:
+            series.append(10.0 * rng.choice([1.05, 1.3, 2.0]))
+        cp.append([series, w, 3.0, rd.detect_change_point(series, w, 3.0)])
+    val = []
+    for _ in range(200):
+        st = {}
+        for d in range(rng.randint(1, 3)):
+            for s in range(rng.randint(1, 3)):
+                e = rng.choice([0.0, rng.uniform(0.1, 1.0)])
+                st[(d, s)] = (e * rng.choice([1.0, 1.2, 1.25, 1.3, 2.0, 0.0]), e)
+        lr = {(a, a + 1): rng.choice([1.0, 1.25, 1.26, 2.5]) for a in range(rng.randint(0, 2))}
+        r = rd.validate(st, lr, threshold=1.25)
+        val.append([[[k[0], k[1], v[0], v[1]] for k, v in st.items()],
+                    [[k[0], k[1], v] for k, v in lr.items()], r.confirmed,
+                    keyed(r.degraded_stages), keyed(r.degraded_links)])
+    dump("detector_units", {"change_point": cp, "validate": val})
+
+    # closed-loop detector traces: the reference's own observe() on records
+    # from the reference simulator, noisy stage costs rounded to float32 so a
+    # float32 device trace reproduces them exactly
+    traces = []
+    for seed in range(6):
+        traces.append(detector_trace(seed))
+    dump("detector_traces", {"traces": traces})
+
+
+def detector_trace(seed: int):
+    rng = np.random.default_rng([seed, 7])
+    tp, dp, pp = [(4, 2, 2), (2, 4, 2), (4, 2, 4), (2, 2, 3), (1, 4, 2), (4, 4, 2)][seed]
+    schedule = "zbh" if seed % 3 == 2 else "1f1b"
+    cfg = rc.ParallelismConfig(tp=tp, dp=dp, pp=pp, schedule=schedule,
+                               layer_partition=[4] * pp)
+    nodes = max(1, -(-tp * dp * pp // 8))
+    state0 = rc.build_cluster(nodes, 8, cfg, 300.0 * 2**30, 25.0 * 2**30)
+    model = rw.CostModel(alpha=2e-6, beta=5e-10)
+    comm = CommSpec()
+    n_iter = 90
+    slow_dev = int(rng.integers(tp * dp * pp))
+    events = [rc.FailureEvent(kind="fail_slow_compute", start=0.0, device=slow_dev,
+                              severity=float(rng.choice([0.4, 0.5, 0.6])))]
+    if nodes > 1:
+        events.append(rc.FailureEvent(kind="fail_slow_comm", start=0.0, link=(0, 1),
+                                      severity=0.5))
+    onset = [40, 70]
+    det = rd.DetectorState(window=int(rng.choice([10, 20])), filter_enabled=seed % 4 != 3)
+    known_speeds: dict[int, float] = {}
+    known_links: dict = {}
+    docs = np.random.default_rng([seed, 0])
+    M = dp * 4
+    iters = []
+    for k in range(n_iter):
+        act = [e for i, e in enumerate(events) if k >= onset[min(i, 1)]]
+        state = rc.apply_failures(state0, act, 0.0) if act else state0.copy()
+        lengths = [int(max(1, min(4096, round(docs.lognormal(7.2, 0.8))))) for _ in range(M * 4)]
+        mbs = rw.pack_sequences(lengths, 4096)[:M]
+        rec = rp.simulate_iteration(state, cfg, mbs, model, comm=comm)
+        known = state.copy()
+        for dev in known.devices:
+            if dev.status != rc.FAIL_STOP:
+                dev.speed = min(1.0, known_speeds.get(dev.id, 1.0))
+        known.link_factors = dict(known_links)
+        ref = rp.simulate_iteration(known, cfg, mbs, model, comm=comm)
+        noisy = {key: float(np.float32(v * (1.0 + 0.01 * float(rng.standard_normal()))))
+                 for key, v in sorted(rec.stage_cost.items())}
+        import dataclasses
+
+        rec2 = dataclasses.replace(rec, stage_cost=noisy)
+        out = det.observe(rec2, ref.observed_time, reference_stage_cost=ref.stage_cost)
+        reset = False
+        if out.validation is not None and out.validation.confirmed:
+            for key in sorted(out.validation.degraded_stages):
+                for dev_id in state.tp_groups.get(key, ()):
+                    known_speeds[dev_id] = state.devices[dev_id].speed
+            for link in out.validation.degraded_links:
+                known_links[link] = state.link_factors.get(link, 1.0)
+            det.reset_series()
+            reset = True
+        iters.append({
+            "mbs": [list(mb.doc_lengths) for mb in mbs],
+            "known": state_to_json(known),
+            "observed": rec.observed_time,
+            "noisy": keyed(noisy),
+            "link_ratio": keyed(rec.link_ratio),
+            "predicted": ref.observed_time,
+            "expected": keyed(ref.stage_cost),
+            "alarms": out.alarms,
+            "verdict": out.verdict,
+            "confirmed": None if out.validation is None else out.validation.confirmed,
+            "degraded": None if out.validation is None else keyed(out.validation.degraded_stages),
+            "reset_after": reset,
+            "series_len": len(det.series),
+        })
+    return {"cfg": cfg_to_json(cfg), "model": model_to_json(model), "window": det.window,
+            "kappa": det.kappa, "filter_enabled": det.filter_enabled, "iterations": iters,
+            "stats": vars(det.stats)}
+
+
+# ----------------------------------------------------------------- scheduler
+def gen_scheduler():
+    rng = random.Random(4)
+    degrees = []
+    for _ in range(100):
+        g = rng.randint(1, 12)
+        f = rng.randint(0, g)
+        k = rng.choice([1, 2, 4])
+        degrees.append([g, f, k, sorted(rs.candidate_tp_degrees(g, f, k))])
+    subgroup = []
+    for _ in range(400):
+        n = rng.randint(1, 10)
+        speeds = {i: rng.choice([1.0, 0.5, rng.uniform(0.01, 1.0)]) for i in range(n)}
+        degs = rs.candidate_tp_degrees(n, 0, rng.choice([1, 2]))
+        try:
+            chosen, standby = rs.select_tp_subgroup(speeds, degs)
+            subgroup.append([list(speeds.values()), sorted(degs), list(chosen), list(standby)])
+        except rs.GroupUnrecoverable:
+            subgroup.append([list(speeds.values()), sorted(degs), None, None])
+    repart = [[[1.0, 0.5, 1.0], 12, 1, [5, 2, 5]]]
+    for _ in range(400):
+        P = rng.randint(1, 16)
+        speeds = [rng.choice([1.0, 1.0, 0.5, rng.uniform(0.05, 1.0)]) for _ in range(P)]
+        L = P * rng.randint(1, 6) + rng.randint(0, P)
+        ml = rng.choice([1, 1, 2])
+        try:
+            repart.append([speeds, L, ml, rs.repartition_layers(speeds, L, ml)])
+        except ValueError:
+            repart.append([speeds, L, ml, None])
+    prop = []
+    for _ in range(300):
+        D = rng.randint(1, 12)
+        w = [rng.choice([1.0, 0.5, 0.0, rng.uniform(0.0, 1.0)]) for _ in range(D)]
+        total = rng.randint(0, 200)
+        try:
+            prop.append([total, w, rpol.proportional_split(total, w)])
+        except ValueError:
+            prop.append([total, w, None])
+    dump("scheduler_units", {"tp_degrees": degrees, "subgroup": subgroup,
+                             "repartition": repart, "proportional": prop})
+
+
+if __name__ == "__main__":
+    gen_workload()
+    gen_pipeline()
+    gen_detector()
+    gen_scheduler()
