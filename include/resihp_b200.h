@@ -175,16 +175,6 @@ int rh_detect_batch(rh_ctx* ctx, const rh_pipe_shape* shape,
                     const rh_trace* trace, double threshold,
                     const rh_pass_out* out, void* stream);
 
-/*
- * Same as rh_detect_batch but every pointer in segs/trace/out is a HOST
- * pointer (pinned memory recommended).  Copies in, runs, copies out and
- * synchronises `stream`.  This is the reference-facing end-to-end call.
- */
-int rh_detect_batch_host(rh_ctx* ctx, const rh_pipe_shape* shape,
-                         const rh_cost_model* model, const rh_segments* segs,
-                         const rh_trace* trace, double threshold,
-                         const rh_pass_out* out, void* stream);
-
 /* ------------------------------------------------------ validate (batch) */
 /* validate (detector.py:127-158) on explicit arrays: flag[i] = measured[i] >
  * thr*expected[i] (skipping non-positive entries), sev[i] = expected/measured
@@ -234,6 +224,23 @@ int rh_screen(rh_ctx* ctx, const rh_screen_params* params, int64_t series_len,
 int rh_pack_sequences(int64_t n_docs, const int32_t* lengths, int32_t budget,
                       int64_t max_bins, int32_t* mb_off, int32_t* doc_len,
                       int64_t* n_bins_out, int64_t* n_entries_out);
+
+/* ------------------------------------------- end-to-end Detector pass */
+/*
+ * The whole Detector for a trace, HOST buffers in and out: copies segs and
+ * trace (and hist/reset) to the device, runs rh_detect_batch then rh_screen
+ * (when screen != NULL), copies `out`, outcome[n] and *series_len_out back
+ * and synchronises `stream`.  This is the reference-facing call: one
+ * DetectorState.observe(...) per iteration of resilsim (harness.py:402-431)
+ * becomes one call per trace.  Pinned host memory gives full PCIe/C2C rate.
+ */
+int rh_detector_pass_host(rh_ctx* ctx, const rh_pipe_shape* shape,
+                          const rh_cost_model* model, const rh_segments* segs,
+                          const rh_trace* trace, double threshold,
+                          const rh_screen_params* screen, int64_t series_len,
+                          const double* hist, const uint8_t* reset,
+                          const rh_pass_out* out, uint8_t* outcome,
+                          int64_t* series_len_out, void* stream);
 
 /* -------------------------------------------- general DAG critical path */
 /*

@@ -90,9 +90,10 @@ _SIGS = {
                           C.c_int),
     "rh_detect_batch": ([_p, C.POINTER(PipeShape), C.POINTER(CostModelC), C.POINTER(Segments),
                          C.POINTER(Trace), C.c_double, C.POINTER(PassOut), _p], C.c_int),
-    "rh_detect_batch_host": ([_p, C.POINTER(PipeShape), C.POINTER(CostModelC),
-                              C.POINTER(Segments), C.POINTER(Trace), C.c_double,
-                              C.POINTER(PassOut), _p], C.c_int),
+    "rh_detector_pass_host": ([_p, C.POINTER(PipeShape), C.POINTER(CostModelC),
+                               C.POINTER(Segments), C.POINTER(Trace), C.c_double,
+                               C.POINTER(ScreenParams), C.c_int64, _p, _p, C.POINTER(PassOut),
+                               _p, C.POINTER(C.c_int64), _p], C.c_int),
     "rh_pack_sequences": ([C.c_int64, _p, C.c_int32, C.c_int64, _p, _p, C.POINTER(C.c_int64),
                            C.POINTER(C.c_int64)], C.c_int),
     "rh_validate": ([_p, C.c_int64, _p, _p, C.c_double, _p, _p, _p], C.c_int),

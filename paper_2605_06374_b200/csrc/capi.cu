@@ -20,23 +20,23 @@ void set_error(const char* fmt, ...) {
   va_end(ap);
 }
 
-int workspace(rh_ctx* ctx, size_t bytes, void** out) {
-  if (bytes > ctx->ws_bytes) {
-    if (ctx->ws) {
+int workspace(rh_ctx* ctx, size_t bytes, void** out, int slot) {
+  if (bytes > ctx->ws_bytes[slot]) {
+    if (ctx->ws[slot]) {
       RH_CUDA(cudaDeviceSynchronize());
-      RH_CUDA(cudaFree(ctx->ws));
-      ctx->ws = nullptr;
-      ctx->ws_bytes = 0;
+      RH_CUDA(cudaFree(ctx->ws[slot]));
+      ctx->ws[slot] = nullptr;
+      ctx->ws_bytes[slot] = 0;
     }
     size_t want = bytes + bytes / 4 + (1u << 20);
-    cudaError_t e = cudaMalloc(&ctx->ws, want);
+    cudaError_t e = cudaMalloc(&ctx->ws[slot], want);
     if (e != cudaSuccess) {
       set_error("workspace of %zu bytes: %s", want, cudaGetErrorString(e));
       return RH_E_NOMEM;
     }
-    ctx->ws_bytes = want;
+    ctx->ws_bytes[slot] = want;
   }
-  *out = ctx->ws;
+  *out = ctx->ws[slot];
   return RH_OK;
 }
 
@@ -144,7 +144,8 @@ int rh_ctx_create(int device, rh_ctx** out) {
 
 int rh_ctx_destroy(rh_ctx* ctx) {
   if (!ctx) return RH_OK;
-  if (ctx->ws) cudaFree(ctx->ws);
+  for (void* w : ctx->ws)
+    if (w) cudaFree(w);
   delete ctx;
   return RH_OK;
 }

@@ -16,10 +16,10 @@ struct rh_ctx {
   int num_sms = 148;
   size_t smem_optin = 0;
   std::atomic<int64_t> launches{0};
-  // grow-only device workspace (host-buffer entry points, screen scratch)
-  void* ws = nullptr;
-  size_t ws_bytes = 0;
-  // grow-only pinned host staging is NOT kept: callers pass pinned memory.
+  // grow-only device workspaces: slot 0 = host-buffer staging,
+  // slot 1 = kernel scratch (screen, general DAG); never aliased
+  void* ws[2] = {nullptr, nullptr};
+  size_t ws_bytes[2] = {0, 0};
 };
 
 namespace rh {
@@ -46,7 +46,7 @@ inline int cuda_fail(cudaError_t e, const char* what) {
 
 // Grow the context workspace to at least `bytes` (stream-ordered free of the
 // old buffer is not needed: callers synchronise before growth).
-int workspace(rh_ctx* ctx, size_t bytes, void** out);
+int workspace(rh_ctx* ctx, size_t bytes, void** out, int slot);
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 

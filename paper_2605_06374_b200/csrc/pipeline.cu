@@ -81,6 +81,10 @@ __device__ __forceinline__ void decode(int k, int w, int m, int& kind, int& j) {
   }
 }
 
+// Exact fp64 division, kept out of line so the common unit-speed path is a
+// branch over it instead of an always-executed predicated sequence.
+__device__ __noinline__ double div_slow(double a, double b) { return __ddiv_rn(a, b); }
+
 template <int ZBH, int DETECT>
 __global__ void __launch_bounds__(1024) pass_kernel(const PassParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -99,11 +103,9 @@ __global__ void __launch_bounds__(1024) pass_kernel(const PassParams p) {
   double* it_ms = reinterpret_cast<double*>(smem_raw);
   unsigned* it_st = reinterpret_cast<unsigned*>(it_ms + p.ipb);
   const int it_bytes = ((p.ipb * 12 + 15) / 16) * 16;
-  const int rows = 2 * P + 1;
+  // per pipeline: base cost alpha*N + beta*Q_j of its micro-batches
   double* gbase = reinterpret_cast<double*>(smem_raw + it_bytes) +
-                  (size_t)(tid >> p.log_pw) * rows * p.mmax;
-  double* Ff = gbase + p.mmax;      // [P][mmax] forward finish of (s, j)
-  double* Bf = Ff + P * p.mmax;     // [P][mmax] backward finish of (s, j)
+                  (size_t)(tid >> p.log_pw) * p.mmax;
 
   if (tid < p.ipb) {
     it_ms[tid] = 0.0;
@@ -153,27 +155,31 @@ __global__ void __launch_bounds__(1024) pass_kernel(const PassParams p) {
       stopped = true;
       n_chain = 0;
     }
-    for (int j = 0; j < md; ++j) {
-      Ff[s * p.mmax + j] = -1.0;
-      Bf[s * p.mmax + j] = -1.0;
-    }
   }
-  __syncthreads();
+  __syncthreads();  // base costs visible; iteration slots initialised
   // a stopped stage invalidates the whole iteration (the reference raises
   // before building any DAG); its pipeline neighbours must not wait on it
   const unsigned bad = __ballot_sync(0xffffffffu, stopped) & gmask;
   if (bad) n_chain = 0;
 
   // ---------------------------------------------------------- wavefront
+  // Each lane walks its stage chain; a step processes the lane's next chunk
+  // once its data predecessor is done.  Neighbour finish times travel by
+  // warp shuffle: every lane publishes (index, finish) of the last F and
+  // last B/BW it completed.  In the canonical 1F1B/ZBH DAG a B dependency is
+  // always produced exactly one step earlier and a producer stage never
+  // runs more than one F ahead of its consumer (checked exhaustively for
+  // P <= 32, M <= 64), so the last-produced value is exactly
+  // the one needed.  A skipped index is detected and flagged, never used.
   const bool unit = sp == 1.0;  // x / 1.0 == x exactly: skip the division
   const int cap = p.sh.capacity;
-  int k = 0, live = 0;
+  const int lim = 2 * md - w;  // end of the steady F/B pairs
+  int k = 0, jf = 0, jb = 0, jw = 0, live = 0;
   bool over = false, hung = false;
   double fin = 0.0, ssum = 0.0;
+  double lastF = 0.0, lastB = 0.0;
+  int lastFi = -1, lastBi = -1;
   bool pending = n_chain > 0;
-  volatile double* vF = Ff;
-  volatile double* vB = Bf;
-  // every step retires >= 1 vertex of each unfinished pipeline (acyclic DAG)
   const int max_steps = (ZBH ? 3 : 2) * p.mmax * P + 2;
   int steps = 0;
   while (__any_sync(0xffffffffu, pending)) {
@@ -181,43 +187,58 @@ __global__ void __launch_bounds__(1024) pass_kernel(const PassParams p) {
       hung = pending;
       break;
     }
+    const double nF = __shfl_up_sync(0xffffffffu, lastF, 1, p.pw);
+    const int nFi = __shfl_up_sync(0xffffffffu, lastFi, 1, p.pw);
+    const double nB = __shfl_down_sync(0xffffffffu, lastB, 1, p.pw);
+    const int nBi = __shfl_down_sync(0xffffffffu, lastBi, 1, p.pw);
     if (pending) {
-      int kind, j;
-      decode<ZBH>(k, w, md, kind, j);
-      double dep = 0.0;
-      bool ready = true;
-      if (kind == KF) {
-        if (s > 0) {
-          const double v = vF[(s - 1) * p.mmax + j];
-          ready = v >= 0.0;
-          dep = __dadd_rn(v, hopf);
-        }
-      } else if (kind != KW) {
-        if (s < P - 1) {
-          const double v = vB[(s + 1) * p.mmax + j];
-          ready = v >= 0.0;
-          dep = __dadd_rn(v, hopb);
-        }
+      // kind at chain position k (pipeline.py:92-118), 0=F 1=B/BW 2=W
+      int kind;
+      if (k < w) {
+        kind = 0;
+      } else if (k < lim) {
+        kind = (k - w) & 1;
+      } else if (!ZBH) {
+        kind = 1;
+      } else if (k < 2 * md + w) {
+        kind = ((k - lim) & 1) ? 2 : 1;
+      } else {
+        kind = 2;
       }
-      if (ready) {
-        const double rl = kind == KF ? rlF : (kind == KW ? rlW : rlB);
-        double c = __dmul_rn(rl, gbase[j]);
-        if (!unit) c = __ddiv_rn(c, sp);
-        const double st = fmax(fin, dep);
-        fin = __dadd_rn(st, c);
+      const int j = kind == 0 ? jf : (kind == 1 ? jb : jw);
+      bool ready = true;
+      double dep = 0.0;
+      if (kind == 0 && s > 0) {
+        ready = nFi == j;
+        if (nFi > j) hung = true;  // violated lead bound: never guess
+        dep = __dadd_rn(nF, hopf);
+      } else if (kind == 1 && s < P - 1) {
+        ready = nBi == j;
+        if (nBi > j) hung = true;
+        dep = __dadd_rn(nB, hopb);
+      }
+      if (hung) {
+        pending = false;
+      } else if (ready) {
+        double c = __dmul_rn(kind == 0 ? rlF : (kind == 1 ? rlB : rlW), gbase[j]);
+        if (!unit) c = div_slow(c, sp);
+        fin = __dadd_rn(fmax(fin, dep), c);
         ssum = __dadd_rn(ssum, c);
-        if (kind == KF) {
-          if (s < P - 1) vF[s * p.mmax + j] = fin;
+        if (kind == 0) {
+          lastF = fin;
+          lastFi = jf++;
           if (cap > 0 && ++live > cap) over = true;
-        } else if (kind != KW) {
-          if (s > 0) vB[s * p.mmax + j] = fin;
+        } else if (kind == 1) {
+          lastB = fin;
+          lastBi = jb++;
           --live;
+        } else {
+          ++jw;
         }
         ++k;
         pending = k < n_chain;
       }
     }
-    __syncwarp();
   }
 
   // ------------------------------------------------------ reductions
@@ -341,7 +362,7 @@ int launch_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
   p.vec4 = (sh->tp % 4 == 0) && ((reinterpret_cast<uintptr_t>(tr->device_time) & 15) == 0);
   const int threads = ((p.ipb * p.lpi + 31) / 32) * 32;
   const int it_bytes = ((p.ipb * 12 + 15) / 16) * 16;
-  const size_t smem = it_bytes + (size_t)(threads / p.pw) * (2 * P + 1) * p.mmax * 8;
+  const size_t smem = it_bytes + (size_t)(threads / p.pw) * p.mmax * 8;
   if (smem > ctx->smem_optin) {
     set_error("pass: %zu bytes of shared memory needed (max_mb_per_replica=%d, pp=%d); "
               "limit %zu", smem, p.mmax, P, ctx->smem_optin);
@@ -380,7 +401,9 @@ struct Carver {
 
 int detect_host(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
                 const rh_segments* sg, const rh_trace* tr, double thr,
-                const rh_pass_out* out, cudaStream_t stream) {
+                const rh_screen_params* screen, int64_t series_len, const double* hist,
+                const uint8_t* reset, const rh_pass_out* out, uint8_t* outcome,
+                int64_t* series_len_out, cudaStream_t stream) {
   if (!ctx || !sh || !sg || !tr || !out || !tr->mb_off) {
     set_error("detect_host: NULL argument");
     return RH_E_INVALID;
@@ -409,10 +432,14 @@ int detect_host(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
     c.take<double>(n * G);
     c.take<uint8_t>(n * G);
     c.take<float>(n * G);
+    c.take<double>(64);
+    c.take<uint8_t>(n);
+    c.take<uint8_t>(n);
+    c.take<int64_t>(1);
     need = c.off + 256;
   }
   void* ws = nullptr;
-  int rc = workspace(ctx, need, &ws);
+  int rc = workspace(ctx, need, &ws, 0);
   if (rc) return rc;
   Carver c{static_cast<char*>(ws)};
   rh_trace dtr = *tr;
@@ -448,8 +475,30 @@ int detect_host(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
   dout.stage_cost = out->stage_cost ? c.take<double>(n * G) : nullptr;
   dout.stage_flag = out->stage_flag ? c.take<uint8_t>(n * G) : nullptr;
   dout.severity = out->severity ? c.take<float>(n * G) : nullptr;
+  double* d_hist = c.take<double>(64);
+  uint8_t* d_reset = c.take<uint8_t>(n);
+  uint8_t* d_outcome = c.take<uint8_t>(n);
+  int64_t* d_len = c.take<int64_t>(1);
+  const int64_t h = screen ? std::min<int64_t>(series_len, screen->window) : 0;
+  if (screen && h > 64) {
+    set_error("detector_pass_host: window > 64");
+    return RH_E_INVALID;
+  }
+  if (h) RH_CUDA(cudaMemcpyAsync(d_hist, hist, h * sizeof(double), cudaMemcpyHostToDevice, stream));
+  if (screen && reset)
+    RH_CUDA(cudaMemcpyAsync(d_reset, reset, n, cudaMemcpyHostToDevice, stream));
   rc = launch_pass(ctx, sh, m, &dsg, &dtr, thr, 1, &dout, stream);
   if (rc) return rc;
+  if (screen) {
+    rc = rh_screen(ctx, screen, series_len, d_hist, n, dtr.observed, dout.status,
+                   reset ? d_reset : nullptr, d_outcome, d_len, stream);
+    if (rc) return rc;
+    if (outcome)
+      RH_CUDA(cudaMemcpyAsync(outcome, d_outcome, n, cudaMemcpyDeviceToHost, stream));
+    if (series_len_out)
+      RH_CUDA(cudaMemcpyAsync(series_len_out, d_len, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                              stream));
+  }
   RH_CUDA(cudaMemcpyAsync(out->makespan, dout.makespan, n * sizeof(double),
                           cudaMemcpyDeviceToHost, stream));
   RH_CUDA(cudaMemcpyAsync(out->status, dout.status, n, cudaMemcpyDeviceToHost, stream));
@@ -483,11 +532,13 @@ int rh_detect_batch(rh_ctx* ctx, const rh_pipe_shape* shape, const rh_cost_model
                          rh::as_stream(stream));
 }
 
-int rh_detect_batch_host(rh_ctx* ctx, const rh_pipe_shape* shape, const rh_cost_model* model,
-                         const rh_segments* segs, const rh_trace* trace, double threshold,
-                         const rh_pass_out* out, void* stream) {
-  return rh::detect_host(ctx, shape, model, segs, trace, threshold, out,
-                         rh::as_stream(stream));
+int rh_detector_pass_host(rh_ctx* ctx, const rh_pipe_shape* shape, const rh_cost_model* model,
+                          const rh_segments* segs, const rh_trace* trace, double threshold,
+                          const rh_screen_params* screen, int64_t series_len,
+                          const double* hist, const uint8_t* reset, const rh_pass_out* out,
+                          uint8_t* outcome, int64_t* series_len_out, void* stream) {
+  return rh::detect_host(ctx, shape, model, segs, trace, threshold, screen, series_len, hist,
+                         reset, out, outcome, series_len_out, rh::as_stream(stream));
 }
 
 }  // extern "C"
