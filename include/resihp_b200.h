@@ -261,6 +261,92 @@ int rh_dag_critical_path(rh_ctx* ctx, int32_t n_vertices, const double* cost,
                          int32_t capacity, double* starts, double* makespan,
                          double* chain_sum, int32_t* flags, void* stream);
 
+/* ------------------------------------------------ Scheduler re-plan search */
+/*
+ * Exhaustive re-plan search over (DP, TP, PP) layouts x layer partitions x
+ * workload-to-replica assignments (BASELINE.json north star; DESIGN.md §5
+ * defines the space).  Every candidate is scored exactly like
+ * resihp_adapt scores its variants (policies.py:329-347):
+ *   score = evaluate_plan(...)          (scheduler.py:543-559: canonical
+ *                                        chunk-DAG makespan incl. terminal
+ *                                        all-reduce, activation capacity)
+ *         + reconfig_cost(...) / max(1, amortize_iterations)
+ * and the best candidate is the lexicographic (score, index) minimum.
+ * Building blocks on the path: candidate_tp_degrees-style power-of-two
+ * degrees (scheduler.py:101-111), fastest-k member selection
+ * (select_tp_subgroup, :114-137), repartition_layers (:146-207),
+ * _replica_speeds + proportional_split (policies.py:138-162).
+ * All pointers in rh_search_desc are HOST pointers (copied at create).
+ */
+typedef struct rh_search_desc {
+  /* cluster: known speed per device (<= 0: not executable, e.g. fail-stop) */
+  int32_t n_devices;
+  int32_t devices_per_node;
+  const double* device_speed;      /* [n_devices]                          */
+  double intra_bw, inter_bw;       /* bytes/s                              */
+  int32_t n_links;                 /* degraded inter-node links            */
+  const int32_t* link_nodes;       /* [n_links][2], a < b                  */
+  const double* link_factor;       /* [n_links]                            */
+  /* workload + cost model */
+  rh_cost_model model;
+  int32_t schedule;                /* RH_SCHED_*                           */
+  int32_t token_budget;
+  int32_t n_micro_batches;
+  const int64_t* quad;             /* [n_micro_batches] sum of l^2         */
+  int32_t total_layers;
+  int32_t min_layers;
+  int32_t capacity;                /* activation capacity (<= 0: none)     */
+  /* communication (CommSpec, comm.py:49-58) */
+  int32_t has_comm;
+  double hidden_bytes_per_token;
+  double layer_bytes;
+  int32_t p2p_optimized;
+  /* candidate space */
+  int32_t nominal_tp;              /* cfg.tp: a T-wide group of slowest speed v runs at
+                                      v*T/nominal_tp (effective_stage_speed, cluster.py:155) */
+  int32_t max_tp;                  /* TP degrees: powers of two dividing devices_per_node */
+  int32_t max_pp;                  /* <= 32                                */
+  int32_t max_dp;
+  double min_utilization;          /* layouts use >= this share of executable devices */
+  /* current plan (reconfiguration surcharge) */
+  int32_t cur_tp, cur_dp, cur_pp;  /* 0 = none                             */
+  const int32_t* cur_groups;       /* [cur_dp*cur_pp][cur_tp] members, replica-major */
+  const int32_t* cur_partition;    /* [cur_pp]                             */
+  double group_rebuild_s;
+  int32_t amortize_iterations;
+} rh_search_desc;
+
+typedef struct rh_search rh_search;
+
+/* One decoded candidate (host memory). */
+typedef struct rh_candidate {
+  int64_t index;
+  int32_t tp, dp, pp;
+  int32_t layout;                  /* layout ordinal                       */
+  int32_t partition_variant;       /* 0 even, 1 repartition, >=2 one move  */
+  int32_t count_variant;           /* 0 even, 1 proportional, >=2 one move */
+  int32_t feasible;
+} rh_candidate;
+
+/* Enumerate layouts, upload inputs and run the per-layout preparation
+ * (placement, hop/ring tables, repartition_layers, proportional_split) on
+ * the GPU.  Synchronises `stream`. */
+int rh_search_create(rh_ctx* ctx, const rh_search_desc* desc, rh_search** out, void* stream);
+int rh_search_destroy(rh_search* search);
+/* total number of candidates / layouts */
+int64_t rh_search_size(const rh_search* search);
+int32_t rh_search_layouts(const rh_search* search);
+/* Score candidates [begin, end) and min-loc them.  best_score/best_index are
+ * DEVICE scalars (+inf / -1 when nothing is feasible); scores (optional,
+ * device, [end-begin]) receives every candidate's score (+inf infeasible). */
+int rh_search_eval(rh_ctx* ctx, rh_search* search, int64_t begin, int64_t end,
+                   double* best_score, int64_t* best_index, double* scores,
+                   void* stream);
+/* Decode a candidate index: layout, variants, and (host arrays, optional)
+ * groups[dp*pp][tp] member ids, partition[pp], counts[dp]. */
+int rh_search_decode(rh_ctx* ctx, rh_search* search, int64_t index, rh_candidate* out,
+                     int32_t* groups, int32_t* partition, int32_t* counts);
+
 #ifdef __cplusplus
 }
 #endif

@@ -124,7 +124,7 @@ int orc_critical_path(int32_t nv, const double* cost, int32_t ne,
 
 /* --------------------------------------------------------------- batch DAG */
 
-typedef struct {
+typedef struct scratch_s {
   /* scratch sized for the largest iteration of a batch */
   int cap_v, cap_e;
   int* kind; int* mb; int* stage; int* rep;
@@ -137,6 +137,16 @@ typedef struct {
   double* ev_t; int* ev_d;
 } scratch_t;
 
+void orc_scratch_init(scratch_t* s, const rh_pipe_shape* sh);
+void orc_scratch_free(scratch_t* s);
+static uint8_t dag_iteration(scratch_t* S, const rh_pipe_shape* sh,
+                             const rh_cost_model* model, const rh_segments* sg, int seg,
+                             double* makespan, double* stage_cost);
+uint8_t orc_dag_iteration(scratch_t* S, const rh_pipe_shape* sh, const rh_cost_model* model,
+                          const rh_segments* sg, int seg, double* makespan,
+                          double* stage_cost) {
+  return dag_iteration(S, sh, model, sg, seg, makespan, stage_cost);
+}
 static void scratch_init(scratch_t* s, const rh_pipe_shape* sh) {
   int c = sh->schedule == RH_SCHED_1F1B ? 2 : 3;
   int M = sh->micro_batches, P = sh->pp, D = sh->dp;
@@ -163,6 +173,19 @@ static void scratch_init(scratch_t* s, const rh_pipe_shape* sh) {
   s->ev_d = malloc(sizeof(int) * (2 * M + 2));
 }
 
+void orc_scratch_init(scratch_t* s, const rh_pipe_shape* sh) { scratch_init(s, sh); }
+void* orc_scratch_new(const rh_pipe_shape* sh) {
+  scratch_t* s = (scratch_t*)malloc(sizeof(scratch_t));
+  scratch_init(s, sh);
+  return s;
+}
+int64_t* orc_scratch_quad(void* s) { return ((scratch_t*)s)->quad; }
+static void scratch_free(scratch_t* s);
+void orc_scratch_free(scratch_t* s) { scratch_free(s); }
+void orc_scratch_delete(void* s) {
+  scratch_free((scratch_t*)s);
+  free(s);
+}
 static void scratch_free(scratch_t* s) {
   free(s->kind); free(s->mb); free(s->stage); free(s->rep); free(s->cost);
   free(s->starts); free(s->src); free(s->dst); free(s->w); free(s->vid_f);
@@ -183,24 +206,36 @@ static int ev_cmp(const void* a, const void* b) {
  * hop weights and AR costs, critical_path, stage sums (pipeline.py:446-453)
  * and _check_activation_memory (pipeline.py:516-539).
  */
+static uint8_t dag_iteration(scratch_t* S, const rh_pipe_shape* sh,
+                             const rh_cost_model* model, const rh_segments* sg, int seg,
+                             double* makespan, double* stage_cost);
+
 static uint8_t run_iteration(scratch_t* S, const rh_pipe_shape* sh,
                              const rh_cost_model* model, const rh_segments* sg,
                              const rh_trace* tr, int64_t it, double* makespan,
                              double* stage_cost /* [D][P] or NULL */) {
+  const int M = sh->micro_batches;
+  for (int j = 0; j < M; ++j) {
+    int64_t a = tr->mb_off[it * M + j], b = tr->mb_off[it * M + j + 1];
+    S->quad[j] = orc_quad_load((int32_t)(b - a), tr->doc_len + a);
+  }
+  return dag_iteration(S, sh, model, sg, tr->seg ? tr->seg[it] : 0, makespan, stage_cost);
+}
+
+/* One iteration given S->quad[]: build_dag + critical_path + stage sums +
+ * activation check for segment `seg`. */
+static uint8_t dag_iteration(scratch_t* S, const rh_pipe_shape* sh,
+                             const rh_cost_model* model, const rh_segments* sg, int seg,
+                             double* makespan, double* stage_cost) {
   const int P = sh->pp, D = sh->dp, M = sh->micro_batches;
   const int zbh = sh->schedule == RH_SCHED_ZBH;
-  const int seg = tr->seg ? tr->seg[it] : 0;
   const int32_t* layers = sg->layers + (int64_t)seg * P;
   const int32_t* mb_start = sg->mb_start + (int64_t)seg * (D + 1);
   const double* speed = sg->speed + (int64_t)seg * D * P;
   const double* hf = sg->hop_fwd + (int64_t)seg * D * P;
   const double* hb = sg->hop_bwd + (int64_t)seg * D * P;
   uint8_t status = 0;
-
-  for (int j = 0; j < M; ++j) {
-    int64_t a = tr->mb_off[it * M + j], b = tr->mb_off[it * M + j + 1];
-    S->quad[j] = orc_quad_load((int32_t)(b - a), tr->doc_len + a);
-  }
+  (void)M;
   /* completeness check (pipeline.py:408-415): every chunk's stage alive */
   for (int d = 0; d < D; ++d)
     if (mb_start[d + 1] > mb_start[d])

@@ -65,6 +65,29 @@ int orc_screen(const rh_screen_params* params, int64_t series_len,
                const uint8_t* it_status, const uint8_t* reset, uint8_t* outcome,
                int64_t* series_len_out);
 
+/* scratch for one canonical DAG evaluation (sized by `sh`) */
+void* orc_scratch_new(const rh_pipe_shape* sh);
+void orc_scratch_delete(void* s);
+int64_t* orc_scratch_quad(void* s);  /* [M] quad loads consumed by orc_dag_iteration */
+struct scratch_s;
+uint8_t orc_dag_iteration(struct scratch_s* S, const rh_pipe_shape* sh,
+                          const rh_cost_model* model, const rh_segments* sg, int seg,
+                          double* makespan, double* stage_cost);
+
+/* ---- re-plan search, restated on the CPU (search_oracle.c) */
+typedef struct orc_search orc_search;
+orc_search* orc_search_create(const rh_search_desc* desc);
+void orc_search_destroy(orc_search* s);
+int64_t orc_search_size(const orc_search* s);
+/* score of one candidate: evaluate_plan makespan (canonical DAG + Kahn,
+ * capacity) + amortised reconfiguration surcharge; +inf when infeasible */
+double orc_search_score(orc_search* s, int64_t index);
+/* lexicographic (score, index) min over [begin, end) on n_threads */
+int orc_search_eval(orc_search* s, int64_t begin, int64_t end, int n_threads,
+                    double* best_score, int64_t* best_index, double* scores);
+int orc_search_decode(orc_search* s, int64_t index, rh_candidate* out, int32_t* groups,
+                      int32_t* partition, int32_t* counts);
+
 #ifdef __cplusplus
 }
 #endif

@@ -27,10 +27,9 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "wavefront.cuh"
 
 namespace rh {
-
-enum { KF = 0, KB = 1, KW = 2, KBW = 3 };
 
 struct PassParams {
   rh_pipe_shape sh;
@@ -45,45 +44,6 @@ struct PassParams {
   int mmax;        // micro-batches per replica (smem row length)
   int vec4;        // device_time rows are float4-aligned
 };
-
-// Position k of the stage chain -> (kind, local micro-batch index).
-// 1F1B (pipeline.py:92-101): F_0..F_{w-1} | (F_{w+t}, BW_t) pairs | BW tail
-// ZBH  (pipeline.py:104-118): F warmup | (F,B) pairs | (B,W) drain | W tail
-template <int ZBH>
-__device__ __forceinline__ void decode(int k, int w, int m, int& kind, int& j) {
-  if (k < w) {
-    kind = KF;
-    j = k;
-  } else if (k < 2 * m - w) {
-    int t = k - w;
-    if (t & 1) {
-      kind = ZBH ? KB : KBW;
-      j = t >> 1;
-    } else {
-      kind = KF;
-      j = w + (t >> 1);
-    }
-  } else if (!ZBH) {
-    kind = KBW;
-    j = k - m;
-  } else if (k < 2 * m + w) {
-    int t = k - (2 * m - w);
-    if (t & 1) {
-      kind = KW;
-      j = t >> 1;
-    } else {
-      kind = KB;
-      j = m - w + (t >> 1);
-    }
-  } else {
-    kind = KW;
-    j = k - 2 * m;
-  }
-}
-
-// Exact fp64 division, kept out of line so the common unit-speed path is a
-// branch over it instead of an always-executed predicated sequence.
-__device__ __noinline__ double div_slow(double a, double b) { return __ddiv_rn(a, b); }
 
 template <int ZBH, int DETECT>
 __global__ void __launch_bounds__(1024) pass_kernel(const PassParams p) {
@@ -163,83 +123,10 @@ __global__ void __launch_bounds__(1024) pass_kernel(const PassParams p) {
   if (bad) n_chain = 0;
 
   // ---------------------------------------------------------- wavefront
-  // Each lane walks its stage chain; a step processes the lane's next chunk
-  // once its data predecessor is done.  Neighbour finish times travel by
-  // warp shuffle: every lane publishes (index, finish) of the last F and
-  // last B/BW it completed.  In the canonical 1F1B/ZBH DAG a B dependency is
-  // always produced exactly one step earlier and a producer stage never
-  // runs more than one F ahead of its consumer (checked exhaustively for
-  // P <= 32, M <= 64), so the last-produced value is exactly
-  // the one needed.  A skipped index is detected and flagged, never used.
-  const bool unit = sp == 1.0;  // x / 1.0 == x exactly: skip the division
-  const int cap = p.sh.capacity;
-  const int lim = 2 * md - w;  // end of the steady F/B pairs
-  int k = 0, jf = 0, jb = 0, jw = 0, live = 0;
-  bool over = false, hung = false;
   double fin = 0.0, ssum = 0.0;
-  double lastF = 0.0, lastB = 0.0;
-  int lastFi = -1, lastBi = -1;
-  bool pending = n_chain > 0;
-  const int max_steps = (ZBH ? 3 : 2) * p.mmax * P + 2;
-  int steps = 0;
-  while (__any_sync(0xffffffffu, pending)) {
-    if (++steps > max_steps) {  // defensive: never spin on a malformed input
-      hung = pending;
-      break;
-    }
-    const double nF = __shfl_up_sync(0xffffffffu, lastF, 1, p.pw);
-    const int nFi = __shfl_up_sync(0xffffffffu, lastFi, 1, p.pw);
-    const double nB = __shfl_down_sync(0xffffffffu, lastB, 1, p.pw);
-    const int nBi = __shfl_down_sync(0xffffffffu, lastBi, 1, p.pw);
-    if (pending) {
-      // kind at chain position k (pipeline.py:92-118), 0=F 1=B/BW 2=W
-      int kind;
-      if (k < w) {
-        kind = 0;
-      } else if (k < lim) {
-        kind = (k - w) & 1;
-      } else if (!ZBH) {
-        kind = 1;
-      } else if (k < 2 * md + w) {
-        kind = ((k - lim) & 1) ? 2 : 1;
-      } else {
-        kind = 2;
-      }
-      const int j = kind == 0 ? jf : (kind == 1 ? jb : jw);
-      bool ready = true;
-      double dep = 0.0;
-      if (kind == 0 && s > 0) {
-        ready = nFi == j;
-        if (nFi > j) hung = true;  // violated lead bound: never guess
-        dep = __dadd_rn(nF, hopf);
-      } else if (kind == 1 && s < P - 1) {
-        ready = nBi == j;
-        if (nBi > j) hung = true;
-        dep = __dadd_rn(nB, hopb);
-      }
-      if (hung) {
-        pending = false;
-      } else if (ready) {
-        double c = __dmul_rn(kind == 0 ? rlF : (kind == 1 ? rlB : rlW), gbase[j]);
-        if (!unit) c = div_slow(c, sp);
-        fin = __dadd_rn(fmax(fin, dep), c);
-        ssum = __dadd_rn(ssum, c);
-        if (kind == 0) {
-          lastF = fin;
-          lastFi = jf++;
-          if (cap > 0 && ++live > cap) over = true;
-        } else if (kind == 1) {
-          lastB = fin;
-          lastBi = jb++;
-          --live;
-        } else {
-          ++jw;
-        }
-        ++k;
-        pending = k < n_chain;
-      }
-    }
-  }
+  bool over = false, hung = false;
+  chain_walk<ZBH>(s, P, p.pw, md, w, n_chain, gbase, rlF, rlB, rlW, sp, hopf, hopb,
+                  p.sh.capacity, p.mmax, fin, ssum, over, hung);
 
   // ------------------------------------------------------ reductions
   double gmax = fin;

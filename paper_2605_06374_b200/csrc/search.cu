@@ -1,0 +1,849 @@
+// Scheduler re-plan search (rh_search_*): DESIGN.md §5.
+//
+// Candidate space (index order defines the (score, index) tie-break):
+//   layouts (T, D, P), T a power of two dividing devices_per_node, ordered by
+//   T, then P, then D; a layout is enumerated when D*P TP blocks of T
+//   executable devices exist, T*D*P >= min_utilization * executable and
+//   D <= min(max_dp, M), P <= min(max_pp, L / min_layers)
+//   x partition variants  v: 0 even split, 1 repartition_layers(stage
+//     speeds) (scheduler.py:146-207), 2.. one layer moved src->dst from it
+//   x count variants      u: 0 even split (cluster.py:318-321), 1
+//     proportional_split(M, replica speeds) (policies.py:138-162), 2.. one
+//     micro-batch moved src->dst from it
+// Placement of a layout: every node's executable devices sorted by (speed
+// desc, id) form blocks of T (the fastest-k rule of select_tp_subgroup,
+// scheduler.py:114-137); the D*P fastest blocks (ties: node, position) are
+// taken in node order and assigned replica-major, which is build_cluster's
+// layout (cluster.py:175-208) on a healthy cluster.
+//
+// GPU work: one warp per layout prepares group speeds/nodes, hop weights,
+// all-reduce ring bandwidths, repartition and proportional split; one warp
+// per candidate evaluates the canonical chunk-DAG makespan replica by
+// replica with the shared wavefront (wavefront.cuh), adds the amortised
+// reconfiguration surcharge and keeps a lexicographic (score, index) min.
+#include <algorithm>
+#include <cmath>
+#include <limits>
+#include <vector>
+
+#include <math_constants.h>
+
+#include "common.cuh"
+#include "wavefront.cuh"
+
+struct rh_search {
+  rh_search_desc d{};
+  int n_nodes = 0;
+  // host copies
+  std::vector<double> speed;
+  std::vector<int32_t> link_nodes;
+  std::vector<double> link_factor;
+  std::vector<int32_t> cur_groups, cur_partition;
+  // layouts
+  std::vector<int32_t> lT, lD, lP, lgoff, lpoff, ldoff, lboff, lnb;
+  std::vector<long long> lbase, lnv, lnu;
+  int64_t total = 0;
+  // blocks (concatenated over the distinct T values)
+  std::vector<int32_t> blk_node, blk_rank, blk_members, blk_moff;
+  std::vector<double> blk_speed;
+  // device memory (one allocation)
+  void* dmem = nullptr;
+  size_t dbytes = 0;
+  struct Dev {
+    int32_t *lT, *lD, *lP, *lgoff, *lpoff, *ldoff, *lboff, *lnb;
+    long long *lbase, *lnv, *lnu;
+    int32_t *blk_node, *blk_rank, *blk_members, *blk_moff;
+    double* blk_speed;
+    int32_t *gblk, *gnode;
+    double *gspeed, *ghop;
+    double *ring, *sspeed;
+    int32_t* repart;
+    double* rspeed;
+    int32_t* pstart;
+    int32_t* same;
+    double* base;
+    int64_t* quad;
+    int32_t *link_nodes, *cur_groups, *cur_partition;
+    double* link_factor;
+    double* blk_best;
+    long long* blk_idx;
+  } dv{};
+  int eval_blocks = 0;
+  size_t n_groups = 0, n_stage = 0, n_rep = 0;
+};
+
+namespace rh {
+
+constexpr int kEvalThreads = 256;
+
+struct SearchArgs {
+  rh_cost_model m;
+  int sched, N, M, L, min_layers, cap, has_comm, p2p_opt, n_layouts, n_links;
+  double intra, inter, nbytes, lb, worst_inter, rebuild_s;
+  int amort;
+  int cur_T, cur_D, cur_P, T0;
+  rh_search::Dev v;
+};
+
+// comm.py:32-36 — inter-node bandwidth of a node pair
+__device__ __forceinline__ double link_inter(const SearchArgs& a, int x, int y) {
+  const int lo = min(x, y), hi = max(x, y);
+  double f = 1.0;
+  for (int q = 0; q < a.n_links; ++q)
+    if (a.v.link_nodes[2 * q] == lo && a.v.link_nodes[2 * q + 1] == hi) {
+      f = a.v.link_factor[q];
+      break;
+    }
+  return __dmul_rn(a.inter, f);
+}
+
+// edge_cost_fn (pipeline.py:336-353) between two T-wide groups
+__device__ __forceinline__ double hop_cost(const SearchArgs& a, int na, int nb, int T) {
+  if (!a.has_comm) return 0.0;
+  if (na == nb) return __ddiv_rn(a.nbytes, a.intra);
+  const double inter = link_inter(a, na, nb);
+  if (!a.p2p_opt) {  // comm.py:73-75
+    const double cross = __dmul_rn((double)T, a.nbytes);
+    return __ddiv_rn(cross, inter);
+  }
+  const double gather = __ddiv_rn(__dmul_rn(a.nbytes, (double)(T - 1)), __dmul_rn((double)T, a.intra));
+  return __dadd_rn(__ddiv_rn(a.nbytes, inter), gather);  // comm.py:76-78
+}
+
+// repartition_layers (scheduler.py:146-207), sequential, one thread
+__device__ void repartition_dev(const double* sp, int n, int L, int ml, int32_t* out) {
+  double tot = 0.0;
+  for (int i = 0; i < n; ++i) tot = __dadd_rn(tot, sp[i]);
+  double frac[32];
+  int lay[32];
+  int sum = 0;
+  for (int i = 0; i < n; ++i) {
+    const double share = __ddiv_rn(__dmul_rn((double)L, sp[i]), tot);
+    lay[i] = (int)floor(share);
+    frac[i] = __dsub_rn(share, (double)lay[i]);
+    sum += lay[i];
+  }
+  // largest remainder, ties to the earlier stage
+  bool used[32];
+  for (int i = 0; i < n; ++i) used[i] = false;
+  for (int r = 0; r < L - sum; ++r) {
+    int bi = -1;
+    for (int i = 0; i < n; ++i)
+      if (!used[i] && (bi < 0 || frac[i] > frac[bi])) bi = i;
+    used[bi] = true;
+    lay[bi] += 1;
+  }
+  // starved stages up to the floor, taking from the largest (ties: lowest)
+  for (;;) {
+    int rec = -1;
+    for (int i = 0; i < n; ++i)
+      if (lay[i] < ml) {
+        rec = i;
+        break;
+      }
+    if (rec < 0) break;
+    int don = -1;
+    for (int i = 0; i < n; ++i)
+      if (lay[i] > ml && (don < 0 || lay[i] > lay[don])) don = i;
+    if (don < 0) break;
+    lay[don] -= 1;
+    lay[rec] += 1;
+  }
+  const double min_gain = __ddiv_rn(1.0, __dmul_rn(2.0, (double)L));
+  auto stage_max = [&]() {
+    double m = 0.0;
+    bool first = true;
+    for (int i = 0; i < n; ++i) {
+      const double x = __ddiv_rn((double)lay[i], sp[i]);
+      if (first || x > m) m = x;
+      first = false;
+    }
+    return m;
+  };
+  for (;;) {
+    const double cur = stage_max();
+    const double bar = __dmul_rn(cur, __dsub_rn(1.0, min_gain));
+    double best = 0.0;
+    int bs = -1, bd = -1;
+    for (int src = 0; src < n; ++src) {
+      if (lay[src] <= ml) continue;
+      for (int dst = 0; dst < n; ++dst) {
+        if (dst == src) continue;
+        lay[src] -= 1;
+        lay[dst] += 1;
+        const double c = stage_max();
+        lay[src] += 1;
+        lay[dst] -= 1;
+        if (c < bar && (bs < 0 || c < best)) {
+          best = c;
+          bs = src;
+          bd = dst;
+        }
+      }
+    }
+    if (bs < 0) break;
+    lay[bs] -= 1;
+    lay[bd] += 1;
+  }
+  for (int i = 0; i < n; ++i) out[i] = lay[i];
+}
+
+// proportional_split (policies.py:151-162) -> prefix starts[n+1]
+__device__ void proportional_dev(int total, const double* w, int n, int32_t* start) {
+  double wsum = 0.0;
+  for (int i = 0; i < n; ++i) wsum = __dadd_rn(wsum, w[i]);
+  int cnt[64];
+  double frac[64];
+  bool used[64];
+  int sum = 0;
+  for (int i = 0; i < n; ++i) {
+    const double share = __ddiv_rn(__dmul_rn((double)total, w[i]), wsum);
+    cnt[i] = (int)share;  // int() truncation, share >= 0
+    frac[i] = __dsub_rn(share, (double)cnt[i]);
+    sum += cnt[i];
+    used[i] = false;
+  }
+  for (int r = 0; r < total - sum; ++r) {
+    int bi = -1;
+    for (int i = 0; i < n; ++i)
+      if (!used[i] && (bi < 0 || frac[i] > frac[bi])) bi = i;
+    used[bi] = true;
+    cnt[bi] += 1;
+  }
+  start[0] = 0;
+  for (int i = 0; i < n; ++i) start[i + 1] = start[i] + cnt[i];
+}
+
+__global__ void base_kernel(SearchArgs a) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= a.M) return;
+  a.v.base[j] = __dadd_rn(__dmul_rn(a.m.alpha, (double)a.N),
+                          __dmul_rn(a.m.beta, (double)a.v.quad[j]));
+}
+
+// one warp per layout
+__global__ void prep_kernel(SearchArgs a) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= a.n_layouts) return;
+  const int T = a.v.lT[warp], D = a.v.lD[warp], P = a.v.lP[warp];
+  const int K = D * P, goff = a.v.lgoff[warp], poff = a.v.lpoff[warp];
+  const int doff = a.v.ldoff[warp], boff = a.v.lboff[warp], nb = a.v.lnb[warp];
+  // placement: the K fastest blocks, kept in node order
+  int taken = 0;
+  for (int c0 = 0; c0 < nb; c0 += 32) {
+    const int b = c0 + lane;
+    const bool sel = b < nb && a.v.blk_rank[boff + b] < K;
+    const unsigned m = __ballot_sync(0xffffffffu, sel);
+    if (sel) {
+      const int g = taken + __popc(m & ((1u << lane) - 1u));
+      a.v.gblk[goff + g] = boff + b;
+      // slowest * |group| / nominal_tp (cluster.py:155-169)
+      a.v.gspeed[goff + g] = __ddiv_rn(__dmul_rn(a.v.blk_speed[boff + b], (double)T),
+                                       (double)a.T0);
+      a.v.gnode[goff + g] = a.v.blk_node[boff + b];
+    }
+    taken += __popc(m);
+  }
+  __syncwarp();
+  // hop weights on stage boundaries (same in both directions: T == T)
+  for (int g = lane; g < K; g += 32) {
+    const int s = g % P;
+    a.v.ghop[goff + g] = s < P - 1 ? hop_cost(a, a.v.gnode[goff + g], a.v.gnode[goff + g + 1], T)
+                                   : 0.0;
+  }
+  // per stage: all-reduce ring bandwidth (comm.py:87-107), min speed
+  for (int s = lane; s < P; s += 32) {
+    bool same_node = true;
+    const int n0 = a.v.gnode[goff + s];
+    double mn = a.v.gspeed[goff + s];
+    for (int d = 1; d < D; ++d) {
+      same_node &= a.v.gnode[goff + d * P + s] == n0;
+      mn = fmin(mn, a.v.gspeed[goff + d * P + s]);
+    }
+    double bw;
+    if (same_node) {
+      bw = a.intra;
+    } else {
+      bw = a.inter;
+      for (int d = 0; d < D; ++d) {
+        const int x = a.v.gnode[goff + d * P + s];
+        const int y = a.v.gnode[goff + ((d + 1) % D) * P + s];
+        if (x != y) bw = fmin(bw, link_inter(a, x, y));
+      }
+    }
+    a.v.ring[poff + s] = bw;
+    a.v.sspeed[poff + s] = mn;
+  }
+  // per replica: min speed over stages (_replica_speeds, policies.py:138-148)
+  for (int d = lane; d < D; d += 32) {
+    double mn = a.v.gspeed[goff + d * P];
+    for (int s = 1; s < P; ++s) mn = fmin(mn, a.v.gspeed[goff + d * P + s]);
+    a.v.rspeed[doff + d] = mn;
+  }
+  // same groups as the current plan?
+  int same = a.cur_T == T && a.cur_D == D && a.cur_P == P;
+  if (same) {
+    for (int g = lane; g < K; g += 32) {
+      const int b = a.v.gblk[goff + g];
+      for (int t = 0; t < T; ++t)
+        if (a.v.blk_members[a.v.blk_moff[b] + t] != a.v.cur_groups[g * T + t]) same = 0;
+    }
+    same = __all_sync(0xffffffffu, same);
+  }
+  __syncwarp();
+  if (lane == 0) {
+    a.v.same[warp] = same;
+    repartition_dev(a.v.sspeed + poff, P, a.L, a.min_layers, a.v.repart + poff);
+    proportional_dev(a.M, a.v.rspeed + doff, D, a.v.pstart + doff + warp);
+  }
+}
+
+__device__ __forceinline__ bool lex_less(double a, long long ia, double b, long long ib) {
+  return a < b || (a == b && ia < ib);
+}
+
+// one warp per candidate (grid-stride over [begin, end))
+template <int ZBH>
+__global__ void __launch_bounds__(kEvalThreads) eval_kernel(SearchArgs a, long long begin,
+                                                           long long end, double* scores) {
+  __shared__ double s_best[kEvalThreads / 32];
+  __shared__ long long s_idx[kEvalThreads / 32];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
+  const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+  double best = CUDART_INF;
+  long long best_i = -1;
+  const int c = ZBH ? 3 : 2;
+  for (long long idx = begin + gw; idx < end; idx += nw) {
+    // layout by binary search over the base indices
+    int lo = 0, hi = a.n_layouts - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (a.v.lbase[mid] <= idx) lo = mid;
+      else hi = mid - 1;
+    }
+    const int li = lo;
+    const int T = a.v.lT[li], D = a.v.lD[li], P = a.v.lP[li];
+    const long long local = idx - a.v.lbase[li];
+    const long long nu = a.v.lnu[li];
+    const int vv = (int)(local / nu), uu = (int)(local % nu);
+    const int goff = a.v.lgoff[li], poff = a.v.lpoff[li], doff = a.v.ldoff[li] + li;
+    const int32_t* rep = a.v.repart + poff;
+    const int32_t* pst = a.v.pstart + doff;
+    int psrc = -1, pdst = -1, csrc = -1, cdst = -1;
+    if (vv >= 2) {
+      const int m = vv - 2, r = m % (P - 1);
+      psrc = m / (P - 1);
+      pdst = r < psrc ? r : r + 1;
+    }
+    if (uu >= 2) {
+      const int m = uu - 2, r = m % (D - 1);
+      csrc = m / (D - 1);
+      cdst = r < csrc ? r : r + 1;
+    }
+    bool feasible = true;
+    if (psrc >= 0 && rep[psrc] - 1 < a.min_layers) feasible = false;
+    if (csrc >= 0 && pst[csrc + 1] - pst[csrc] == 0) feasible = false;
+    double score = CUDART_INF;
+    if (feasible) {
+      int pw = 1, lpw = 0;
+      while (pw < P) {
+        pw <<= 1;
+        ++lpw;
+      }
+      const int s = lane & (pw - 1), slot = lane >> lpw, R = 32 >> lpw;
+      // layers on stage s under variant vv
+      int Ls = 0;
+      if (s < P) {
+        if (vv == 0) Ls = a.L / P + (s < a.L % P ? 1 : 0);
+        else Ls = rep[s] + (s == pdst ? 1 : 0) - (s == psrc ? 1 : 0);
+      }
+      const double L = (double)Ls;
+      const double rlF = __dmul_rn(a.m.ratio_f, L);
+      const double rlB = __dmul_rn(ZBH ? a.m.ratio_b : __dadd_rn(a.m.ratio_b, a.m.ratio_w), L);
+      const double rlW = __dmul_rn(a.m.ratio_w, L);
+      // terminal all-reduce: max over stages of the ring cost (pipeline.py:356-372)
+      const bool has_ar = a.has_comm && D > 1;
+      double ar = 0.0;
+      if (has_ar && s < P) {
+        const double nbytes = __dmul_rn(L, a.lb);
+        ar = __ddiv_rn(__dmul_rn(__dmul_rn(2.0, nbytes), (double)(D - 1)),
+                       __dmul_rn((double)D, a.v.ring[poff + s]));
+      }
+      for (int o = 16; o > 0; o >>= 1) ar = fmax(ar, __shfl_xor_sync(0xffffffffu, ar, o));
+      double ms = 0.0;
+      bool over = false, hung = false;
+      for (int d0 = 0; d0 < D; d0 += R) {
+        const int d = d0 + slot;
+        const bool on = d < D && s < P;
+        int start = 0, md = 0;
+        if (d < D) {
+          if (uu == 0) {
+            const int base = a.M / D, extra = a.M % D;
+            start = d * base + min(d, extra);
+            md = base + (d < extra ? 1 : 0);
+          } else {
+            int s0 = pst[d], s1 = pst[d + 1];
+            if (csrc >= 0) {
+              s0 += (d > cdst ? 1 : 0) - (d > csrc ? 1 : 0);
+              s1 += (d + 1 > cdst ? 1 : 0) - (d + 1 > csrc ? 1 : 0);
+            }
+            start = s0;
+            md = s1 - s0;
+          }
+        }
+        double sp = 1.0, hopf = 0.0, hopb = 0.0;
+        if (on) {
+          sp = a.v.gspeed[goff + d * P + s];
+          if (s > 0) hopf = a.v.ghop[goff + d * P + s - 1];
+          if (s < P - 1) hopb = a.v.ghop[goff + d * P + s];
+        }
+        const int w = min(P - 1 - s, md);
+        const int n_chain = on ? c * md : 0;
+        double fin = 0.0, ssum = 0.0;
+        chain_walk<ZBH>(s, P, pw, md, w, n_chain, a.v.base + start, rlF, rlB, rlW, sp, hopf,
+                        hopb, a.cap, a.M, fin, ssum, over, hung);
+        double g = fin;
+        for (int o = pw >> 1; o > 0; o >>= 1) g = fmax(g, __shfl_xor_sync(0xffffffffu, g, o));
+        if (d < D) ms = fmax(ms, has_ar ? __dadd_rn(g, ar) : g);
+      }
+      for (int o = 16; o > 0; o >>= 1) ms = fmax(ms, __shfl_xor_sync(0xffffffffu, ms, o));
+      const bool bad = __any_sync(0xffffffffu, over || hung);
+      if (!bad) {
+        // reconfiguration surcharge (scheduler.py:562-593) / amortisation
+        // horizon (policies.py:341-345); every lane computes it (uniform)
+        const bool same_layout = a.v.same[li] != 0;
+        bool part_changed = false;
+        long long moved = 0;
+        const bool sameP = P == a.cur_P;
+        double reshard = 0.0;
+        for (int q = 0; q < P; ++q) {
+          const int lq = vv == 0 ? a.L / P + (q < a.L % P ? 1 : 0)
+                                 : rep[q] + (q == pdst ? 1 : 0) - (q == psrc ? 1 : 0);
+          if (sameP) {
+            const int old = a.v.cur_partition[q];
+            if (lq != old) part_changed = true;
+            if (lq > old) moved += lq - old;
+          }
+        }
+        if (!same_layout) {
+          for (int dd = 0; dd < D; ++dd)
+            for (int q = 0; q < P; ++q) {
+              const int lq = vv == 0 ? a.L / P + (q < a.L % P ? 1 : 0)
+                                     : rep[q] + (q == pdst ? 1 : 0) - (q == psrc ? 1 : 0);
+              reshard = __dadd_rn(reshard, __dmul_rn((double)lq, a.lb));
+            }
+        }
+        if (!sameP) moved = 0;
+        double sur = 0.0;
+        if (!same_layout || part_changed) {
+          const double transfer = __ddiv_rn(__dadd_rn(__dmul_rn((double)moved, a.lb), reshard),
+                                            a.worst_inter);
+          sur = __ddiv_rn(__dadd_rn(a.rebuild_s, transfer), (double)max(1, a.amort));
+        }
+        score = __dadd_rn(ms, sur);
+      }
+    }
+    if (scores && lane == 0) scores[idx - begin] = score;
+    if (lex_less(score, idx, best, best_i)) {
+      best = score;
+      best_i = idx;
+    }
+  }
+  if (lane == 0) {
+    s_best[wib] = best;
+    s_idx[wib] = best_i;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = s_best[0];
+    long long bi = s_idx[0];
+    for (int q = 1; q < (int)(blockDim.x >> 5); ++q)
+      if (s_idx[q] >= 0 && (bi < 0 || lex_less(s_best[q], s_idx[q], b, bi))) {
+        b = s_best[q];
+        bi = s_idx[q];
+      }
+    a.v.blk_best[blockIdx.x] = b;
+    a.v.blk_idx[blockIdx.x] = bi;
+  }
+}
+
+__global__ void minloc_kernel(const double* sc, const long long* ix, int n, double* out_s,
+                              int64_t* out_i) {
+  __shared__ double sb[32];
+  __shared__ long long si[32];
+  double b = CUDART_INF;
+  long long bi = -1;
+  for (int q = threadIdx.x; q < n; q += blockDim.x)
+    if (ix[q] >= 0 && (bi < 0 || lex_less(sc[q], ix[q], b, bi))) {
+      b = sc[q];
+      bi = ix[q];
+    }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, b, o);
+    const long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (oi >= 0 && (bi < 0 || lex_less(ob, oi, b, bi))) {
+      b = ob;
+      bi = oi;
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sb[threadIdx.x >> 5] = b;
+    si[threadIdx.x >> 5] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    b = sb[0];
+    bi = si[0];
+    for (int q = 1; q < (int)(blockDim.x >> 5); ++q)
+      if (si[q] >= 0 && (bi < 0 || lex_less(sb[q], si[q], b, bi))) {
+        b = sb[q];
+        bi = si[q];
+      }
+    // nothing feasible -> (+inf, -1)
+    if (!(b < CUDART_INF)) bi = -1;
+    *out_s = b;
+    *out_i = bi;
+  }
+}
+
+static SearchArgs make_args(const rh_search* S) {
+  SearchArgs a{};
+  const rh_search_desc& d = S->d;
+  a.m = d.model;
+  a.sched = d.schedule;
+  a.N = d.token_budget;
+  a.M = d.n_micro_batches;
+  a.L = d.total_layers;
+  a.min_layers = d.min_layers;
+  a.cap = d.capacity;
+  a.has_comm = d.has_comm;
+  a.p2p_opt = d.p2p_optimized;
+  a.n_layouts = (int)S->lT.size();
+  a.n_links = d.n_links;
+  a.intra = d.intra_bw;
+  a.inter = d.inter_bw;
+  a.nbytes = d.hidden_bytes_per_token * (double)d.token_budget;  // comm.py:57-58
+  a.lb = d.layer_bytes;
+  double f = 1.0;
+  bool any = false;
+  for (double x : S->link_factor) {
+    f = any ? std::min(f, x) : x;
+    any = true;
+  }
+  a.worst_inter = d.inter_bw * (any ? f : 1.0);  // comm.py:38-40
+  a.rebuild_s = d.group_rebuild_s;
+  a.amort = d.amortize_iterations;
+  a.cur_T = d.cur_tp;
+  a.cur_D = d.cur_dp;
+  a.cur_P = d.cur_pp;
+  a.T0 = d.nominal_tp > 0 ? d.nominal_tp : 1;
+  a.v = S->dv;
+  return a;
+}
+
+}  // namespace rh
+
+using namespace rh;
+
+extern "C" {
+
+int rh_search_create(rh_ctx* ctx, const rh_search_desc* desc, rh_search** out, void* stream) {
+  if (!ctx || !desc || !out || desc->n_devices <= 0 || desc->devices_per_node <= 0 ||
+      !desc->device_speed || desc->n_micro_batches <= 0 || !desc->quad ||
+      desc->total_layers <= 0 || desc->min_layers < 0 || desc->token_budget <= 0 ||
+      (desc->schedule != RH_SCHED_1F1B && desc->schedule != RH_SCHED_ZBH) ||
+      desc->intra_bw <= 0 || desc->inter_bw <= 0 || (desc->n_links && !desc->link_nodes)) {
+    set_error("rh_search_create: invalid descriptor");
+    return RH_E_INVALID;
+  }
+  cudaStream_t st = as_stream(stream);
+  rh_search* S = new rh_search();
+  S->d = *desc;
+  const rh_search_desc& d = *desc;
+  const int dpn = d.devices_per_node;
+  S->n_nodes = (d.n_devices + dpn - 1) / dpn;
+  S->speed.assign(d.device_speed, d.device_speed + d.n_devices);
+  S->link_nodes.assign(d.link_nodes, d.link_nodes + 2 * d.n_links);
+  S->link_factor.assign(d.link_factor, d.link_factor + d.n_links);
+  const int cur_groups_n = d.cur_tp * d.cur_dp * d.cur_pp;
+  if (d.cur_groups && cur_groups_n > 0)
+    S->cur_groups.assign(d.cur_groups, d.cur_groups + cur_groups_n);
+  else
+    S->cur_groups.assign(1, -1);
+  if (d.cur_partition && d.cur_pp > 0)
+    S->cur_partition.assign(d.cur_partition, d.cur_partition + d.cur_pp);
+  else
+    S->cur_partition.assign(1, 0);
+  S->d.device_speed = nullptr;
+  S->d.link_nodes = nullptr;
+  S->d.link_factor = nullptr;
+  S->d.quad = nullptr;
+  S->d.cur_groups = nullptr;
+  S->d.cur_partition = nullptr;
+  int executable = 0;
+  for (double x : S->speed) executable += x > 0.0;
+
+  // ---- blocks per TP degree: node-local fastest-first chunks of T
+  std::vector<int> degrees;
+  for (int T = 1; T <= dpn && T <= std::max(1, d.max_tp); T <<= 1)
+    if (dpn % T == 0) degrees.push_back(T);
+  std::vector<int> t_off(degrees.size()), t_nb(degrees.size());
+  for (size_t ti = 0; ti < degrees.size(); ++ti) {
+    const int T = degrees[ti];
+    t_off[ti] = (int)S->blk_node.size();
+    std::vector<int> order;
+    for (int n = 0; n < S->n_nodes; ++n) {
+      order.clear();
+      for (int q = n * dpn; q < std::min(d.n_devices, (n + 1) * dpn); ++q)
+        if (S->speed[q] > 0.0) order.push_back(q);
+      std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+        return S->speed[x] > S->speed[y];
+      });
+      for (size_t b = 0; b + T <= order.size(); b += T) {
+        std::vector<int> mem(order.begin() + b, order.begin() + b + T);
+        double mn = S->speed[mem[0]];
+        for (int q : mem) mn = std::min(mn, S->speed[q]);
+        std::sort(mem.begin(), mem.end());
+        S->blk_moff.push_back((int)S->blk_members.size());
+        S->blk_members.insert(S->blk_members.end(), mem.begin(), mem.end());
+        S->blk_node.push_back(n);
+        S->blk_speed.push_back(mn);
+      }
+    }
+    const int nb = (int)S->blk_node.size() - t_off[ti];
+    t_nb[ti] = nb;
+    std::vector<int> idx(nb);
+    for (int q = 0; q < nb; ++q) idx[q] = q;
+    std::stable_sort(idx.begin(), idx.end(), [&](int x, int y) {
+      return S->blk_speed[t_off[ti] + x] > S->blk_speed[t_off[ti] + y];
+    });
+    S->blk_rank.resize(S->blk_node.size());
+    for (int r = 0; r < nb; ++r) S->blk_rank[t_off[ti] + idx[r]] = r;
+  }
+  // ---- layouts
+  const int max_pp = std::min(32, d.max_pp > 0 ? d.max_pp : 32);
+  const int max_dp = std::min(64, d.max_dp > 0 ? d.max_dp : 64);
+  const int ml = std::max(1, d.min_layers);
+  long long base = 0;
+  int goff = 0, poff = 0, doff = 0;
+  for (size_t ti = 0; ti < degrees.size(); ++ti) {
+    const int T = degrees[ti];
+    for (int P = 1; P <= max_pp && P * ml <= d.total_layers; ++P) {
+      for (int D = 1; D <= max_dp && D <= d.n_micro_batches; ++D) {
+        if (D * P > t_nb[ti]) break;
+        if ((double)T * D * P < d.min_utilization * executable) continue;
+        const long long nv = 2 + (long long)P * (P - 1);
+        const long long nu = 2 + (long long)D * (D - 1);
+        S->lT.push_back(T);
+        S->lD.push_back(D);
+        S->lP.push_back(P);
+        S->lgoff.push_back(goff);
+        S->lpoff.push_back(poff);
+        S->ldoff.push_back(doff);
+        S->lboff.push_back(t_off[ti]);
+        S->lnb.push_back(t_nb[ti]);
+        S->lbase.push_back(base);
+        S->lnv.push_back(nv);
+        S->lnu.push_back(nu);
+        base += nv * nu;
+        goff += D * P;
+        poff += P;
+        doff += D;
+      }
+    }
+  }
+  S->total = base;
+  S->n_groups = goff;
+  S->n_stage = poff;
+  S->n_rep = doff;
+  const int NL = (int)S->lT.size();
+  if (NL == 0) {
+    *out = S;
+    return RH_OK;
+  }
+  // ---- device memory
+  int max_blocks_per_sm = 0;
+  RH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_blocks_per_sm, eval_kernel<0>,
+                                                        kEvalThreads, 0));
+  S->eval_blocks = ctx->num_sms * std::max(1, max_blocks_per_sm);
+  size_t bytes = 0;
+  auto take = [&](size_t n) {
+    const size_t o = bytes;
+    bytes = (bytes + std::max<size_t>(n, 8) + 255) & ~size_t(255);
+    return o;
+  };
+  const size_t nblk = S->blk_node.size(), nmem = S->blk_members.size();
+  struct Up {
+    size_t off;
+    const void* src;
+    size_t n;
+  };
+  std::vector<Up> ups;
+  auto up = [&](const void* src, size_t n) {
+    const size_t o = take(n);
+    ups.push_back({o, src, n});
+    return o;
+  };
+  const size_t o_lT = up(S->lT.data(), 4 * NL), o_lD = up(S->lD.data(), 4 * NL),
+               o_lP = up(S->lP.data(), 4 * NL), o_lgoff = up(S->lgoff.data(), 4 * NL),
+               o_lpoff = up(S->lpoff.data(), 4 * NL), o_ldoff = up(S->ldoff.data(), 4 * NL),
+               o_lboff = up(S->lboff.data(), 4 * NL), o_lnb = up(S->lnb.data(), 4 * NL),
+               o_lbase = up(S->lbase.data(), 8 * NL), o_lnv = up(S->lnv.data(), 8 * NL),
+               o_lnu = up(S->lnu.data(), 8 * NL);
+  const size_t o_bnode = up(S->blk_node.data(), 4 * nblk),
+               o_brank = up(S->blk_rank.data(), 4 * nblk),
+               o_bmem = up(S->blk_members.data(), 4 * nmem),
+               o_bmoff = up(S->blk_moff.data(), 4 * nblk),
+               o_bspeed = up(S->blk_speed.data(), 8 * nblk);
+  const size_t o_quad = up(desc->quad, 8 * (size_t)d.n_micro_batches);
+  const size_t o_ln = up(S->link_nodes.data(), 4 * S->link_nodes.size()),
+               o_lf = up(S->link_factor.data(), 8 * S->link_factor.size()),
+               o_cg = up(S->cur_groups.data(), 4 * S->cur_groups.size()),
+               o_cp = up(S->cur_partition.data(), 4 * S->cur_partition.size());
+  const size_t o_gblk = take(4 * S->n_groups), o_gnode = take(4 * S->n_groups),
+               o_gspeed = take(8 * S->n_groups), o_ghop = take(8 * S->n_groups),
+               o_ring = take(8 * S->n_stage), o_sspeed = take(8 * S->n_stage),
+               o_repart = take(4 * S->n_stage), o_rspeed = take(8 * S->n_rep),
+               o_pstart = take(4 * (S->n_rep + NL)), o_same = take(4 * NL),
+               o_base = take(8 * (size_t)d.n_micro_batches),
+               o_bb = take(8 * (size_t)S->eval_blocks), o_bi = take(8 * (size_t)S->eval_blocks);
+  cudaError_t e = cudaMalloc(&S->dmem, bytes);
+  if (e != cudaSuccess) {
+    delete S;
+    set_error("rh_search_create: %zu bytes: %s", bytes, cudaGetErrorString(e));
+    return RH_E_NOMEM;
+  }
+  S->dbytes = bytes;
+  char* B = static_cast<char*>(S->dmem);
+  for (const Up& u : ups)
+    if (u.n) RH_CUDA(cudaMemcpyAsync(B + u.off, u.src, u.n, cudaMemcpyHostToDevice, st));
+  auto I = [&](size_t o) { return reinterpret_cast<int32_t*>(B + o); };
+  auto Dp = [&](size_t o) { return reinterpret_cast<double*>(B + o); };
+  auto LL = [&](size_t o) { return reinterpret_cast<long long*>(B + o); };
+  rh_search::Dev& v = S->dv;
+  v.lT = I(o_lT); v.lD = I(o_lD); v.lP = I(o_lP); v.lgoff = I(o_lgoff); v.lpoff = I(o_lpoff);
+  v.ldoff = I(o_ldoff); v.lboff = I(o_lboff); v.lnb = I(o_lnb);
+  v.lbase = LL(o_lbase); v.lnv = LL(o_lnv); v.lnu = LL(o_lnu);
+  v.blk_node = I(o_bnode); v.blk_rank = I(o_brank); v.blk_members = I(o_bmem);
+  v.blk_moff = I(o_bmoff); v.blk_speed = Dp(o_bspeed);
+  v.quad = reinterpret_cast<int64_t*>(B + o_quad);
+  v.link_nodes = I(o_ln); v.link_factor = Dp(o_lf); v.cur_groups = I(o_cg);
+  v.cur_partition = I(o_cp);
+  v.gblk = I(o_gblk); v.gnode = I(o_gnode); v.gspeed = Dp(o_gspeed); v.ghop = Dp(o_ghop);
+  v.ring = Dp(o_ring); v.sspeed = Dp(o_sspeed); v.repart = I(o_repart);
+  v.rspeed = Dp(o_rspeed); v.pstart = I(o_pstart); v.same = I(o_same); v.base = Dp(o_base);
+  v.blk_best = Dp(o_bb); v.blk_idx = LL(o_bi);
+  SearchArgs a = make_args(S);
+  base_kernel<<<(d.n_micro_batches + 255) / 256, 256, 0, st>>>(a);
+  RH_CHECK_LAUNCH(ctx);
+  prep_kernel<<<(NL * 32 + 127) / 128, 128, 0, st>>>(a);
+  RH_CHECK_LAUNCH(ctx);
+  RH_CUDA(cudaStreamSynchronize(st));
+  *out = S;
+  return RH_OK;
+}
+
+int rh_search_destroy(rh_search* S) {
+  if (!S) return RH_OK;
+  if (S->dmem) cudaFree(S->dmem);
+  delete S;
+  return RH_OK;
+}
+
+int64_t rh_search_size(const rh_search* S) { return S ? S->total : 0; }
+int32_t rh_search_layouts(const rh_search* S) { return S ? (int32_t)S->lT.size() : 0; }
+
+int rh_search_eval(rh_ctx* ctx, rh_search* S, int64_t begin, int64_t end, double* best_score,
+                   int64_t* best_index, double* scores, void* stream) {
+  if (!ctx || !S || !best_score || !best_index || begin < 0 || end < begin ||
+      end > S->total) {
+    set_error("rh_search_eval: invalid range [%lld, %lld) of %lld", (long long)begin,
+              (long long)end, (long long)(S ? S->total : 0));
+    return RH_E_INVALID;
+  }
+  cudaStream_t st = as_stream(stream);
+  if (begin == end) {
+    const double inf = std::numeric_limits<double>::infinity();
+    const int64_t none = -1;
+    RH_CUDA(cudaMemcpyAsync(best_score, &inf, 8, cudaMemcpyHostToDevice, st));
+    RH_CUDA(cudaMemcpyAsync(best_index, &none, 8, cudaMemcpyHostToDevice, st));
+    return RH_OK;
+  }
+  SearchArgs a = make_args(S);
+  const long long n = end - begin;
+  const int warps_per_block = kEvalThreads / 32;
+  const int blocks = (int)std::min<long long>(S->eval_blocks, (n + warps_per_block - 1) / warps_per_block);
+  if (S->d.schedule == RH_SCHED_ZBH)
+    eval_kernel<1><<<blocks, kEvalThreads, 0, st>>>(a, begin, end, scores);
+  else
+    eval_kernel<0><<<blocks, kEvalThreads, 0, st>>>(a, begin, end, scores);
+  RH_CHECK_LAUNCH(ctx);
+  minloc_kernel<<<1, 1024, 0, st>>>(S->dv.blk_best, S->dv.blk_idx, blocks, best_score,
+                                    best_index);
+  RH_CHECK_LAUNCH(ctx);
+  return RH_OK;
+}
+
+int rh_search_decode(rh_ctx* ctx, rh_search* S, int64_t index, rh_candidate* out,
+                     int32_t* groups, int32_t* partition, int32_t* counts) {
+  if (!ctx || !S || !out || index < 0 || index >= S->total) {
+    set_error("rh_search_decode: index out of range");
+    return RH_E_INVALID;
+  }
+  const int NL = (int)S->lT.size();
+  int li = (int)(std::upper_bound(S->lbase.begin(), S->lbase.end(), (long long)index) -
+                 S->lbase.begin()) - 1;
+  li = std::max(0, std::min(li, NL - 1));
+  const int T = S->lT[li], D = S->lD[li], P = S->lP[li];
+  const long long local = index - S->lbase[li];
+  const int vv = (int)(local / S->lnu[li]), uu = (int)(local % S->lnu[li]);
+  out->index = index;
+  out->tp = T;
+  out->dp = D;
+  out->pp = P;
+  out->layout = li;
+  out->partition_variant = vv;
+  out->count_variant = uu;
+  std::vector<int32_t> gblk(D * P), rep(P), pst(D + 1);
+  RH_CUDA(cudaMemcpy(gblk.data(), S->dv.gblk + S->lgoff[li], 4 * D * P, cudaMemcpyDeviceToHost));
+  RH_CUDA(cudaMemcpy(rep.data(), S->dv.repart + S->lpoff[li], 4 * P, cudaMemcpyDeviceToHost));
+  RH_CUDA(cudaMemcpy(pst.data(), S->dv.pstart + S->ldoff[li] + li, 4 * (D + 1),
+                     cudaMemcpyDeviceToHost));
+  const rh_search_desc& d = S->d;
+  std::vector<int> part(P), cnt(D);
+  int psrc = -1, pdst = -1, csrc = -1, cdst = -1;
+  if (vv >= 2) {
+    const int m = vv - 2, r = m % (P - 1);
+    psrc = m / (P - 1);
+    pdst = r < psrc ? r : r + 1;
+  }
+  if (uu >= 2) {
+    const int m = uu - 2, r = m % (D - 1);
+    csrc = m / (D - 1);
+    cdst = r < csrc ? r : r + 1;
+  }
+  for (int s = 0; s < P; ++s)
+    part[s] = vv == 0 ? d.total_layers / P + (s < d.total_layers % P ? 1 : 0)
+                      : rep[s] + (s == pdst) - (s == psrc);
+  for (int q = 0; q < D; ++q) {
+    if (uu == 0) cnt[q] = d.n_micro_batches / D + (q < d.n_micro_batches % D ? 1 : 0);
+    else cnt[q] = pst[q + 1] - pst[q] + (q == cdst) - (q == csrc);
+  }
+  bool feas = true;
+  for (int s = 0; s < P; ++s) feas &= part[s] >= d.min_layers;
+  for (int q = 0; q < D; ++q) feas &= cnt[q] >= 0;
+  out->feasible = feas;
+  if (groups)
+    for (int g = 0; g < D * P; ++g)
+      for (int t = 0; t < T; ++t) groups[g * T + t] = S->blk_members[S->blk_moff[gblk[g]] + t];
+  if (partition)
+    for (int s = 0; s < P; ++s) partition[s] = part[s];
+  if (counts)
+    for (int q = 0; q < D; ++q) counts[q] = cnt[q];
+  return RH_OK;
+}
+
+}  // extern "C"

@@ -24,6 +24,7 @@ import numpy as np
 REF = Path(os.environ.get("RESIHP_REFERENCE", "/root/reference/pkg/src"))
 sys.dont_write_bytecode = True
 sys.path.insert(0, str(REF))
+sys.path.insert(1, str(Path(__file__).resolve().parents[2]))  # this repo (oracle decode)
 
 import resilsim  # noqa: E402
 from resilsim import cluster as rc  # noqa: E402
@@ -350,8 +351,110 @@ def gen_scheduler():
                              "repartition": repart, "proportional": prop})
 
 
+# ----------------------------------------------------------------- search
+def search_cases():
+    """Small re-plan problems: (name, nodes, dpn, cfg, events, M, N, comm, capacity, sched)."""
+    return [
+        ("slow32", 4, 8, (4, 4, 2), [("fail_slow_compute", 5, 0.5)], 16, 4096, True, 8, "1f1b"),
+        ("stop32", 4, 8, (4, 4, 2), [("fail_stop", 3, None), ("fail_slow_compute", 17, 0.6)],
+         16, 4096, True, 8, "1f1b"),
+        ("link32", 4, 8, (2, 4, 4), [("fail_slow_comm", (1, 2), 0.4)], 16, 2048, True, 6, "zbh"),
+        ("nocomm16", 2, 8, (2, 2, 4), [("fail_slow_compute", 9, 0.3)], 12, 4096, False, 0,
+         "1f1b"),
+    ]
+
+
+def gen_search():
+    """Reference evaluate_plan + reconfig_cost on candidates of the re-plan space.
+
+    The candidate space is this repo's definition; the
+    oracle decodes candidate indices (placement, partition, counts) and the
+    REFERENCE scores them, which pins the oracle's and the GPU's scores."""
+    from paper_2605_06374_b200 import cluster as mc
+    from paper_2605_06374_b200.search import build_desc
+    from tests.oracle_bind import Oracle
+
+    oracle = Oracle()
+    out = []
+    for name, nodes, dpn, (T, D, P), evs, M, N, has_comm, cap, sched in search_cases():
+        rng = random.Random(sum(map(ord, name)))
+        L = 8 * P
+        cfg_r = rc.ParallelismConfig(tp=T, dp=D, pp=P, schedule=sched, layer_partition=[8] * P)
+        st_r = rc.build_cluster(nodes, dpn, cfg_r, 300.0 * 2**30, 25.0 * 2**30)
+        events = []
+        for kind, target, sev in evs:
+            if kind == "fail_slow_comm":
+                events.append(rc.FailureEvent(kind=kind, start=0.0, link=target, severity=sev))
+            else:
+                events.append(rc.FailureEvent(kind=kind, start=0.0, device=target, severity=sev))
+        st_r = rc.apply_failures(st_r, events, 0.0)
+        docs = [max(1, min(N, int(rng.lognormvariate(7.2, 0.8)))) for _ in range(M * 8)]
+        mbs_r = rw.pack_sequences(docs, N)[:M]
+        model_r = rw.CostModel(alpha=2e-6, beta=5e-10)
+        comm_r = CommSpec() if has_comm else None
+        # the same problem in this package's types for the descriptor
+        st_m = mc.ClusterState(
+            devices=[mc.Device(d.id, d.node_id, d.speed, d.status) for d in st_r.devices],
+            devices_per_node=dpn, tp_groups=dict(st_r.tp_groups), intra_bw=st_r.intra_bw,
+            inter_bw=st_r.inter_bw, link_factors=dict(st_r.link_factors))
+        cfg_m = mc.ParallelismConfig(T, D, P, sched, [8] * P)
+        from paper_2605_06374_b200.comm import CommSpec as MCS
+
+        quad = [rw.quad_load(mb) for mb in mbs_r]
+        inp = build_desc(st_m, cfg_m, mbs_r, model_r, MCS() if has_comm else None,
+                         capacity=cap or None, quad=quad, min_utilization=0.6)
+        srch = oracle.search(inp)
+        best, bi = srch.best()
+        picks = sorted({0, bi, srch.size - 1} | {rng.randrange(srch.size) for _ in range(90)})
+        rows = []
+        for idx in picks:
+            c = srch.decode(idx)
+            if not c.feasible:  # a move out of an empty replica / below min_layers
+                rows.append([idx, None, "infeasible variant"])
+                continue
+            st2 = st_r.copy()
+            st2.tp_groups = {(g // c.pp, g % c.pp): tuple(m) for g, m in enumerate(c.groups)}
+            members = {m for g in c.groups for m in g}
+            for dev in st2.devices:
+                if dev.status == rc.FAIL_STOP:
+                    continue
+                dev.status = ((rc.FAIL_SLOW if dev.speed < 1.0 else rc.HEALTHY)
+                              if dev.id in members else rc.STANDBY)
+            cfg2 = rc.ParallelismConfig(tp=T, dp=c.dp, pp=c.pp, schedule=sched,
+                                        layer_partition=list(c.partition))
+            plan = rs.AdaptationPlan(dp_assignment=list(c.counts))
+            try:
+                ms = rs.evaluate_plan(plan, st2, cfg2, mbs_r, model_r, comm=comm_r,
+                                      capacity=cap or None)
+            except rp.SimulationError as exc:
+                rows.append([idx, None, str(exc)[:40]])
+                continue
+            same = (c.tp == T and c.dp == D and c.pp == P and
+                    all(tuple(sorted(st_r.tp_groups[(g // P, g % P)])) == tuple(m)
+                        for g, m in enumerate(c.groups)))
+            if same:  # the reference's own reconfig_cost
+                rplan = rs.AdaptationPlan(layer_partition=list(c.partition))
+                reconf = rs.reconfig_cost(rplan, st_r, cfg_r, layer_bytes=256.0 * 2**20)
+            else:      # DESIGN.md §5 extension: full reshard over the worst link
+                moved = (sum(max(0, a - b) for a, b in zip(c.partition, cfg_r.layer_partition))
+                         if c.pp == P else 0)
+                reshard = 0.0
+                for _d in range(c.dp):
+                    for q in range(c.pp):
+                        reshard += c.partition[q] * (256.0 * 2**20)
+                worst = rc.ClusterState.copy(st_r).inter_bw * min(
+                    st_r.link_factors.values(), default=1.0)
+                reconf = 2.0 + (moved * (256.0 * 2**20) + reshard) / worst
+            rows.append([idx, ms, reconf / max(1, 25)])
+        out.append({"name": name, "nodes": nodes, "dpn": dpn, "cfg": [T, D, P], "sched": sched,
+                    "events": [[k, list(t) if isinstance(t, tuple) else t, s] for k, t, s in evs],
+                    "mbs": [list(mb.doc_lengths) for mb in mbs_r], "N": N, "comm": has_comm,
+                    "capacity": cap, "size": srch.size, "best": [best, bi], "rows": rows})
+        print(name, "size", srch.size, "best", best, bi)
+    dump("search", {"cases": out})
+
+
 if __name__ == "__main__":
-    gen_workload()
-    gen_pipeline()
-    gen_detector()
-    gen_scheduler()
+    which = sys.argv[1:] or ["workload", "pipeline", "detector", "scheduler", "search"]
+    for w in which:
+        globals()[f"gen_{w}"]()

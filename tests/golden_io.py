@@ -53,3 +53,27 @@ def keyed(rows) -> dict:
 
 def bits(x) -> np.ndarray:
     return np.asarray(x, dtype=np.float64).view(np.uint64)
+
+
+def search_problem(case):
+    """(state, cfg, micro-batches, model, comm, SearchInputs) of a search fixture."""
+    from paper_2605_06374_b200.cluster import FailureEvent, apply_failures, build_cluster
+    from paper_2605_06374_b200.search import build_desc
+
+    T, D, P = case["cfg"]
+    cfg = ParallelismConfig(T, D, P, case["sched"], [8] * P)
+    st = build_cluster(case["nodes"], case["dpn"], cfg, 300.0 * 2**30, 25.0 * 2**30)
+    evs = []
+    for kind, target, sev in case["events"]:
+        if kind == "fail_slow_comm":
+            evs.append(FailureEvent(kind, 0.0, link=tuple(target), severity=sev))
+        else:
+            evs.append(FailureEvent(kind, 0.0, device=target, severity=sev))
+    st = apply_failures(st, evs, 0.0)
+    mbs = [MicroBatch(i, tuple(d), case["N"]) for i, d in enumerate(case["mbs"])]
+    model = CostModel(alpha=2e-6, beta=5e-10)
+    comm = CommSpec() if case["comm"] else None
+    quad = [sum(x * x for x in mb.doc_lengths) for mb in mbs]
+    inputs = build_desc(st, cfg, mbs, model, comm, capacity=case["capacity"] or None, quad=quad,
+                        min_utilization=0.6)
+    return st, cfg, mbs, model, comm, inputs

@@ -79,6 +79,22 @@ class Oracle:
         L.orc_screen.argtypes = [C.POINTER(_lib.ScreenParams), C.c_int64, p, C.c_int64, p, p,
                                  p, p, C.POINTER(C.c_int64)]
         L.orc_screen.restype = C.c_int
+        from paper_2605_06374_b200.search import Candidate, SearchDesc
+
+        L.orc_search_create.argtypes = [C.POINTER(SearchDesc)]
+        L.orc_search_create.restype = p
+        L.orc_search_destroy.argtypes = [p]
+        L.orc_search_size.argtypes = [p]
+        L.orc_search_size.restype = C.c_int64
+        L.orc_search_score.argtypes = [p, C.c_int64]
+        L.orc_search_score.restype = C.c_double
+        L.orc_search_eval.argtypes = [p, C.c_int64, C.c_int64, C.c_int, C.POINTER(C.c_double),
+                                      C.POINTER(C.c_int64), p]
+        L.orc_search_decode.argtypes = [p, C.c_int64, C.POINTER(Candidate), p, p, p]
+
+    # ------------------------------------------------------------ search
+    def search(self, inputs):
+        return OracleSearch(self, inputs)
 
     # ------------------------------------------------------------ scalar
     def quad_load(self, docs) -> int:
@@ -179,3 +195,43 @@ def pipe_shape_of(trace, capacity, max_mb):
 
     return pipe_shape(trace.cfg, trace.M, trace.N, capacity=capacity,
                       has_allreduce=trace.has_allreduce, max_mb=max_mb)
+
+
+class OracleSearch:
+    """CPU restatement of the re-plan search (oracle/search_oracle.c)."""
+
+    def __init__(self, oracle: Oracle, inputs):
+        self.o, self.inputs = oracle, inputs
+        self.h = oracle.lib.orc_search_create(C.byref(inputs.desc))
+        self.size = int(oracle.lib.orc_search_size(self.h))
+
+    def __del__(self):
+        try:
+            self.o.lib.orc_search_destroy(self.h)
+        except Exception:
+            pass
+
+    def score(self, index: int) -> float:
+        return float(self.o.lib.orc_search_score(self.h, int(index)))
+
+    def best(self, begin=0, end=None, threads=0, with_scores=False):
+        end = self.size if end is None else end
+        b, i = C.c_double(), C.c_int64()
+        sc = np.zeros(max(end - begin, 1)) if with_scores else None
+        self.o.lib.orc_search_eval(self.h, begin, end, threads, C.byref(b), C.byref(i),
+                                   None if sc is None else sc.ctypes.data)
+        return (b.value, i.value, sc[:end - begin]) if with_scores else (b.value, i.value)
+
+    def decode(self, index: int):
+        from paper_2605_06374_b200.search import Candidate, CandidatePlan
+
+        c = Candidate()
+        groups = np.zeros(self.inputs.desc.n_devices + 1, np.int32)
+        part = np.zeros(64, np.int32)
+        cnt = np.zeros(128, np.int32)
+        self.o.lib.orc_search_decode(self.h, int(index), C.byref(c), groups.ctypes.data,
+                                     part.ctypes.data, cnt.ctypes.data)
+        g = [tuple(int(x) for x in groups[k * c.tp:(k + 1) * c.tp]) for k in range(c.dp * c.pp)]
+        return CandidatePlan(int(c.index), c.tp, c.dp, c.pp, part[:c.pp].tolist(),
+                             cnt[:c.dp].tolist(), g, c.partition_variant, c.count_variant,
+                             bool(c.feasible))

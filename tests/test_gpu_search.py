@@ -1,0 +1,89 @@
+"""GPU re-plan search vs the CPU oracle: every candidate's score bit-exact,
+the same lexicographic (score, index) winner, the same decoded plan."""
+
+import math
+
+import numpy as np
+import pytest
+
+from tests.golden_io import bits, load, search_problem
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("k", range(4))
+def test_all_scores_match_oracle(k, oracle, cuda_device):
+    from paper_2605_06374_b200.search import ReplanSearch
+
+    case = load("search")["cases"][k]
+    *_, inputs = search_problem(case)
+    gpu = ReplanSearch(inputs)
+    cpu = oracle.search(inputs)
+    assert gpu.size == cpu.size == case["size"]
+    g = gpu.scores()
+    _, _, c = cpu.best(with_scores=True)
+    np.testing.assert_array_equal(np.isinf(g), np.isinf(c))
+    fin = np.isfinite(c)
+    np.testing.assert_array_equal(bits(g[fin]), bits(c[fin]))
+    assert gpu.best() == tuple(case["best"])
+    # reference-scored sample (fixture) through the GPU
+    for idx, ms, extra in case["rows"]:
+        if ms is None:
+            assert math.isinf(g[idx])
+        else:
+            assert bits(g[idx]) == bits(ms + extra)
+
+
+@pytest.mark.parametrize("k", range(4))
+def test_decode_matches_oracle(k, oracle, cuda_device):
+    from paper_2605_06374_b200.search import ReplanSearch
+
+    case = load("search")["cases"][k]
+    *_, inputs = search_problem(case)
+    gpu = ReplanSearch(inputs)
+    cpu = oracle.search(inputs)
+    rng = np.random.default_rng(k)
+    for idx in [0, gpu.size - 1, *rng.integers(0, gpu.size, 40)]:
+        assert gpu.decode(int(idx)) == cpu.decode(int(idx))
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_problems(seed, oracle, cuda_device):
+    """Bigger random clusters: sampled ranges, plus the range min-loc."""
+    from paper_2605_06374_b200.cluster import (FailureEvent, ParallelismConfig, apply_failures,
+                                               build_cluster)
+    from paper_2605_06374_b200.comm import CommSpec
+    from paper_2605_06374_b200.search import ReplanSearch, build_desc
+    from paper_2605_06374_b200.trace import synth_iterations
+    from paper_2605_06374_b200.workload import CostModel, MicroBatch
+
+    rng = np.random.default_rng(100 + seed)
+    T, D, P = [(8, 4, 4), (4, 8, 4), (8, 8, 2), (2, 8, 8), (4, 4, 8), (8, 2, 8)][seed]
+    nodes = T * D * P // 8
+    sched = "zbh" if seed % 2 else "1f1b"
+    L = int(rng.choice([32, 40, 48]))
+    cfg = ParallelismConfig(T, D, P, sched, [L // P + (1 if i < L % P else 0) for i in range(P)])
+    st = build_cluster(nodes, 8, cfg, 300.0 * 2**30, 25.0 * 2**30)
+    evs = [FailureEvent("fail_slow_compute", 0.0, device=int(x), severity=float(s))
+           for x, s in zip(rng.integers(0, T * D * P, 3), rng.uniform(0.3, 0.8, 3))]
+    evs.append(FailureEvent("fail_stop", 0.0, device=int(rng.integers(0, T * D * P))))
+    if nodes > 2:
+        evs.append(FailureEvent("fail_slow_comm", 0.0, link=(0, 2), severity=0.5))
+    st = apply_failures(st, evs, 0.0)
+    M = D * int(rng.integers(2, 5))
+    off, docs = synth_iterations(1, M, 4096, 7.2, 0.8, seed)
+    mbs = [MicroBatch(j, tuple(int(x) for x in docs[off[j]:off[j + 1]]), 4096) for j in range(M)]
+    inputs = build_desc(st, cfg, mbs, CostModel(2e-6, 5e-10), CommSpec(), capacity=P + 2,
+                        quad=[sum(x * x for x in mb.doc_lengths) for mb in mbs],
+                        min_utilization=0.85)
+    gpu = ReplanSearch(inputs)
+    cpu = oracle.search(inputs)
+    assert gpu.size == cpu.size
+    a = int(rng.integers(0, max(1, gpu.size - 3000)))
+    b = min(gpu.size, a + 3000)
+    g = gpu.scores(a, b)
+    _, _, c = cpu.best(a, b, with_scores=True)
+    np.testing.assert_array_equal(np.isinf(g), np.isinf(c))
+    fin = np.isfinite(c)
+    np.testing.assert_array_equal(bits(g[fin]), bits(c[fin]))
+    assert gpu.best(a, b) == cpu.best(a, b)
