@@ -346,6 +346,87 @@ def run_e2e(tr, p, args, dev):
     return {"step_s": step, "h2d": int(h2d), "d2h": int(d2h)}
 
 
+def run_scheduler(args, world, rank, local, names=("C3", "C4", "C5")):
+    """Re-plan search (BASELINE configs[2..4]): candidates/s and re-plan latency.
+
+    Each rank scores its contiguous shard of the candidate index range; one
+    NCCL all-gather of (score, index) pairs finishes the min-loc.  Latency =
+    wall clock from host inputs to the decoded best plan (create + per-layout
+    GPU prep + sharded scoring + collective + decode)."""
+    import torch
+
+    from paper_2605_06374_b200.replan_scenarios import replan_problem
+    from paper_2605_06374_b200.search import ReplanSearch, distributed_best, shard_range
+
+    dev = torch.device("cuda", local)
+    out = {}
+    for name in names:
+        st, cfg, mbs, inputs = replan_problem(name)
+        s = ReplanSearch(inputs, dev)
+        a, b = shard_range(s.size, rank, world)
+        s.eval_async(a, b)  # warm-up (module load, caches)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        best_t, idx_t = s.eval_async(a, b)
+        e1.record()
+        torch.cuda.synchronize()
+        eval_ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([eval_ms], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            eval_ms = float(t.item())
+        # end-to-end re-plan latency (fresh search each time), median of 3
+        lat = []
+        for _ in range(3):
+            if world > 1:
+                torch.distributed.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            s2 = ReplanSearch(inputs, dev)
+            score, idx = distributed_best(s2)
+            plan = s2.decode(idx) if idx >= 0 else None
+            torch.cuda.synchronize()
+            lat.append((time.perf_counter() - t0) * 1e3)
+            del s2
+        lat_ms = float(np.median(lat))
+        if world > 1:
+            t = torch.tensor([lat_ms], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            lat_ms = float(t.item())
+        out[name] = {
+            "devices": len(st.devices), "candidates": s.size, "layouts": s.layouts,
+            "candidates_per_s": s.size / (eval_ms * 1e-3), "eval_ms": eval_ms,
+            "replan_latency_ms": lat_ms, "best_score_s": score, "best_index": idx,
+            "best_plan": None if plan is None else {
+                "tp": plan.tp, "dp": plan.dp, "pp": plan.pp, "partition": plan.partition,
+                "counts": plan.counts},
+        }
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            out[name]["cpu_baseline"] = search_cpu_baseline(inputs, s.size)
+    return out
+
+
+def search_cpu_baseline(inputs, size, budget_s=4.0):
+    """Oracle re-plan scoring on all host cores over a bounded contiguous sample."""
+    from tests.oracle_bind import Oracle
+
+    o = Oracle().search(inputs)
+    cores = os.cpu_count() or 1
+    k = 256
+    while True:  # grow the sample until it costs ~budget_s
+        mid = size // 3
+        t0 = time.perf_counter()
+        o.best(mid, min(size, mid + k), threads=cores)
+        dt = time.perf_counter() - t0
+        if dt > budget_s / 4 or mid + k >= size:
+            break
+        k *= 4
+    return {"value": k / dt, "unit": "candidates/s", "cores": cores, "kind": "port",
+            "sample": f"{k} contiguous candidates from index {size // 3} (oracle: build_dag + "
+                      "Kahn per candidate, pthreads)"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -353,6 +434,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-scheduler", action="store_true")
+    ap.add_argument("--scheduler-only", default="", help="comma list of C3,C4,C5: only these")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -360,7 +443,17 @@ def main():
     if args.impl == "reference":
         run_reference(args, world, rank)
         return
+    if args.scheduler_only:
+        import torch
+
+        torch.cuda.set_device(local)
+        res = run_scheduler(args, world, rank, local, tuple(args.scheduler_only.split(",")))
+        if rank == 0:
+            print(json.dumps({"scheduler": res}), flush=True)
+        return
     line, tr = run_ours(args, world, rank, local)
+    if not args.no_scheduler:
+        line["scheduler"] = run_scheduler(args, world, rank, local)
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(tr)

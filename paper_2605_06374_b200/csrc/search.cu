@@ -41,8 +41,8 @@ struct rh_search {
   std::vector<int32_t> cur_groups, cur_partition;
   // layouts
   std::vector<int32_t> lT, lD, lP, lgoff, lpoff, ldoff, lboff, lnb;
-  std::vector<long long> lbase, lnv, lnu;
-  int64_t total = 0;
+  std::vector<long long> lbase, lnv, lnu, lpair, lrt;
+  int64_t total = 0, n_pairs = 0, n_rt = 0;
   // blocks (concatenated over the distinct T values)
   std::vector<int32_t> blk_node, blk_rank, blk_members, blk_moff;
   std::vector<double> blk_speed;
@@ -51,7 +51,10 @@ struct rh_search {
   size_t dbytes = 0;
   struct Dev {
     int32_t *lT, *lD, *lP, *lgoff, *lpoff, *ldoff, *lboff, *lnb;
-    long long *lbase, *lnv, *lnu;
+    long long *lbase, *lnv, *lnu, *lpair, *lrt;
+    double* rtab;   // replica table [sum over layouts nv*8*D]
+    double* pinfo;  // per (layout, v): all-reduce cost (-1: none), surcharge (inf: infeasible)
+    void* tasks;    // PhaseTask[n_layouts]
     int32_t *blk_node, *blk_rank, *blk_members, *blk_moff;
     double* blk_speed;
     int32_t *gblk, *gnode;
@@ -303,68 +306,73 @@ __device__ __forceinline__ bool lex_less(double a, long long ia, double b, long 
   return a < b || (a == b && ia < ib);
 }
 
-// one warp per candidate (grid-stride over [begin, end))
+// ---- phase 1: replica pipeline table --------------------------------------
+// For every (layout, partition variant v) in the evaluated range and every
+// replica d, the makespan contribution of d's pipeline is computed for the 8
+// micro-batch ranges that count variants can give it:
+//   case 0 even split, 1 proportional, then proportional shifted by
+//   (start, end) = 2 (0,-1)  3 (-1,-1)  4 (-1,0)  5 (0,+1)  6 (+1,+1)  7 (+1,0)
+// (moving one micro-batch src->dst shifts every replica between them by one).
+// Infeasible ranges / capacity overflow are stored as +inf.
+__constant__ int kDs[8] = {0, 0, 0, -1, -1, 0, 1, 1};
+__constant__ int kDe[8] = {0, 0, -1, -1, 0, 1, 1, 0};
+
+struct PhaseTask {
+  int layout;
+  int v_lo;
+  long long task_base;
+};
+
+__device__ __forceinline__ int layer_of(const SearchArgs& a, const int32_t* rep, int P, int vv,
+                                        int psrc, int pdst, int s) {
+  return vv == 0 ? a.L / P + (s < a.L % P ? 1 : 0)
+                 : rep[s] + (s == pdst ? 1 : 0) - (s == psrc ? 1 : 0);
+}
+
 template <int ZBH>
-__global__ void __launch_bounds__(kEvalThreads) eval_kernel(SearchArgs a, long long begin,
-                                                           long long end, double* scores) {
-  __shared__ double s_best[kEvalThreads / 32];
-  __shared__ long long s_idx[kEvalThreads / 32];
+__global__ void __launch_bounds__(kEvalThreads) table_kernel(SearchArgs a, const PhaseTask* tk,
+                                                            int n_tk, long long n_tasks) {
   const int lane = threadIdx.x & 31;
-  const int wib = threadIdx.x >> 5;
-  const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
-  const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
-  double best = CUDART_INF;
-  long long best_i = -1;
+  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
   const int c = ZBH ? 3 : 2;
-  for (long long idx = begin + gw; idx < end; idx += nw) {
-    // layout by binary search over the base indices
-    int lo = 0, hi = a.n_layouts - 1;
+  for (long long t = gw; t < n_tasks; t += nw) {
+    int lo = 0, hi = n_tk - 1;
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
-      if (a.v.lbase[mid] <= idx) lo = mid;
+      if (tk[mid].task_base <= t) lo = mid;
       else hi = mid - 1;
     }
-    const int li = lo;
-    const int T = a.v.lT[li], D = a.v.lD[li], P = a.v.lP[li];
-    const long long local = idx - a.v.lbase[li];
-    const long long nu = a.v.lnu[li];
-    const int vv = (int)(local / nu), uu = (int)(local % nu);
-    const int goff = a.v.lgoff[li], poff = a.v.lpoff[li], doff = a.v.ldoff[li] + li;
+    const int li = tk[lo].layout;
+    const int D = a.v.lD[li], P = a.v.lP[li];
+    int pw = 1, lpw = 0;
+    while (pw < P) {
+      pw <<= 1;
+      ++lpw;
+    }
+    const int R = 32 >> lpw, nb = (D + R - 1) / R;
+    const long long tl = t - tk[lo].task_base;
+    const int vv = tk[lo].v_lo + (int)(tl / (8 * nb));
+    const int rr = (int)(tl % (8 * nb));
+    const int cs = rr / nb, batch = rr % nb;
+    const int s = lane & (pw - 1), slot = lane >> lpw;
+    const int goff = a.v.lgoff[li], poff = a.v.lpoff[li];
     const int32_t* rep = a.v.repart + poff;
-    const int32_t* pst = a.v.pstart + doff;
-    int psrc = -1, pdst = -1, csrc = -1, cdst = -1;
+    const int32_t* pst = a.v.pstart + a.v.ldoff[li] + li;
+    int psrc = -1, pdst = -1;
     if (vv >= 2) {
       const int m = vv - 2, r = m % (P - 1);
       psrc = m / (P - 1);
       pdst = r < psrc ? r : r + 1;
     }
-    if (uu >= 2) {
-      const int m = uu - 2, r = m % (D - 1);
-      csrc = m / (D - 1);
-      cdst = r < csrc ? r : r + 1;
-    }
-    bool feasible = true;
-    if (psrc >= 0 && rep[psrc] - 1 < a.min_layers) feasible = false;
-    if (csrc >= 0 && pst[csrc + 1] - pst[csrc] == 0) feasible = false;
-    double score = CUDART_INF;
-    if (feasible) {
-      int pw = 1, lpw = 0;
-      while (pw < P) {
-        pw <<= 1;
-        ++lpw;
-      }
-      const int s = lane & (pw - 1), slot = lane >> lpw, R = 32 >> lpw;
-      // layers on stage s under variant vv
-      int Ls = 0;
-      if (s < P) {
-        if (vv == 0) Ls = a.L / P + (s < a.L % P ? 1 : 0);
-        else Ls = rep[s] + (s == pdst ? 1 : 0) - (s == psrc ? 1 : 0);
-      }
-      const double L = (double)Ls;
-      const double rlF = __dmul_rn(a.m.ratio_f, L);
-      const double rlB = __dmul_rn(ZBH ? a.m.ratio_b : __dadd_rn(a.m.ratio_b, a.m.ratio_w), L);
-      const double rlW = __dmul_rn(a.m.ratio_w, L);
-      // terminal all-reduce: max over stages of the ring cost (pipeline.py:356-372)
+    const bool feas_v = !(psrc >= 0 && rep[psrc] - 1 < a.min_layers);
+    const long long pair = a.v.lpair[li] + vv;
+    double* Rp = a.v.rtab + a.v.lrt[li] + (long long)vv * 8 * D;
+    const int Ls = s < P ? layer_of(a, rep, P, vv, psrc, pdst, s) : 0;
+    const double L = (double)Ls;
+    if (cs == 0 && batch == 0) {
+      // per (layout, v): all-reduce vertex (pipeline.py:356-372) and the
+      // amortised reconfiguration surcharge (scheduler.py:562-593)
       const bool has_ar = a.has_comm && D > 1;
       double ar = 0.0;
       if (has_ar && s < P) {
@@ -373,88 +381,133 @@ __global__ void __launch_bounds__(kEvalThreads) eval_kernel(SearchArgs a, long l
                        __dmul_rn((double)D, a.v.ring[poff + s]));
       }
       for (int o = 16; o > 0; o >>= 1) ar = fmax(ar, __shfl_xor_sync(0xffffffffu, ar, o));
-      double ms = 0.0;
-      bool over = false, hung = false;
-      for (int d0 = 0; d0 < D; d0 += R) {
-        const int d = d0 + slot;
-        const bool on = d < D && s < P;
-        int start = 0, md = 0;
-        if (d < D) {
-          if (uu == 0) {
-            const int base = a.M / D, extra = a.M % D;
-            start = d * base + min(d, extra);
-            md = base + (d < extra ? 1 : 0);
-          } else {
-            int s0 = pst[d], s1 = pst[d + 1];
-            if (csrc >= 0) {
-              s0 += (d > cdst ? 1 : 0) - (d > csrc ? 1 : 0);
-              s1 += (d + 1 > cdst ? 1 : 0) - (d + 1 > csrc ? 1 : 0);
-            }
-            start = s0;
-            md = s1 - s0;
-          }
-        }
-        double sp = 1.0, hopf = 0.0, hopb = 0.0;
-        if (on) {
-          sp = a.v.gspeed[goff + d * P + s];
-          if (s > 0) hopf = a.v.ghop[goff + d * P + s - 1];
-          if (s < P - 1) hopb = a.v.ghop[goff + d * P + s];
-        }
-        const int w = min(P - 1 - s, md);
-        const int n_chain = on ? c * md : 0;
-        double fin = 0.0, ssum = 0.0;
-        chain_walk<ZBH>(s, P, pw, md, w, n_chain, a.v.base + start, rlF, rlB, rlW, sp, hopf,
-                        hopb, a.cap, a.M, fin, ssum, over, hung);
-        double g = fin;
-        for (int o = pw >> 1; o > 0; o >>= 1) g = fmax(g, __shfl_xor_sync(0xffffffffu, g, o));
-        if (d < D) ms = fmax(ms, has_ar ? __dadd_rn(g, ar) : g);
-      }
-      for (int o = 16; o > 0; o >>= 1) ms = fmax(ms, __shfl_xor_sync(0xffffffffu, ms, o));
-      const bool bad = __any_sync(0xffffffffu, over || hung);
-      if (!bad) {
-        // reconfiguration surcharge (scheduler.py:562-593) / amortisation
-        // horizon (policies.py:341-345); every lane computes it (uniform)
+      if (lane == 0) {
         const bool same_layout = a.v.same[li] != 0;
-        bool part_changed = false;
-        long long moved = 0;
         const bool sameP = P == a.cur_P;
+        bool changed = false;
+        long long moved = 0;
+        for (int q = 0; q < P && sameP; ++q) {
+          const int lq = layer_of(a, rep, P, vv, psrc, pdst, q);
+          const int old = a.v.cur_partition[q];
+          if (lq != old) changed = true;
+          if (lq > old) moved += lq - old;
+        }
         double reshard = 0.0;
-        for (int q = 0; q < P; ++q) {
-          const int lq = vv == 0 ? a.L / P + (q < a.L % P ? 1 : 0)
-                                 : rep[q] + (q == pdst ? 1 : 0) - (q == psrc ? 1 : 0);
-          if (sameP) {
-            const int old = a.v.cur_partition[q];
-            if (lq != old) part_changed = true;
-            if (lq > old) moved += lq - old;
-          }
-        }
-        if (!same_layout) {
+        if (!same_layout)
           for (int dd = 0; dd < D; ++dd)
-            for (int q = 0; q < P; ++q) {
-              const int lq = vv == 0 ? a.L / P + (q < a.L % P ? 1 : 0)
-                                     : rep[q] + (q == pdst ? 1 : 0) - (q == psrc ? 1 : 0);
-              reshard = __dadd_rn(reshard, __dmul_rn((double)lq, a.lb));
-            }
-        }
-        if (!sameP) moved = 0;
+            for (int q = 0; q < P; ++q)
+              reshard = __dadd_rn(reshard,
+                                  __dmul_rn((double)layer_of(a, rep, P, vv, psrc, pdst, q), a.lb));
         double sur = 0.0;
-        if (!same_layout || part_changed) {
+        if (!same_layout || changed) {
           const double transfer = __ddiv_rn(__dadd_rn(__dmul_rn((double)moved, a.lb), reshard),
                                             a.worst_inter);
           sur = __ddiv_rn(__dadd_rn(a.rebuild_s, transfer), (double)max(1, a.amort));
         }
-        score = __dadd_rn(ms, sur);
+        a.v.pinfo[2 * pair] = has_ar ? ar : -1.0;  // -1: no all-reduce vertex
+        a.v.pinfo[2 * pair + 1] = feas_v ? sur : CUDART_INF;
       }
     }
-    if (scores && lane == 0) scores[idx - begin] = score;
+    const int d = batch * R + slot;
+    int start = 0, md = 0;
+    bool valid = d < D;
+    if (valid) {
+      if (cs == 0) {
+        const int base = a.M / D, extra = a.M % D;
+        start = d * base + min(d, extra);
+        md = base + (d < extra ? 1 : 0);
+      } else {
+        start = pst[d] + kDs[cs];
+        md = pst[d + 1] + kDe[cs] - start;
+        valid = start >= 0 && md >= 0 && start + md <= a.M;
+      }
+    }
+    const bool on = feas_v && valid && s < P;
+    double sp = 1.0, hopf = 0.0, hopb = 0.0;
+    if (on) {
+      sp = a.v.gspeed[goff + d * P + s];
+      if (s > 0) hopf = a.v.ghop[goff + d * P + s - 1];
+      if (s < P - 1) hopb = a.v.ghop[goff + d * P + s];
+    }
+    const double rlF = __dmul_rn(a.m.ratio_f, L);
+    const double rlB = __dmul_rn(ZBH ? a.m.ratio_b : __dadd_rn(a.m.ratio_b, a.m.ratio_w), L);
+    const double rlW = __dmul_rn(a.m.ratio_w, L);
+    const int w = min(P - 1 - s, md);
+    double fin = 0.0, ssum = 0.0;
+    bool over = false, hung = false;
+    chain_walk<ZBH>(s, P, pw, on ? md : 0, w, on ? c * md : 0, a.v.base + (on ? start : 0), rlF,
+                    rlB, rlW, sp, hopf, hopb, a.cap, a.M, fin, ssum, over, hung);
+    double g = fin;
+    for (int o = pw >> 1; o > 0; o >>= 1) g = fmax(g, __shfl_xor_sync(0xffffffffu, g, o));
+    const unsigned gm = pw == 32 ? 0xffffffffu : (((1u << pw) - 1u) << (slot * pw));
+    const bool bad = (__ballot_sync(0xffffffffu, over || hung) & gm) != 0;
+    if (s == 0 && d < D) Rp[cs * D + d] = (bad || !valid || !feas_v) ? CUDART_INF : g;
+  }
+}
+
+// ---- phase 2: every candidate from the table (thread per candidate) -------
+__global__ void __launch_bounds__(kEvalThreads) combine_kernel(SearchArgs a, long long begin,
+                                                              long long end, double* scores) {
+  __shared__ double s_best[kEvalThreads / 32];
+  __shared__ long long s_idx[kEvalThreads / 32];
+  double best = CUDART_INF;
+  long long best_i = -1;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long idx = begin + (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < end;
+       idx += stride) {
+    int lo = 0, hi = a.n_layouts - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (a.v.lbase[mid] <= idx) lo = mid;
+      else hi = mid - 1;
+    }
+    const int li = lo;
+    const int D = a.v.lD[li];
+    const long long local = idx - a.v.lbase[li];
+    const long long nu = a.v.lnu[li];
+    const int vv = (int)(local / nu), uu = (int)(local % nu);
+    const long long pair = a.v.lpair[li] + vv;
+    const double ar = a.v.pinfo[2 * pair], sur = a.v.pinfo[2 * pair + 1];
+    const double* Rp = a.v.rtab + a.v.lrt[li] + (long long)vv * 8 * D;
+    double ms = 0.0;
+    bool feasible = sur < CUDART_INF;
+    if (uu <= 1) {
+      for (int d = 0; d < D; ++d) ms = fmax(ms, Rp[uu * D + d]);
+    } else {
+      const int m = uu - 2, r = m % (D - 1);
+      const int src = m / (D - 1), dst = r < src ? r : r + 1;
+      const int32_t* pst = a.v.pstart + a.v.ldoff[li] + li;
+      if (pst[src + 1] - pst[src] == 0) feasible = false;
+      for (int d = 0; d < D && feasible; ++d) {
+        int cs = 1;
+        if (src < dst) cs = d == src ? 2 : (d == dst ? 4 : ((d > src && d < dst) ? 3 : 1));
+        else cs = d == dst ? 5 : (d == src ? 7 : ((d > dst && d < src) ? 6 : 1));
+        ms = fmax(ms, Rp[cs * D + d]);
+      }
+    }
+    double score = CUDART_INF;
+    if (feasible && ms < CUDART_INF) {
+      // max_d(g_d + AR) == max_d(g_d) + AR: rounding is monotone
+      if (ar >= 0.0) ms = __dadd_rn(ms, ar);
+      score = __dadd_rn(ms, sur);
+    }
+    if (scores) scores[idx - begin] = score;
     if (lex_less(score, idx, best, best_i)) {
       best = score;
       best_i = idx;
     }
   }
-  if (lane == 0) {
-    s_best[wib] = best;
-    s_idx[wib] = best_i;
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const long long oi = __shfl_xor_sync(0xffffffffu, best_i, o);
+    if (oi >= 0 && (best_i < 0 || lex_less(ob, oi, best, best_i))) {
+      best = ob;
+      best_i = oi;
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+    s_best[threadIdx.x >> 5] = best;
+    s_idx[threadIdx.x >> 5] = best_i;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -648,6 +701,10 @@ int rh_search_create(rh_ctx* ctx, const rh_search_desc* desc, rh_search** out, v
         S->lbase.push_back(base);
         S->lnv.push_back(nv);
         S->lnu.push_back(nu);
+        S->lpair.push_back(S->n_pairs);
+        S->lrt.push_back(S->n_rt);
+        S->n_pairs += nv;
+        S->n_rt += nv * 8 * D;
         base += nv * nu;
         goff += D * P;
         poff += P;
@@ -666,7 +723,7 @@ int rh_search_create(rh_ctx* ctx, const rh_search_desc* desc, rh_search** out, v
   }
   // ---- device memory
   int max_blocks_per_sm = 0;
-  RH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_blocks_per_sm, eval_kernel<0>,
+  RH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_blocks_per_sm, table_kernel<0>,
                                                         kEvalThreads, 0));
   S->eval_blocks = ctx->num_sms * std::max(1, max_blocks_per_sm);
   size_t bytes = 0;
@@ -692,7 +749,8 @@ int rh_search_create(rh_ctx* ctx, const rh_search_desc* desc, rh_search** out, v
                o_lpoff = up(S->lpoff.data(), 4 * NL), o_ldoff = up(S->ldoff.data(), 4 * NL),
                o_lboff = up(S->lboff.data(), 4 * NL), o_lnb = up(S->lnb.data(), 4 * NL),
                o_lbase = up(S->lbase.data(), 8 * NL), o_lnv = up(S->lnv.data(), 8 * NL),
-               o_lnu = up(S->lnu.data(), 8 * NL);
+               o_lnu = up(S->lnu.data(), 8 * NL), o_lpair = up(S->lpair.data(), 8 * NL),
+               o_lrt = up(S->lrt.data(), 8 * NL);
   const size_t o_bnode = up(S->blk_node.data(), 4 * nblk),
                o_brank = up(S->blk_rank.data(), 4 * nblk),
                o_bmem = up(S->blk_members.data(), 4 * nmem),
@@ -709,7 +767,9 @@ int rh_search_create(rh_ctx* ctx, const rh_search_desc* desc, rh_search** out, v
                o_repart = take(4 * S->n_stage), o_rspeed = take(8 * S->n_rep),
                o_pstart = take(4 * (S->n_rep + NL)), o_same = take(4 * NL),
                o_base = take(8 * (size_t)d.n_micro_batches),
-               o_bb = take(8 * (size_t)S->eval_blocks), o_bi = take(8 * (size_t)S->eval_blocks);
+               o_bb = take(8 * (size_t)S->eval_blocks), o_bi = take(8 * (size_t)S->eval_blocks),
+               o_rtab = take(8 * (size_t)S->n_rt), o_pinfo = take(16 * (size_t)S->n_pairs),
+               o_tasks = take(sizeof(PhaseTask) * (size_t)NL);
   cudaError_t e = cudaMalloc(&S->dmem, bytes);
   if (e != cudaSuccess) {
     delete S;
@@ -727,6 +787,8 @@ int rh_search_create(rh_ctx* ctx, const rh_search_desc* desc, rh_search** out, v
   v.lT = I(o_lT); v.lD = I(o_lD); v.lP = I(o_lP); v.lgoff = I(o_lgoff); v.lpoff = I(o_lpoff);
   v.ldoff = I(o_ldoff); v.lboff = I(o_lboff); v.lnb = I(o_lnb);
   v.lbase = LL(o_lbase); v.lnv = LL(o_lnv); v.lnu = LL(o_lnu);
+  v.lpair = LL(o_lpair); v.lrt = LL(o_lrt);
+  v.rtab = Dp(o_rtab); v.pinfo = Dp(o_pinfo); v.tasks = B + o_tasks;
   v.blk_node = I(o_bnode); v.blk_rank = I(o_brank); v.blk_members = I(o_bmem);
   v.blk_moff = I(o_bmoff); v.blk_speed = Dp(o_bspeed);
   v.quad = reinterpret_cast<int64_t*>(B + o_quad);
@@ -774,12 +836,32 @@ int rh_search_eval(rh_ctx* ctx, rh_search* S, int64_t begin, int64_t end, double
   }
   SearchArgs a = make_args(S);
   const long long n = end - begin;
-  const int warps_per_block = kEvalThreads / 32;
-  const int blocks = (int)std::min<long long>(S->eval_blocks, (n + warps_per_block - 1) / warps_per_block);
+  // phase 1 tasks: (layout, partition variant) pairs overlapping the range
+  std::vector<PhaseTask> tk;
+  long long n_tasks = 0;
+  for (int li = 0; li < (int)S->lT.size(); ++li) {
+    const long long lb = S->lbase[li], le = lb + S->lnv[li] * S->lnu[li];
+    if (le <= begin || lb >= end) continue;
+    const int v_lo = (int)((std::max<long long>(begin, lb) - lb) / S->lnu[li]);
+    const int v_hi = (int)((std::min<long long>(end, le) - 1 - lb) / S->lnu[li]);
+    int pw = 1;
+    while (pw < S->lP[li]) pw <<= 1;
+    const int R = 32 / pw, nb = (S->lD[li] + R - 1) / R;
+    tk.push_back({li, v_lo, n_tasks});
+    n_tasks += (long long)(v_hi - v_lo + 1) * 8 * nb;
+  }
+  RH_CUDA(cudaMemcpyAsync(S->dv.tasks, tk.data(), sizeof(PhaseTask) * tk.size(),
+                          cudaMemcpyHostToDevice, st));
+  const int tblocks = (int)std::min<long long>(S->eval_blocks, (n_tasks + 7) / 8);
   if (S->d.schedule == RH_SCHED_ZBH)
-    eval_kernel<1><<<blocks, kEvalThreads, 0, st>>>(a, begin, end, scores);
+    table_kernel<1><<<tblocks, kEvalThreads, 0, st>>>(
+        a, reinterpret_cast<const PhaseTask*>(S->dv.tasks), (int)tk.size(), n_tasks);
   else
-    eval_kernel<0><<<blocks, kEvalThreads, 0, st>>>(a, begin, end, scores);
+    table_kernel<0><<<tblocks, kEvalThreads, 0, st>>>(
+        a, reinterpret_cast<const PhaseTask*>(S->dv.tasks), (int)tk.size(), n_tasks);
+  RH_CHECK_LAUNCH(ctx);
+  const int blocks = (int)std::min<long long>(S->eval_blocks, (n + kEvalThreads - 1) / kEvalThreads);
+  combine_kernel<<<blocks, kEvalThreads, 0, st>>>(a, begin, end, scores);
   RH_CHECK_LAUNCH(ctx);
   minloc_kernel<<<1, 1024, 0, st>>>(S->dv.blk_best, S->dv.blk_idx, blocks, best_score,
                                     best_index);
