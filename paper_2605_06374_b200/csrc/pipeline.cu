@@ -45,8 +45,10 @@ struct PassParams {
   int vec4;        // device_time rows are float4-aligned
 };
 
-template <int ZBH, int DETECT>
-__global__ void __launch_bounds__(1024) pass_kernel(const PassParams p) {
+// MAXT = launch bound: 256 for the common case (more registers per lane),
+// 1024 when one iteration needs D*pw > 256 lanes.
+template <int ZBH, int DETECT, int MAXT>
+__global__ void __launch_bounds__(MAXT) pass_kernel(const PassParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x;
   const int P = p.sh.pp, D = p.sh.dp, M = p.sh.micro_batches, T = p.sh.tp;
@@ -198,6 +200,245 @@ __global__ void __launch_bounds__(1024) pass_kernel(const PassParams p) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Small-P variant (P <= 4, D <= 256): one THREAD per replica pipeline.  The
+// thread walks all P stage chains level by level (same closed-form levels as
+// wavefront.cuh), with every stage's state in registers (P is a template
+// parameter, the stage loop is unrolled).  Data dependencies between stages
+// are read from a start-of-level snapshot of each stage's last F / B finish
+// — the same exactness argument as the shuffle wavefront, without shuffles or
+// idle lanes.  Replicas of a warp share one level schedule when their
+// micro-batch counts agree, so the per-stage branches are warp-uniform.
+constexpr int kSmallThreads = 128;
+constexpr int kDocStage = 4096;  // documents staged per CTA (16 KB)
+
+// Copy n ints global -> shared with U independent loads in flight per thread.
+template <int U>
+__device__ __forceinline__ void stage_ints(int32_t* dst, const int32_t* src, int n) {
+  for (int q0 = threadIdx.x; q0 < n; q0 += U * blockDim.x) {
+    int32_t v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int q = q0 + u * blockDim.x;
+      v[u] = q < n ? __ldg(src + q) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int q = q0 + u * blockDim.x;
+      if (q < n) dst[q] = v[u];
+    }
+  }
+}
+
+template <int P, int ZBH, int DETECT>
+__global__ void __launch_bounds__(kSmallThreads, 4) pass_small_kernel(const PassParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int tid = threadIdx.x;
+  const int D = p.sh.dp, M = p.sh.micro_batches, T = p.sh.tp;
+  const int li = tid / D, d = tid - li * D;
+  const int64_t it0 = (int64_t)blockIdx.x * p.ipb;
+  const int64_t it = it0 + li;
+  const int n_it = (int)min((int64_t)p.ipb, p.tr.n_iter - it0);
+  const bool on = li < n_it;
+  double* it_ms = reinterpret_cast<double*>(smem_raw);
+  unsigned* it_st = reinterpret_cast<unsigned*>(it_ms + p.ipb);
+  const int it_bytes = ((p.ipb * 12 + 15) / 16) * 16;
+  double* base = reinterpret_cast<double*>(smem_raw + it_bytes) + (size_t)tid * p.mmax;
+  int32_t* s_off = reinterpret_cast<int32_t*>(smem_raw + it_bytes + (size_t)p.ipb * D * p.mmax * 8);
+  int32_t* s_doc = s_off + ((p.ipb * M + 1 + 3) & ~3);
+  if (tid < p.ipb) {
+    it_ms[tid] = 0.0;
+    it_st[tid] = 0u;
+  }
+  // stage this CTA's micro-batch offsets and documents (coalesced)
+  const int n_mb = n_it * M;
+  stage_ints<8>(s_off, p.tr.mb_off + it0 * M, n_mb + 1);
+  __syncthreads();
+  const int32_t d_lo = s_off[0];
+  const int n_doc = s_off[n_mb] - d_lo;
+  const bool staged = n_doc <= kDocStage;
+  if (staged) stage_ints<8>(s_doc, p.tr.doc_len + d_lo, n_doc);
+  __syncthreads();
+  int seg = 0, md = 0;
+  if (on) {
+    seg = p.tr.seg ? __ldg(p.tr.seg + it) : 0;
+    const int32_t* ms = p.sg.mb_start + (int64_t)seg * (D + 1);
+    const int m0 = __ldg(ms + d);
+    md = __ldg(ms + d + 1) - m0;
+    if (md > p.mmax) md = -1;
+    if (md > 0) {
+      const double lin = __dmul_rn(p.m.alpha, (double)p.sh.token_budget);
+      const int32_t* off = s_off + li * M + m0;
+      for (int j = 0; j < md; ++j) {
+        long long q = 0;
+        for (int32_t k = off[j] - d_lo; k < off[j + 1] - d_lo; ++k) {
+          const long long l = staged ? s_doc[k] : __ldg(p.tr.doc_len + d_lo + k);
+          q += l * l;
+        }
+        base[j] = __dadd_rn(lin, __dmul_rn(p.m.beta, (double)q));
+      }
+    }
+  }
+  const int m = md > 0 ? md : 0;
+  double rlF[P], rlB[P], rlW[P], sp[P], hf[P], hb[P], fin[P], ssum[P], lastF[P], lastB[P];
+  int LF[P], LB[P], LW[P], jf[P], jb[P], jw[P], live[P];
+  bool stopped = false, over = false;
+  int last = 0;
+#pragma unroll
+  for (int s = 0; s < P; ++s) {
+    const int64_t gs = ((int64_t)seg * D + d) * P + s;
+    sp[s] = 1.0;
+    hf[s] = hb[s] = 0.0;
+    rlF[s] = rlB[s] = rlW[s] = 0.0;
+    if (on && m > 0) {
+      sp[s] = __ldg(p.sg.speed + gs);
+      const double L = (double)__ldg(p.sg.layers + (int64_t)seg * P + s);
+      rlF[s] = __dmul_rn(p.m.ratio_f, L);
+      rlB[s] = __dmul_rn(ZBH ? p.m.ratio_b : __dadd_rn(p.m.ratio_b, p.m.ratio_w), L);
+      rlW[s] = __dmul_rn(p.m.ratio_w, L);
+      if (s > 0) hf[s] = __ldg(p.sg.hop_fwd + gs - 1);
+      if (s < P - 1) hb[s] = __ldg(p.sg.hop_bwd + gs);
+      if (sp[s] <= 0.0) stopped = true;
+    }
+    fin[s] = ssum[s] = lastF[s] = lastB[s] = 0.0;
+    jf[s] = jb[s] = jw[s] = live[s] = 0;
+  }
+  const int mm = stopped ? 0 : m;
+#pragma unroll
+  for (int s = 0; s < P; ++s) {
+    const ChainLevels lv{s, P, mm, min(P - 1 - s, mm)};
+    LF[s] = lv.F(0);
+    LB[s] = lv.B(0);
+    LW[s] = ZBH ? lv.W(0) : INT_MAX;
+    if (mm > 0) last = max(last, 1 + (ZBH ? lv.W(mm - 1) : lv.B(mm - 1)));
+  }
+  __syncthreads();
+  const int cap = p.sh.capacity;
+  for (int t = 0; t < last; ++t) {
+    double snapF[P], snapB[P];
+#pragma unroll
+    for (int s = 0; s < P; ++s) {
+      snapF[s] = lastF[s];
+      snapB[s] = lastB[s];
+    }
+#pragma unroll
+    for (int s = 0; s < P; ++s) {
+      const bool doF = t == LF[s], doB = t == LB[s], doW = ZBH && t == LW[s];
+      if (doF || doB || doW) {
+        const ChainLevels lv{s, P, mm, min(P - 1 - s, mm)};
+        double dep = 0.0, rl;
+        int j;
+        if (doF) {
+          if (s > 0) dep = __dadd_rn(snapF[s - 1], hf[s]);
+          rl = rlF[s];
+          j = jf[s];
+        } else if (doB) {
+          if (s < P - 1) dep = __dadd_rn(snapB[s + 1], hb[s]);
+          rl = rlB[s];
+          j = jb[s];
+        } else {
+          rl = rlW[s];
+          j = jw[s];
+        }
+        double c = __dmul_rn(rl, base[j]);
+        if (sp[s] != 1.0) c = div_slow(c, sp[s]);
+        const double st = fin[s] > dep ? fin[s] : dep;
+        fin[s] = __dadd_rn(st, c);
+        ssum[s] = __dadd_rn(ssum[s], c);
+        if (doF) {
+          lastF[s] = fin[s];
+          LF[s] = lv.F(++jf[s]);
+          if (cap > 0 && ++live[s] > cap) over = true;
+        } else if (doB) {
+          lastB[s] = fin[s];
+          LB[s] = lv.B(++jb[s]);
+          --live[s];
+        } else {
+          LW[s] = lv.W(++jw[s]);
+        }
+      }
+    }
+  }
+  // ---- replica makespan, validation, iteration reductions
+  uint8_t flag[P];
+  float sev[P];
+  unsigned bits = 0;
+  if (on) {
+    double g = 0.0;
+#pragma unroll
+    for (int s = 0; s < P; ++s) g = fmax(g, fin[s]);
+    if (md < 0) bits |= RH_IT_OVERFLOW;
+    if (stopped && m > 0) bits |= RH_IT_STOPPED;
+    if (over) bits |= RH_IT_CAPACITY;
+    if (p.sh.has_allreduce && D > 1)
+      g = __dadd_rn(g, __ldg(p.sg.allreduce + (int64_t)seg * D + d));
+    atomic_max_nonneg(it_ms + li, g);
+#pragma unroll
+    for (int s = 0; s < P; ++s) {
+      flag[s] = 0;
+      sev[s] = 0.0f;
+      if (DETECT && md >= 0) {
+        const float* dt = p.tr.device_time + ((it * D + d) * P + s) * (int64_t)T;
+        float mx = 0.0f;
+        if (p.vec4) {
+          for (int q = 0; q < T; q += 4) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(dt + q));
+            mx = fmaxf(mx, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
+          }
+        } else {
+          for (int q = 0; q < T; ++q) mx = fmaxf(mx, __ldg(dt + q));
+        }
+        const double meas = (double)mx;
+        if (!(ssum[s] <= 0.0 || meas <= 0.0) && meas > __dmul_rn(p.thr, ssum[s])) {
+          flag[s] = 1;
+          sev[s] = (float)__ddiv_rn(ssum[s], meas);
+          bits |= RH_IT_STAGE_FLAG;
+        }
+      }
+    }
+    if (DETECT && p.sg.link_off) {  // exercised-link ratios, split over the replicas
+      const int32_t q0 = __ldg(p.sg.link_off + seg), q1 = __ldg(p.sg.link_off + seg + 1);
+      for (int32_t q = q0 + d; q < q1; q += D)
+        if (__ldg(p.sg.link_ratio + q) > p.thr) bits |= RH_IT_LINK_FLAG;
+    }
+    if (bits) atomicOr(it_st + li, bits);
+  }
+  __syncthreads();
+  if (!on) return;
+  const unsigned st_bits = it_st[li];
+  const bool dead = (st_bits & (RH_IT_STOPPED | RH_IT_OVERFLOW)) != 0;
+#pragma unroll
+  for (int s = 0; s < P; ++s) {
+    const int64_t o = (it * D + d) * P + s;
+    if (p.out.stage_cost) p.out.stage_cost[o] = dead ? 0.0 : ssum[s];
+    if (DETECT) {
+      if (p.out.stage_flag) p.out.stage_flag[o] = dead ? 0 : flag[s];
+      if (p.out.severity) p.out.severity[o] = dead ? 0.0f : sev[s];
+    }
+  }
+  if (d == 0) {
+    unsigned st = st_bits;
+    double ms = dead ? 0.0 : it_ms[li];
+    if (dead) st &= (RH_IT_STOPPED | RH_IT_OVERFLOW);
+    if (DETECT && !dead) {
+      const double obs = __ldg(p.tr.observed + it);
+      if (ms <= 0.0 || obs > __dmul_rn(p.thr, ms)) st |= RH_IT_ESCALATE;
+    }
+    p.out.makespan[it] = ms;
+    p.out.status[it] = (uint8_t)st;
+  }
+}
+
+template <int ZBH, int DETECT>
+static void* small_kernel(int P) {
+  switch (P) {
+    case 1: return (void*)pass_small_kernel<1, ZBH, DETECT>;
+    case 2: return (void*)pass_small_kernel<2, ZBH, DETECT>;
+    case 3: return (void*)pass_small_kernel<3, ZBH, DETECT>;
+    default: return (void*)pass_small_kernel<4, ZBH, DETECT>;
+  }
+}
+
 static int next_pow2(int x) {
   int p = 1;
   while (p < x) p <<= 1;
@@ -245,8 +486,27 @@ int launch_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
     return RH_E_SHAPE;
   }
   p.mmax = sh->max_mb_per_replica > 0 ? sh->max_mb_per_replica : M;
-  p.ipb = std::max(1, 256 / p.lpi);
   p.vec4 = (sh->tp % 4 == 0) && ((reinterpret_cast<uintptr_t>(tr->device_time) & 15) == 0);
+  if (P <= 4 && D <= kSmallThreads && !getenv("RH_FORCE_LANE_KERNEL")) {
+    // thread-per-replica kernel for short pipelines
+    p.ipb = std::max(1, kSmallThreads / D);
+    const int threads = p.ipb * D;
+    const int it_bytes = ((p.ipb * 12 + 15) / 16) * 16;
+    const size_t smem = it_bytes + (size_t)threads * p.mmax * 8 +
+                        4 * (size_t)(((p.ipb * M + 1 + 3) & ~3) + kDocStage);
+    if (smem <= ctx->smem_optin) {
+      const int64_t blocks = (tr->n_iter + p.ipb - 1) / p.ipb;
+      const bool zbh = sh->schedule == RH_SCHED_ZBH;
+      void* kern = zbh ? (detect ? small_kernel<1, 1>(P) : small_kernel<1, 0>(P))
+                       : (detect ? small_kernel<0, 1>(P) : small_kernel<0, 0>(P));
+      RH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      void* args[] = {&p};
+      RH_CUDA(cudaLaunchKernel(kern, dim3((unsigned)blocks), dim3(threads), args, smem, stream));
+      RH_CHECK_LAUNCH(ctx);
+      return RH_OK;
+    }
+  }
+  p.ipb = std::max(1, 256 / p.lpi);
   const int threads = ((p.ipb * p.lpi + 31) / 32) * 32;
   const int it_bytes = ((p.ipb * 12 + 15) / 16) * 16;
   const size_t smem = it_bytes + (size_t)(threads / p.pw) * p.mmax * 8;
@@ -261,10 +521,13 @@ int launch_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
     return RH_E_SHAPE;
   }
   void (*kern)(const PassParams);
+  const bool big = threads > 256;
   if (sh->schedule == RH_SCHED_ZBH)
-    kern = detect ? pass_kernel<1, 1> : pass_kernel<1, 0>;
+    kern = detect ? (big ? pass_kernel<1, 1, 1024> : pass_kernel<1, 1, 256>)
+                  : (big ? pass_kernel<1, 0, 1024> : pass_kernel<1, 0, 256>);
   else
-    kern = detect ? pass_kernel<0, 1> : pass_kernel<0, 0>;
+    kern = detect ? (big ? pass_kernel<0, 1, 1024> : pass_kernel<0, 1, 256>)
+                  : (big ? pass_kernel<0, 0, 1024> : pass_kernel<0, 0, 256>);
   RH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<(unsigned)blocks, threads, smem, stream>>>(p);
   RH_CHECK_LAUNCH(ctx);

@@ -11,17 +11,27 @@
 // chain-order cost sum (pipeline.py:446-453) and the activation check
 // (pipeline.py:516-539: on one resource the chain order is the time order).
 //
-// Data predecessors live on the neighbouring lanes and travel by warp
-// shuffle: each lane publishes (index, finish) of the last F and the last
-// B/BW it completed.  In the canonical DAG a B dependency is produced exactly
-// one step before it is consumed and a producer never runs more than one F
-// ahead of its consumer (verified exhaustively for P <= 32, M <= 64, both
-// schedules — DESIGN.md §3), so the published value is exactly the needed
-// one; an index skip is detected and reported through `hung`.
+// Static wavefront.  Every chunk is processed at its DAG level (longest path
+// from a source, in chunks), which has a closed form for the canonical
+// schedules (w = min(P-1-s, M), M = micro-batches of the replica):
+//   F_j           : s + j               if j <= w, else 2j + s
+//   B_j / BW_j    : 2P - 1 - s + 2j
+//   W_j (ZBH)     : 2P - s + 2(M - w + j)                 if j < w (drain)
+//                   last drain/B level + (j - w + 1)      otherwise (tail)
+// (checked against the exact DAG levels for P <= 32, M <= 64, both
+// schedules — tests/test_wavefront_property.py).  Along a chain these levels
+// strictly increase, so a lane only compares the step t with the level of its
+// next F, next B and next W.  At the start of step t the neighbours publish,
+// by warp shuffle, the finish of the last F / B they completed; a B
+// dependency is always exactly one level old and a producer never leads its
+// consumer by more than one F, so those are exactly the needed values.  No
+// readiness checks, no shared memory.
 //
-// Every lane of the warp must call this (warp-synchronous: __any_sync and
-// full-mask shuffles).  All fp64 ops are explicit _rn intrinsics.
+// Every lane of the warp must call this (full-mask shuffles / reductions).
+// All fp64 ops are explicit _rn intrinsics (no FMA contraction).
 #pragma once
+
+#include <climits>
 
 #include "common.cuh"
 
@@ -31,78 +41,64 @@ namespace rh {
 // over it rather than an always-executed predicated sequence.
 __device__ __noinline__ inline double div_slow(double a, double b) { return __ddiv_rn(a, b); }
 
+struct ChainLevels {
+  int s, P, m, w;
+  __device__ __forceinline__ int F(int j) const {
+    return j >= m ? INT_MAX : (j <= w ? s + j : 2 * j + s);
+  }
+  __device__ __forceinline__ int B(int j) const { return j >= m ? INT_MAX : 2 * P - 1 - s + 2 * j; }
+  __device__ __forceinline__ int W(int j) const {
+    if (j >= m) return INT_MAX;
+    if (j < w) return 2 * P - s + 2 * (m - w + j);
+    return (w > 0 ? 2 * P - s + 2 * m - 2 : 2 * P - 1 - s + 2 * (m - 1)) + (j - w + 1);
+  }
+};
+
 template <int ZBH>
 __device__ __forceinline__ void chain_walk(int s, int P, int pw, int md, int w, int n_chain,
                                            const double* base, double rlF, double rlB,
                                            double rlW, double sp, double hopf, double hopb,
-                                           int cap, int mmax, double& fin, double& ssum,
-                                           bool& over, bool& hung) {
+                                           int cap, int /*mmax*/, double& fin, double& ssum,
+                                           bool& over, bool& /*hung*/) {
   const bool unit = sp == 1.0;  // x / 1.0 == x exactly: skip the division
-  const int lim = 2 * md - w;   // end of the steady F/B pairs
-  int k = 0, jf = 0, jb = 0, jw = 0, live = 0;
+  const ChainLevels lv{s, P, n_chain > 0 ? md : 0, w};
+  int jf = 0, jb = 0, jw = 0, live = 0;
+  int LF = lv.F(0), LB = lv.B(0), LW = ZBH ? lv.W(0) : INT_MAX;
+  const int last = lv.m == 0 ? 0 : 1 + (ZBH ? lv.W(lv.m - 1) : lv.B(lv.m - 1));
+  const int T = __reduce_max_sync(0xffffffffu, last);
+  const double hF = s > 0 ? hopf : 0.0, hB = s < P - 1 ? hopb : 0.0;
+  const bool getF = s > 0, getB = s < P - 1;
   double lastF = 0.0, lastB = 0.0;
-  int lastFi = -1, lastBi = -1;
-  bool pending = n_chain > 0;
-  // every step retires >= 1 chunk of each unfinished pipeline (acyclic DAG)
-  const int max_steps = (ZBH ? 3 : 2) * mmax * P + 2;
-  int steps = 0;
-  while (__any_sync(0xffffffffu, pending)) {
-    if (++steps > max_steps) {  // defensive: never spin on a malformed input
-      hung = hung || pending;
-      break;
-    }
+  // Branch-free step: F-, B- and idle lanes of a warp execute the same
+  // instruction stream (selects instead of divergent paths); only the rare
+  // non-unit-speed division is a real branch.
+  const int jmax = lv.m > 0 ? lv.m - 1 : 0;
+  for (int t = 0; t < T; ++t) {
     const double nF = __shfl_up_sync(0xffffffffu, lastF, 1, pw);
-    const int nFi = __shfl_up_sync(0xffffffffu, lastFi, 1, pw);
     const double nB = __shfl_down_sync(0xffffffffu, lastB, 1, pw);
-    const int nBi = __shfl_down_sync(0xffffffffu, lastBi, 1, pw);
-    if (pending) {
-      // kind at chain position k (pipeline.py:92-118): 0=F 1=B/BW 2=W
-      int kind;
-      if (k < w) {
-        kind = 0;
-      } else if (k < lim) {
-        kind = (k - w) & 1;
-      } else if (!ZBH) {
-        kind = 1;
-      } else if (k < 2 * md + w) {
-        kind = ((k - lim) & 1) ? 2 : 1;
-      } else {
-        kind = 2;
-      }
-      const int j = kind == 0 ? jf : (kind == 1 ? jb : jw);
-      bool ready = true;
-      double dep = 0.0;
-      if (kind == 0 && s > 0) {
-        ready = nFi == j;
-        if (nFi > j) hung = true;  // lead bound violated: never guess
-        dep = __dadd_rn(nF, hopf);
-      } else if (kind == 1 && s < P - 1) {
-        ready = nBi == j;
-        if (nBi > j) hung = true;
-        dep = __dadd_rn(nB, hopb);
-      }
-      if (hung) {
-        pending = false;
-      } else if (ready) {
-        double c = __dmul_rn(kind == 0 ? rlF : (kind == 1 ? rlB : rlW), base[j]);
-        if (!unit) c = div_slow(c, sp);
-        fin = __dadd_rn(fmax(fin, dep), c);
-        ssum = __dadd_rn(ssum, c);
-        if (kind == 0) {
-          lastF = fin;
-          lastFi = jf++;
-          if (cap > 0 && ++live > cap) over = true;
-        } else if (kind == 1) {
-          lastB = fin;
-          lastBi = jb++;
-          --live;
-        } else {
-          ++jw;
-        }
-        ++k;
-        pending = k < n_chain;
-      }
-    }
+    const bool doF = t == LF, doB = t == LB, doW = ZBH && t == LW;
+    const bool act = doF || doB || doW;
+    const double dF = getF ? __dadd_rn(nF, hF) : 0.0;
+    const double dB = getB ? __dadd_rn(nB, hB) : 0.0;
+    const double dep = doF ? dF : (doB ? dB : 0.0);
+    const double rl = doF ? rlF : (doB ? rlB : rlW);
+    const int j = min(doF ? jf : (doB ? jb : jw), jmax);
+    double c = __dmul_rn(rl, base[j]);
+    if (!unit && act) c = div_slow(c, sp);
+    const double st = fin > dep ? fin : dep;  // max (no NaNs on this path)
+    const double nf = __dadd_rn(st, c);
+    fin = act ? nf : fin;
+    ssum = act ? __dadd_rn(ssum, c) : ssum;
+    lastF = doF ? nf : lastF;
+    lastB = doB ? nf : lastB;
+    jf += doF;
+    jb += doB;
+    if (ZBH) jw += doW;
+    LF = doF ? lv.F(jf) : LF;
+    LB = doB ? lv.B(jb) : LB;
+    if (ZBH) LW = doW ? lv.W(jw) : LW;
+    live += (int)doF - (int)doB;
+    over = over || (cap > 0 && doF && live > cap);
   }
 }
 
