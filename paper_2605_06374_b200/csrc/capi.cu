@@ -4,6 +4,7 @@
 #include <stdarg.h>
 
 #include <mutex>
+#include <unordered_map>
 
 #include "common.cuh"
 
@@ -37,6 +38,17 @@ int workspace(rh_ctx* ctx, size_t bytes, void** out, int slot) {
     ctx->ws_bytes[slot] = want;
   }
   *out = ctx->ws[slot];
+  return RH_OK;
+}
+
+int ensure_smem(const void* kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, size_t> granted;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = granted.find(kernel);
+  if (it != granted.end() && it->second >= bytes) return RH_OK;
+  RH_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  granted[kernel] = bytes;
   return RH_OK;
 }
 
@@ -146,6 +158,9 @@ int rh_ctx_destroy(rh_ctx* ctx) {
   if (!ctx) return RH_OK;
   for (void* w : ctx->ws)
     if (w) cudaFree(w);
+  for (cudaEvent_t e : ctx->chunk_ev)
+    if (e) cudaEventDestroy(e);
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   delete ctx;
   return RH_OK;
 }

@@ -20,6 +20,10 @@ struct rh_ctx {
   // slot 1 = kernel scratch (screen, general DAG); never aliased
   void* ws[2] = {nullptr, nullptr};
   size_t ws_bytes[2] = {0, 0};
+  // host-buffer entry points: copy stream + per-chunk events (lazily made)
+  static constexpr int kChunkEvents = 8;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t chunk_ev[kChunkEvents] = {};
 };
 
 namespace rh {
@@ -47,6 +51,10 @@ inline int cuda_fail(cudaError_t e, const char* what) {
 // Grow the context workspace to at least `bytes` (stream-ordered free of the
 // old buffer is not needed: callers synchronise before growth).
 int workspace(rh_ctx* ctx, size_t bytes, void** out, int slot);
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) only when a kernel needs
+// more than it was last granted (the call costs microseconds per launch)
+int ensure_smem(const void* kernel, size_t bytes);
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 

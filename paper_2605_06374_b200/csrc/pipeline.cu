@@ -499,7 +499,7 @@ int launch_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
       const bool zbh = sh->schedule == RH_SCHED_ZBH;
       void* kern = zbh ? (detect ? small_kernel<1, 1>(P) : small_kernel<1, 0>(P))
                        : (detect ? small_kernel<0, 1>(P) : small_kernel<0, 0>(P));
-      RH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      if (int e = ensure_smem(kern, smem)) return e;
       void* args[] = {&p};
       RH_CUDA(cudaLaunchKernel(kern, dim3((unsigned)blocks), dim3(threads), args, smem, stream));
       RH_CHECK_LAUNCH(ctx);
@@ -528,7 +528,7 @@ int launch_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
   else
     kern = detect ? (big ? pass_kernel<0, 1, 1024> : pass_kernel<0, 1, 256>)
                   : (big ? pass_kernel<0, 0, 1024> : pass_kernel<0, 0, 256>);
-  RH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (int e = ensure_smem((const void*)kern, smem)) return e;
   kern<<<(unsigned)blocks, threads, smem, stream>>>(p);
   RH_CHECK_LAUNCH(ctx);
   return RH_OK;
@@ -592,34 +592,23 @@ int detect_host(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
   int rc = workspace(ctx, need, &ws, 0);
   if (rc) return rc;
   Carver c{static_cast<char*>(ws)};
-  rh_trace dtr = *tr;
+  // device buffers: every trace array lands at its own offsets, so the
+  // absolute CSR offsets of mb_off stay valid for any chunk of iterations
+  int32_t* d_seg = tr->seg ? c.take<int32_t>(n) : nullptr;
+  int32_t* d_off = c.take<int32_t>(n * M + 1);
+  int32_t* d_doc = c.take<int32_t>(n_docs);
+  float* d_dt = c.take<float>(n * G * T);
+  double* d_obs = c.take<double>(n);
   rh_segments dsg = *sg;
+  int32_t* d_layers = c.take<int32_t>(S * P);
+  int32_t* d_mbs = c.take<int32_t>(S * (D + 1));
+  double* d_speed = c.take<double>(S * G);
+  double* d_hf = c.take<double>(S * G);
+  double* d_hb = c.take<double>(S * G);
+  double* d_ar = c.take<double>(S * D);
+  int32_t* d_loff = c.take<int32_t>(S + 1);
+  double* d_lr = c.take<double>(n_links + 1);
   rh_pass_out dout = {};
-  auto h2d = [&](auto* dst, const auto* src, size_t count) -> int {
-    if (!src || !count) return RH_OK;
-    RH_CUDA(cudaMemcpyAsync(dst, src, count * sizeof(*src), cudaMemcpyHostToDevice, stream));
-    return RH_OK;
-  };
-#define RH_H2D(field_dst, src, count, T_)                \
-  do {                                                   \
-    T_* _d = c.take<T_>(count);                          \
-    if ((rc = h2d(_d, src, count))) return rc;           \
-    field_dst = src ? _d : nullptr;                      \
-  } while (0)
-  RH_H2D(dtr.seg, tr->seg, (size_t)n, int32_t);
-  RH_H2D(dtr.mb_off, tr->mb_off, (size_t)(n * M + 1), int32_t);
-  RH_H2D(dtr.doc_len, tr->doc_len, (size_t)n_docs, int32_t);
-  RH_H2D(dtr.device_time, tr->device_time, (size_t)(n * G * T), float);
-  RH_H2D(dtr.observed, tr->observed, (size_t)n, double);
-  RH_H2D(dsg.layers, sg->layers, (size_t)(S * P), int32_t);
-  RH_H2D(dsg.mb_start, sg->mb_start, (size_t)(S * (D + 1)), int32_t);
-  RH_H2D(dsg.speed, sg->speed, (size_t)(S * G), double);
-  RH_H2D(dsg.hop_fwd, sg->hop_fwd, (size_t)(S * G), double);
-  RH_H2D(dsg.hop_bwd, sg->hop_bwd, (size_t)(S * G), double);
-  RH_H2D(dsg.allreduce, sg->allreduce, (size_t)(S * D), double);
-  RH_H2D(dsg.link_off, sg->link_off, (size_t)(S + 1), int32_t);
-  RH_H2D(dsg.link_ratio, sg->link_ratio, (size_t)n_links, double);
-#undef RH_H2D
   dout.makespan = c.take<double>(n);
   dout.status = c.take<uint8_t>(n);
   dout.stage_cost = out->stage_cost ? c.take<double>(n * G) : nullptr;
@@ -629,38 +618,93 @@ int detect_host(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
   uint8_t* d_reset = c.take<uint8_t>(n);
   uint8_t* d_outcome = c.take<uint8_t>(n);
   int64_t* d_len = c.take<int64_t>(1);
+  auto cp = [&](void* dst, const void* src, size_t bytes, cudaMemcpyKind kind,
+                cudaStream_t st) -> int {
+    if (!src || !bytes) return RH_OK;
+    RH_CUDA(cudaMemcpyAsync(dst, src, bytes, kind, st));
+    return RH_OK;
+  };
+  const auto H2D = cudaMemcpyHostToDevice;
+  const auto D2H = cudaMemcpyDeviceToHost;
+  // segment tables + screen state on the compute stream
+  if ((rc = cp(d_layers, sg->layers, 4 * S * P, H2D, stream)) ||
+      (rc = cp(d_mbs, sg->mb_start, 4 * S * (D + 1), H2D, stream)) ||
+      (rc = cp(d_speed, sg->speed, 8 * S * G, H2D, stream)) ||
+      (rc = cp(d_hf, sg->hop_fwd, 8 * S * G, H2D, stream)) ||
+      (rc = cp(d_hb, sg->hop_bwd, 8 * S * G, H2D, stream)) ||
+      (rc = cp(d_ar, sg->allreduce, 8 * S * D, H2D, stream)) ||
+      (rc = cp(d_loff, sg->link_off, 4 * (S + 1), H2D, stream)) ||
+      (rc = cp(d_lr, sg->link_ratio, 8 * n_links, H2D, stream)))
+    return rc;
+  dsg.layers = d_layers;
+  dsg.mb_start = d_mbs;
+  dsg.speed = d_speed;
+  dsg.hop_fwd = d_hf;
+  dsg.hop_bwd = d_hb;
+  dsg.allreduce = sg->allreduce ? d_ar : nullptr;
+  dsg.link_off = sg->link_off ? d_loff : nullptr;
+  dsg.link_ratio = sg->link_off ? d_lr : nullptr;
   const int64_t h = screen ? std::min<int64_t>(series_len, screen->window) : 0;
   if (screen && h > 64) {
     set_error("detector_pass_host: window > 64");
     return RH_E_INVALID;
   }
-  if (h) RH_CUDA(cudaMemcpyAsync(d_hist, hist, h * sizeof(double), cudaMemcpyHostToDevice, stream));
-  if (screen && reset)
-    RH_CUDA(cudaMemcpyAsync(d_reset, reset, n, cudaMemcpyHostToDevice, stream));
-  rc = launch_pass(ctx, sh, m, &dsg, &dtr, thr, 1, &dout, stream);
-  if (rc) return rc;
+  if ((rc = cp(d_hist, hist, 8 * h, H2D, stream))) return rc;
+  if (screen && reset && (rc = cp(d_reset, reset, n, H2D, stream))) return rc;
+  // chunked pipeline: chunk k+1 crosses PCIe on the copy stream while chunk k
+  // is processed (and its results copied back) on the caller's stream
+  if (!ctx->copy_stream)
+    RH_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+  const int n_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(4, n / 1024));
+  for (int k = 0; k < n_chunks; ++k)
+    if (!ctx->chunk_ev[k])
+      RH_CUDA(cudaEventCreateWithFlags(&ctx->chunk_ev[k], cudaEventDisableTiming));
+  // the copy stream must not overwrite buffers earlier work on `stream` reads
+  RH_CUDA(cudaEventRecord(ctx->chunk_ev[0], stream));
+  RH_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->chunk_ev[0], 0));
+  cudaStream_t cs = ctx->copy_stream;
+  for (int k = 0; k < n_chunks; ++k) {
+    const int64_t i0 = n * k / n_chunks, i1 = n * (k + 1) / n_chunks, ni = i1 - i0;
+    const int64_t o0 = tr->mb_off[i0 * M], o1 = tr->mb_off[i1 * M];
+    if ((rc = cp(d_seg ? d_seg + i0 : nullptr, tr->seg ? tr->seg + i0 : nullptr, 4 * ni, H2D, cs)) ||
+        (rc = cp(d_off + i0 * M, tr->mb_off + i0 * M, 4 * (ni * M + 1), H2D, cs)) ||
+        (rc = cp(d_doc + o0, tr->doc_len + o0, 4 * (o1 - o0), H2D, cs)) ||
+        (rc = cp(d_dt + i0 * G * T, tr->device_time + i0 * G * T, 4 * ni * G * T, H2D, cs)) ||
+        (rc = cp(d_obs + i0, tr->observed + i0, 8 * ni, H2D, cs)))
+      return rc;
+    RH_CUDA(cudaEventRecord(ctx->chunk_ev[k], cs));
+    RH_CUDA(cudaStreamWaitEvent(stream, ctx->chunk_ev[k], 0));
+    rh_trace ct = *tr;
+    ct.n_iter = ni;
+    ct.seg = d_seg ? d_seg + i0 : nullptr;
+    ct.mb_off = d_off + i0 * M;
+    ct.doc_len = d_doc;
+    ct.device_time = d_dt + i0 * G * T;
+    ct.observed = d_obs + i0;
+    rh_pass_out co = dout;
+    co.makespan += i0;
+    co.status += i0;
+    if (co.stage_cost) co.stage_cost += i0 * G;
+    if (co.stage_flag) co.stage_flag += i0 * G;
+    if (co.severity) co.severity += i0 * G;
+    rc = launch_pass(ctx, sh, m, &dsg, &ct, thr, 1, &co, stream);
+    if (rc) return rc;
+    if ((rc = cp(out->makespan + i0, co.makespan, 8 * ni, D2H, stream)) ||
+        (rc = cp(out->status + i0, co.status, ni, D2H, stream)) ||
+        (out->stage_cost && (rc = cp(out->stage_cost + i0 * G, co.stage_cost, 8 * ni * G, D2H, stream))) ||
+        (out->stage_flag && (rc = cp(out->stage_flag + i0 * G, co.stage_flag, ni * G, D2H, stream))) ||
+        (out->severity && (rc = cp(out->severity + i0 * G, co.severity, 4 * ni * G, D2H, stream))))
+      return rc;
+  }
   if (screen) {
-    rc = rh_screen(ctx, screen, series_len, d_hist, n, dtr.observed, dout.status,
+    rc = rh_screen(ctx, screen, series_len, d_hist, n, d_obs, dout.status,
                    reset ? d_reset : nullptr, d_outcome, d_len, stream);
     if (rc) return rc;
     if (outcome)
-      RH_CUDA(cudaMemcpyAsync(outcome, d_outcome, n, cudaMemcpyDeviceToHost, stream));
+      RH_CUDA(cudaMemcpyAsync(outcome, d_outcome, n, D2H, stream));
     if (series_len_out)
-      RH_CUDA(cudaMemcpyAsync(series_len_out, d_len, sizeof(int64_t), cudaMemcpyDeviceToHost,
-                              stream));
+      RH_CUDA(cudaMemcpyAsync(series_len_out, d_len, sizeof(int64_t), D2H, stream));
   }
-  RH_CUDA(cudaMemcpyAsync(out->makespan, dout.makespan, n * sizeof(double),
-                          cudaMemcpyDeviceToHost, stream));
-  RH_CUDA(cudaMemcpyAsync(out->status, dout.status, n, cudaMemcpyDeviceToHost, stream));
-  if (out->stage_cost)
-    RH_CUDA(cudaMemcpyAsync(out->stage_cost, dout.stage_cost, n * G * sizeof(double),
-                            cudaMemcpyDeviceToHost, stream));
-  if (out->stage_flag)
-    RH_CUDA(cudaMemcpyAsync(out->stage_flag, dout.stage_flag, n * G,
-                            cudaMemcpyDeviceToHost, stream));
-  if (out->severity)
-    RH_CUDA(cudaMemcpyAsync(out->severity, dout.severity, n * G * sizeof(float),
-                            cudaMemcpyDeviceToHost, stream));
   RH_CUDA(cudaStreamSynchronize(stream));
   return RH_OK;
 }

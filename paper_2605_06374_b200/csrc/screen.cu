@@ -416,9 +416,11 @@ extern "C" int rh_screen(rh_ctx* ctx, const rh_screen_params* params, int64_t se
   }
   const bool w20 = params->window == 20;
   void* coop = w20 ? (void*)screen_kernel<20> : (void*)screen_kernel<0>;
-  int max_blocks_per_sm = 0;
-  RH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_blocks_per_sm, coop,
-                                                        kScreenThreads, 0));
+  static int occ[2] = {-1, -1};  // cached occupancy of the two instantiations
+  int& max_blocks_per_sm = occ[w20 ? 1 : 0];
+  if (max_blocks_per_sm < 0)
+    RH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_blocks_per_sm, coop,
+                                                          kScreenThreads, 0));
   if (max_blocks_per_sm < 1) {
     set_error("rh_screen: kernel does not fit on an SM");
     return RH_E_SHAPE;

@@ -84,3 +84,46 @@ def test_screen_matches_oracle(seed, oracle, cuda_device):
                              hist=hist, reset=reset)
     np.testing.assert_array_equal(oc, ooc)
     assert ln == oln
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_detector_pass_host_chunked(seed, oracle, cuda_device):
+    """rh_detector_pass_host (host buffers, chunked H2D/compute overlap) == oracle."""
+    import ctypes as C
+
+    from paper_2605_06374_b200 import _lib
+    from paper_2605_06374_b200.tables import pipe_shape
+    from paper_2605_06374_b200.workload import cost_model_c
+    from tests.oracle_bind import HostSegments
+
+    tr = with_measurements(random_trace(300 + seed, n_iter=3000 + 517 * seed, n_seg=3,
+                                        pp=int(2 + seed * 3)), oracle, noise=0.02, seed=seed)
+    tr.reset[::700] = 1
+    segs = HostSegments(tr.known)
+    n, G = tr.n_iter, tr.cfg.dp * tr.cfg.pp
+    keep = [np.ascontiguousarray(a) for a in (tr.seg, tr.mb_off, tr.doc_len,
+                                               tr.device_time.astype(np.float32), tr.observed,
+                                               tr.reset)]
+    seg, off, doc, dt, obs, rst = keep
+    ms, st = np.zeros(n), np.zeros(n, np.uint8)
+    fl, sv = np.zeros(n * G, np.uint8), np.zeros(n * G, np.float32)
+    oc, ln = np.zeros(n, np.uint8), C.c_int64()
+    trc = _lib.Trace(n, seg.ctypes.data, off.ctypes.data, doc.ctypes.data, dt.ctypes.data,
+                     obs.ctypes.data)
+    out = _lib.PassOut(ms.ctypes.data, st.ctypes.data, None, fl.ctypes.data, sv.ctypes.data)
+    shape = pipe_shape(tr.cfg, tr.M, tr.N, has_allreduce=tr.has_allreduce, max_mb=segs.max_mb)
+    sp = _lib.ScreenParams(20, 1, 3.0)
+    lib = _lib.load_library()
+    _lib.check(lib.rh_detector_pass_host(_lib.context(), C.byref(shape),
+                                         C.byref(cost_model_c(tr.model)), C.byref(segs.c),
+                                         C.byref(trc), 1.25, C.byref(sp), 0, None,
+                                         rst.ctypes.data, C.byref(out), oc.ctypes.data,
+                                         C.byref(ln), None), "rh_detector_pass_host")
+    oms, ost, _, ofl, osv = oracle.detect(tr)
+    ooc, oln = oracle.screen(tr.observed, ost, reset=tr.reset)
+    np.testing.assert_array_equal(st, ost)
+    np.testing.assert_array_equal(_bits(ms), _bits(oms))
+    np.testing.assert_array_equal(fl, ofl.reshape(-1))
+    np.testing.assert_array_equal(sv.view(np.uint32), osv.reshape(-1).view(np.uint32))
+    np.testing.assert_array_equal(oc, ooc)
+    assert ln.value == oln
