@@ -261,6 +261,40 @@ int rh_dag_critical_path(rh_ctx* ctx, int32_t n_vertices, const double* cost,
                          int32_t capacity, double* starts, double* makespan,
                          double* chain_sum, int32_t* flags, void* stream);
 
+/* ---------------------------------------- progress-aware migration (Alg. 1) */
+/*
+ * plan_migration (scheduler.py:272-513), HOST function: the work-conserving
+ * co-simulation of one iteration with progress-aware stage-level migration
+ * (migration_decision, scheduler.py:210-251).  Micro-batch ids are 0..n_mb-1
+ * in order.  Hop weights are tables (edge_seconds evaluated by the caller):
+ *   hop_next[s][a][b] = edge(s, a, s+1, b)   hop_prev[s][a][b] = edge(s, a, s-1, b)
+ *   hop_same[s][a][b] = edge(s, a, s,   b)   ([P][D][D]; NULL = no comm)
+ * Outputs (host): migrations[k] = (mb, stage, source, executor) in decision
+ * order; start_log[c] = (replica, stage, kind 0=F 1=B/BW 2=W, mb) in start
+ * order (stage_orders); *makespan.  Returns RH_E_STRANDED with the
+ * reference's message when work is unexecutable.
+ */
+enum { RH_E_STRANDED = -5 };
+
+typedef struct rh_migration_desc {
+  int32_t pp, dp, schedule, n_mb;
+  int32_t token_budget;
+  rh_cost_model model;
+  const int32_t* mb_off;      /* [n_mb+1] CSR of packed documents   */
+  const int32_t* doc_len;
+  const int32_t* layers;      /* [pp]                               */
+  const double* speed;        /* [dp][pp]; <= 0 = stopped stage     */
+  const int32_t* dp_counts;   /* [dp] or NULL (even split)          */
+  int32_t delta, capacity, migrate;
+  const int32_t* preset;      /* [n_mb][pp] executor or -1; or NULL */
+  const double* hop_next;     /* [pp][dp][dp] or NULL               */
+  const double* hop_prev;
+  const double* hop_same;
+} rh_migration_desc;
+
+int rh_plan_migration(const rh_migration_desc* desc, int32_t* migrations, int32_t* n_migrations,
+                      int32_t* start_log, int32_t* n_started, double* makespan);
+
 /* ------------------------------------------------ Scheduler re-plan search */
 /*
  * Exhaustive re-plan search over (DP, TP, PP) layouts x layer partitions x

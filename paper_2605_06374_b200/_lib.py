@@ -15,7 +15,7 @@ from pathlib import Path
 _HERE = Path(__file__).resolve().parent
 LIB_PATH = Path(os.environ.get("RESIHP_B200_LIB", _HERE / "libresihp_b200.so"))
 
-RH_OK, RH_E_INVALID, RH_E_CUDA, RH_E_NOMEM, RH_E_SHAPE = 0, -1, -2, -3, -4
+RH_OK, RH_E_INVALID, RH_E_CUDA, RH_E_NOMEM, RH_E_SHAPE, RH_E_STRANDED = 0, -1, -2, -3, -4, -5
 
 RH_IT_ESCALATE = 1
 RH_IT_STAGE_FLAG = 2
@@ -72,6 +72,15 @@ class PassOut(C.Structure):
                 ("stage_flag", _p), ("severity", _p)]
 
 
+class MigrationDesc(C.Structure):
+    _fields_ = [("pp", C.c_int32), ("dp", C.c_int32), ("schedule", C.c_int32),
+                ("n_mb", C.c_int32), ("token_budget", C.c_int32), ("model", CostModelC),
+                ("mb_off", _p), ("doc_len", _p), ("layers", _p), ("speed", _p),
+                ("dp_counts", _p),
+                ("delta", C.c_int32), ("capacity", C.c_int32), ("migrate", C.c_int32),
+                ("preset", _p), ("hop_next", _p), ("hop_prev", _p), ("hop_same", _p)]
+
+
 class ScreenParams(C.Structure):
     _fields_ = [("window", C.c_int32), ("filter_enabled", C.c_int32), ("kappa", C.c_double)]
 
@@ -96,6 +105,8 @@ _SIGS = {
                                _p, C.POINTER(C.c_int64), _p], C.c_int),
     "rh_pack_sequences": ([C.c_int64, _p, C.c_int32, C.c_int64, _p, _p, C.POINTER(C.c_int64),
                            C.POINTER(C.c_int64)], C.c_int),
+    "rh_plan_migration": ([C.POINTER(MigrationDesc), _p, C.POINTER(C.c_int32), _p,
+                           C.POINTER(C.c_int32), C.POINTER(C.c_double)], C.c_int),
     "rh_validate": ([_p, C.c_int64, _p, _p, C.c_double, _p, _p, _p], C.c_int),
     "rh_screen": ([_p, C.POINTER(ScreenParams), C.c_int64, _p, C.c_int64, _p, _p, _p, _p, _p,
                    _p], C.c_int),

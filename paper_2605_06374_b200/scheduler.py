@@ -49,6 +49,109 @@ class AdaptationPlan:
                     or self.dp_assignment is not None or self.migrations)
 
 
+@dataclass
+class ProgressTable:
+    """scheduler.py:73-98: forward progress per (replica, stage) + delta."""
+
+    counts: list[list[int]]
+    delta: int = 0
+
+    @classmethod
+    def zeros(cls, dp: int, pp: int, delta: int = 0) -> "ProgressTable":
+        return cls(counts=[[0] * pp for _ in range(dp)], delta=delta)
+
+    def bump(self, replica: int, stage: int) -> None:
+        self.counts[replica][stage] += 1
+
+    def gap(self, stage: int) -> int:
+        col = [row[stage] for row in self.counts]
+        return max(col) - min(col)
+
+
+@dataclass
+class MigrationPlanResult:
+    migrations: list[Migration]
+    makespan: float
+    stage_orders: dict = field(default_factory=dict)
+    slots: list = field(default_factory=list)
+
+
+_KIND_NAMES = {0: "F", 2: "W"}
+
+
+def plan_migration(cfg, micro_batches, model, speeds, *, dp_counts=None, delta: int = 0,
+                   capacity: int = 8, edge_seconds=None, record_trace: bool = False,
+                   preset_executors=None, migrate: bool = True) -> MigrationPlanResult:
+    """scheduler.py:272-513 — progress-aware migration co-simulation.
+
+    Runs natively (rh_plan_migration, csrc/migration.cu).  ``edge_seconds`` is
+    evaluated into per-stage hop tables first.  ``record_trace`` slot traces
+    are a reference debugging aid and are not produced."""
+    import ctypes as C
+
+    import numpy as np
+
+    from . import _lib
+    from .cluster import SCHEDULE_1F1B
+    from .workload import cost_model_c, csr_of
+
+    P, D, M = cfg.pp, cfg.dp, len(micro_batches)
+    ids = [mb.id for mb in micro_batches]
+    if ids != sorted(ids) or len(set(ids)) != M:
+        raise ValueError("micro-batch ids must be unique and ascending in list order")
+    pos = {j: k for k, j in enumerate(ids)}
+    if len(cfg.layer_partition) != P:
+        raise ValueError("layer partition does not match stage count")
+    speed = np.array([speeds[(d, s)] for d in range(D) for s in range(P)], dtype=np.float64)
+    mb_off, doc_len = csr_of(micro_batches)
+    doc_len = doc_len if doc_len.size else np.zeros(1, np.int32)
+    layers = np.asarray(cfg.layer_partition, dtype=np.int32)
+    counts = None if dp_counts is None else np.asarray(dp_counts, dtype=np.int32)
+    preset = None
+    if preset_executors:
+        preset = np.full(M * P, -1, dtype=np.int32)
+        for (j, s), d in preset_executors.items():
+            preset[pos[j] * P + s] = d
+    tabs = [None, None, None]
+    if edge_seconds is not None:
+        nxt = np.zeros((P, D, D))
+        prv = np.zeros((P, D, D))
+        same = np.zeros((P, D, D))
+        for s in range(P):
+            for a in range(D):
+                for b in range(D):
+                    if s + 1 < P:
+                        nxt[s, a, b] = edge_seconds(s, a, s + 1, b)
+                    if s > 0:
+                        prv[s, a, b] = edge_seconds(s, a, s - 1, b)
+                    same[s, a, b] = edge_seconds(s, a, s, b)
+        tabs = [nxt, prv, same]
+    desc = _lib.MigrationDesc(
+        P, D, 0 if cfg.schedule == SCHEDULE_1F1B else 1, M, micro_batches[0].token_budget,
+        cost_model_c(model), mb_off.ctypes.data, doc_len.ctypes.data, layers.ctypes.data,
+        speed.ctypes.data,
+        None if counts is None else counts.ctypes.data, int(delta), int(capacity),
+        1 if migrate else 0, None if preset is None else preset.ctypes.data,
+        *[None if t is None else t.ctypes.data for t in tabs])
+    c = 2 if cfg.schedule == SCHEDULE_1F1B else 3
+    mig = np.zeros(4 * M * P, dtype=np.int32)
+    log = np.zeros(4 * M * P * c, dtype=np.int32)
+    n_mig, n_log, ms = C.c_int32(), C.c_int32(), C.c_double()
+    lib = _lib.load_library()
+    rc = lib.rh_plan_migration(C.byref(desc), mig.ctypes.data, C.byref(n_mig), log.ctypes.data,
+                               C.byref(n_log), C.byref(ms))
+    if rc == _lib.RH_E_STRANDED:
+        raise StrandedWorkload(lib.rh_last_error().decode())
+    _lib.check(rc, "rh_plan_migration")
+    back = "BW" if cfg.schedule == SCHEDULE_1F1B else "B"
+    migrations = [Migration(ids[a], s, src, dst) for a, s, src, dst in
+                  mig[:4 * n_mig.value].reshape(-1, 4).tolist()]
+    orders: dict = {}
+    for d, s, k, j in log[:4 * n_log.value].reshape(-1, 4).tolist():
+        orders.setdefault((d, s), []).append((_KIND_NAMES.get(k, back), ids[j]))
+    return MigrationPlanResult(migrations=migrations, makespan=ms.value, stage_orders=orders)
+
+
 def apply_plan(state, cfg, plan):
     """scheduler.py:516-540: materialise group / layer changes on copies."""
     out, new_cfg = state.copy(), cfg.copy()

@@ -454,7 +454,68 @@ def gen_search():
     dump("search", {"cases": out})
 
 
+# ----------------------------------------------------------------- migration
+def gen_migration():
+    """Reference plan_migration (scheduler.py:272-513) on random problems."""
+    rng = random.Random(6)
+    cases = []
+    while len(cases) < 80:
+        state, cfg, mbs, model, comm = random_scenario(rng, allow_fail_stop=False)
+        if cfg.dp < 2:
+            continue
+        speeds = rp._stage_speed_maps(state, cfg)[0]
+        kind = rng.random()
+        if kind < 0.3:  # a dead stage to drain
+            d0, s0 = rng.randrange(cfg.dp), rng.randrange(cfg.pp)
+            speeds[(d0, s0)] = 0.0
+        counts = None
+        if rng.random() < 0.3:
+            cuts = sorted(rng.randint(0, len(mbs)) for _ in range(cfg.dp - 1))
+            counts = [b - a for a, b in zip([0] + cuts, cuts + [len(mbs)])]
+        edge = None
+        if comm is not None:
+            links = rc.ClusterState.copy(state)
+            from resilsim.comm import LinkModel
+
+            edge = rp.edge_cost_fn(state, cfg, comm, LinkModel.from_cluster(state),
+                                   mbs[0].token_budget)
+        delta = rng.choice([0, 0, 1, 2, 10**9])
+        capacity = rng.choice([cfg.pp + 2, 8, 3])
+        migrate = rng.random() < 0.85
+        preset = {}
+        if not migrate or rng.random() < 0.2:
+            for mb in mbs[: max(1, len(mbs) // 3)]:
+                preset[(mb.id, rng.randrange(cfg.pp))] = rng.randrange(cfg.dp)
+        case = {"cfg": cfg_to_json(cfg), "mbs": mbs_to_json(mbs), "model": model_to_json(model),
+                "speeds": keyed(speeds), "counts": counts, "delta": delta, "capacity": capacity,
+                "migrate": migrate, "preset": [[j, s, d] for (j, s), d in preset.items()],
+                "edges": None}
+        if edge is not None:
+            P, D = cfg.pp, cfg.dp
+            case["edges"] = {
+                "next": [[[edge(s, a, s + 1, b) if s + 1 < P else 0.0 for b in range(D)]
+                          for a in range(D)] for s in range(P)],
+                "prev": [[[edge(s, a, s - 1, b) if s > 0 else 0.0 for b in range(D)]
+                          for a in range(D)] for s in range(P)],
+                "same": [[[edge(s, a, s, b) for b in range(D)] for a in range(D)]
+                         for s in range(P)]}
+        try:
+            res = rs.plan_migration(cfg, mbs, model, speeds, dp_counts=counts, delta=delta,
+                                    capacity=capacity, edge_seconds=edge,
+                                    preset_executors=preset or None, migrate=migrate)
+            case["result"] = {
+                "migrations": [[m.mb, m.stage, m.source, m.executor] for m in res.migrations],
+                "makespan": res.makespan,
+                "orders": [[d, s, [[k, j] for k, j in seq]]
+                           for (d, s), seq in sorted(res.stage_orders.items())]}
+        except rs.StrandedWorkload as exc:
+            case["error"] = str(exc)
+        cases.append(case)
+    dump("migration", {"cases": cases})
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["workload", "pipeline", "detector", "scheduler", "search"]
+    which = sys.argv[1:] or ["workload", "pipeline", "detector", "scheduler", "search",
+                             "migration"]
     for w in which:
         globals()[f"gen_{w}"]()

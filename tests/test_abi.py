@@ -40,6 +40,7 @@ STRUCTS = {
     "rh_trace": _lib.Trace,
     "rh_pass_out": _lib.PassOut,
     "rh_screen_params": _lib.ScreenParams,
+    "rh_migration_desc": _lib.MigrationDesc,
     "rh_search_desc": search.SearchDesc,
     "rh_candidate": search.Candidate,
 }
