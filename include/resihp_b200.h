@@ -261,6 +261,25 @@ int rh_dag_critical_path(rh_ctx* ctx, int32_t n_vertices, const double* cost,
                          int32_t capacity, double* starts, double* makespan,
                          double* chain_sum, int32_t* flags, void* stream);
 
+/* ------------------------------------------- batched scalar Scheduler rows */
+/* One thread per problem; problems are CSR slices off[i]..off[i+1] (device).
+ * repartition_layers (scheduler.py:146-207), <= 32 stages per problem;
+ *   err[i]: 0 ok, 1 non-positive speed, 2 too few layers, 3 too many stages. */
+int rh_repartition_batch(rh_ctx* ctx, int32_t n, const int32_t* off, const double* speeds,
+                         const int32_t* total_layers, const int32_t* min_layers, int32_t* out,
+                         int32_t* err, void* stream);
+/* proportional_split (policies.py:151-162), <= 64 weights per problem;
+ *   err[i]: 0 ok, 1 sum(weights) <= 0, 3 too many weights. */
+int rh_proportional_split_batch(rh_ctx* ctx, int32_t n, const int32_t* off,
+                                const double* weights, const int32_t* totals, int32_t* counts,
+                                int32_t* err, void* stream);
+/* select_tp_subgroup (scheduler.py:114-137): ranked[] = member ids by
+ * (-speed, id); best_k[i] = chosen degree (0 = GroupUnrecoverable).
+ * degree_mask bit e allows degree 2^e (candidate_tp_degrees, :101-111). */
+int rh_select_subgroup_batch(rh_ctx* ctx, int32_t n, const int32_t* off, const double* speeds,
+                             const int32_t* ids, const uint32_t* degree_mask, int32_t* ranked,
+                             int32_t* best_k, void* stream);
+
 /* ---------------------------------------- progress-aware migration (Alg. 1) */
 /*
  * plan_migration (scheduler.py:272-513), HOST function: the work-conserving

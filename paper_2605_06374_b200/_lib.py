@@ -105,6 +105,9 @@ _SIGS = {
                                _p, C.POINTER(C.c_int64), _p], C.c_int),
     "rh_pack_sequences": ([C.c_int64, _p, C.c_int32, C.c_int64, _p, _p, C.POINTER(C.c_int64),
                            C.POINTER(C.c_int64)], C.c_int),
+    "rh_repartition_batch": ([_p, C.c_int32, _p, _p, _p, _p, _p, _p, _p], C.c_int),
+    "rh_proportional_split_batch": ([_p, C.c_int32, _p, _p, _p, _p, _p, _p], C.c_int),
+    "rh_select_subgroup_batch": ([_p, C.c_int32, _p, _p, _p, _p, _p, _p, _p], C.c_int),
     "rh_plan_migration": ([C.POINTER(MigrationDesc), _p, C.POINTER(C.c_int32), _p,
                            C.POINTER(C.c_int32), C.POINTER(C.c_double)], C.c_int),
     "rh_validate": ([_p, C.c_int64, _p, _p, C.c_double, _p, _p, _p], C.c_int),

@@ -929,3 +929,123 @@ int rh_search_decode(rh_ctx* ctx, rh_search* S, int64_t index, rh_candidate* out
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Batched scalar Scheduler rows (one thread per problem): the same device
+// functions the search prep uses, exposed for the drop-in resihp_adapt.
+namespace rh {
+
+__global__ void repartition_batch_kernel(int n, const int32_t* off, const double* sp,
+                                         const int32_t* L, const int32_t* ml, int32_t* out,
+                                         int32_t* err) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int a = off[i], P = off[i + 1] - a;
+  int e = 0;
+  if (P > 32) e = 3;
+  for (int s = 0; s < P && !e; ++s)
+    if (!(sp[a + s] > 0.0)) e = 1;  // "all stage speeds must be positive"
+  if (!e && L[i] < P * ml[i]) e = 2;  // "cannot give n stages ..."
+  err[i] = e;
+  if (!e) repartition_dev(sp + a, P, L[i], ml[i], out + a);
+}
+
+__global__ void proportional_batch_kernel(int n, const int32_t* off, const double* w,
+                                          const int32_t* total, int32_t* counts, int32_t* err) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int a = off[i], D = off[i + 1] - a;
+  double wsum = 0.0;
+  for (int q = 0; q < D; ++q) wsum = __dadd_rn(wsum, w[a + q]);
+  int e = D > 64 ? 3 : (wsum <= 0.0 ? 1 : 0);  // "no capacity left to assign work to"
+  err[i] = e;
+  if (e) return;
+  int32_t start[65];
+  proportional_dev(total[i], w + a, D, start);
+  for (int q = 0; q < D; ++q) counts[a + q] = start[q + 1] - start[q];
+}
+
+// select_tp_subgroup (scheduler.py:114-137): rank by (-speed, id); for each
+// allowed power-of-two degree k (ascending) keep the first strictly better
+// k * speed_k; ties go to the smaller group.
+__global__ void subgroup_batch_kernel(int n, const int32_t* off, const double* sp,
+                                      const int32_t* ids, const uint32_t* degree_mask,
+                                      int32_t* ranked, int32_t* best_k) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int a = off[i], m = off[i + 1] - a;
+  int32_t* r = ranked + a;
+  for (int q = 0; q < m; ++q) r[q] = q;
+  for (int q = 1; q < m; ++q) {  // insertion sort by (-speed, id)
+    const int v = r[q];
+    int k = q - 1;
+    while (k >= 0 && (sp[a + r[k]] < sp[a + v] ||
+                      (sp[a + r[k]] == sp[a + v] && ids[a + r[k]] > ids[a + v]))) {
+      r[k + 1] = r[k];
+      --k;
+    }
+    r[k + 1] = v;
+  }
+  int bk = 0;
+  double bs = -1.0;
+  for (int e = 0; e < 31; ++e) {
+    if (!(degree_mask[i] >> e & 1u)) continue;
+    const int k = 1 << e;
+    if (k > m) continue;
+    const double score = __dmul_rn((double)k, sp[a + r[k - 1]]);
+    if (score > bs) {
+      bs = score;
+      bk = k;
+    }
+  }
+  for (int q = 0; q < m; ++q) r[q] = ids[a + r[q]];
+  best_k[i] = bk;  // 0: GroupUnrecoverable
+}
+
+}  // namespace rh
+
+extern "C" {
+
+int rh_repartition_batch(rh_ctx* ctx, int32_t n, const int32_t* off, const double* speeds,
+                         const int32_t* total_layers, const int32_t* min_layers, int32_t* out,
+                         int32_t* err, void* stream) {
+  if (!ctx || n < 0 || (n && (!off || !speeds || !total_layers || !min_layers || !out || !err))) {
+    set_error("rh_repartition_batch: invalid arguments");
+    return RH_E_INVALID;
+  }
+  if (!n) return RH_OK;
+  repartition_batch_kernel<<<(n + 127) / 128, 128, 0, as_stream(stream)>>>(
+      n, off, speeds, total_layers, min_layers, out, err);
+  RH_CHECK_LAUNCH(ctx);
+  return RH_OK;
+}
+
+int rh_proportional_split_batch(rh_ctx* ctx, int32_t n, const int32_t* off,
+                                const double* weights, const int32_t* totals, int32_t* counts,
+                                int32_t* err, void* stream) {
+  if (!ctx || n < 0 || (n && (!off || !weights || !totals || !counts || !err))) {
+    set_error("rh_proportional_split_batch: invalid arguments");
+    return RH_E_INVALID;
+  }
+  if (!n) return RH_OK;
+  proportional_batch_kernel<<<(n + 127) / 128, 128, 0, as_stream(stream)>>>(n, off, weights,
+                                                                           totals, counts, err);
+  RH_CHECK_LAUNCH(ctx);
+  return RH_OK;
+}
+
+int rh_select_subgroup_batch(rh_ctx* ctx, int32_t n, const int32_t* off, const double* speeds,
+                             const int32_t* ids, const uint32_t* degree_mask, int32_t* ranked,
+                             int32_t* best_k, void* stream) {
+  if (!ctx || n < 0 || (n && (!off || !speeds || !ids || !degree_mask || !ranked || !best_k))) {
+    set_error("rh_select_subgroup_batch: invalid arguments");
+    return RH_E_INVALID;
+  }
+  if (!n) return RH_OK;
+  subgroup_batch_kernel<<<(n + 127) / 128, 128, 0, as_stream(stream)>>>(n, off, speeds, ids,
+                                                                       degree_mask, ranked, best_k);
+  RH_CHECK_LAUNCH(ctx);
+  return RH_OK;
+}
+
+}  // extern "C"

@@ -9,6 +9,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
+import numpy as np
+
 from .cluster import FAIL_SLOW, FAIL_STOP, HEALTHY, STANDBY
 from .comm import LinkModel
 from .pipeline import SimulationError, simulate_iteration
@@ -198,3 +200,86 @@ def reconfig_cost(plan, state, cfg, *, layer_bytes: float, group_rebuild_s: floa
         if set(members) != set(state.tp_groups.get((d, s), ())):
             reshard += part[s] * layer_bytes
     return group_rebuild_s + (moved * layer_bytes + reshard) / LinkModel.from_cluster(state).worst_inter()
+
+
+# ------------------------------------------------ scalar rows on the GPU
+def _batch(fn_name: str, *host_arrays_and_outputs):
+    """Run one rh_*_batch kernel on host numpy arrays (copied in and out)."""
+    import torch
+
+    from . import _lib
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    tens = [torch.from_numpy(a).to(dev) if isinstance(a, np.ndarray) else a
+            for a in host_arrays_and_outputs]
+    lib = _lib.load_library()
+    args = [t.data_ptr() if hasattr(t, "data_ptr") else t for t in tens]
+    _lib.check(getattr(lib, fn_name)(_lib.context(), *args, _lib.stream_handle()), fn_name)
+    return tens
+
+
+def candidate_tp_degrees(group_size: int, fail_stop_count: int, k_min: int) -> set[int]:
+    """scheduler.py:101-111 (Eq. 3): powers of two in [k_min, survivors]."""
+    if k_min < 1 or (k_min & (k_min - 1)) != 0:
+        raise ValueError("k_min must be a power of two >= 1")
+    out, k = set(), k_min
+    while k <= group_size - fail_stop_count:
+        out.add(k)
+        k *= 2
+    return out
+
+
+def select_tp_subgroup(device_speeds: dict, degrees: set[int]):
+    """scheduler.py:114-137 (Eq. 4) via rh_select_subgroup_batch."""
+    import torch
+
+    if not degrees:
+        raise GroupUnrecoverable("no feasible TP degree")
+    ids = np.array(list(device_speeds), dtype=np.int32)
+    sp = np.array([device_speeds[i] for i in ids], dtype=np.float64)
+    mask = 0
+    for k in degrees:
+        if k >= 1 and (k & (k - 1)) == 0 and k < 2**31:
+            mask |= 1 << (k.bit_length() - 1)
+    n = len(ids)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    ranked = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    best = torch.empty(1, dtype=torch.int32, device=dev)
+    _batch("rh_select_subgroup_batch", 1, np.array([0, n], np.int32),
+           sp if n else np.zeros(1), ids if n else np.zeros(1, np.int32),
+           np.array([mask], np.uint32), ranked, best)
+    k = int(best.item())
+    if k == 0:
+        raise GroupUnrecoverable("group smaller than every candidate degree")
+    order = ranked.cpu().numpy()[:n].tolist()
+    return tuple(sorted(order[:k])), tuple(sorted(order[k:]))
+
+
+def subgroup_score(device_speeds: dict, members) -> float:
+    """scheduler.py:140-143: |members| * slowest member."""
+    if not members:
+        return 0.0
+    return len(members) * min(device_speeds[d] for d in members)
+
+
+def repartition_layers(stage_speeds: list[float], total_layers: int,
+                       min_layers: int = 1) -> list[int]:
+    """scheduler.py:146-207 via rh_repartition_batch."""
+    import torch
+
+    n = len(stage_speeds)
+    if any(s <= 0 for s in stage_speeds):
+        raise ValueError("all stage speeds must be positive")
+    if total_layers < n * min_layers:
+        raise ValueError(f"cannot give {n} stages {min_layers} layers each out of {total_layers}")
+    if n > 32:
+        raise ValueError("repartition_layers: at most 32 stages on this path")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    out = torch.empty(n, dtype=torch.int32, device=dev)
+    err = torch.empty(1, dtype=torch.int32, device=dev)
+    _batch("rh_repartition_batch", 1, np.array([0, n], np.int32),
+           np.asarray(stage_speeds, np.float64), np.array([total_layers], np.int32),
+           np.array([min_layers], np.int32), out, err)
+    if int(err.item()):
+        raise ValueError("repartition_layers: infeasible problem")
+    return [int(x) for x in out.cpu().numpy()]

@@ -514,8 +514,69 @@ def gen_migration():
     dump("migration", {"cases": cases})
 
 
+# ----------------------------------------------------------------- policies
+def gen_policies():
+    """Reference resihp_adapt (policies.py:189-352) decisions on random contexts."""
+    rng = random.Random(8)
+    cases = []
+    while len(cases) < 40:
+        tp = rng.choice([2, 4])
+        dp = rng.choice([1, 2, 3])
+        pp = rng.choice([2, 3, 4])
+        layers = pp * rng.randint(2, 4)
+        cfg = rc.ParallelismConfig(tp=tp, dp=dp, pp=pp,
+                                   schedule=rng.choice(["1f1b", "zbh"]),
+                                   layer_partition=[layers // pp] * pp)
+        n_dev = tp * dp * pp
+        nodes = max(1, -(-n_dev // 8)) + rng.choice([0, 0, 1])
+        state = rc.build_cluster(nodes, 8, cfg, 300.0 * 2**30, 25.0 * 2**30)
+        events, known, new_stop = [], {}, []
+        for _ in range(rng.randint(1, 3)):
+            dev = rng.randrange(n_dev)
+            if rng.random() < 0.35:
+                events.append(rc.FailureEvent(kind="fail_stop", start=0.0, device=dev))
+                new_stop.append("stop")
+            else:
+                sev = rng.choice([0.2, 0.4, 0.5, 0.7])
+                events.append(rc.FailureEvent(kind="fail_slow_compute", start=0.0, device=dev,
+                                              severity=sev))
+                known[dev] = sev
+        state = rc.apply_failures(state, events, 0.0)
+        M = dp * rng.randint(2, 6)
+        docs = [max(1, min(4096, int(rng.lognormvariate(7.2, 0.8)))) for _ in range(M * 6)]
+        mbs = rw.pack_sequences(docs, 4096)[:M]
+        if len(mbs) < M:
+            continue
+        confirmed = None
+        slow_keys = sorted({k for k, g in state.tp_groups.items() if any(d in known for d in g)})
+        if slow_keys:
+            confirmed = rd.ValidationResult(True, {k: 0.5 for k in slow_keys}, {}, 3.0)
+        ctx = rpol.PlanningContext(state=state, cfg=cfg, model=rw.CostModel(2e-6, 5e-10),
+                                   micro_batches=mbs, comm=CommSpec(), known_speeds=known,
+                                   new_fail_stop=new_stop, confirmed=confirmed,
+                                   delta=rng.choice([0, 1]), capacity=pp + 2)
+        case = {"nodes": nodes, "cfg": cfg_to_json(cfg),
+                "events": [[e.kind, e.device, e.severity] for e in events],
+                "known": [[k, v] for k, v in known.items()], "mbs": mbs_to_json(mbs),
+                "confirmed": [list(k) for k in slow_keys], "new_fail_stop": len(new_stop),
+                "delta": ctx.delta, "capacity": ctx.capacity}
+        try:
+            plan = rpol.resihp_adapt(ctx)
+            case["plan"] = {
+                "tp_subgroups": [[d, s, list(m), list(sb)]
+                                 for (d, s), (m, sb) in sorted(plan.tp_subgroups.items())],
+                "excluded": [list(k) for k in plan.excluded_groups],
+                "layer_partition": plan.layer_partition, "dp_assignment": plan.dp_assignment,
+                "migrations": [[m.mb, m.stage, m.source, m.executor] for m in plan.migrations],
+                "predicted": plan.predicted_makespan_s}
+        except (rs.StrandedWorkload, rs.GroupUnrecoverable) as exc:
+            case["error"] = type(exc).__name__
+        cases.append(case)
+    dump("policies", {"cases": cases})
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["workload", "pipeline", "detector", "scheduler", "search",
-                             "migration"]
+                             "migration", "policies"]
     for w in which:
         globals()[f"gen_{w}"]()
