@@ -113,7 +113,13 @@ def dist_init():
         import torch.distributed as dist
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl" if os.environ.get("RESIHP_BACKEND") != "gloo" else "gloo")
+        if os.environ.get("RESIHP_BACKEND") == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            import torch
+
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return world, rank, local
 
 
@@ -271,7 +277,9 @@ def run_ours(args, world, rank, local):
                 "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"]},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "pass_kernel<1F1B,detect>", "algorithmic_bytes": nbytes,
+                     "kernel": ("pass_small_kernel<P=%d,1F1B,detect>" % tr.cfg.pp
+                                if tr.cfg.pp <= 4 else "pass_kernel<1F1B,detect>"),
+                     "algorithmic_bytes": nbytes,
                      "kernel_ms": det_avg, "peak_source": peak_src},
         "breakdown_ms": {"detect": det_avg, "screen": sum(scr_ms) / len(scr_ms)},
         "gpu_launches": int(launches),
@@ -430,7 +438,7 @@ def search_cpu_baseline(inputs, size, budget_s=4.0):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
