@@ -11,21 +11,36 @@
 // B200 formulation: the pop decision of iteration i is a pure function of
 // the kept-set of earlier iterations.  We solve the triangular system
 //     kept[i] = f_i(kept[0..i-1])
-// by Jacobi iteration on the whole grid: start from kept = all, recompute
-// every decision in parallel from the current kept-set (prefix sums +
-// compaction give each iteration its window in O(window)), repeat until no
-// decision changes.  The fixpoint of this system is unique and equal to the
+// by Jacobi iteration on the whole GPU: start from kept = all, recompute
+// every decision in parallel from the previous round's kept-set, repeat
+// until no decision changes.  The fixpoint is unique and equal to the
 // sequential answer (induction on i); each round fixes at least one more
 // leading decision, so it terminates, and in practice pops are sparse and it
-// converges in 2-3 rounds.  One cooperative launch; rounds are separated by
-// a grid barrier (the blocks are co-resident by construction).
+// converges in 3 rounds.
+//
+// One persistent cooperative launch, one grid barrier per round.  Per round
+// and iteration, one warp
+//   * scans the previous round's state bytes (bit 0 = popped, bit 1 =
+//     changed in that round) backwards from i, 32 at a time with ballots,
+//     until it has found the last `window` kept entries or reached the reset;
+//     the kept lanes drop their observation straight into the warp's window
+//     slots in shared memory, so no global prefix sum / compaction exists;
+//   * skips the decision when no change lies inside that window span (or,
+//     while the series is short, since the reset): it cannot differ;
+//   * otherwise sorts the window across lanes (two 32-lane bitonic sorts on
+//     shuffles -> median and MAD) and applies the filter / validation bits.
+// The kept-state is double-buffered, so every round reads one consistent
+// kept-set (pure Jacobi) while writing the next.
 #include <algorithm>
 
 #include "common.cuh"
 
 namespace rh {
 
-constexpr int kScreenThreads = 128;
+constexpr int kScanThreads = 128;  // reset_scan_kernel block (= bres granularity)
+constexpr int kScreenThreads = 512;
+constexpr int kScreenWarps = kScreenThreads / 32;
+constexpr int kScreenBlocksPerSm = 2;
 constexpr int kMaxWindow = 64;
 
 struct ScreenArgs {
@@ -42,16 +57,12 @@ struct ScreenArgs {
   uint8_t* outcome;
   int64_t* len_out;
   // scratch
-  int32_t* R;        // [n] last reset index <= i, or -1
-  int32_t* Pk;       // [n+1] exclusive count of kept before i
-  int32_t* Cc;       // [n+1] exclusive count of changed decisions before i
-  int32_t* Kidx;     // [n] compacted position -> iteration index
-  double* Vk;        // [n] compacted kept observations
-  uint8_t* pop;      // [n] current pop decisions
-  uint8_t* chg;      // [n] decision changed in the last round
-  int32_t* bsum;     // [2*blocks] per-block (kept, changed)
-  int32_t* bres;     // [blocks] last reset in block chunk
-  unsigned* bar;     // [2] barrier count, generation
+  int32_t* R;                      // [n] last reset index <= i, or -1
+  int32_t* bres;                   // [n/128] last reset inside each scan block
+  uint8_t* state;                  // [2][n] bit0 popped, bit1 changed in that round
+  unsigned* cnt;                   // [3] changes per round (rotating)
+  unsigned* bar;                   // [2] barrier count, generation
+  unsigned long long* kept_total;  // [2] kept count, block ticket
 };
 
 __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
@@ -73,40 +84,6 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
   __syncthreads();
 }
 
-// exclusive block scan of two ints per thread; returns the block totals
-__device__ int2 block_exclusive_scan2(int2 v, int2* out_excl, int2* smem) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  int2 x = v;
-  for (int o = 1; o < 32; o <<= 1) {
-    const int a = __shfl_up_sync(0xffffffffu, x.x, o);
-    const int b = __shfl_up_sync(0xffffffffu, x.y, o);
-    if (lane >= o) {
-      x.x += a;
-      x.y += b;
-    }
-  }
-  if (lane == 31) smem[wid] = x;
-  __syncthreads();
-  if (wid == 0) {
-    int2 t = lane < (int)(blockDim.x >> 5) ? smem[lane] : make_int2(0, 0);
-    for (int o = 1; o < 32; o <<= 1) {
-      const int a = __shfl_up_sync(0xffffffffu, t.x, o);
-      const int b = __shfl_up_sync(0xffffffffu, t.y, o);
-      if (lane >= o) {
-        t.x += a;
-        t.y += b;
-      }
-    }
-    smem[lane] = t;  // inclusive warp totals
-  }
-  __syncthreads();
-  const int2 off = wid ? smem[wid - 1] : make_int2(0, 0);
-  *out_excl = make_int2(off.x + x.x - v.x, off.y + x.y - v.y);
-  const int2 total = smem[(blockDim.x >> 5) - 1];
-  __syncthreads();
-  return total;
-}
-
 __device__ __forceinline__ void sort_small(double* a, int n) {
   for (int i = 1; i < n; ++i) {
     const double v = a[i];
@@ -124,48 +101,11 @@ __device__ __forceinline__ double median_sorted(const double* a, int n) {
   return (n & 1) ? a[n >> 1] : __ddiv_rn(__dadd_rn(a[(n >> 1) - 1], a[n >> 1]), 2.0);
 }
 
-// odd-even transposition sort, fully unrolled: the array stays in registers
-template <int W>
-__device__ __forceinline__ void sort_net(double (&a)[W]) {
-#pragma unroll
-  for (int r = 0; r < W; ++r) {
-#pragma unroll
-    for (int i = r & 1; i + 1 < W; i += 2) {
-      const double lo = fmin(a[i], a[i + 1]);
-      const double hi = fmax(a[i], a[i + 1]);
-      a[i] = lo;
-      a[i + 1] = hi;
-    }
-  }
-}
-
-template <int W>
-__device__ __forceinline__ double median_net(const double (&a)[W]) {
-  if (W & 1) return a[W >> 1];
-  return __ddiv_rn(__dadd_rn(a[(W >> 1) - 1], a[W >> 1]), 2.0);
-}
-
-// |x - median| > kappa * MAD over a window (statistics.median semantics)
-template <int W>
-__device__ __forceinline__ bool outlier_fixed(const double* win_src, bool cg, double x,
-                                              double kappa) {
-  double v[W], d[W];
-#pragma unroll
-  for (int q = 0; q < W; ++q) v[q] = cg ? __ldcg(win_src + q) : win_src[q];
-#pragma unroll
-  for (int q = 0; q < W; ++q) d[q] = v[q];
-  sort_net<W>(d);
-  const double med = median_net<W>(d);
-#pragma unroll
-  for (int q = 0; q < W; ++q) d[q] = fabs(__dsub_rn(v[q], med));
-  sort_net<W>(d);
-  const double mad = median_net<W>(d);
-  return fabs(__dsub_rn(x, med)) > __dmul_rn(kappa, mad);
-}
-
-__device__ __noinline__ bool outlier_generic(const double* win, int w, double x, double kappa) {
-  double dev[kMaxWindow];
-  for (int q = 0; q < w; ++q) dev[q] = win[q];
+// windows wider than a warp: lane 0 alone, insertion sorts in local memory
+__device__ __noinline__ bool outlier_generic(const double* win_smem, int w, double x,
+                                             double kappa) {
+  double win[kMaxWindow], dev[kMaxWindow];
+  for (int q = 0; q < w; ++q) dev[q] = win[q] = win_smem[q];
   sort_small(dev, w);
   const double med = median_sorted(dev, w);
   for (int q = 0; q < w; ++q) dev[q] = fabs(__dsub_rn(win[q], med));
@@ -174,51 +114,117 @@ __device__ __noinline__ bool outlier_generic(const double* win, int w, double x,
   return fabs(__dsub_rn(x, med)) > __dmul_rn(kappa, mad);
 }
 
-// Pop decision + outcome bits of iteration i under the current kept-set.
-// identity: every earlier iteration is kept (round 0: positions == indices).
-// Returns false (and leaves outputs alone) when the iteration is provably
-// unaffected by the last round's changes.
-template <int WF>
-__device__ bool decide(const ScreenArgs& a, int64_t i, bool identity, uint8_t& oc_out,
-                       bool& pop) {
-  const int w = WF > 0 ? WF : a.w;
-  const int32_t r = a.R[i];
-  const int64_t pb = identity ? i : __ldcg(a.Pk + i);
-  const int64_t base = r >= 0 ? (identity ? r : __ldcg(a.Pk + r)) : 0;
-  const int64_t nk = pb - base;
-  if (!identity) {
-    // only changes inside the window span -- or, while the series is short,
-    // anywhere since the reset (length thresholds) -- can alter the decision
-    const int64_t first = r >= 0 ? r : 0;
-    const int32_t ci = __ldcg(a.Cc + i);
-    const int32_t c_all = ci - __ldcg(a.Cc + first);
-    if (c_all == 0) return false;
-    if (nk - c_all >= w + 2) {
-      const int64_t lb = __ldcg(a.Kidx + (pb - w));
-      if (ci - __ldcg(a.Cc + lb) == 0) return false;
+// ascending bitonic sort of one value per lane (32 values, pads = +inf)
+__device__ __forceinline__ double warp_sort(double v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const double o = __shfl_xor_sync(0xffffffffu, v, j);
+      const bool take_min = ((lane & j) == 0) == ((lane & k) == 0);
+      v = (take_min == (o < v)) ? o : v;
     }
   }
-  const int64_t len = (r >= 0 ? nk : a.len0 + nk) + 1;
+  return v;
+}
+
+// statistics.median of w sorted lane values (lanes 0..w-1)
+__device__ __forceinline__ double warp_median(double s, int w) {
+  const double hi = __shfl_sync(0xffffffffu, s, w >> 1);
+  const double lo = __shfl_sync(0xffffffffu, s, w > 1 ? (w >> 1) - 1 : 0);
+  return (w & 1) ? hi : __ddiv_rn(__dadd_rn(lo, hi), 2.0);
+}
+
+// last reset index <= i: block-local inclusive max-scan, one element per
+// thread; block summaries land in bres and are folded in by screen_kernel
+__global__ void __launch_bounds__(kScanThreads) reset_scan_kernel(ScreenArgs a) {
+  __shared__ int sm[32];
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int x = (i < a.n && a.reset[i]) ? (int)i : -1;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x = max(x, y);
+  }
+  if (lane == 31) sm[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    int t = lane < (int)(blockDim.x >> 5) ? sm[lane] : -1;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t = max(t, y);
+    }
+    sm[lane] = t;
+  }
+  __syncthreads();
+  if (wid) x = max(x, sm[wid - 1]);
+  if (i < a.n) a.R[i] = x;
+  if (threadIdx.x == 0) a.bres[blockIdx.x] = sm[(blockDim.x >> 5) - 1];
+}
+
+// One Jacobi step for iteration i, executed by a whole warp (uniform result).
+// Returns the new pop bit, or kUnchanged when no change of the previous round
+// lies where it could reach iteration i.
+constexpr unsigned kUnchanged = 0xffu;
+
+__device__ __forceinline__ unsigned step_warp(const ScreenArgs& a, int64_t i, int r,
+                                              const uint8_t* cur, bool first_round,
+                                              double* win) {
+  const int lane = threadIdx.x & 31;
+  const int w = a.w;
+  const int64_t first = r >= 0 ? r : 0;
+  // backward scan for the last w kept entries in [first, i)
+  int found = 0;
+  bool any_chg = first_round;
+  for (int64_t hi = i; hi > first && found < w; hi -= 32) {
+    const int64_t j = hi - 32 + lane;
+    const bool in = j >= first;
+    const unsigned sv = in ? (first_round ? 0u : (unsigned)__ldcg(cur + j)) : 1u;
+    const bool kept = !(sv & 1u);
+    const unsigned km = __ballot_sync(0xffffffffu, kept);
+    const unsigned cm = __ballot_sync(0xffffffffu, (sv & 2u) != 0u);
+    // rank of this lane's kept entry counted from i downwards (0 = newest)
+    const int rank = found + __popc(km >> lane) - 1;
+    if (kept && rank < w) win[w - 1 - rank] = a.obs[j];
+    const int cnt = __popc(km);
+    if (found + cnt >= w) {
+      // the window starts at the kept lane of rank w-1: changes below it
+      // cannot reach iteration i
+      const int pos = __ffs(__ballot_sync(0xffffffffu, kept && rank == w - 1)) - 1;
+      any_chg |= (cm >> pos) != 0u;
+      found = w;
+    } else {
+      found += cnt;
+      any_chg |= cm != 0u;
+    }
+  }
+  __syncwarp();
+  if (!any_chg) return kUnchanged;
+  // kept entries since the reset: exact below w, which is all the length
+  // thresholds need
+  const int64_t len = (r >= 0 ? found : a.len0 + found) + 1;
   const double x = a.obs[i];
-  const double* V = identity ? a.obs : a.Vk;
   bool cand = false;
   if (len >= w + 1) {
-    if (nk >= w && WF > 0) {
-      cand = outlier_fixed<(WF > 0 ? WF : 1)>(V + (pb - w), !identity, x, a.kappa);
+    const int need = w - found;  // > 0 only without a reset: history entries
+    if (w <= 32) {
+      double v = __longlong_as_double(0x7ff0000000000000LL);  // +inf pad
+      if (lane < w) v = lane < need ? a.hist[a.h - need + lane] : win[lane];
+      const double med = warp_median(warp_sort(v), w);
+      const double d = lane < w ? fabs(__dsub_rn(v, med)) : v;
+      const double mad = warp_median(warp_sort(d), w);
+      cand = fabs(__dsub_rn(x, med)) > __dmul_rn(a.kappa, mad);
     } else {
-      double win[kMaxWindow];
+      for (int q = lane; q < need; q += 32) win[q] = a.hist[a.h - need + q];
+      __syncwarp();
       int c = 0;
-      if (nk < w) {  // only without a reset: the window starts in the history
-        for (int q = a.h - (w - (int)nk); q < a.h; ++q) win[c++] = a.hist[q];
-        for (int64_t q = base; q < pb; ++q) win[c++] = identity ? V[q] : __ldcg(V + q);
-      } else {
-        for (int64_t q = pb - w; q < pb; ++q) win[c++] = identity ? V[q] : __ldcg(V + q);
-      }
-      cand = outlier_generic(win, w, x, a.kappa);
+      if (lane == 0) c = outlier_generic(win, w, x, a.kappa);
+      cand = __shfl_sync(0xffffffffu, c, 0) != 0;
     }
   }
   const bool refill = !cand && a.fe && len <= w;
-  pop = false;
+  bool pop = false;
   uint8_t oc = 0;
   if (cand || refill) {
     oc = cand ? RH_SC_CANDIDATE : 0;
@@ -244,148 +250,75 @@ __device__ bool decide(const ScreenArgs& a, int64_t i, bool identity, uint8_t& o
       }
     }
   }
-  oc_out = oc;
-  return true;
+  if (lane == 0) a.outcome[i] = oc;
+  __syncwarp();  // the window slots are reused by the warp's next iteration
+  return pop ? 1u : 0u;
 }
 
-// last reset index <= i: block-local inclusive max-scan, one element per
-// thread; block summaries land in bres and are folded in by round0_kernel
-__global__ void __launch_bounds__(kScreenThreads) reset_scan_kernel(ScreenArgs a) {
-  __shared__ int sm[32];
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  int x = (i < a.n && a.reset && a.reset[i]) ? (int)i : -1;
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x = max(x, y);
-  }
-  if (lane == 31) sm[wid] = x;
-  __syncthreads();
-  if (wid == 0) {
-    int t = lane < (int)(blockDim.x >> 5) ? sm[lane] : -1;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, t, o);
-      if (lane >= o) t = max(t, y);
-    }
-    sm[lane] = t;
-  }
-  __syncthreads();
-  if (wid) x = max(x, sm[wid - 1]);
-  if (i < a.n) a.R[i] = x;
-  if (threadIdx.x == 0) a.bres[blockIdx.x] = sm[(blockDim.x >> 5) - 1];
-}
-
-// round 0 on every SM: each iteration decided as if all earlier were kept
-template <int WF>
-__global__ void __launch_bounds__(kScreenThreads) round0_kernel(ScreenArgs a) {
-  __shared__ int s_prev;
-  if (threadIdx.x < 32) {
-    int m = -1;
-    for (unsigned b = threadIdx.x; b < blockIdx.x; b += 32) m = max(m, a.bres[b]);
-    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (threadIdx.x == 0) s_prev = m;
-  }
-  __syncthreads();
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= a.n) return;
-  if (a.R[i] < s_prev) a.R[i] = s_prev;
-  uint8_t oc;
-  bool p;
-  decide<WF>(a, i, true, oc, p);
-  a.outcome[i] = oc;
-  a.pop[i] = p;
-  a.chg[i] = p;
-}
-
-template <int WF>
 __global__ void __launch_bounds__(kScreenThreads) screen_kernel(const ScreenArgs a) {
-  __shared__ int2 sm2[32];
-  __shared__ int s_pref_k, s_pref_c, s_total_c;
-  const unsigned nb = gridDim.x;
-  const int64_t per_block = (a.n + nb - 1) / nb;
-  const int64_t b0 = (int64_t)blockIdx.x * per_block;
-  const int64_t b1 = min(a.n, b0 + per_block);
-  const int64_t per_thread = (per_block + blockDim.x - 1) / blockDim.x;
-  const int64_t t0 = min(b1, b0 + (int64_t)threadIdx.x * per_thread);
-  const int64_t t1 = min(b1, t0 + per_thread);
+  __shared__ double s_win[kScreenWarps][kMaxWindow];
+  __shared__ unsigned s_cnt;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t gw = (int64_t)blockIdx.x * kScreenWarps + wid;
+  const int64_t n_warps = (int64_t)gridDim.x * kScreenWarps;
+  double* win = s_win[wid];
 
-  for (int64_t round = 1; round <= a.n + 2; ++round) {
-    // ---- phase A: kept / changed counts
-    int2 cnt = make_int2(0, 0);
-    for (int64_t i = t0; i < t1; ++i) {
-      cnt.x += a.pop[i] ? 0 : 1;
-      cnt.y += a.chg[i];
-    }
-    int2 excl;
-    const int2 tot = block_exclusive_scan2(cnt, &excl, sm2);
-    if (threadIdx.x == 0) {
-      a.bsum[2 * blockIdx.x] = tot.x;
-      a.bsum[2 * blockIdx.x + 1] = tot.y;
-    }
-    grid_barrier(a.bar, nb);
-    // ---- phase B: global prefixes + compaction
-    if (wid == 0) {
-      int pk = 0, pc = 0, tc = 0;
-      for (unsigned b = lane; b < nb; b += 32) {
-        const int k = __ldcg(a.bsum + 2 * b), c = __ldcg(a.bsum + 2 * b + 1);
-        if (b < blockIdx.x) {
-          pk += k;
-          pc += c;
-        }
-        tc += c;
-      }
-      for (int o = 16; o > 0; o >>= 1) {
-        pk += __shfl_xor_sync(0xffffffffu, pk, o);
-        pc += __shfl_xor_sync(0xffffffffu, pc, o);
-        tc += __shfl_xor_sync(0xffffffffu, tc, o);
-      }
-      if (lane == 0) {
-        s_pref_k = pk;
-        s_pref_c = pc;
-        s_total_c = tc;
-      }
-    }
+  int round = 0;
+  for (;; ++round) {
+    const uint8_t* cur = a.state + (size_t)(round & 1) * a.n;
+    uint8_t* nxt = a.state + (size_t)((round + 1) & 1) * a.n;
+    if (threadIdx.x == 0) s_cnt = 0;
     __syncthreads();
-    {
-      int64_t pos = (int64_t)s_pref_k + excl.x;
-      int32_t cc = s_pref_c + excl.y;
-      for (int64_t i = t0; i < t1; ++i) {
-        a.Pk[i] = (int32_t)pos;
-        a.Cc[i] = cc;
-        cc += a.chg[i];
-        if (!a.pop[i]) {
-          a.Vk[pos] = a.obs[i];
-          a.Kidx[pos] = (int32_t)i;
-          ++pos;
+    unsigned changes = 0;
+    for (int64_t i = gw; i < a.n; i += n_warps) {
+      int r;
+      if (round == 0) {  // fold in the resets of earlier scan blocks, once
+        r = a.R[i];
+        if (r < 0 && a.reset) {
+          const int nb = (int)(i / kScanThreads);
+          for (int b = lane; b < nb; b += 32) r = max(r, a.bres[b]);
+          for (int o = 16; o > 0; o >>= 1) r = max(r, __shfl_xor_sync(0xffffffffu, r, o));
         }
+        __syncwarp();
+        if (lane == 0) a.R[i] = r;
+      } else {
+        r = __ldcg(a.R + i);
       }
-      if (t1 == a.n && t1 > t0) {
-        a.Pk[a.n] = (int32_t)pos;
-        a.Cc[a.n] = cc;
-      }
+      const unsigned old = round == 0 ? 0u : (__ldcg(cur + i) & 1u);
+      unsigned pop = step_warp(a, i, r, cur, round == 0, win);
+      if (pop == kUnchanged) pop = old;
+      const unsigned changed = pop != old;
+      if (lane == 0) nxt[i] = (uint8_t)(pop | (changed << 1));
+      changes += changed;
     }
-    if (s_total_c == 0) break;  // fixpoint: the last round changed nothing
-    grid_barrier(a.bar, nb);
-    // ---- phase C: re-decide the iterations the changes can reach
-    for (int64_t i = t0; i < t1; ++i) {
-      uint8_t oc;
-      bool p;
-      uint8_t changed = 0;
-      if (decide<WF>(a, i, false, oc, p)) {
-        a.outcome[i] = oc;
-        changed = (uint8_t)p != a.pop[i];
-        a.pop[i] = p;
-      }
-      a.chg[i] = changed;
-    }
+    if (lane == 0 && changes) atomicAdd(&s_cnt, changes);
+    // the next round's counter was last read before this round began
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.cnt[(round + 1) % 3] = 0;
+    __syncthreads();
+    if (threadIdx.x == 0 && s_cnt) atomicAdd(a.cnt + round % 3, s_cnt);
+    grid_barrier(a.bar, gridDim.x);
+    if (__ldcg(a.cnt + round % 3) == 0) break;  // fixpoint: nothing changed
   }
-  // final series length (Pk reflects the fixpoint decisions)
-  if (a.len_out && t1 == a.n && t1 > t0) {
-    const int64_t last = a.n - 1;
-    const int32_t r = a.R[last];
-    const int64_t kept_total = a.Pk[last] + (a.pop[last] ? 0 : 1);
-    *a.len_out = r >= 0 ? kept_total - __ldcg(a.Pk + r) : a.len0 + kept_total;
+  // final series length: kept entries since the last reset (+ history)
+  if (a.len_out) {
+    const int32_t r_last = __ldcg(a.R + (a.n - 1));
+    const int64_t first = r_last >= 0 ? r_last : 0;
+    const uint8_t* fin = a.state + (size_t)((round + 1) & 1) * a.n;  // written last
+    unsigned long long k = 0;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (int64_t i = first + tid; i < a.n; i += (int64_t)gridDim.x * blockDim.x)
+      k += (__ldcg(fin + i) & 1u) ? 0 : 1;
+    for (int o = 16; o > 0; o >>= 1) k += __shfl_xor_sync(0xffffffffu, k, o);
+    if (lane == 0 && k) atomicAdd(a.kept_total, k);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned long long ticket = atomicAdd(a.kept_total + 1, 1ull);
+      if (ticket == gridDim.x - 1) {
+        const unsigned long long total = atomicAdd(a.kept_total, 0ull);
+        *a.len_out = r_last >= 0 ? (int64_t)total : a.len0 + (int64_t)total;
+      }
+    }
   }
 }
 
@@ -414,31 +347,31 @@ extern "C" int rh_screen(rh_ctx* ctx, const rh_screen_params* params, int64_t se
                               cudaMemcpyHostToDevice, st));
     return RH_OK;
   }
-  const bool w20 = params->window == 20;
-  void* coop = w20 ? (void*)screen_kernel<20> : (void*)screen_kernel<0>;
-  static int occ[2] = {-1, -1};  // cached occupancy of the two instantiations
-  int& max_blocks_per_sm = occ[w20 ? 1 : 0];
-  if (max_blocks_per_sm < 0)
-    RH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_blocks_per_sm, coop,
+  static int occ = -1;  // cached occupancy of the cooperative kernel
+  if (occ < 0)
+    RH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (void*)screen_kernel,
                                                           kScreenThreads, 0));
-  if (max_blocks_per_sm < 1) {
+  if (occ < 1) {
     set_error("rh_screen: kernel does not fit on an SM");
     return RH_E_SHAPE;
   }
-  int blocks = ctx->num_sms;  // one co-resident CTA per SM (cooperative launch)
-  const int64_t grid0 = (n + kScreenThreads - 1) / kScreenThreads;
-  if (grid0 < blocks) blocks = (int)std::max<int64_t>(1, grid0);
+  // co-resident CTAs (cooperative launch), about one warp per 2 iterations
+  int blocks = ctx->num_sms * std::min(occ, kScreenBlocksPerSm);
+  blocks = (int)std::max<int64_t>(
+      1, std::min<int64_t>(blocks, (n + 2 * kScreenWarps - 1) / (2 * kScreenWarps)));
+  const int64_t grid0 = (n + kScanThreads - 1) / kScanThreads;
   size_t bytes = 0;
   auto take = [&](size_t n_bytes) {
     const size_t o = bytes;
     bytes = (bytes + n_bytes + 255) & ~size_t(255);
     return o;
   };
-  const size_t oR = take(sizeof(int32_t) * n), oP = take(sizeof(int32_t) * (n + 1));
-  const size_t oC = take(sizeof(int32_t) * (n + 1)), oK = take(sizeof(int32_t) * n);
-  const size_t oV = take(sizeof(double) * n), oPop = take(n), oChg = take(n);
-  const size_t oB = take(sizeof(int32_t) * blocks * 2);
-  const size_t oRes = take(sizeof(int32_t) * grid0), oBar = take(sizeof(unsigned) * 2);
+  // the control words first: one memset clears them all
+  const size_t oBar = take(sizeof(unsigned) * 2), oCnt = take(sizeof(unsigned) * 3);
+  const size_t oKept = take(sizeof(unsigned long long) * 2);
+  const size_t ctrl = bytes;
+  const size_t oR = take(sizeof(int32_t) * n), oRes = take(sizeof(int32_t) * grid0);
+  const size_t oSt = take(2 * (size_t)n);
   void* ws = nullptr;
   int rc = workspace(ctx, bytes, &ws, 1);
   if (rc) return rc;
@@ -456,26 +389,22 @@ extern "C" int rh_screen(rh_ctx* ctx, const rh_screen_params* params, int64_t se
   a.reset = reset;
   a.outcome = outcome;
   a.len_out = series_len_out;
-  a.R = reinterpret_cast<int32_t*>(base + oR);
-  a.Pk = reinterpret_cast<int32_t*>(base + oP);
-  a.Cc = reinterpret_cast<int32_t*>(base + oC);
-  a.Kidx = reinterpret_cast<int32_t*>(base + oK);
-  a.Vk = reinterpret_cast<double*>(base + oV);
-  a.pop = reinterpret_cast<uint8_t*>(base + oPop);
-  a.chg = reinterpret_cast<uint8_t*>(base + oChg);
-  a.bsum = reinterpret_cast<int32_t*>(base + oB);
-  a.bres = reinterpret_cast<int32_t*>(base + oRes);
   a.bar = reinterpret_cast<unsigned*>(base + oBar);
-  RH_CUDA(cudaMemsetAsync(a.bar, 0, sizeof(unsigned) * 2, st));
-  reset_scan_kernel<<<(unsigned)grid0, kScreenThreads, 0, st>>>(a);
-  RH_CHECK_LAUNCH(ctx);
-  if (w20)
-    round0_kernel<20><<<(unsigned)grid0, kScreenThreads, 0, st>>>(a);
-  else
-    round0_kernel<0><<<(unsigned)grid0, kScreenThreads, 0, st>>>(a);
-  RH_CHECK_LAUNCH(ctx);
+  a.cnt = reinterpret_cast<unsigned*>(base + oCnt);
+  a.kept_total = reinterpret_cast<unsigned long long*>(base + oKept);
+  a.R = reinterpret_cast<int32_t*>(base + oR);
+  a.bres = reinterpret_cast<int32_t*>(base + oRes);
+  a.state = reinterpret_cast<uint8_t*>(base + oSt);
+  RH_CUDA(cudaMemsetAsync(base, 0, ctrl, st));
+  if (reset) {
+    reset_scan_kernel<<<(unsigned)grid0, kScanThreads, 0, st>>>(a);
+    RH_CHECK_LAUNCH(ctx);
+  } else {
+    RH_CUDA(cudaMemsetAsync(a.R, 0xff, sizeof(int32_t) * n, st));  // no resets: all -1
+  }
   void* kargs[] = {&a};
-  RH_CUDA(cudaLaunchCooperativeKernel(coop, dim3(blocks), dim3(kScreenThreads), kargs, 0, st));
+  RH_CUDA(cudaLaunchCooperativeKernel((void*)screen_kernel, dim3(blocks), dim3(kScreenThreads),
+                                      kargs, 0, st));
   RH_CHECK_LAUNCH(ctx);
   return RH_OK;
 }

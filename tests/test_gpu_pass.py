@@ -61,21 +61,25 @@ def test_detect_matches_oracle(seed, oracle, cuda_device):
     np.testing.assert_array_equal(r["severity"].view(np.uint32), osv.view(np.uint32))
 
 
-@pytest.mark.parametrize("seed", range(16))
+@pytest.mark.parametrize("seed", range(40))
 def test_screen_matches_oracle(seed, oracle, cuda_device):
-    """rh_screen (Jacobi fixpoint) == the sequential state machine."""
+    """rh_screen (Jacobi fixpoint) == the sequential state machine: windows
+    1..64 (above 32 the lane-0 path), with and without resets, long pop runs
+    (multi-chunk backward scans) and quantised series (ties in the sorts)."""
     from paper_2605_06374_b200.detector import _screen
 
     rng = np.random.default_rng(seed)
-    n = int(rng.integers(1, 3000))
+    n = int(rng.integers(1, 3000)) if seed % 4 else int(rng.integers(3000, 40000))
     base = 10.0 + rng.standard_normal(n) * rng.choice([0.05, 0.5, 2.0])
-    spikes = rng.random(n) < rng.choice([0.02, 0.1, 0.3])
+    if seed % 5 == 0:
+        base = np.round(base, 1)
+    spikes = rng.random(n) < rng.choice([0.02, 0.1, 0.3, 0.6])
     obs = np.where(spikes, base * rng.uniform(1.1, 3.0, n), base)
     st = np.zeros(n, np.uint8)
-    st |= (rng.random(n) < 0.3).astype(np.uint8)  # escalate
+    st |= (rng.random(n) < rng.choice([0.05, 0.3])).astype(np.uint8)  # escalate
     st |= ((rng.random(n) < 0.2).astype(np.uint8) << 1)  # stage flag
-    reset = (rng.random(n) < 0.003).astype(np.uint8)
-    w = int(rng.choice([3, 5, 20, 21]))
+    reset = None if seed % 3 == 0 else (rng.random(n) < 0.003).astype(np.uint8)
+    w = int(rng.choice([1, 2, 3, 5, 20, 21, 32, 33, 64]))
     fe = bool(rng.integers(0, 2))
     L0 = int(rng.choice([0, 2, w, 50]))
     hist = list(10.0 + rng.standard_normal(min(L0, w)))
