@@ -161,6 +161,7 @@ int rh_ctx_destroy(rh_ctx* ctx) {
   for (cudaEvent_t e : ctx->chunk_ev)
     if (e) cudaEventDestroy(e);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+  for (auto& t : ctx->sched) cudaFree(t.dev);
   delete ctx;
   return RH_OK;
 }

@@ -7,6 +7,8 @@
 #include <stdio.h>
 
 #include <atomic>
+#include <mutex>
+#include <vector>
 #include <string>
 
 #include "../../include/resihp_b200.h"
@@ -24,6 +26,14 @@ struct rh_ctx {
   static constexpr int kChunkEvents = 8;
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t chunk_ev[kChunkEvents] = {};
+  // per-(pp, schedule, max micro-batches) op-order tables of the
+  // thread-per-replica pass kernel, built and uploaded on first use
+  struct SchedTable {
+    int pp, zbh, mmax;
+    void* dev;
+  };
+  std::vector<SchedTable> sched;
+  std::mutex sched_mu;
 };
 
 namespace rh {

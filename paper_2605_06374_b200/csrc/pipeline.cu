@@ -25,6 +25,7 @@
 // the earliest unprocessed vertex is always ready and the loop terminates.
 // All fp64 ops use explicit _rn intrinsics: no FMA contraction anywhere.
 #include <algorithm>
+#include <type_traits>
 
 #include "common.cuh"
 #include "wavefront.cuh"
@@ -43,6 +44,12 @@ struct PassParams {
   int ipb;         // iterations per CTA
   int mmax;        // micro-batches per replica (smem row length)
   int vec4;        // device_time rows are float4-aligned
+  // thread-per-replica kernel only
+  const unsigned long long* sched;  // level table (sched_table)
+  const int32_t* sched_off;         // [mmax+2] first level word of each micro-batch count
+  const int32_t* sched_peak;        // [mmax+1] peak in-flight forward chunks on any stage
+  int region_off;            // smem offset of the document / base-cost region
+  int doc_stage;             // documents that fit in that region
 };
 
 // MAXT = launch bound: 256 for the common case (more registers per lane),
@@ -201,16 +208,27 @@ __global__ void __launch_bounds__(MAXT) pass_kernel(const PassParams p) {
 }
 
 // ---------------------------------------------------------------------------
-// Small-P variant (P <= 4, D <= 256): one THREAD per replica pipeline.  The
-// thread walks all P stage chains level by level (same closed-form levels as
-// wavefront.cuh), with every stage's state in registers (P is a template
-// parameter, the stage loop is unrolled).  Data dependencies between stages
-// are read from a start-of-level snapshot of each stage's last F / B finish
-// — the same exactness argument as the shuffle wavefront, without shuffles or
-// idle lanes.  Replicas of a warp share one level schedule when their
-// micro-batch counts agree, so the per-stage branches are warp-uniform.
+// Small-P variant (P <= 4, D <= 128): one THREAD per replica pipeline.
+//
+// Op order.  The thread executes its replica's chunks in a precomputed order
+// (sched_table): sorted by DAG level (wavefront.cuh closed forms), and inside
+// a level by DESCENDING stage.  With every stage's state in registers (P is a
+// template parameter, the stage switch is unrolled) the dependencies then
+// read straight from the neighbours' registers:
+//   * F(s,j) needs F(s-1,j) (one level earlier); stage s-1's next F may sit
+//     on the same level as F(s,j), but in descending order it runs after;
+//   * B(s,j) needs B(s+1,j) (one level earlier); B levels of neighbouring
+//     stages have opposite parity, so no B of stage s+1 shares its level.
+// That is exactly the level-synchronous wavefront, without per-level tests.
+// Replicas with equal micro-batch counts share one op list, so in a warp the
+// op fetch is a broadcast and the stage switch is uniform.
+//
+// Quadratic loads.  The CTA stages its micro-batch offsets and documents in
+// shared memory and sums l^2 document-parallel (contiguous doc ranges per
+// thread, segment boundaries flushed with shared 64-bit atomics), then each
+// thread turns its replica's sums into base costs stored [j][thread]
+// (conflict-free reads in the op loop), aliasing the dead document buffer.
 constexpr int kSmallThreads = 128;
-constexpr int kDocStage = 4096;  // documents staged per CTA (16 KB)
 
 // Copy n ints global -> shared with U independent loads in flight per thread.
 template <int U>
@@ -230,35 +248,218 @@ __device__ __forceinline__ void stage_ints(int32_t* dst, const int32_t* src, int
   }
 }
 
+// sched_table entry: one 64-bit word per DAG level, 16 bits per stage:
+// 0 = idle, else kind (1 F, 2 B / BW, 3 W) | j << 2
+enum : unsigned { kOpF = 1, kOpB = 2, kOpW = 3 };
+
+// Register state of one replica's walk (references into the kernel's arrays).
+template <int P>
+struct WalkArgs {
+  const double* bt;  // base costs of this thread: bt[j * kSmallThreads]
+  const double (&rlF)[P];
+  const double (&rlB)[P];
+  const double (&rlW)[P];
+  const double (&sp)[P];
+  const double (&hf)[P];
+  const double (&hb)[P];
+  double (&fin)[P];
+  double (&ssum)[P];
+};
+
+// One chunk of stage s: c = (rl * base_j) [/ speed], start = max(chain
+// finish, dependency finish + hop), finish = start + c (pipeline.py:275-291).
+template <bool DIV>
+__device__ __forceinline__ double chunk(double& fin, double& ssum, double rl, double b,
+                                        double sp, double dep) {
+  double c = __dmul_rn(rl, b);
+  if (DIV && sp != 1.0) c = __ddiv_rn(c, sp);
+  const double st = fin > dep ? fin : dep;
+  fin = __dadd_rn(st, c);
+  ssum = __dadd_rn(ssum, c);
+  return fin;
+}
+
+// Dynamic walk over the level table: one 64-bit word per level, 16 bits per
+// stage (0 idle, else kind | j << 2); stages in descending order.
+template <int P, bool DIV>
+__device__ __forceinline__ void walk_table(const WalkArgs<P>& a, const unsigned long long* lv,
+                                           const unsigned long long* lv_end) {
+  double lastF[P], lastB[P];
+#pragma unroll
+  for (int s = 0; s < P; ++s) lastF[s] = lastB[s] = 0.0;
+  for (; lv < lv_end; ++lv) {
+    const unsigned long long codes = __ldg(lv);
+#pragma unroll
+    for (int s = P - 1; s >= 0; --s) {
+      const unsigned code = (unsigned)(codes >> (16 * s)) & 0xffffu;
+      if (code == 0) continue;
+      const unsigned kind = code & 3u;
+      const bool isF = kind == kOpF, isB = kind == kOpB;
+      const double dF = s > 0 ? __dadd_rn(lastF[s > 0 ? s - 1 : 0], a.hf[s]) : 0.0;
+      const double dB = s < P - 1 ? __dadd_rn(lastB[s < P - 1 ? s + 1 : 0], a.hb[s]) : 0.0;
+      const double nf = chunk<DIV>(a.fin[s], a.ssum[s],
+                                   isF ? a.rlF[s] : (isB ? a.rlB[s] : a.rlW[s]),
+                                   a.bt[(code >> 2) * kSmallThreads], a.sp[s],
+                                   isF ? dF : (isB ? dB : 0.0));
+      lastF[s] = isF ? nf : lastF[s];
+      lastB[s] = isB ? nf : lastB[s];
+    }
+  }
+}
+
+// The chunk of stage s at DAG level t for MM micro-batches (inverse of the
+// wavefront.cuh closed forms): kind (0 none) and micro-batch j.  Evaluated
+// on compile-time constants inside walk_static, so it folds away.
+__host__ __device__ constexpr int op_at(int P, int MM, int zbh, int t, int s, int& j) {
+  const int w = (P - 1 - s) < MM ? (P - 1 - s) : MM;
+  const int k = t - s;
+  if (k >= 0 && k <= w && k < MM) {
+    j = k;
+    return kOpF;
+  }
+  if (k > 2 * w && (k & 1) == 0 && k / 2 > w && k / 2 < MM) {
+    j = k / 2;
+    return kOpF;
+  }
+  const int kb = t - (2 * P - 1 - s);
+  if (kb >= 0 && (kb & 1) == 0 && kb / 2 < MM) {
+    j = kb / 2;
+    return kOpB;
+  }
+  if (zbh) {
+    const int kw = t - (2 * P - s) - 2 * (MM - w);
+    if (kw >= 0 && (kw & 1) == 0 && kw / 2 < w) {
+      j = kw / 2;
+      return kOpW;
+    }
+    const int tail = (w > 0 ? 2 * P - s + 2 * MM - 2 : 2 * P - 1 - s + 2 * (MM - 1));
+    const int jt = t - tail + w - 1;
+    if (jt >= w && jt < MM) {
+      j = jt;
+      return kOpW;
+    }
+  }
+  j = 0;
+  return 0;
+}
+
+// Upper bound on the DAG levels of an MM-micro-batch replica (levels past the
+// last chunk are idle and fold away).
+__host__ __device__ constexpr int n_levels(int P, int MM) { return 2 * P + 3 * MM + 2; }
+
+// Fully unrolled walk for a compile-time micro-batch count: every op, its
+// kind and j are constants, so a chunk is ~8 instructions with no dispatch.
+template <int P, int ZBH, int MM, bool DIV>
+__device__ __forceinline__ void walk_static(const WalkArgs<P>& a) {
+  double lastF[P], lastB[P];
+#pragma unroll
+  for (int s = 0; s < P; ++s) lastF[s] = lastB[s] = 0.0;
+  constexpr int L = n_levels(P, MM);
+#pragma unroll
+  for (int t = 0; t < L; ++t) {
+#pragma unroll
+    for (int s = P - 1; s >= 0; --s) {
+      int j = 0;
+      const int kind = op_at(P, MM, ZBH, t, s, j);
+      if (kind == kOpF) {
+        const double dep = s > 0 ? __dadd_rn(lastF[s > 0 ? s - 1 : 0], a.hf[s]) : 0.0;
+        lastF[s] = chunk<DIV>(a.fin[s], a.ssum[s], a.rlF[s], a.bt[j * kSmallThreads], a.sp[s], dep);
+      } else if (kind == kOpB) {
+        const double dep = s < P - 1 ? __dadd_rn(lastB[s < P - 1 ? s + 1 : 0], a.hb[s]) : 0.0;
+        lastB[s] = chunk<DIV>(a.fin[s], a.ssum[s], a.rlB[s], a.bt[j * kSmallThreads], a.sp[s], dep);
+      } else if (kind == kOpW) {
+        chunk<DIV>(a.fin[s], a.ssum[s], a.rlW[s], a.bt[j * kSmallThreads], a.sp[s], 0.0);
+      }
+    }
+  }
+}
+
+constexpr int kStaticMaxMB = 12;  // replicas with <= 12 micro-batches
+
+template <int P, int ZBH, bool DIV, int MM = 1>
+__device__ __forceinline__ bool walk_static_dispatch(const WalkArgs<P>& a, int mm) {
+  if constexpr (MM > kStaticMaxMB) {
+    return false;
+  } else {
+    if (mm == MM) {
+      walk_static<P, ZBH, MM, DIV>(a);
+      return true;
+    }
+    return walk_static_dispatch<P, ZBH, DIV, MM + 1>(a, mm);
+  }
+}
+
 template <int P, int ZBH, int DETECT>
 __global__ void __launch_bounds__(kSmallThreads, 4) pass_small_kernel(const PassParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, nt = blockDim.x;
   const int D = p.sh.dp, M = p.sh.micro_batches, T = p.sh.tp;
   const int li = tid / D, d = tid - li * D;
   const int64_t it0 = (int64_t)blockIdx.x * p.ipb;
   const int64_t it = it0 + li;
   const int n_it = (int)min((int64_t)p.ipb, p.tr.n_iter - it0);
   const bool on = li < n_it;
+  // layout: it_ms[ipb] it_st[ipb] | q[ipb*M] int64 | off[ipb*M+1] | docs / base
   double* it_ms = reinterpret_cast<double*>(smem_raw);
   unsigned* it_st = reinterpret_cast<unsigned*>(it_ms + p.ipb);
   const int it_bytes = ((p.ipb * 12 + 15) / 16) * 16;
-  double* base = reinterpret_cast<double*>(smem_raw + it_bytes) + (size_t)tid * p.mmax;
-  int32_t* s_off = reinterpret_cast<int32_t*>(smem_raw + it_bytes + (size_t)p.ipb * D * p.mmax * 8);
-  int32_t* s_doc = s_off + ((p.ipb * M + 1 + 3) & ~3);
+  unsigned long long* s_q = reinterpret_cast<unsigned long long*>(smem_raw + it_bytes);
+  int32_t* s_off = reinterpret_cast<int32_t*>(s_q + p.ipb * M);
+  double* base_t = reinterpret_cast<double*>(smem_raw + p.region_off);
+  int32_t* s_doc = reinterpret_cast<int32_t*>(base_t);
   if (tid < p.ipb) {
     it_ms[tid] = 0.0;
     it_st[tid] = 0u;
   }
-  // stage this CTA's micro-batch offsets and documents (coalesced)
+  // ---- stage offsets, zero the sums
   const int n_mb = n_it * M;
   stage_ints<8>(s_off, p.tr.mb_off + it0 * M, n_mb + 1);
+  for (int q = tid; q < n_mb; q += nt) s_q[q] = 0ull;
   __syncthreads();
   const int32_t d_lo = s_off[0];
   const int n_doc = s_off[n_mb] - d_lo;
-  const bool staged = n_doc <= kDocStage;
-  if (staged) stage_ints<8>(s_doc, p.tr.doc_len + d_lo, n_doc);
-  __syncthreads();
+  if (n_doc <= p.doc_stage) {
+    stage_ints<8>(s_doc, p.tr.doc_len + d_lo, n_doc);
+    __syncthreads();
+    // document-parallel segmented sum of l^2
+    const int per = (n_doc + nt - 1) / nt;
+    const int k0 = min(n_doc, tid * per), k1 = min(n_doc, k0 + per);
+    if (k0 < k1) {
+      int lo = 0, hi = n_mb;  // last micro-batch starting at or before k0
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (s_off[mid] - d_lo <= k0)
+          lo = mid;
+        else
+          hi = mid;
+      }
+      int mb = lo, next = s_off[mb + 1] - d_lo;
+      unsigned long long acc = 0;
+      for (int k = k0; k < k1; ++k) {
+        if (k >= next) {
+          atomicAdd(s_q + mb, acc);
+          acc = 0;
+          do {
+            ++mb;
+            next = s_off[mb + 1] - d_lo;
+          } while (next <= k);
+        }
+        const long long l = s_doc[k];
+        acc += (unsigned long long)(l * l);
+      }
+      atomicAdd(s_q + mb, acc);
+    }
+  } else {  // too many documents to stage: one thread per micro-batch
+    for (int mb = tid; mb < n_mb; mb += nt) {
+      unsigned long long q = 0;
+      for (int32_t k = s_off[mb]; k < s_off[mb + 1]; ++k) {
+        const long long l = __ldg(p.tr.doc_len + k);
+        q += (unsigned long long)(l * l);
+      }
+      s_q[mb] = q;
+    }
+  }
+  __syncthreads();  // sums complete; the document buffer is dead from here
   int seg = 0, md = 0;
   if (on) {
     seg = p.tr.seg ? __ldg(p.tr.seg + it) : 0;
@@ -268,22 +469,15 @@ __global__ void __launch_bounds__(kSmallThreads, 4) pass_small_kernel(const Pass
     if (md > p.mmax) md = -1;
     if (md > 0) {
       const double lin = __dmul_rn(p.m.alpha, (double)p.sh.token_budget);
-      const int32_t* off = s_off + li * M + m0;
-      for (int j = 0; j < md; ++j) {
-        long long q = 0;
-        for (int32_t k = off[j] - d_lo; k < off[j + 1] - d_lo; ++k) {
-          const long long l = staged ? s_doc[k] : __ldg(p.tr.doc_len + d_lo + k);
-          q += l * l;
-        }
-        base[j] = __dadd_rn(lin, __dmul_rn(p.m.beta, (double)q));
-      }
+      const unsigned long long* q = s_q + li * M + m0;
+      for (int j = 0; j < md; ++j)
+        base_t[j * kSmallThreads + tid] =
+            __dadd_rn(lin, __dmul_rn(p.m.beta, (double)(long long)q[j]));
     }
   }
   const int m = md > 0 ? md : 0;
-  double rlF[P], rlB[P], rlW[P], sp[P], hf[P], hb[P], fin[P], ssum[P], lastF[P], lastB[P];
-  int LF[P], LB[P], LW[P], jf[P], jb[P], jw[P], live[P];
-  bool stopped = false, over = false;
-  int last = 0;
+  double rlF[P], rlB[P], rlW[P], sp[P], hf[P], hb[P], fin[P], ssum[P];
+  bool stopped = false;
 #pragma unroll
   for (int s = 0; s < P; ++s) {
     const int64_t gs = ((int64_t)seg * D + d) * P + s;
@@ -300,65 +494,28 @@ __global__ void __launch_bounds__(kSmallThreads, 4) pass_small_kernel(const Pass
       if (s < P - 1) hb[s] = __ldg(p.sg.hop_bwd + gs);
       if (sp[s] <= 0.0) stopped = true;
     }
-    fin[s] = ssum[s] = lastF[s] = lastB[s] = 0.0;
-    jf[s] = jb[s] = jw[s] = live[s] = 0;
+    fin[s] = ssum[s] = 0.0;
   }
+  // ---- the replica's chunks, level by level
   const int mm = stopped ? 0 : m;
+  // activation capacity: the in-flight count along a chain is fixed by the
+  // schedule, so its peak per micro-batch count is precomputed
+  const bool over = p.sh.capacity > 0 && mm > 0 && __ldg(p.sched_peak + mm) > p.sh.capacity;
+  const double* bt = base_t + tid;
+  bool unit = true;  // x / 1.0 == x exactly: healthy replicas never divide
 #pragma unroll
-  for (int s = 0; s < P; ++s) {
-    const ChainLevels lv{s, P, mm, min(P - 1 - s, mm)};
-    LF[s] = lv.F(0);
-    LB[s] = lv.B(0);
-    LW[s] = ZBH ? lv.W(0) : INT_MAX;
-    if (mm > 0) last = max(last, 1 + (ZBH ? lv.W(mm - 1) : lv.B(mm - 1)));
-  }
-  __syncthreads();
-  const int cap = p.sh.capacity;
-  for (int t = 0; t < last; ++t) {
-    double snapF[P], snapB[P];
-#pragma unroll
-    for (int s = 0; s < P; ++s) {
-      snapF[s] = lastF[s];
-      snapB[s] = lastB[s];
-    }
-#pragma unroll
-    for (int s = 0; s < P; ++s) {
-      const bool doF = t == LF[s], doB = t == LB[s], doW = ZBH && t == LW[s];
-      if (doF || doB || doW) {
-        const ChainLevels lv{s, P, mm, min(P - 1 - s, mm)};
-        double dep = 0.0, rl;
-        int j;
-        if (doF) {
-          if (s > 0) dep = __dadd_rn(snapF[s - 1], hf[s]);
-          rl = rlF[s];
-          j = jf[s];
-        } else if (doB) {
-          if (s < P - 1) dep = __dadd_rn(snapB[s + 1], hb[s]);
-          rl = rlB[s];
-          j = jb[s];
-        } else {
-          rl = rlW[s];
-          j = jw[s];
-        }
-        double c = __dmul_rn(rl, base[j]);
-        if (sp[s] != 1.0) c = div_slow(c, sp[s]);
-        const double st = fin[s] > dep ? fin[s] : dep;
-        fin[s] = __dadd_rn(st, c);
-        ssum[s] = __dadd_rn(ssum[s], c);
-        if (doF) {
-          lastF[s] = fin[s];
-          LF[s] = lv.F(++jf[s]);
-          if (cap > 0 && ++live[s] > cap) over = true;
-        } else if (doB) {
-          lastB[s] = fin[s];
-          LB[s] = lv.B(++jb[s]);
-          --live[s];
-        } else {
-          LW[s] = lv.W(++jw[s]);
-        }
-      }
+  for (int s = 0; s < P; ++s) unit = unit && sp[s] == 1.0;
+  WalkArgs<P> wa{bt, rlF, rlB, rlW, sp, hf, hb, fin, ssum};
+  if (mm > 0) {
+    const unsigned long long* l0 = p.sched + __ldg(p.sched_off + mm);
+    const unsigned long long* l1 = p.sched + __ldg(p.sched_off + mm + 1);
+    if (unit) {
+      if (!walk_static_dispatch<P, ZBH, false>(wa, mm)) walk_table<P, false>(wa, l0, l1);
+    } else {
+      if (!walk_static_dispatch<P, ZBH, true>(wa, mm)) walk_table<P, true>(wa, l0, l1);
     }
   }
+  __syncthreads();  // iteration slots initialised before the reductions
   // ---- replica makespan, validation, iteration reductions
   uint8_t flag[P];
   float sev[P];
@@ -429,6 +586,71 @@ __global__ void __launch_bounds__(kSmallThreads, 4) pass_small_kernel(const Pass
   }
 }
 
+// Level table for (P, schedule, mmax): for every micro-batch count
+// mm = 0..mmax, one 64-bit word per DAG level holding each stage's chunk at
+// that level (wavefront.cuh closed forms; a chain has at most one chunk per
+// level).  Device layout [off: mmax+2 int32, padded to 8 B][levels: uint64].
+// Built once per context.
+static int sched_table(rh_ctx* ctx, int P, int zbh, int mmax,
+                       const unsigned long long** lv_out, const int32_t** off_out,
+                       const int32_t** peak_out) {
+  // [off: mmax+2][peak: mmax+1] int32, padded to 8 B, then the level words
+  const size_t off_words = ((size_t)(2 * mmax + 3) + 1) & ~size_t(1);
+  auto view = [&](void* dev) {
+    *off_out = static_cast<const int32_t*>(dev);
+    *peak_out = *off_out + (mmax + 2);
+    *lv_out = reinterpret_cast<const unsigned long long*>(*off_out + off_words);
+  };
+  std::lock_guard<std::mutex> lock(ctx->sched_mu);
+  for (const auto& t : ctx->sched) {
+    if (t.pp == P && t.zbh == zbh && t.mmax == mmax) {
+      view(t.dev);
+      return RH_OK;
+    }
+  }
+  std::vector<int32_t> o(off_words, 0);
+  std::vector<unsigned long long> v;
+  for (int mm = 0; mm <= mmax; ++mm) {
+    o[mm] = (int32_t)v.size();
+    if (mm == 0) continue;
+    const size_t base = v.size();
+    auto put = [&](int level, int s, unsigned kind, int j) {
+      if ((size_t)level >= v.size() - base) v.resize(base + level + 1, 0ull);
+      v[base + level] |= (unsigned long long)(kind | ((unsigned)j << 2)) << (16 * s);
+    };
+    for (int s = 0; s < P; ++s) {
+      const ChainLevels lv{s, P, mm, std::min(P - 1 - s, mm)};
+      for (int j = 0; j < mm; ++j) {
+        put(lv.F(j), s, kOpF, j);
+        put(lv.B(j), s, kOpB, j);
+        if (zbh) put(lv.W(j), s, kOpW, j);
+      }
+    }
+    // peak in-flight forward chunks (F done, its B not yet) on any stage
+    int peak = 0;
+    for (int s = 0; s < P; ++s) {
+      int live = 0;
+      for (size_t t = base; t < v.size(); ++t) {
+        const unsigned kind = (unsigned)(v[t] >> (16 * s)) & 3u;
+        if (kind == kOpF) peak = std::max(peak, ++live);
+        if (kind == kOpB) --live;
+      }
+    }
+    o[mmax + 2 + mm] = peak;
+  }
+  o[mmax + 1] = (int32_t)v.size();
+  const size_t bytes = sizeof(int32_t) * off_words + sizeof(unsigned long long) * (v.size() + 1);
+  void* dev = nullptr;
+  RH_CUDA(cudaMalloc(&dev, bytes));
+  RH_CUDA(cudaMemcpy(dev, o.data(), sizeof(int32_t) * off_words, cudaMemcpyHostToDevice));
+  if (!v.empty())
+    RH_CUDA(cudaMemcpy(static_cast<int32_t*>(dev) + off_words, v.data(),
+                       sizeof(unsigned long long) * v.size(), cudaMemcpyHostToDevice));
+  ctx->sched.push_back({P, zbh, mmax, dev});
+  view(dev);
+  return RH_OK;
+}
+
 template <int ZBH, int DETECT>
 static void* small_kernel(int P) {
   switch (P) {
@@ -487,16 +709,23 @@ int launch_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
   }
   p.mmax = sh->max_mb_per_replica > 0 ? sh->max_mb_per_replica : M;
   p.vec4 = (sh->tp % 4 == 0) && ((reinterpret_cast<uintptr_t>(tr->device_time) & 15) == 0);
-  if (P <= 4 && D <= kSmallThreads && !getenv("RH_FORCE_LANE_KERNEL")) {
+  if (P <= 4 && D <= kSmallThreads && p.mmax < 16384 && !getenv("RH_FORCE_LANE_KERNEL")) {
     // thread-per-replica kernel for short pipelines
     p.ipb = std::max(1, kSmallThreads / D);
     const int threads = p.ipb * D;
+    // j is stored in 14 bits of a level word
     const int it_bytes = ((p.ipb * 12 + 15) / 16) * 16;
-    const size_t smem = it_bytes + (size_t)threads * p.mmax * 8 +
-                        4 * (size_t)(((p.ipb * M + 1 + 3) & ~3) + kDocStage);
-    if (smem <= ctx->smem_optin) {
-      const int64_t blocks = (tr->n_iter + p.ipb - 1) / p.ipb;
+    const size_t head = it_bytes + 8 * (size_t)p.ipb * M + 4 * (size_t)(p.ipb * M + 1);
+    p.region_off = (int)((head + 15) & ~size_t(15));
+    // the region holds the staged documents, later the base costs
+    const size_t region = std::max<size_t>(16 * 1024, (size_t)threads * p.mmax * 8);
+    p.doc_stage = (int)(region / 4);
+    const size_t smem = p.region_off + region;
+    if (smem <= ctx->smem_optin && smem <= 56 * 1024) {
       const bool zbh = sh->schedule == RH_SCHED_ZBH;
+      if (int e = sched_table(ctx, P, zbh, p.mmax, &p.sched, &p.sched_off, &p.sched_peak))
+        return e;
+      const int64_t blocks = (tr->n_iter + p.ipb - 1) / p.ipb;
       void* kern = zbh ? (detect ? small_kernel<1, 1>(P) : small_kernel<1, 0>(P))
                        : (detect ? small_kernel<0, 1>(P) : small_kernel<0, 0>(P));
       if (int e = ensure_smem(kern, smem)) return e;

@@ -18,8 +18,10 @@
 // leading decision, so it terminates, and in practice pops are sparse and it
 // converges in 3 rounds.
 //
-// One persistent cooperative launch, one grid barrier per round.  Per round
-// and iteration, one warp
+// One persistent cooperative launch, one grid barrier per round.  A warp owns
+// a fixed set of iterations and keeps their constants (observation, status,
+// reset, the 32 preceding observations, last decision) in shared memory
+// across rounds.  Per round and iteration, the warp
 //   * scans the previous round's state bytes (bit 0 = popped, bit 1 =
 //     changed in that round) backwards from i, 32 at a time with ballots,
 //     until it has found the last `window` kept entries or reached the reset;
@@ -27,8 +29,8 @@
 //     slots in shared memory, so no global prefix sum / compaction exists;
 //   * skips the decision when no change lies inside that window span (or,
 //     while the series is short, since the reset): it cannot differ;
-//   * otherwise sorts the window across lanes (two 32-lane bitonic sorts on
-//     shuffles -> median and MAD) and applies the filter / validation bits.
+//   * otherwise takes the median and MAD by lane-parallel rank selection over
+//     the window in shared memory and applies the filter / validation bits.
 // The kept-state is double-buffered, so every round reads one consistent
 // kept-set (pure Jacobi) while writing the next.
 #include <algorithm>
@@ -84,56 +86,28 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
   __syncthreads();
 }
 
-__device__ __forceinline__ void sort_small(double* a, int n) {
-  for (int i = 1; i < n; ++i) {
-    const double v = a[i];
-    int j = i - 1;
-    while (j >= 0 && a[j] > v) {
-      a[j + 1] = a[j];
-      --j;
-    }
-    a[j + 1] = v;
-  }
-}
-
-// statistics.median on a sorted array
-__device__ __forceinline__ double median_sorted(const double* a, int n) {
-  return (n & 1) ? a[n >> 1] : __ddiv_rn(__dadd_rn(a[(n >> 1) - 1], a[n >> 1]), 2.0);
-}
-
-// windows wider than a warp: lane 0 alone, insertion sorts in local memory
-__device__ __noinline__ bool outlier_generic(const double* win_smem, int w, double x,
-                                             double kappa) {
-  double win[kMaxWindow], dev[kMaxWindow];
-  for (int q = 0; q < w; ++q) dev[q] = win[q] = win_smem[q];
-  sort_small(dev, w);
-  const double med = median_sorted(dev, w);
-  for (int q = 0; q < w; ++q) dev[q] = fabs(__dsub_rn(win[q], med));
-  sort_small(dev, w);
-  const double mad = median_sorted(dev, w);
-  return fabs(__dsub_rn(x, med)) > __dmul_rn(kappa, mad);
-}
-
-// ascending bitonic sort of one value per lane (32 values, pads = +inf)
-__device__ __forceinline__ double warp_sort(double v) {
+// statistics.median of the w values in a[] (shared memory, warp-visible):
+// lane-parallel rank selection.  Slot q's rank is the number of entries that
+// sort before it (ties broken by slot index, i.e. a stable sort), so exactly
+// one slot holds each rank; the slots of rank w/2-1 and w/2 are the middle.
+// Every lane reads every entry as a shared-memory broadcast, so the w loads
+// are independent and pipeline, unlike a sorting network's dependent stages.
+__device__ __forceinline__ double warp_median(const double* a, int w, double* sel) {
   const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int k = 2; k <= 32; k <<= 1) {
-#pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      const double o = __shfl_xor_sync(0xffffffffu, v, j);
-      const bool take_min = ((lane & j) == 0) == ((lane & k) == 0);
-      v = (take_min == (o < v)) ? o : v;
+  for (int q = lane; q < w; q += 32) {
+    const double v = a[q];
+    int rank = 0;
+#pragma unroll 4
+    for (int p = 0; p < w; ++p) {
+      const double u = a[p];
+      rank += (u < v) | ((u == v) & (p < q));
     }
+    if (rank == (w >> 1)) sel[1] = v;
+    if (rank == (w >> 1) - 1) sel[0] = v;
   }
-  return v;
-}
-
-// statistics.median of w sorted lane values (lanes 0..w-1)
-__device__ __forceinline__ double warp_median(double s, int w) {
-  const double hi = __shfl_sync(0xffffffffu, s, w >> 1);
-  const double lo = __shfl_sync(0xffffffffu, s, w > 1 ? (w >> 1) - 1 : 0);
-  return (w & 1) ? hi : __ddiv_rn(__dadd_rn(lo, hi), 2.0);
+  __syncwarp();
+  const double hi = sel[1];
+  return (w & 1) ? hi : __ddiv_rn(__dadd_rn(sel[0], hi), 2.0);
 }
 
 // last reset index <= i: block-local inclusive max-scan, one element per
@@ -163,14 +137,24 @@ __global__ void __launch_bounds__(kScanThreads) reset_scan_kernel(ScreenArgs a) 
   if (threadIdx.x == 0) a.bres[blockIdx.x] = sm[(blockDim.x >> 5) - 1];
 }
 
+// Per-warp shared scratch: the window, its deviations, the median selection.
+struct WarpScratch {
+  double win[kMaxWindow];
+  double dev[kMaxWindow];
+  double sel[2];
+};
+
 // One Jacobi step for iteration i, executed by a whole warp (uniform result).
+// x / stb are the iteration's observation and status; ob (optional) holds
+// obs[i-32+lane] so the common single-chunk window needs no global gather.
 // Returns the new pop bit, or kUnchanged when no change of the previous round
 // lies where it could reach iteration i.
 constexpr unsigned kUnchanged = 0xffu;
 
-__device__ __forceinline__ unsigned step_warp(const ScreenArgs& a, int64_t i, int r,
+__device__ __forceinline__ unsigned step_warp(const ScreenArgs& a, int64_t i, int r, double x,
+                                              unsigned stb, const double* ob,
                                               const uint8_t* cur, bool first_round,
-                                              double* win) {
+                                              WarpScratch& ws) {
   const int lane = threadIdx.x & 31;
   const int w = a.w;
   const int64_t first = r >= 0 ? r : 0;
@@ -186,7 +170,7 @@ __device__ __forceinline__ unsigned step_warp(const ScreenArgs& a, int64_t i, in
     const unsigned cm = __ballot_sync(0xffffffffu, (sv & 2u) != 0u);
     // rank of this lane's kept entry counted from i downwards (0 = newest)
     const int rank = found + __popc(km >> lane) - 1;
-    if (kept && rank < w) win[w - 1 - rank] = a.obs[j];
+    if (kept && rank < w) ws.win[w - 1 - rank] = (ob && hi == i) ? ob[lane] : a.obs[j];
     const int cnt = __popc(km);
     if (found + cnt >= w) {
       // the window starts at the kept lane of rank w-1: changes below it
@@ -199,40 +183,33 @@ __device__ __forceinline__ unsigned step_warp(const ScreenArgs& a, int64_t i, in
       any_chg |= cm != 0u;
     }
   }
-  __syncwarp();
-  if (!any_chg) return kUnchanged;
+  if (!any_chg) {
+    __syncwarp();
+    return kUnchanged;
+  }
   // kept entries since the reset: exact below w, which is all the length
   // thresholds need
   const int64_t len = (r >= 0 ? found : a.len0 + found) + 1;
-  const double x = a.obs[i];
   bool cand = false;
   if (len >= w + 1) {
     const int need = w - found;  // > 0 only without a reset: history entries
-    if (w <= 32) {
-      double v = __longlong_as_double(0x7ff0000000000000LL);  // +inf pad
-      if (lane < w) v = lane < need ? a.hist[a.h - need + lane] : win[lane];
-      const double med = warp_median(warp_sort(v), w);
-      const double d = lane < w ? fabs(__dsub_rn(v, med)) : v;
-      const double mad = warp_median(warp_sort(d), w);
-      cand = fabs(__dsub_rn(x, med)) > __dmul_rn(a.kappa, mad);
-    } else {
-      for (int q = lane; q < need; q += 32) win[q] = a.hist[a.h - need + q];
-      __syncwarp();
-      int c = 0;
-      if (lane == 0) c = outlier_generic(win, w, x, a.kappa);
-      cand = __shfl_sync(0xffffffffu, c, 0) != 0;
-    }
+    for (int q = lane; q < need; q += 32) ws.win[q] = a.hist[a.h - need + q];
+    __syncwarp();
+    const double med = warp_median(ws.win, w, ws.sel);
+    for (int q = lane; q < w; q += 32) ws.dev[q] = fabs(__dsub_rn(ws.win[q], med));
+    __syncwarp();
+    const double mad = warp_median(ws.dev, w, ws.sel);
+    cand = fabs(__dsub_rn(x, med)) > __dmul_rn(a.kappa, mad);
   }
   const bool refill = !cand && a.fe && len <= w;
   bool pop = false;
   uint8_t oc = 0;
   if (cand || refill) {
     oc = cand ? RH_SC_CANDIDATE : 0;
-    const uint8_t st = a.st[i];
     bool done = false;
     if (a.fe) {
       oc |= RH_SC_FILTERED;
-      if (!(st & RH_IT_ESCALATE)) {
+      if (!(stb & RH_IT_ESCALATE)) {
         if (cand) {
           pop = true;
           oc |= RH_SC_POPPED;
@@ -242,7 +219,7 @@ __device__ __forceinline__ unsigned step_warp(const ScreenArgs& a, int64_t i, in
     }
     if (!done) {
       oc |= RH_SC_ESCALATED;
-      if (!(st & (RH_IT_STAGE_FLAG | RH_IT_LINK_FLAG))) {
+      if (!(stb & (RH_IT_STAGE_FLAG | RH_IT_LINK_FLAG))) {
         pop = true;
         oc |= RH_SC_POPPED;
       } else {
@@ -251,17 +228,47 @@ __device__ __forceinline__ unsigned step_warp(const ScreenArgs& a, int64_t i, in
     }
   }
   if (lane == 0) a.outcome[i] = oc;
-  __syncwarp();  // the window slots are reused by the warp's next iteration
+  __syncwarp();  // the scratch is reused by the warp's next iteration
   return pop ? 1u : 0u;
 }
 
+// What a warp keeps across rounds for each of its first kCache iterations.
+constexpr int kCache = 4;
+struct IterCache {
+  double x;
+  int32_t r;
+  uint8_t st;
+  uint8_t pop;
+};
+
+#ifdef RH_SCREEN_TRACE
+// debug build only (tools/screen_trace.py): per round, block 0's timestamps
+// around the barrier and the slowest block's compute time
+__device__ unsigned long long g_trace_t[3 * 32];
+__device__ unsigned long long g_trace_slow[32];
+__device__ unsigned g_trace_chg[32];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+extern "C" int rh_debug_screen_trace(unsigned long long* t, unsigned long long* slow,
+                                     unsigned* chg) {
+  cudaMemcpyFromSymbol(t, g_trace_t, sizeof(g_trace_t));
+  cudaMemcpyFromSymbol(slow, g_trace_slow, sizeof(g_trace_slow));
+  cudaMemcpyFromSymbol(chg, g_trace_chg, sizeof(g_trace_chg));
+  return 0;
+}
+#endif
+
 __global__ void __launch_bounds__(kScreenThreads) screen_kernel(const ScreenArgs a) {
-  __shared__ double s_win[kScreenWarps][kMaxWindow];
+  __shared__ WarpScratch s_ws[kScreenWarps];
+  __shared__ double s_ob[kScreenWarps][kCache][32];
+  __shared__ IterCache s_it[kScreenWarps][kCache];
   __shared__ unsigned s_cnt;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t gw = (int64_t)blockIdx.x * kScreenWarps + wid;
   const int64_t n_warps = (int64_t)gridDim.x * kScreenWarps;
-  double* win = s_win[wid];
 
   int round = 0;
   for (;; ++round) {
@@ -269,26 +276,53 @@ __global__ void __launch_bounds__(kScreenThreads) screen_kernel(const ScreenArgs
     uint8_t* nxt = a.state + (size_t)((round + 1) & 1) * a.n;
     if (threadIdx.x == 0) s_cnt = 0;
     __syncthreads();
+#ifdef RH_SCREEN_TRACE
+    const unsigned long long t_start = gtimer();
+#endif
     unsigned changes = 0;
-    for (int64_t i = gw; i < a.n; i += n_warps) {
+    int k = 0;
+    for (int64_t i = gw; i < a.n; i += n_warps, ++k) {
+      const bool cached = k < kCache;
       int r;
-      if (round == 0) {  // fold in the resets of earlier scan blocks, once
-        r = a.R[i];
-        if (r < 0 && a.reset) {
-          const int nb = (int)(i / kScanThreads);
-          for (int b = lane; b < nb; b += 32) r = max(r, a.bres[b]);
-          for (int o = 16; o > 0; o >>= 1) r = max(r, __shfl_xor_sync(0xffffffffu, r, o));
+      double x;
+      unsigned stb, old;
+      if (round == 0 || !cached) {
+        x = a.obs[i];
+        stb = a.st[i];
+        if (round == 0) {  // fold in the resets of earlier scan blocks, once
+          r = a.R[i];
+          if (r < 0 && a.reset) {
+            const int nb = (int)(i / kScanThreads);
+            for (int b = lane; b < nb; b += 32) r = max(r, a.bres[b]);
+            for (int o = 16; o > 0; o >>= 1) r = max(r, __shfl_xor_sync(0xffffffffu, r, o));
+          }
+          old = 0;
+        } else {
+          r = __ldcg(a.R + i);
+          old = __ldcg(cur + i) & 1u;
+        }
+        if (round == 0 && cached) {
+          const int64_t j = i - 32 + lane;
+          s_ob[wid][k][lane] = j >= 0 ? a.obs[j] : 0.0;
+          if (lane == 0) s_it[wid][k] = IterCache{x, r, (uint8_t)stb, 0};
         }
         __syncwarp();
-        if (lane == 0) a.R[i] = r;
+        if (round == 0 && lane == 0) a.R[i] = r;
       } else {
-        r = __ldcg(a.R + i);
+        const IterCache c = s_it[wid][k];
+        x = c.x;
+        r = c.r;
+        stb = c.st;
+        old = c.pop;
       }
-      const unsigned old = round == 0 ? 0u : (__ldcg(cur + i) & 1u);
-      unsigned pop = step_warp(a, i, r, cur, round == 0, win);
+      unsigned pop = step_warp(a, i, r, x, stb, cached ? s_ob[wid][k] : nullptr, cur,
+                               round == 0, s_ws[wid]);
       if (pop == kUnchanged) pop = old;
       const unsigned changed = pop != old;
-      if (lane == 0) nxt[i] = (uint8_t)(pop | (changed << 1));
+      if (lane == 0) {
+        nxt[i] = (uint8_t)(pop | (changed << 1));
+        if (cached) s_it[wid][k].pop = (uint8_t)pop;
+      }
       changes += changed;
     }
     if (lane == 0 && changes) atomicAdd(&s_cnt, changes);
@@ -296,7 +330,19 @@ __global__ void __launch_bounds__(kScreenThreads) screen_kernel(const ScreenArgs
     if (blockIdx.x == 0 && threadIdx.x == 0) a.cnt[(round + 1) % 3] = 0;
     __syncthreads();
     if (threadIdx.x == 0 && s_cnt) atomicAdd(a.cnt + round % 3, s_cnt);
+#ifdef RH_SCREEN_TRACE
+    const unsigned long long t_arrive = gtimer();
+    if (threadIdx.x == 0 && round < 32) atomicMax(&g_trace_slow[round], t_arrive - t_start);
+#endif
     grid_barrier(a.bar, gridDim.x);
+#ifdef RH_SCREEN_TRACE
+    if (blockIdx.x == 0 && threadIdx.x == 0 && round < 32) {
+      g_trace_t[3 * round] = t_start;
+      g_trace_t[3 * round + 1] = t_arrive;
+      g_trace_t[3 * round + 2] = gtimer();
+      g_trace_chg[round] = __ldcg(a.cnt + round % 3);
+    }
+#endif
     if (__ldcg(a.cnt + round % 3) == 0) break;  // fixpoint: nothing changed
   }
   // final series length: kept entries since the last reset (+ history)

@@ -43,11 +43,11 @@ __device__ __noinline__ inline double div_slow(double a, double b) { return __dd
 
 struct ChainLevels {
   int s, P, m, w;
-  __device__ __forceinline__ int F(int j) const {
+  __host__ __device__ __forceinline__ int F(int j) const {
     return j >= m ? INT_MAX : (j <= w ? s + j : 2 * j + s);
   }
-  __device__ __forceinline__ int B(int j) const { return j >= m ? INT_MAX : 2 * P - 1 - s + 2 * j; }
-  __device__ __forceinline__ int W(int j) const {
+  __host__ __device__ __forceinline__ int B(int j) const { return j >= m ? INT_MAX : 2 * P - 1 - s + 2 * j; }
+  __host__ __device__ __forceinline__ int W(int j) const {
     if (j >= m) return INT_MAX;
     if (j < w) return 2 * P - s + 2 * (m - w + j);
     return (w > 0 ? 2 * P - s + 2 * m - 2 : 2 * P - 1 - s + 2 * (m - 1)) + (j - w + 1);
