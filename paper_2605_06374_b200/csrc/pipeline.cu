@@ -50,6 +50,7 @@ struct PassParams {
   const int32_t* sched_peak;        // [mmax+1] peak in-flight forward chunks on any stage
   int region_off;            // smem offset of the document / base-cost region
   int doc_stage;             // documents that fit in that region
+  int static_max, static_div_max;  // largest counts walked by the unrolled code
 };
 
 // MAXT = launch bound: 256 for the common case (more registers per lane),
@@ -229,6 +230,10 @@ __global__ void __launch_bounds__(MAXT) pass_kernel(const PassParams p) {
 // thread turns its replica's sums into base costs stored [j][thread]
 // (conflict-free reads in the op loop), aliasing the dead document buffer.
 constexpr int kSmallThreads = 128;
+#ifndef RH_SMALL_MIN_BLOCKS
+#define RH_SMALL_MIN_BLOCKS 5
+#endif
+constexpr int kSmallMinBlocks = RH_SMALL_MIN_BLOCKS;  // CTAs per SM the register budget targets
 
 // Copy n ints global -> shared with U independent loads in flight per thread.
 template <int U>
@@ -272,7 +277,7 @@ template <bool DIV>
 __device__ __forceinline__ double chunk(double& fin, double& ssum, double rl, double b,
                                         double sp, double dep) {
   double c = __dmul_rn(rl, b);
-  if (DIV && sp != 1.0) c = __ddiv_rn(c, sp);
+  if (DIV && sp != 1.0) c = div_slow(c, sp);  // out of line: keeps the unrolled walks small
   const double st = fin > dep ? fin : dep;
   fin = __dadd_rn(st, c);
   ssum = __dadd_rn(ssum, c);
@@ -390,7 +395,7 @@ __device__ __forceinline__ bool walk_static_dispatch(const WalkArgs<P>& a, int m
 }
 
 template <int P, int ZBH, int DETECT>
-__global__ void __launch_bounds__(kSmallThreads, 4) pass_small_kernel(const PassParams p) {
+__global__ void __launch_bounds__(kSmallThreads, kSmallMinBlocks) pass_small_kernel(const PassParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x, nt = blockDim.x;
   const int D = p.sh.dp, M = p.sh.micro_batches, T = p.sh.tp;
@@ -411,10 +416,52 @@ __global__ void __launch_bounds__(kSmallThreads, 4) pass_small_kernel(const Pass
     it_ms[tid] = 0.0;
     it_st[tid] = 0u;
   }
-  // ---- stage offsets, zero the sums
+  // ---- everything that does not depend on shared memory is issued first,
+  // so its latency hides behind the offset / document staging
+  const int seg = on && p.tr.seg ? __ldg(p.tr.seg + it) : 0;
   const int n_mb = n_it * M;
   stage_ints<8>(s_off, p.tr.mb_off + it0 * M, n_mb + 1);
   for (int q = tid; q < n_mb; q += nt) s_q[q] = 0ull;
+  int m0 = 0, md = 0;
+  double rlF[P], rlB[P], rlW[P], sp[P], hf[P], hb[P], fin[P], ssum[P];
+  float meas[P];
+  if (on) {
+    const int32_t* ms = p.sg.mb_start + (int64_t)seg * (D + 1);
+    m0 = __ldg(ms + d);
+    md = __ldg(ms + d + 1) - m0;
+  }
+#pragma unroll
+  for (int s = 0; s < P; ++s) {
+    const int64_t gs = ((int64_t)seg * D + d) * P + s;
+    sp[s] = 1.0;
+    hf[s] = hb[s] = 0.0;
+    rlF[s] = rlB[s] = rlW[s] = 0.0;
+    if (on) {
+      sp[s] = __ldg(p.sg.speed + gs);
+      const double L = (double)__ldg(p.sg.layers + (int64_t)seg * P + s);
+      rlF[s] = __dmul_rn(p.m.ratio_f, L);
+      rlB[s] = __dmul_rn(ZBH ? p.m.ratio_b : __dadd_rn(p.m.ratio_b, p.m.ratio_w), L);
+      rlW[s] = __dmul_rn(p.m.ratio_w, L);
+      if (s > 0) hf[s] = __ldg(p.sg.hop_fwd + gs - 1);
+      if (s < P - 1) hb[s] = __ldg(p.sg.hop_bwd + gs);
+    }
+    fin[s] = ssum[s] = 0.0;
+    // measured stage time: max over the TP group's device times
+    meas[s] = 0.0f;
+    if (DETECT && on) {
+      const float* dt = p.tr.device_time + ((it * D + d) * P + s) * (int64_t)T;
+      float mx = 0.0f;
+      if (p.vec4) {
+        for (int q = 0; q < T; q += 4) {
+          const float4 v = __ldg(reinterpret_cast<const float4*>(dt + q));
+          mx = fmaxf(mx, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
+        }
+      } else {
+        for (int q = 0; q < T; ++q) mx = fmaxf(mx, __ldg(dt + q));
+      }
+      meas[s] = mx;
+    }
+  }
   __syncthreads();
   const int32_t d_lo = s_off[0];
   const int n_doc = s_off[n_mb] - d_lo;
@@ -460,41 +507,23 @@ __global__ void __launch_bounds__(kSmallThreads, 4) pass_small_kernel(const Pass
     }
   }
   __syncthreads();  // sums complete; the document buffer is dead from here
-  int seg = 0, md = 0;
-  if (on) {
-    seg = p.tr.seg ? __ldg(p.tr.seg + it) : 0;
-    const int32_t* ms = p.sg.mb_start + (int64_t)seg * (D + 1);
-    const int m0 = __ldg(ms + d);
-    md = __ldg(ms + d + 1) - m0;
-    if (md > p.mmax) md = -1;
-    if (md > 0) {
-      const double lin = __dmul_rn(p.m.alpha, (double)p.sh.token_budget);
-      const unsigned long long* q = s_q + li * M + m0;
-      for (int j = 0; j < md; ++j)
-        base_t[j * kSmallThreads + tid] =
-            __dadd_rn(lin, __dmul_rn(p.m.beta, (double)(long long)q[j]));
-    }
+  if (md > p.mmax) md = -1;
+  if (md > 0) {
+    const double lin = __dmul_rn(p.m.alpha, (double)p.sh.token_budget);
+    const unsigned long long* q = s_q + li * M + m0;
+    for (int j = 0; j < md; ++j)
+      base_t[j * kSmallThreads + tid] =
+          __dadd_rn(lin, __dmul_rn(p.m.beta, (double)(long long)q[j]));
   }
   const int m = md > 0 ? md : 0;
-  double rlF[P], rlB[P], rlW[P], sp[P], hf[P], hb[P], fin[P], ssum[P];
   bool stopped = false;
 #pragma unroll
   for (int s = 0; s < P; ++s) {
-    const int64_t gs = ((int64_t)seg * D + d) * P + s;
-    sp[s] = 1.0;
-    hf[s] = hb[s] = 0.0;
-    rlF[s] = rlB[s] = rlW[s] = 0.0;
-    if (on && m > 0) {
-      sp[s] = __ldg(p.sg.speed + gs);
-      const double L = (double)__ldg(p.sg.layers + (int64_t)seg * P + s);
-      rlF[s] = __dmul_rn(p.m.ratio_f, L);
-      rlB[s] = __dmul_rn(ZBH ? p.m.ratio_b : __dadd_rn(p.m.ratio_b, p.m.ratio_w), L);
-      rlW[s] = __dmul_rn(p.m.ratio_w, L);
-      if (s > 0) hf[s] = __ldg(p.sg.hop_fwd + gs - 1);
-      if (s < P - 1) hb[s] = __ldg(p.sg.hop_bwd + gs);
-      if (sp[s] <= 0.0) stopped = true;
+    if (m == 0) {  // nothing runs: no speeds, no costs
+      sp[s] = 1.0;
+      rlF[s] = rlB[s] = rlW[s] = 0.0;
     }
-    fin[s] = ssum[s] = 0.0;
+    if (sp[s] <= 0.0) stopped = true;
   }
   // ---- the replica's chunks, level by level
   const int mm = stopped ? 0 : m;
@@ -510,9 +539,11 @@ __global__ void __launch_bounds__(kSmallThreads, 4) pass_small_kernel(const Pass
     const unsigned long long* l0 = p.sched + __ldg(p.sched_off + mm);
     const unsigned long long* l1 = p.sched + __ldg(p.sched_off + mm + 1);
     if (unit) {
-      if (!walk_static_dispatch<P, ZBH, false>(wa, mm)) walk_table<P, false>(wa, l0, l1);
+      if (mm > p.static_max || !walk_static_dispatch<P, ZBH, false>(wa, mm))
+        walk_table<P, false>(wa, l0, l1);
     } else {
-      if (!walk_static_dispatch<P, ZBH, true>(wa, mm)) walk_table<P, true>(wa, l0, l1);
+      if (mm > p.static_div_max || !walk_static_dispatch<P, ZBH, true>(wa, mm))
+        walk_table<P, true>(wa, l0, l1);
     }
   }
   __syncthreads();  // iteration slots initialised before the reductions
@@ -535,20 +566,10 @@ __global__ void __launch_bounds__(kSmallThreads, 4) pass_small_kernel(const Pass
       flag[s] = 0;
       sev[s] = 0.0f;
       if (DETECT && md >= 0) {
-        const float* dt = p.tr.device_time + ((it * D + d) * P + s) * (int64_t)T;
-        float mx = 0.0f;
-        if (p.vec4) {
-          for (int q = 0; q < T; q += 4) {
-            const float4 v = __ldg(reinterpret_cast<const float4*>(dt + q));
-            mx = fmaxf(mx, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
-          }
-        } else {
-          for (int q = 0; q < T; ++q) mx = fmaxf(mx, __ldg(dt + q));
-        }
-        const double meas = (double)mx;
-        if (!(ssum[s] <= 0.0 || meas <= 0.0) && meas > __dmul_rn(p.thr, ssum[s])) {
+        const double ms_d = (double)meas[s];
+        if (!(ssum[s] <= 0.0 || ms_d <= 0.0) && ms_d > __dmul_rn(p.thr, ssum[s])) {
           flag[s] = 1;
-          sev[s] = (float)__ddiv_rn(ssum[s], meas);
+          sev[s] = (float)__ddiv_rn(ssum[s], ms_d);
           bits |= RH_IT_STAGE_FLAG;
         }
       }
@@ -720,6 +741,12 @@ int launch_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
     // the region holds the staged documents, later the base costs
     const size_t region = std::max<size_t>(16 * 1024, (size_t)threads * p.mmax * 8);
     p.doc_stage = (int)(region / 4);
+    {
+      const char* e1 = getenv("RH_STATIC_MAX");
+      const char* e2 = getenv("RH_STATIC_DIV_MAX");
+      p.static_max = e1 ? atoi(e1) : kStaticMaxMB;
+      p.static_div_max = e2 ? atoi(e2) : kStaticMaxMB;
+    }
     const size_t smem = p.region_off + region;
     if (smem <= ctx->smem_optin && smem <= 56 * 1024) {
       const bool zbh = sh->schedule == RH_SCHED_ZBH;
