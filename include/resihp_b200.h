@@ -212,6 +212,20 @@ int rh_screen(rh_ctx* ctx, const rh_screen_params* params, int64_t series_len,
               const uint8_t* it_status, const uint8_t* reset, uint8_t* outcome,
               int64_t* series_len_out, void* stream);
 
+/*
+ * Optional early half of rh_screen: the parts that depend only on the inputs
+ * (reset indices and the round-0 median/MAD verdicts, which read observed,
+ * hist and reset but not it_status).  Launch it on a side stream as soon as
+ * those inputs are ready -- typically before rh_detect_batch, so it overlaps
+ * the detect kernel.  The next rh_screen on the same context with the same
+ * (params, series_len, hist, n, observed, reset) waits on it instead of
+ * recomputing; inputs must not change in between.  Any other rh_screen call
+ * recomputes as usual.
+ */
+int rh_screen_prepare(rh_ctx* ctx, const rh_screen_params* params, int64_t series_len,
+                      const double* hist, int64_t n, const double* observed,
+                      const uint8_t* reset, void* stream);
+
 /* ---------------------------------------------------- workload ingest */
 /*
  * pack_sequences (workload.py:52-80), HOST function: first-fit-decreasing

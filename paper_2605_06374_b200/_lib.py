@@ -113,6 +113,8 @@ _SIGS = {
     "rh_validate": ([_p, C.c_int64, _p, _p, C.c_double, _p, _p, _p], C.c_int),
     "rh_screen": ([_p, C.POINTER(ScreenParams), C.c_int64, _p, C.c_int64, _p, _p, _p, _p, _p,
                    _p], C.c_int),
+    "rh_screen_prepare": ([_p, C.POINTER(ScreenParams), C.c_int64, _p, C.c_int64, _p, _p, _p],
+                          C.c_int),
     "rh_dag_critical_path": ([_p, C.c_int32, _p, _p, _p, _p, C.c_int32, _p, _p, C.c_int32,
                               _p, _p, _p, _p, _p], C.c_int),
 }

@@ -162,6 +162,8 @@ int rh_ctx_destroy(rh_ctx* ctx) {
     if (e) cudaEventDestroy(e);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   for (auto& t : ctx->sched) cudaFree(t.dev);
+  if (ctx->prep.done) cudaEventDestroy(ctx->prep.done);
+  if (ctx->prep.consumed) cudaEventDestroy(ctx->prep.consumed);
   delete ctx;
   return RH_OK;
 }

@@ -19,9 +19,10 @@ struct rh_ctx {
   size_t smem_optin = 0;
   std::atomic<int64_t> launches{0};
   // grow-only device workspaces: slot 0 = host-buffer staging,
-  // slot 1 = kernel scratch (screen, general DAG); never aliased
-  void* ws[2] = {nullptr, nullptr};
-  size_t ws_bytes[2] = {0, 0};
+  // slot 1 = kernel scratch (screen, general DAG), slot 2 = rh_screen_prepare
+  // results (reset indices, round-0 verdicts); never aliased
+  void* ws[3] = {nullptr, nullptr, nullptr};
+  size_t ws_bytes[3] = {0, 0, 0};
   // host-buffer entry points: copy stream + per-chunk events (lazily made)
   static constexpr int kChunkEvents = 8;
   cudaStream_t copy_stream = nullptr;
@@ -34,6 +35,18 @@ struct rh_ctx {
   };
   std::vector<SchedTable> sched;
   std::mutex sched_mu;
+  // the last rh_screen_prepare: its arguments and completion event
+  struct ScreenPrep {
+    bool valid = false;
+    int32_t window = 0, filter_enabled = 0;
+    double kappa = 0.0;
+    int64_t series_len = 0, n = 0;
+    const void *hist = nullptr, *observed = nullptr, *reset = nullptr;
+    cudaEvent_t done = nullptr;
+    // recorded after each rh_screen: the slot-2 results are free again
+    cudaEvent_t consumed = nullptr;
+    bool consumed_recorded = false;
+  } prep;
 };
 
 namespace rh {

@@ -62,6 +62,7 @@ struct ScreenArgs {
   int32_t* R;                      // [n] last reset index <= i, or -1
   int32_t* bres;                   // [n/128] last reset inside each scan block
   uint8_t* state;                  // [2][n] bit0 popped, bit1 changed in that round
+  uint8_t* c0;                     // [n] round-0 verdicts (round0_kernel)
   unsigned* cnt;                   // [3] changes per round (rotating)
   unsigned* bar;                   // [2] barrier count, generation
   unsigned long long* kept_total;  // [2] kept count, block ticket
@@ -144,17 +145,17 @@ struct WarpScratch {
   double sel[2];
 };
 
-// One Jacobi step for iteration i, executed by a whole warp (uniform result).
-// x / stb are the iteration's observation and status; ob (optional) holds
+// Window part of one Jacobi step for iteration i, executed by a whole warp
+// (uniform result).  x is the iteration's observation; ob (optional) holds
 // obs[i-32+lane] so the common single-chunk window needs no global gather.
-// Returns the new pop bit, or kUnchanged when no change of the previous round
-// lies where it could reach iteration i.
-constexpr unsigned kUnchanged = 0xffu;
+// skip = no change of the previous round lies where it could reach i.
+struct WindowTest {
+  bool skip, cand, refill_len;  // refill_len: series still at most `window` long
+};
 
-__device__ __forceinline__ unsigned step_warp(const ScreenArgs& a, int64_t i, int r, double x,
-                                              unsigned stb, const double* ob,
-                                              const uint8_t* cur, bool first_round,
-                                              WarpScratch& ws) {
+__device__ __forceinline__ WindowTest window_test(const ScreenArgs& a, int64_t i, int r, double x,
+                                                  const double* ob, const uint8_t* cur,
+                                                  bool first_round, WarpScratch& ws) {
   const int lane = threadIdx.x & 31;
   const int w = a.w;
   const int64_t first = r >= 0 ? r : 0;
@@ -183,14 +184,15 @@ __device__ __forceinline__ unsigned step_warp(const ScreenArgs& a, int64_t i, in
       any_chg |= cm != 0u;
     }
   }
+  WindowTest t{false, false, false};
   if (!any_chg) {
     __syncwarp();
-    return kUnchanged;
+    t.skip = true;
+    return t;
   }
   // kept entries since the reset: exact below w, which is all the length
   // thresholds need
   const int64_t len = (r >= 0 ? found : a.len0 + found) + 1;
-  bool cand = false;
   if (len >= w + 1) {
     const int need = w - found;  // > 0 only without a reset: history entries
     for (int q = lane; q < need; q += 32) ws.win[q] = a.hist[a.h - need + q];
@@ -199,15 +201,24 @@ __device__ __forceinline__ unsigned step_warp(const ScreenArgs& a, int64_t i, in
     for (int q = lane; q < w; q += 32) ws.dev[q] = fabs(__dsub_rn(ws.win[q], med));
     __syncwarp();
     const double mad = warp_median(ws.dev, w, ws.sel);
-    cand = fabs(__dsub_rn(x, med)) > __dmul_rn(a.kappa, mad);
+    t.cand = fabs(__dsub_rn(x, med)) > __dmul_rn(a.kappa, mad);
   }
-  const bool refill = !cand && a.fe && len <= w;
+  t.refill_len = len <= w;
+  __syncwarp();  // the scratch is reused by the warp's next iteration
+  return t;
+}
+
+// Filter / validation part (detector.py:223-271): the pop decision and the
+// outcome bits from the screen verdict and the iteration's status bits.
+__device__ __forceinline__ unsigned outcome_of(bool cand, bool refill_len, unsigned stb, int fe,
+                                               uint8_t& oc_out) {
+  const bool refill = !cand && fe && refill_len;
   bool pop = false;
   uint8_t oc = 0;
   if (cand || refill) {
     oc = cand ? RH_SC_CANDIDATE : 0;
     bool done = false;
-    if (a.fe) {
+    if (fe) {
       oc |= RH_SC_FILTERED;
       if (!(stb & RH_IT_ESCALATE)) {
         if (cand) {
@@ -227,9 +238,32 @@ __device__ __forceinline__ unsigned step_warp(const ScreenArgs& a, int64_t i, in
       }
     }
   }
-  if (lane == 0) a.outcome[i] = oc;
-  __syncwarp();  // the scratch is reused by the warp's next iteration
+  oc_out = oc;
   return pop ? 1u : 0u;
+}
+
+// Round 0 (kept = all) of every iteration, one warp each over the whole GPU:
+// folds the reset index and runs the window test, which in this round only
+// depends on the inputs.  c0 = cand | refill_len << 1.
+constexpr int kRound0Threads = 256;
+
+__global__ void __launch_bounds__(kRound0Threads) round0_kernel(ScreenArgs a) {
+  __shared__ WarpScratch s_ws[kRound0Threads / 32];
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (i >= a.n) return;
+  const int lane = threadIdx.x & 31;
+  const double x = a.obs[i];
+  int r = a.R[i];
+  if (r < 0 && a.reset) {  // fold in the resets of earlier scan blocks
+    const int nb = (int)(i / kScanThreads);
+    for (int b = lane; b < nb; b += 32) r = max(r, a.bres[b]);
+    for (int o = 16; o > 0; o >>= 1) r = max(r, __shfl_xor_sync(0xffffffffu, r, o));
+  }
+  const WindowTest t = window_test(a, i, r, x, nullptr, nullptr, true, s_ws[threadIdx.x >> 5]);
+  if (lane == 0) {
+    a.R[i] = r;
+    a.c0[i] = (uint8_t)((t.cand ? 1 : 0) | (t.refill_len ? 2 : 0));
+  }
 }
 
 // What a warp keeps across rounds for each of its first kCache iterations.
@@ -286,38 +320,49 @@ __global__ void __launch_bounds__(kScreenThreads) screen_kernel(const ScreenArgs
       int r;
       double x;
       unsigned stb, old;
-      if (round == 0 || !cached) {
+      unsigned pop;
+      if (round == 0) {
+        // verdicts of round 0 came from round0_kernel; cache what later
+        // rounds need
         x = a.obs[i];
         stb = a.st[i];
-        if (round == 0) {  // fold in the resets of earlier scan blocks, once
-          r = a.R[i];
-          if (r < 0 && a.reset) {
-            const int nb = (int)(i / kScanThreads);
-            for (int b = lane; b < nb; b += 32) r = max(r, a.bres[b]);
-            for (int o = 16; o > 0; o >>= 1) r = max(r, __shfl_xor_sync(0xffffffffu, r, o));
-          }
-          old = 0;
+        r = a.R[i];
+        const unsigned c0 = a.c0[i];
+        if (cached) {
+          const int64_t j = i - 32 + lane;
+          s_ob[wid][k][lane] = j >= 0 ? a.obs[j] : 0.0;
+        }
+        uint8_t oc;
+        pop = outcome_of(c0 & 1u, (c0 & 2u) != 0u, stb, a.fe, oc);
+        if (lane == 0) {
+          a.outcome[i] = oc;
+          if (cached) s_it[wid][k] = IterCache{x, r, (uint8_t)stb, 0};
+        }
+        __syncwarp();
+        old = 0;
+      } else {
+        if (cached) {
+          const IterCache c = s_it[wid][k];
+          x = c.x;
+          r = c.r;
+          stb = c.st;
+          old = c.pop;
         } else {
+          x = a.obs[i];
+          stb = a.st[i];
           r = __ldcg(a.R + i);
           old = __ldcg(cur + i) & 1u;
         }
-        if (round == 0 && cached) {
-          const int64_t j = i - 32 + lane;
-          s_ob[wid][k][lane] = j >= 0 ? a.obs[j] : 0.0;
-          if (lane == 0) s_it[wid][k] = IterCache{x, r, (uint8_t)stb, 0};
+        const WindowTest t = window_test(a, i, r, x, cached ? s_ob[wid][k] : nullptr, cur, false,
+                                         s_ws[wid]);
+        if (t.skip) {
+          pop = old;
+        } else {
+          uint8_t oc;
+          pop = outcome_of(t.cand, t.refill_len, stb, a.fe, oc);
+          if (lane == 0) a.outcome[i] = oc;
         }
-        __syncwarp();
-        if (round == 0 && lane == 0) a.R[i] = r;
-      } else {
-        const IterCache c = s_it[wid][k];
-        x = c.x;
-        r = c.r;
-        stb = c.st;
-        old = c.pop;
       }
-      unsigned pop = step_warp(a, i, r, x, stb, cached ? s_ob[wid][k] : nullptr, cur,
-                               round == 0, s_ws[wid]);
-      if (pop == kUnchanged) pop = old;
       const unsigned changed = pop != old;
       if (lane == 0) {
         nxt[i] = (uint8_t)(pop | (changed << 1));
@@ -372,13 +417,29 @@ __global__ void __launch_bounds__(kScreenThreads) screen_kernel(const ScreenArgs
 
 using namespace rh;
 
-extern "C" int rh_screen(rh_ctx* ctx, const rh_screen_params* params, int64_t series_len,
-                         const double* hist, int64_t n, const double* observed,
-                         const uint8_t* it_status, const uint8_t* reset, uint8_t* outcome,
-                         int64_t* series_len_out, void* stream) {
+namespace {
+
+// Workspace carve shared by rh_screen_prepare and rh_screen.
+struct PrepLayout {
+  size_t oR, oRes, oC0, bytes;
+  explicit PrepLayout(int64_t n) {
+    size_t b = 0;
+    auto take = [&](size_t n_bytes) {
+      const size_t o = b;
+      b = (b + n_bytes + 255) & ~size_t(255);
+      return o;
+    };
+    oR = take(sizeof(int32_t) * n);
+    oRes = take(sizeof(int32_t) * ((n + kScanThreads - 1) / kScanThreads));
+    oC0 = take((size_t)n);
+    bytes = b;
+  }
+};
+
+int check_screen_args(const rh_ctx* ctx, const rh_screen_params* params, int64_t series_len,
+                      const double* hist, int64_t n, const double* observed) {
   if (!ctx || !params || n < 0 || series_len < 0 || params->window < 1 ||
-      params->window > kMaxWindow || (n && (!observed || !it_status || !outcome)) ||
-      (series_len > 0 && !hist)) {
+      params->window > kMaxWindow || (n && !observed) || (series_len > 0 && !hist)) {
     set_error("rh_screen: invalid arguments (window must be 1..%d)", kMaxWindow);
     return RH_E_INVALID;
   }
@@ -386,7 +447,94 @@ extern "C" int rh_screen(rh_ctx* ctx, const rh_screen_params* params, int64_t se
     set_error("rh_screen: batch too large");
     return RH_E_SHAPE;
   }
+  return RH_OK;
+}
+
+void fill_inputs(ScreenArgs& a, const rh_screen_params* params, int64_t series_len,
+                 const double* hist, int64_t n, const double* observed, const uint8_t* reset) {
+  a = ScreenArgs{};
+  a.w = params->window;
+  a.fe = params->filter_enabled != 0;
+  a.kappa = params->kappa;
+  a.len0 = series_len;
+  a.h = (int)std::min<int64_t>(series_len, params->window);
+  a.hist = hist;
+  a.n = n;
+  a.obs = observed;
+  a.reset = reset;
+}
+
+// reset indices + round-0 verdicts into the slot-2 workspace
+int launch_prepare(rh_ctx* ctx, ScreenArgs& a, cudaStream_t st) {
+  const PrepLayout L(a.n);
+  void* ws = nullptr;
+  if (int rc = workspace(ctx, L.bytes, &ws, 2)) return rc;
+  char* base = static_cast<char*>(ws);
+  a.R = reinterpret_cast<int32_t*>(base + L.oR);
+  a.bres = reinterpret_cast<int32_t*>(base + L.oRes);
+  a.c0 = reinterpret_cast<uint8_t*>(base + L.oC0);
+  const int64_t grid0 = (a.n + kScanThreads - 1) / kScanThreads;
+  if (a.reset) {
+    reset_scan_kernel<<<(unsigned)grid0, kScanThreads, 0, st>>>(a);
+    RH_CHECK_LAUNCH(ctx);
+  } else {
+    RH_CUDA(cudaMemsetAsync(a.R, 0xff, sizeof(int32_t) * a.n, st));  // no resets: all -1
+  }
+  const int64_t grid_r0 = (a.n * 32 + kRound0Threads - 1) / kRound0Threads;
+  round0_kernel<<<(unsigned)grid_r0, kRound0Threads, 0, st>>>(a);
+  RH_CHECK_LAUNCH(ctx);
+  return RH_OK;
+}
+
+}  // namespace
+
+extern "C" int rh_screen_prepare(rh_ctx* ctx, const rh_screen_params* params,
+                                 int64_t series_len, const double* hist, int64_t n,
+                                 const double* observed, const uint8_t* reset, void* stream) {
+  if (int rc = check_screen_args(ctx, params, series_len, hist, n, observed)) return rc;
+  ctx->prep.valid = false;
+  if (n == 0) return RH_OK;
   cudaStream_t st = as_stream(stream);
+  // the previous rh_screen may still read the slot-2 results
+  if (ctx->prep.consumed_recorded) RH_CUDA(cudaStreamWaitEvent(st, ctx->prep.consumed, 0));
+  ScreenArgs a;
+  fill_inputs(a, params, series_len, hist, n, observed, reset);
+  if (int rc = launch_prepare(ctx, a, st)) return rc;
+  if (!ctx->prep.done) RH_CUDA(cudaEventCreateWithFlags(&ctx->prep.done, cudaEventDisableTiming));
+  RH_CUDA(cudaEventRecord(ctx->prep.done, st));
+  auto& pr = ctx->prep;
+  pr.window = params->window;
+  pr.filter_enabled = params->filter_enabled;
+  pr.kappa = params->kappa;
+  pr.series_len = series_len;
+  pr.n = n;
+  pr.hist = hist;
+  pr.observed = observed;
+  pr.reset = reset;
+  pr.valid = true;
+  return RH_OK;
+}
+
+extern "C" int rh_screen(rh_ctx* ctx, const rh_screen_params* params, int64_t series_len,
+                         const double* hist, int64_t n, const double* observed,
+                         const uint8_t* it_status, const uint8_t* reset, uint8_t* outcome,
+                         int64_t* series_len_out, void* stream) {
+  if (int rc = check_screen_args(ctx, params, series_len, hist, n, observed)) return rc;
+  if (n && (!it_status || !outcome)) {
+    set_error("rh_screen: invalid arguments (NULL status / outcome)");
+    return RH_E_INVALID;
+  }
+  cudaStream_t st = as_stream(stream);
+  const auto& pr = ctx->prep;
+  const bool prepared = pr.valid && pr.window == params->window &&
+                        pr.filter_enabled == params->filter_enabled && pr.kappa == params->kappa &&
+                        pr.series_len == series_len && pr.n == n && pr.hist == hist &&
+                        pr.observed == observed && pr.reset == reset;
+  // a pending prepare may still be writing the slot-2 results: whether or not
+  // they are usable here, nothing below may touch them before it finishes
+  const bool pending = pr.valid;
+  ctx->prep.valid = false;  // one use
+  if (pending) RH_CUDA(cudaStreamWaitEvent(as_stream(stream), ctx->prep.done, 0));
   if (n == 0) {
     if (series_len_out)
       RH_CUDA(cudaMemcpyAsync(series_len_out, &series_len, sizeof(int64_t),
@@ -405,7 +553,20 @@ extern "C" int rh_screen(rh_ctx* ctx, const rh_screen_params* params, int64_t se
   int blocks = ctx->num_sms * std::min(occ, kScreenBlocksPerSm);
   blocks = (int)std::max<int64_t>(
       1, std::min<int64_t>(blocks, (n + 2 * kScreenWarps - 1) / (2 * kScreenWarps)));
-  const int64_t grid0 = (n + kScanThreads - 1) / kScanThreads;
+  ScreenArgs a;
+  fill_inputs(a, params, series_len, hist, n, observed, reset);
+  a.st = it_status;
+  a.outcome = outcome;
+  a.len_out = series_len_out;
+  if (prepared) {
+    const PrepLayout L(n);
+    char* pbase = static_cast<char*>(ctx->ws[2]);
+    a.R = reinterpret_cast<int32_t*>(pbase + L.oR);
+    a.bres = reinterpret_cast<int32_t*>(pbase + L.oRes);
+    a.c0 = reinterpret_cast<uint8_t*>(pbase + L.oC0);
+  } else if (int rc = launch_prepare(ctx, a, st)) {
+    return rc;
+  }
   size_t bytes = 0;
   auto take = [&](size_t n_bytes) {
     const size_t o = bytes;
@@ -416,41 +577,22 @@ extern "C" int rh_screen(rh_ctx* ctx, const rh_screen_params* params, int64_t se
   const size_t oBar = take(sizeof(unsigned) * 2), oCnt = take(sizeof(unsigned) * 3);
   const size_t oKept = take(sizeof(unsigned long long) * 2);
   const size_t ctrl = bytes;
-  const size_t oR = take(sizeof(int32_t) * n), oRes = take(sizeof(int32_t) * grid0);
   const size_t oSt = take(2 * (size_t)n);
   void* ws = nullptr;
-  int rc = workspace(ctx, bytes, &ws, 1);
-  if (rc) return rc;
+  if (int rc = workspace(ctx, bytes, &ws, 1)) return rc;
   char* base = static_cast<char*>(ws);
-  ScreenArgs a;
-  a.w = params->window;
-  a.fe = params->filter_enabled != 0;
-  a.kappa = params->kappa;
-  a.len0 = series_len;
-  a.h = (int)std::min<int64_t>(series_len, params->window);
-  a.hist = hist;
-  a.n = n;
-  a.obs = observed;
-  a.st = it_status;
-  a.reset = reset;
-  a.outcome = outcome;
-  a.len_out = series_len_out;
   a.bar = reinterpret_cast<unsigned*>(base + oBar);
   a.cnt = reinterpret_cast<unsigned*>(base + oCnt);
   a.kept_total = reinterpret_cast<unsigned long long*>(base + oKept);
-  a.R = reinterpret_cast<int32_t*>(base + oR);
-  a.bres = reinterpret_cast<int32_t*>(base + oRes);
   a.state = reinterpret_cast<uint8_t*>(base + oSt);
   RH_CUDA(cudaMemsetAsync(base, 0, ctrl, st));
-  if (reset) {
-    reset_scan_kernel<<<(unsigned)grid0, kScanThreads, 0, st>>>(a);
-    RH_CHECK_LAUNCH(ctx);
-  } else {
-    RH_CUDA(cudaMemsetAsync(a.R, 0xff, sizeof(int32_t) * n, st));  // no resets: all -1
-  }
   void* kargs[] = {&a};
   RH_CUDA(cudaLaunchCooperativeKernel((void*)screen_kernel, dim3(blocks), dim3(kScreenThreads),
                                       kargs, 0, st));
   RH_CHECK_LAUNCH(ctx);
+  if (!ctx->prep.consumed)
+    RH_CUDA(cudaEventCreateWithFlags(&ctx->prep.consumed, cudaEventDisableTiming));
+  RH_CUDA(cudaEventRecord(ctx->prep.consumed, st));
+  ctx->prep.consumed_recorded = true;
   return RH_OK;
 }

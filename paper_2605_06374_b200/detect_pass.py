@@ -1,11 +1,13 @@
 """Batched Detector pass over a device x iteration trace (the product path).
 
 ``DetectorPass(trace)`` moves a DetectorTrace into HBM once; ``run()`` is
-two launches on the current stream:
+``detect()`` then ``screen()``:
 
   1. rh_detect_batch — per iteration: quad loads, chunk costs, the
      canonical chunk-DAG critical path of the known view (Eq. 2), stage cost
      sums, the workload-aware filter and per-(replica,stage)/link validation;
+     alongside it, on a side stream, rh_screen_prepare (reset indices and the
+     round-0 median/MAD verdicts, which need only the observed series);
   2. rh_screen — the DetectorState.observe state machine (median/MAD
      change-point screen with benign/unconfirmed pops) for the whole trace.
 
@@ -55,6 +57,8 @@ class DetectorPass:
         self.model_c = cost_model_c(trace.model)
         self.lib = _lib.load_library()
         self.ctx = _lib.context(self.dev.index)
+        self._side = torch.cuda.Stream(self.dev)
+        self._start = torch.cuda.Event()
 
     def _shape(self, segs, capacity=None):
         tr = self.trace
@@ -85,7 +89,19 @@ class DetectorPass:
                                               _lib.stream_handle()), "rh_pipeline_batch")
         return ms, st, sc.view(n, G)
 
-    def detect(self, stream=None):
+    def detect(self, stream=None, prepare_screen: bool = True):
+        import torch
+
+        if prepare_screen and self.observed is not None:
+            # the screen's input-only half overlaps the detect kernel; it starts
+            # no earlier than this point of the main stream
+            main = stream if stream is not None else torch.cuda.current_stream(self.dev)
+            self._start.record(main)
+            self._side.wait_event(self._start)
+            _lib.check(self.lib.rh_screen_prepare(
+                self.ctx, _lib.C.byref(self.screen_params), 0, self.hist.data_ptr(),
+                self.trace.n_iter, self.observed.data_ptr(), self.reset.data_ptr(),
+                _lib.stream_handle(self._side)), "rh_screen_prepare")
         out = _lib.PassOut(self.makespan.data_ptr(), self.status.data_ptr(),
                            self.stage_cost.data_ptr() if self.stage_cost is not None else None,
                            self.stage_flag.data_ptr(), self.severity.data_ptr())

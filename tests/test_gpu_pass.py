@@ -131,3 +131,51 @@ def test_detector_pass_host_chunked(seed, oracle, cuda_device):
     np.testing.assert_array_equal(sv.view(np.uint32), osv.reshape(-1).view(np.uint32))
     np.testing.assert_array_equal(oc, ooc)
     assert ln.value == oln
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_screen_prepare_protocol(seed, oracle, cuda_device):
+    """rh_screen_prepare on a side stream + rh_screen == the oracle; a prepare
+    with different arguments is ignored (rh_screen recomputes); repeated
+    prepare/screen pairs do not race on the shared results."""
+    import torch
+
+    from paper_2605_06374_b200 import _lib
+
+    rng = np.random.default_rng(100 + seed)
+    n = 5000 + 1000 * seed
+    obs_h = 10.0 + rng.standard_normal(n) * 0.5
+    obs_h = np.where(rng.random(n) < 0.1, obs_h * 2.0, obs_h)
+    st_h = ((rng.random(n) < 0.3) | ((rng.random(n) < 0.2) << 1)).astype(np.uint8)
+    rst_h = (rng.random(n) < 0.002).astype(np.uint8)
+    dev = torch.device("cuda", 0)
+    obs = torch.from_numpy(obs_h).to(dev)
+    st = torch.from_numpy(st_h).to(dev)
+    rst = torch.from_numpy(rst_h).to(dev)
+    hist = torch.zeros(1, dtype=torch.float64, device=dev)
+    lib, ctx = _lib.load_library(), _lib.context(0)
+    side = torch.cuda.Stream(dev)
+    main = torch.cuda.current_stream(dev)
+
+    def run(w_prep, w_screen):
+        oc = torch.empty(n, dtype=torch.uint8, device=dev)
+        ln = torch.zeros(1, dtype=torch.int64, device=dev)
+        ev = torch.cuda.Event()
+        ev.record(main)
+        side.wait_event(ev)
+        _lib.check(lib.rh_screen_prepare(ctx, _lib.C.byref(_lib.ScreenParams(w_prep, 1, 3.0)), 0,
+                                         hist.data_ptr(), n, obs.data_ptr(), rst.data_ptr(),
+                                         _lib.stream_handle(side)), "prepare")
+        _lib.check(lib.rh_screen(ctx, _lib.C.byref(_lib.ScreenParams(w_screen, 1, 3.0)), 0,
+                                 hist.data_ptr(), n, obs.data_ptr(), st.data_ptr(),
+                                 rst.data_ptr(), oc.data_ptr(), ln.data_ptr(),
+                                 _lib.stream_handle(main)), "screen")
+        return oc, ln
+
+    for w_prep, w_screen in [(20, 20), (20, 20), (7, 20), (20, 5), (20, 20)]:
+        outs = [run(w_prep, w_screen) for _ in range(3)]
+        torch.cuda.synchronize()
+        ooc, oln = oracle.screen(obs_h, st_h, window=w_screen, reset=rst_h)
+        for oc, ln in outs:
+            np.testing.assert_array_equal(oc.cpu().numpy(), ooc)
+            assert int(ln.item()) == oln
