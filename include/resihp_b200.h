@@ -399,6 +399,9 @@ typedef struct rh_candidate {
  * (placement, hop/ring tables, repartition_layers, proportional_split) on
  * the GPU.  Synchronises `stream`. */
 int rh_search_create(rh_ctx* ctx, const rh_search_desc* desc, rh_search** out, void* stream);
+/* Returns the search's device memory to the stream-ordered pool on the stream
+ * of its latest create / eval call (so pending work on that stream finishes
+ * first); that stream must still exist. */
 int rh_search_destroy(rh_search* search);
 /* total number of candidates / layouts */
 int64_t rh_search_size(const rh_search* search);

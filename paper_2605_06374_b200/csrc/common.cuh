@@ -35,6 +35,8 @@ struct rh_ctx {
   };
   std::vector<SchedTable> sched;
   std::mutex sched_mu;
+  // the device's default memory pool keeps freed memory (re-plan searches)
+  bool pool_ready = false;
   // the last rh_screen_prepare: its arguments and completion event
   struct ScreenPrep {
     bool valid = false;

@@ -23,6 +23,7 @@
 // reconfiguration surcharge and keeps a lexicographic (score, index) min.
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <limits>
 #include <vector>
 
@@ -49,6 +50,7 @@ struct rh_search {
   // device memory (one allocation)
   void* dmem = nullptr;
   size_t dbytes = 0;
+  cudaStream_t last_stream = nullptr;  // stream of the latest create / eval
   struct Dev {
     int32_t *lT, *lD, *lP, *lgoff, *lpoff, *ldoff, *lboff, *lnb;
     long long *lbase, *lnv, *lnu, *lpair, *lrt;
@@ -113,82 +115,117 @@ __device__ __forceinline__ double hop_cost(const SearchArgs& a, int na, int nb, 
   return __dadd_rn(__ddiv_rn(a.nbytes, inter), gather);  // comm.py:76-78
 }
 
-// repartition_layers (scheduler.py:146-207), sequential, one thread
-__device__ void repartition_dev(const double* sp, int n, int L, int ml, int32_t* out) {
-  double tot = 0.0;
-  for (int i = 0; i < n; ++i) tot = __dadd_rn(tot, sp[i]);
-  double frac[32];
-  int lay[32];
-  int sum = 0;
-  for (int i = 0; i < n; ++i) {
-    const double share = __ddiv_rn(__dmul_rn((double)L, sp[i]), tot);
-    lay[i] = (int)floor(share);
-    frac[i] = __dsub_rn(share, (double)lay[i]);
-    sum += lay[i];
-  }
-  // largest remainder, ties to the earlier stage
-  bool used[32];
-  for (int i = 0; i < n; ++i) used[i] = false;
-  for (int r = 0; r < L - sum; ++r) {
-    int bi = -1;
-    for (int i = 0; i < n; ++i)
-      if (!used[i] && (bi < 0 || frac[i] > frac[bi])) bi = i;
-    used[bi] = true;
-    lay[bi] += 1;
-  }
-  // starved stages up to the floor, taking from the largest (ties: lowest)
-  for (;;) {
-    int rec = -1;
-    for (int i = 0; i < n; ++i)
-      if (lay[i] < ml) {
-        rec = i;
-        break;
-      }
-    if (rec < 0) break;
-    int don = -1;
-    for (int i = 0; i < n; ++i)
-      if (lay[i] > ml && (don < 0 || lay[i] > lay[don])) don = i;
-    if (don < 0) break;
-    lay[don] -= 1;
-    lay[rec] += 1;
-  }
-  const double min_gain = __ddiv_rn(1.0, __dmul_rn(2.0, (double)L));
-  auto stage_max = [&]() {
-    double m = 0.0;
-    bool first = true;
+// repartition_layers (scheduler.py:146-207), executed by a whole warp
+// (n <= 32 stages, lane i owns stage i).  The largest-remainder split and
+// the min_layers fix-up are tiny and run on lane 0; the greedy improvement
+// loop is lane-parallel: lane src scans every dst.  A move changes only two
+// stages, so its stage max is max(top value among the other stages,
+// (lay[src]-1)/sp[src], (lay[dst]+1)/sp[dst]) -- the same set of quotients
+// the reference maximises, hence the same double.  The reference's scan
+// order (src outer, dst inner, strict <) is reproduced by a lexicographic
+// (c, src, dst) warp argmin.
+__device__ void repartition_warp(const double* sp_in, int n, int L, int ml, int32_t* out) {
+  const int lane = threadIdx.x & 31;
+  const unsigned full = 0xffffffffu;
+  int lay0 = 0;
+  if (lane == 0) {
+    double tot = 0.0;
+    for (int i = 0; i < n; ++i) tot = __dadd_rn(tot, sp_in[i]);
+    double frac[32];
+    int lay[32];
+    int sum = 0;
     for (int i = 0; i < n; ++i) {
-      const double x = __ddiv_rn((double)lay[i], sp[i]);
-      if (first || x > m) m = x;
-      first = false;
+      const double share = __ddiv_rn(__dmul_rn((double)L, sp_in[i]), tot);
+      lay[i] = (int)floor(share);
+      frac[i] = __dsub_rn(share, (double)lay[i]);
+      sum += lay[i];
     }
-    return m;
-  };
-  for (;;) {
-    const double cur = stage_max();
-    const double bar = __dmul_rn(cur, __dsub_rn(1.0, min_gain));
-    double best = 0.0;
-    int bs = -1, bd = -1;
-    for (int src = 0; src < n; ++src) {
-      if (lay[src] <= ml) continue;
-      for (int dst = 0; dst < n; ++dst) {
-        if (dst == src) continue;
-        lay[src] -= 1;
-        lay[dst] += 1;
-        const double c = stage_max();
-        lay[src] += 1;
-        lay[dst] -= 1;
-        if (c < bar && (bs < 0 || c < best)) {
-          best = c;
-          bs = src;
-          bd = dst;
+    // largest remainder, ties to the earlier stage
+    unsigned used = 0u;
+    for (int r = 0; r < L - sum; ++r) {
+      int bi = -1;
+      for (int i = 0; i < n; ++i)
+        if (!(used >> i & 1u) && (bi < 0 || frac[i] > frac[bi])) bi = i;
+      used |= 1u << bi;
+      lay[bi] += 1;
+    }
+    // starved stages up to the floor, taking from the largest (ties: lowest)
+    for (;;) {
+      int rec = -1;
+      for (int i = 0; i < n; ++i)
+        if (lay[i] < ml) {
+          rec = i;
+          break;
         }
+      if (rec < 0) break;
+      int don = -1;
+      for (int i = 0; i < n; ++i)
+        if (lay[i] > ml && (don < 0 || lay[i] > lay[don])) don = i;
+      if (don < 0) break;
+      lay[don] -= 1;
+      lay[rec] += 1;
+    }
+    for (int i = 0; i < n; ++i) out[i] = lay[i];
+  }
+  __syncwarp();
+  const bool mine = lane < n;
+  int lay = mine ? out[lane] : 0;
+  const double sp = mine ? sp_in[lane] : 1.0;
+  (void)lay0;
+  const double min_gain = __ddiv_rn(1.0, __dmul_rn(2.0, (double)L));
+  const double NEG = -CUDART_INF;
+  for (;;) {
+    const double t = mine ? __ddiv_rn((double)lay, sp) : NEG;
+    const double dec = mine ? __ddiv_rn((double)(lay - 1), sp) : NEG;
+    const double inc = mine ? __ddiv_rn((double)(lay + 1), sp) : NEG;
+    // top three quotients (distinct stages, ties in any order)
+    double v1 = t;
+    for (int o = 16; o > 0; o >>= 1) v1 = fmax(v1, __shfl_xor_sync(full, v1, o));
+    const int i1 = __ffs(__ballot_sync(full, t == v1)) - 1;
+    const double t2 = lane == i1 ? NEG : t;
+    double v2 = t2;
+    for (int o = 16; o > 0; o >>= 1) v2 = fmax(v2, __shfl_xor_sync(full, v2, o));
+    const int i2 = __ffs(__ballot_sync(full, t2 == v2 && lane != i1)) - 1;
+    const double t3 = (lane == i1 || lane == i2) ? NEG : t;
+    double v3 = t3;
+    for (int o = 16; o > 0; o >>= 1) v3 = fmax(v3, __shfl_xor_sync(full, v3, o));
+    const int i3 = __ffs(__ballot_sync(full, t3 == v3 && lane != i1 && lane != i2)) - 1;
+    const double cur = v1;  // stage max of the current partition
+    const double bar = __dmul_rn(cur, __dsub_rn(1.0, min_gain));
+    // lane = src: the first dst (ascending) with the smallest c < bar
+    double best = CUDART_INF;
+    int bd = -1;
+    const bool can = mine && lay > ml;
+    for (int dst = 0; dst < n; ++dst) {
+      const double inc_d = __shfl_sync(full, inc, dst);
+      if (!can || dst == lane) continue;
+      const double rest = (i1 != lane && i1 != dst) ? v1 : (i2 != lane && i2 != dst) ? v2
+                                                        : (i3 >= 0 ? v3 : NEG);
+      double c = rest > dec ? rest : dec;
+      c = c > inc_d ? c : inc_d;
+      if (c < bar && (bd < 0 || c < best)) {
+        best = c;
+        bd = dst;
       }
     }
-    if (bs < 0) break;
-    lay[bs] -= 1;
-    lay[bd] += 1;
+    // lexicographic (c, src) argmin over lanes: ties keep the smaller src
+    double wb = bd >= 0 ? best : CUDART_INF;
+    int ws = bd >= 0 ? lane : 64;
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(full, wb, o);
+      const int os = __shfl_xor_sync(full, ws, o);
+      if (ob < wb || (ob == wb && os < ws)) {
+        wb = ob;
+        ws = os;
+      }
+    }
+    if (ws == 64) break;  // no improving move
+    const int wd = __shfl_sync(full, bd, ws);
+    if (lane == ws) lay -= 1;
+    if (lane == wd) lay += 1;
   }
-  for (int i = 0; i < n; ++i) out[i] = lay[i];
+  if (mine) out[lane] = lay;
+  __syncwarp();
 }
 
 // proportional_split (policies.py:151-162) -> prefix starts[n+1]
@@ -295,9 +332,9 @@ __global__ void prep_kernel(SearchArgs a) {
     same = __all_sync(0xffffffffu, same);
   }
   __syncwarp();
+  repartition_warp(a.v.sspeed + poff, P, a.L, a.min_layers, a.v.repart + poff);
   if (lane == 0) {
     a.v.same[warp] = same;
-    repartition_dev(a.v.sspeed + poff, P, a.L, a.min_layers, a.v.repart + poff);
     proportional_dev(a.M, a.v.rspeed + doff, D, a.v.pstart + doff + warp);
   }
 }
@@ -722,9 +759,10 @@ int rh_search_create(rh_ctx* ctx, const rh_search_desc* desc, rh_search** out, v
     return RH_OK;
   }
   // ---- device memory
-  int max_blocks_per_sm = 0;
-  RH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_blocks_per_sm, table_kernel<0>,
-                                                        kEvalThreads, 0));
+  static int max_blocks_per_sm = -1;  // cached occupancy of the table kernel
+  if (max_blocks_per_sm < 0)
+    RH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_blocks_per_sm, table_kernel<0>,
+                                                          kEvalThreads, 0));
   S->eval_blocks = ctx->num_sms * std::max(1, max_blocks_per_sm);
   size_t bytes = 0;
   auto take = [&](size_t n) {
@@ -761,6 +799,7 @@ int rh_search_create(rh_ctx* ctx, const rh_search_desc* desc, rh_search** out, v
                o_lf = up(S->link_factor.data(), 8 * S->link_factor.size()),
                o_cg = up(S->cur_groups.data(), 4 * S->cur_groups.size()),
                o_cp = up(S->cur_partition.data(), 4 * S->cur_partition.size());
+  const size_t up_bytes = bytes;  // everything uploaded sits in front
   const size_t o_gblk = take(4 * S->n_groups), o_gnode = take(4 * S->n_groups),
                o_gspeed = take(8 * S->n_groups), o_ghop = take(8 * S->n_groups),
                o_ring = take(8 * S->n_stage), o_sspeed = take(8 * S->n_stage),
@@ -770,16 +809,31 @@ int rh_search_create(rh_ctx* ctx, const rh_search_desc* desc, rh_search** out, v
                o_bb = take(8 * (size_t)S->eval_blocks), o_bi = take(8 * (size_t)S->eval_blocks),
                o_rtab = take(8 * (size_t)S->n_rt), o_pinfo = take(16 * (size_t)S->n_pairs),
                o_tasks = take(sizeof(PhaseTask) * (size_t)NL);
-  cudaError_t e = cudaMalloc(&S->dmem, bytes);
+  // stream-ordered pool: after the first re-plan the memory is reused, not
+  // mapped again (the pool keeps what it has; see rh_ctx::pool_ready)
+  if (!ctx->pool_ready) {
+    cudaMemPool_t pool;
+    RH_CUDA(cudaDeviceGetDefaultMemPool(&pool, ctx->device));
+    uint64_t keep = ~0ull;
+    RH_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    ctx->pool_ready = true;
+  }
+  cudaError_t e = cudaMallocAsync(&S->dmem, bytes, st);
   if (e != cudaSuccess) {
     delete S;
     set_error("rh_search_create: %zu bytes: %s", bytes, cudaGetErrorString(e));
     return RH_E_NOMEM;
   }
   S->dbytes = bytes;
+  S->last_stream = st;
   char* B = static_cast<char*>(S->dmem);
-  for (const Up& u : ups)
-    if (u.n) RH_CUDA(cudaMemcpyAsync(B + u.off, u.src, u.n, cudaMemcpyHostToDevice, st));
+  {  // one host staging buffer, one copy
+    std::vector<char> stage(up_bytes, 0);
+    for (const Up& u : ups)
+      if (u.n) memcpy(stage.data() + u.off, u.src, u.n);
+    RH_CUDA(cudaMemcpyAsync(B, stage.data(), up_bytes, cudaMemcpyHostToDevice, st));
+    RH_CUDA(cudaStreamSynchronize(st));  // the staging buffer dies here
+  }
   auto I = [&](size_t o) { return reinterpret_cast<int32_t*>(B + o); };
   auto Dp = [&](size_t o) { return reinterpret_cast<double*>(B + o); };
   auto LL = [&](size_t o) { return reinterpret_cast<long long*>(B + o); };
@@ -810,7 +864,8 @@ int rh_search_create(rh_ctx* ctx, const rh_search_desc* desc, rh_search** out, v
 
 int rh_search_destroy(rh_search* S) {
   if (!S) return RH_OK;
-  if (S->dmem) cudaFree(S->dmem);
+  // back to the pool, ordered after the latest work issued on the search
+  if (S->dmem) cudaFreeAsync(S->dmem, S->last_stream);
   delete S;
   return RH_OK;
 }
@@ -834,6 +889,7 @@ int rh_search_eval(rh_ctx* ctx, rh_search* S, int64_t begin, int64_t end, double
     RH_CUDA(cudaMemcpyAsync(best_index, &none, 8, cudaMemcpyHostToDevice, st));
     return RH_OK;
   }
+  S->last_stream = st;
   SearchArgs a = make_args(S);
   const long long n = end - begin;
   // phase 1 tasks: (layout, partition variant) pairs overlapping the range
@@ -935,10 +991,11 @@ int rh_search_decode(rh_ctx* ctx, rh_search* S, int64_t index, rh_candidate* out
 // functions the search prep uses, exposed for the drop-in resihp_adapt.
 namespace rh {
 
+// one warp per problem
 __global__ void repartition_batch_kernel(int n, const int32_t* off, const double* sp,
                                          const int32_t* L, const int32_t* ml, int32_t* out,
                                          int32_t* err) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (i >= n) return;
   const int a = off[i], P = off[i + 1] - a;
   int e = 0;
@@ -946,8 +1003,8 @@ __global__ void repartition_batch_kernel(int n, const int32_t* off, const double
   for (int s = 0; s < P && !e; ++s)
     if (!(sp[a + s] > 0.0)) e = 1;  // "all stage speeds must be positive"
   if (!e && L[i] < P * ml[i]) e = 2;  // "cannot give n stages ..."
-  err[i] = e;
-  if (!e) repartition_dev(sp + a, P, L[i], ml[i], out + a);
+  if ((threadIdx.x & 31) == 0) err[i] = e;
+  if (!e) repartition_warp(sp + a, P, L[i], ml[i], out + a);
 }
 
 __global__ void proportional_batch_kernel(int n, const int32_t* off, const double* w,
@@ -1014,7 +1071,7 @@ int rh_repartition_batch(rh_ctx* ctx, int32_t n, const int32_t* off, const doubl
     return RH_E_INVALID;
   }
   if (!n) return RH_OK;
-  repartition_batch_kernel<<<(n + 127) / 128, 128, 0, as_stream(stream)>>>(
+  repartition_batch_kernel<<<(n * 32 + 127) / 128, 128, 0, as_stream(stream)>>>(
       n, off, speeds, total_layers, min_layers, out, err);
   RH_CHECK_LAUNCH(ctx);
   return RH_OK;
