@@ -56,7 +56,7 @@ struct rh_search {
     long long *lbase, *lnv, *lnu, *lpair, *lrt;
     double* rtab;   // replica table [sum over layouts nv*8*D]
     double* pinfo;  // per (layout, v): all-reduce cost (-1: none), surcharge (inf: infeasible)
-    void* tasks;    // PhaseTask[n_layouts]
+    void* tasks;    // PipeTask[n_layouts]
     int32_t *blk_node, *blk_rank, *blk_members, *blk_moff;
     double* blk_speed;
     int32_t *gblk, *gnode;
@@ -72,7 +72,12 @@ struct rh_search {
     double* link_factor;
     double* blk_best;
     long long* blk_idx;
+    double* rl;  // [n_pairs][3][32] ratio * layers (rl_kernel)
+    // op lists of the pipe kernel (separate pooled allocation)
+    const uint32_t* ops;
+    const int32_t *tab_off, *tab_cnt, *tab_peak;  // [33][M+2]
   } dv{};
+  void* dops = nullptr;
   int eval_blocks = 0;
   size_t n_groups = 0, n_stage = 0, n_rep = 0;
 };
@@ -87,6 +92,8 @@ struct SearchArgs {
   double intra, inter, nbytes, lb, worst_inter, rebuild_s;
   int amort;
   int cur_T, cur_D, cur_P, T0;
+  double r_bw;     // ratio_b + ratio_w (1F1B's fused BW chunk)
+  int tab_stride;  // op-list index: slot = P * tab_stride + md
   rh_search::Dev v;
 };
 
@@ -127,7 +134,6 @@ __device__ __forceinline__ double hop_cost(const SearchArgs& a, int na, int nb, 
 __device__ void repartition_warp(const double* sp_in, int n, int L, int ml, int32_t* out) {
   const int lane = threadIdx.x & 31;
   const unsigned full = 0xffffffffu;
-  int lay0 = 0;
   if (lane == 0) {
     double tot = 0.0;
     for (int i = 0; i < n; ++i) tot = __dadd_rn(tot, sp_in[i]);
@@ -171,7 +177,6 @@ __device__ void repartition_warp(const double* sp_in, int n, int L, int ml, int3
   const bool mine = lane < n;
   int lay = mine ? out[lane] : 0;
   const double sp = mine ? sp_in[lane] : 1.0;
-  (void)lay0;
   const double min_gain = __ddiv_rn(1.0, __dmul_rn(2.0, (double)L));
   const double NEG = -CUDART_INF;
   for (;;) {
@@ -351,14 +356,59 @@ __device__ __forceinline__ bool lex_less(double a, long long ia, double b, long 
 //   (start, end) = 2 (0,-1)  3 (-1,-1)  4 (-1,0)  5 (0,+1)  6 (+1,+1)  7 (+1,0)
 // (moving one micro-batch src->dst shifts every replica between them by one).
 // Infeasible ranges / capacity overflow are stored as +inf.
+//
+// One THREAD per (layout, v, case, replica) pipeline.  It walks the
+// replica's chunks in the order of the op list for (P, md) -- DAG level
+// ascending, stage descending (wavefront.cuh closed forms), built on the
+// host for the (P, md) pairs that can occur -- so every dependency is final
+// when read (see pipeline.cu's small kernel for the argument) and no lane
+// idles.  Per-stage state lives in shared memory laid out [field][stage]
+// [thread] (conflict-free):  for 1F1B the finish of the last F and of the
+// last BW -- the chain's own finish is their max, finishes being monotone
+// along a chain -- and for ZBH also the chain finish (W feeds nothing).
 __constant__ int kDs[8] = {0, 0, 0, -1, -1, 0, 1, 1};
 __constant__ int kDe[8] = {0, 0, -1, -1, 0, 1, 1, 0};
 
-struct PhaseTask {
+struct PipeTask {
   int layout;
   int v_lo;
-  long long task_base;
+  long long pipe_base;  // first pipeline id of this task
+  long long row_base;   // first (layout, v) row of this task (rl_kernel)
 };
+
+// op list entry: stage (bits 0-5) | kind << 6 (1 F, 2 B or BW, 3 W)
+//                | dependency << 8 (0 none, 1 F of stage-1, 2 B of stage+1) | j << 10
+enum : unsigned { kOpF = 1, kOpB = 2, kOpW = 3 };
+
+// per (layout, v) pair: rl[kind-1][s] = ratio(kind) * L_s  (workload.py:88-98)
+__global__ void rl_kernel(SearchArgs a, const PipeTask* tk, int n_tk, int P, long long n_rows) {
+  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n_rows * P) return;
+  const long long row = g / P;
+  const int s = (int)(g % P);
+  int lo = 0, hi = n_tk - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (tk[mid].row_base <= row) lo = mid;
+    else hi = mid - 1;
+  }
+  const int li = tk[lo].layout;
+  const int vv = tk[lo].v_lo + (int)(row - tk[lo].row_base);
+  const int32_t* rep = a.v.repart + a.v.lpoff[li];
+  int psrc = -1, pdst = -1;
+  if (vv >= 2) {
+    const int m = vv - 2, r = m % (P - 1);
+    psrc = m / (P - 1);
+    pdst = r < psrc ? r : r + 1;
+  }
+  const int Ls = vv == 0 ? a.L / P + (s < a.L % P ? 1 : 0)
+                         : rep[s] + (s == pdst ? 1 : 0) - (s == psrc ? 1 : 0);
+  const double L = (double)Ls;
+  double* out = a.v.rl + (a.v.lpair[li] + vv) * 3LL * 32;
+  out[s] = __dmul_rn(a.m.ratio_f, L);
+  out[32 + s] = __dmul_rn(a.sched == RH_SCHED_ZBH ? a.m.ratio_b : a.r_bw, L);
+  out[64 + s] = __dmul_rn(a.m.ratio_w, L);
+}
 
 __device__ __forceinline__ int layer_of(const SearchArgs& a, const int32_t* rep, int P, int vv,
                                         int psrc, int pdst, int s) {
@@ -366,33 +416,27 @@ __device__ __forceinline__ int layer_of(const SearchArgs& a, const int32_t* rep,
                  : rep[s] + (s == pdst ? 1 : 0) - (s == psrc ? 1 : 0);
 }
 
+constexpr int kPipeThreads = 128;
+
 template <int ZBH>
-__global__ void __launch_bounds__(kEvalThreads) table_kernel(SearchArgs a, const PhaseTask* tk,
-                                                            int n_tk, long long n_tasks) {
-  const int lane = threadIdx.x & 31;
-  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
-  const int c = ZBH ? 3 : 2;
-  for (long long t = gw; t < n_tasks; t += nw) {
+__global__ void __launch_bounds__(kPipeThreads) pipe_kernel(SearchArgs a, const PipeTask* tk,
+                                                           int n_tk, long long n_pipes, int P) {
+  extern __shared__ double pipe_smem[];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (long long g = (long long)blockIdx.x * nt + tid; g < n_pipes;
+       g += (long long)gridDim.x * nt) {
     int lo = 0, hi = n_tk - 1;
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
-      if (tk[mid].task_base <= t) lo = mid;
+      if (tk[mid].pipe_base <= g) lo = mid;
       else hi = mid - 1;
     }
     const int li = tk[lo].layout;
-    const int D = a.v.lD[li], P = a.v.lP[li];
-    int pw = 1, lpw = 0;
-    while (pw < P) {
-      pw <<= 1;
-      ++lpw;
-    }
-    const int R = 32 >> lpw, nb = (D + R - 1) / R;
-    const long long tl = t - tk[lo].task_base;
-    const int vv = tk[lo].v_lo + (int)(tl / (8 * nb));
-    const int rr = (int)(tl % (8 * nb));
-    const int cs = rr / nb, batch = rr % nb;
-    const int s = lane & (pw - 1), slot = lane >> lpw;
+    const int D = a.v.lD[li];
+    const long long local = g - tk[lo].pipe_base;
+    const int vv = tk[lo].v_lo + (int)(local / (8 * D));
+    const int rr = (int)(local % (8 * D));
+    const int cs = rr / D, d = rr % D;
     const int goff = a.v.lgoff[li], poff = a.v.lpoff[li];
     const int32_t* rep = a.v.repart + poff;
     const int32_t* pst = a.v.pstart + a.v.ldoff[li] + li;
@@ -404,81 +448,125 @@ __global__ void __launch_bounds__(kEvalThreads) table_kernel(SearchArgs a, const
     }
     const bool feas_v = !(psrc >= 0 && rep[psrc] - 1 < a.min_layers);
     const long long pair = a.v.lpair[li] + vv;
-    double* Rp = a.v.rtab + a.v.lrt[li] + (long long)vv * 8 * D;
-    const int Ls = s < P ? layer_of(a, rep, P, vv, psrc, pdst, s) : 0;
-    const double L = (double)Ls;
-    if (cs == 0 && batch == 0) {
+    if (cs == 0 && d == 0) {
       // per (layout, v): all-reduce vertex (pipeline.py:356-372) and the
       // amortised reconfiguration surcharge (scheduler.py:562-593)
       const bool has_ar = a.has_comm && D > 1;
       double ar = 0.0;
-      if (has_ar && s < P) {
-        const double nbytes = __dmul_rn(L, a.lb);
-        ar = __ddiv_rn(__dmul_rn(__dmul_rn(2.0, nbytes), (double)(D - 1)),
-                       __dmul_rn((double)D, a.v.ring[poff + s]));
-      }
-      for (int o = 16; o > 0; o >>= 1) ar = fmax(ar, __shfl_xor_sync(0xffffffffu, ar, o));
-      if (lane == 0) {
-        const bool same_layout = a.v.same[li] != 0;
-        const bool sameP = P == a.cur_P;
-        bool changed = false;
-        long long moved = 0;
-        for (int q = 0; q < P && sameP; ++q) {
-          const int lq = layer_of(a, rep, P, vv, psrc, pdst, q);
-          const int old = a.v.cur_partition[q];
-          if (lq != old) changed = true;
-          if (lq > old) moved += lq - old;
+      if (has_ar)
+        for (int q = 0; q < P; ++q) {
+          const double nbytes = __dmul_rn((double)layer_of(a, rep, P, vv, psrc, pdst, q), a.lb);
+          ar = fmax(ar, __ddiv_rn(__dmul_rn(__dmul_rn(2.0, nbytes), (double)(D - 1)),
+                                  __dmul_rn((double)D, a.v.ring[poff + q])));
         }
-        double reshard = 0.0;
-        if (!same_layout)
-          for (int dd = 0; dd < D; ++dd)
-            for (int q = 0; q < P; ++q)
-              reshard = __dadd_rn(reshard,
-                                  __dmul_rn((double)layer_of(a, rep, P, vv, psrc, pdst, q), a.lb));
-        double sur = 0.0;
-        if (!same_layout || changed) {
-          const double transfer = __ddiv_rn(__dadd_rn(__dmul_rn((double)moved, a.lb), reshard),
-                                            a.worst_inter);
-          sur = __ddiv_rn(__dadd_rn(a.rebuild_s, transfer), (double)max(1, a.amort));
-        }
-        a.v.pinfo[2 * pair] = has_ar ? ar : -1.0;  // -1: no all-reduce vertex
-        a.v.pinfo[2 * pair + 1] = feas_v ? sur : CUDART_INF;
+      const bool same_layout = a.v.same[li] != 0;
+      const bool sameP = P == a.cur_P;
+      bool changed = false;
+      long long moved = 0;
+      for (int q = 0; q < P && sameP; ++q) {
+        const int lq = layer_of(a, rep, P, vv, psrc, pdst, q);
+        const int old = a.v.cur_partition[q];
+        if (lq != old) changed = true;
+        if (lq > old) moved += lq - old;
       }
+      double reshard = 0.0;
+      if (!same_layout)
+        for (int dd = 0; dd < D; ++dd)
+          for (int q = 0; q < P; ++q)
+            reshard = __dadd_rn(reshard,
+                                __dmul_rn((double)layer_of(a, rep, P, vv, psrc, pdst, q), a.lb));
+      double sur = 0.0;
+      if (!same_layout || changed) {
+        const double transfer = __ddiv_rn(__dadd_rn(__dmul_rn((double)moved, a.lb), reshard),
+                                          a.worst_inter);
+        sur = __ddiv_rn(__dadd_rn(a.rebuild_s, transfer), (double)max(1, a.amort));
+      }
+      a.v.pinfo[2 * pair] = has_ar ? ar : -1.0;  // -1: no all-reduce vertex
+      a.v.pinfo[2 * pair + 1] = feas_v ? sur : CUDART_INF;
     }
-    const int d = batch * R + slot;
     int start = 0, md = 0;
-    bool valid = d < D;
-    if (valid) {
-      if (cs == 0) {
-        const int base = a.M / D, extra = a.M % D;
-        start = d * base + min(d, extra);
-        md = base + (d < extra ? 1 : 0);
-      } else {
-        start = pst[d] + kDs[cs];
-        md = pst[d + 1] + kDe[cs] - start;
-        valid = start >= 0 && md >= 0 && start + md <= a.M;
+    bool valid = true;
+    if (cs == 0) {
+      const int base = a.M / D, extra = a.M % D;
+      start = d * base + min(d, extra);
+      md = base + (d < extra ? 1 : 0);
+    } else {
+      start = pst[d] + kDs[cs];
+      md = pst[d + 1] + kDe[cs] - start;
+      valid = start >= 0 && md >= 0 && start + md <= a.M;
+    }
+    double res = CUDART_INF;
+    if (feas_v && valid) {
+      const int slot = P * a.tab_stride + md;
+      const int e0 = __ldg(a.v.tab_off + slot), ne = __ldg(a.v.tab_cnt + slot);
+      const bool over = a.cap > 0 && __ldg(a.v.tab_peak + slot) > a.cap;
+      // state index: ((field * P) + stage) * kPipeThreads + tid; fields 0 LF, 1 LB, 2 FN
+      const int fB = P * kPipeThreads, fN = 2 * P * kPipeThreads;
+      for (int q = 0; q < P; ++q) {
+        pipe_smem[q * kPipeThreads + tid] = 0.0;
+        pipe_smem[fB + q * kPipeThreads + tid] = 0.0;
+        if (ZBH) pipe_smem[fN + q * kPipeThreads + tid] = 0.0;
       }
+      const double* bs = a.v.base + start;
+      const double* sp_d = a.v.gspeed + goff + d * P;
+      const double* hop_d = a.v.ghop + goff + d * P;
+      const double* rlt = a.v.rl + pair * 3LL * 32 - 32;  // indexed by kind * 32 + s
+      const uint32_t* opp = a.v.ops + e0;
+      // software pipeline: op codes two ahead, their global operands one ahead,
+      // so only the shared-memory state chain is serial
+      struct Operands {
+        unsigned op;
+        double rl, b, sp, hop;
+      };
+      auto fetch = [&](unsigned op) {
+        Operands o;
+        o.op = op;
+        const int st = op & 63u;
+        const unsigned kind = (op >> 6) & 3u, dk = (op >> 8) & 3u;
+        o.rl = __ldg(rlt + kind * 32 + st);
+        o.b = __ldg(bs + (op >> 10));
+        o.sp = __ldg(sp_d + st);
+        o.hop = dk ? __ldg(hop_d + st - (dk == 1 ? 1 : 0)) : 0.0;
+        return o;
+      };
+      unsigned op2 = ne > 1 ? __ldg(opp + 1) : 0u;
+      Operands nx = ne > 0 ? fetch(__ldg(opp)) : Operands{};
+      for (int e = 0; e < ne; ++e) {
+        const Operands o = nx;
+        const unsigned op3 = e + 2 < ne ? __ldg(opp + e + 2) : 0u;
+        if (e + 1 < ne) nx = fetch(op2);
+        op2 = op3;
+        const int st = o.op & 63u;
+        const unsigned kind = (o.op >> 6) & 3u, dk = (o.op >> 8) & 3u;
+        double c = __dmul_rn(o.rl, o.b);
+        if (o.sp != 1.0) c = div_slow(c, o.sp);  // out of line: unit speeds skip it
+        const int self = st * kPipeThreads + tid;
+        double dep = 0.0;
+        if (dk) {
+          // F: last F of stage-1 (+ hop s-1 -> s); B: last B of stage+1 (+ hop s)
+          const int src = dk == 1 ? self - kPipeThreads : fB + self + kPipeThreads;
+          dep = __dadd_rn(pipe_smem[src], o.hop);
+        }
+        double fin;
+        if (ZBH) {
+          fin = pipe_smem[fN + self];
+        } else {
+          const double x = pipe_smem[self], y = pipe_smem[fB + self];
+          fin = x > y ? x : y;
+        }
+        const double nf = __dadd_rn(fin > dep ? fin : dep, c);
+        if (ZBH) pipe_smem[fN + self] = nf;
+        if (kind != kOpW) pipe_smem[(kind == kOpF ? 0 : fB) + self] = nf;
+      }
+      double gm = 0.0;
+      for (int q = 0; q < P; ++q) {
+        const int self = q * kPipeThreads + tid;
+        const double f = ZBH ? pipe_smem[fN + self] : fmax(pipe_smem[self], pipe_smem[fB + self]);
+        gm = fmax(gm, f);
+      }
+      res = over ? CUDART_INF : gm;
     }
-    const bool on = feas_v && valid && s < P;
-    double sp = 1.0, hopf = 0.0, hopb = 0.0;
-    if (on) {
-      sp = a.v.gspeed[goff + d * P + s];
-      if (s > 0) hopf = a.v.ghop[goff + d * P + s - 1];
-      if (s < P - 1) hopb = a.v.ghop[goff + d * P + s];
-    }
-    const double rlF = __dmul_rn(a.m.ratio_f, L);
-    const double rlB = __dmul_rn(ZBH ? a.m.ratio_b : __dadd_rn(a.m.ratio_b, a.m.ratio_w), L);
-    const double rlW = __dmul_rn(a.m.ratio_w, L);
-    const int w = min(P - 1 - s, md);
-    double fin = 0.0, ssum = 0.0;
-    bool over = false, hung = false;
-    chain_walk<ZBH>(s, P, pw, on ? md : 0, w, on ? c * md : 0, a.v.base + (on ? start : 0), rlF,
-                    rlB, rlW, sp, hopf, hopb, a.cap, a.M, fin, ssum, over, hung);
-    double g = fin;
-    for (int o = pw >> 1; o > 0; o >>= 1) g = fmax(g, __shfl_xor_sync(0xffffffffu, g, o));
-    const unsigned gm = pw == 32 ? 0xffffffffu : (((1u << pw) - 1u) << (slot * pw));
-    const bool bad = (__ballot_sync(0xffffffffu, over || hung) & gm) != 0;
-    if (s == 0 && d < D) Rp[cs * D + d] = (bad || !valid || !feas_v) ? CUDART_INF : g;
+    a.v.rtab[a.v.lrt[li] + (long long)vv * 8 * D + cs * D + d] = res;
   }
 }
 
@@ -630,8 +718,97 @@ static SearchArgs make_args(const rh_search* S) {
   a.cur_D = d.cur_dp;
   a.cur_P = d.cur_pp;
   a.T0 = d.nominal_tp > 0 ? d.nominal_tp : 1;
+  a.r_bw = d.model.ratio_b + d.model.ratio_w;
+  a.tab_stride = d.n_micro_batches + 2;
   a.v = S->dv;
   return a;
+}
+
+}  // namespace rh
+
+namespace rh {
+
+// Op lists of the pipe kernel for every (P, md) a pipeline of this search can
+// have: the even split (M/D, M/D+1) and the proportional counts +-1 of every
+// layout (read back after prep_kernel).  Entry order: DAG level ascending,
+// stage descending; peak = most forward chunks in flight on any stage.
+static int build_op_lists(rh_ctx* ctx, rh_search* S, cudaStream_t st) {
+  const int NL = (int)S->lT.size(), M = S->d.n_micro_batches;
+  const int stride = M + 2;
+  const bool zbh = S->d.schedule == RH_SCHED_ZBH;
+  std::vector<int32_t> pst(S->n_rep + NL);
+  RH_CUDA(cudaMemcpyAsync(pst.data(), S->dv.pstart, 4 * pst.size(), cudaMemcpyDeviceToHost, st));
+  RH_CUDA(cudaStreamSynchronize(st));
+  std::vector<char> need(33 * (size_t)stride, 0);
+  for (int li = 0; li < NL; ++li) {
+    const int D = S->lD[li], P = S->lP[li];
+    char* row = need.data() + (size_t)P * stride;
+    row[M / D] = 1;
+    row[std::min(M, M / D + 1)] = 1;
+    const int32_t* ps = pst.data() + S->ldoff[li] + li;
+    for (int dd = 0; dd < D; ++dd) {
+      const int c = ps[dd + 1] - ps[dd];
+      for (int x = c - 1; x <= c + 1; ++x)
+        if (x >= 0 && x <= M) row[x] = 1;
+    }
+  }
+  std::vector<int32_t> off(33 * (size_t)stride, 0), cnt(33 * (size_t)stride, 0),
+      peak(33 * (size_t)stride, 0);
+  std::vector<uint32_t> ops;
+  struct Op {
+    int level, s;
+    uint32_t code;
+  };
+  std::vector<Op> tmp;
+  for (int P = 1; P <= 32; ++P)
+    for (int md = 0; md <= M; ++md) {
+      const size_t slot = (size_t)P * stride + md;
+      if (!need[slot]) continue;
+      tmp.clear();
+      for (int s2 = 0; s2 < P; ++s2) {
+        const ChainLevels lv{s2, P, md, std::min(P - 1 - s2, md)};
+        const uint32_t depF = s2 > 0 ? 1u : 0u, depB = s2 < P - 1 ? 2u : 0u;
+        for (int j = 0; j < md; ++j) {
+          tmp.push_back({lv.F(j), s2,
+                         (uint32_t)s2 | (kOpF << 6) | (depF << 8) | ((uint32_t)j << 10)});
+          tmp.push_back({lv.B(j), s2,
+                         (uint32_t)s2 | (kOpB << 6) | (depB << 8) | ((uint32_t)j << 10)});
+          if (zbh)
+            tmp.push_back({lv.W(j), s2, (uint32_t)s2 | (kOpW << 6) | ((uint32_t)j << 10)});
+        }
+      }
+      std::sort(tmp.begin(), tmp.end(), [](const Op& x, const Op& y) {
+        return x.level != y.level ? x.level < y.level : x.s > y.s;
+      });
+      std::vector<int> live(P, 0);
+      int pk = 0;
+      for (const Op& o : tmp) {
+        const unsigned kind = (o.code >> 6) & 3u;
+        if (kind == kOpF) pk = std::max(pk, ++live[o.s]);
+        if (kind == kOpB) --live[o.s];
+      }
+      off[slot] = (int32_t)ops.size();
+      cnt[slot] = (int32_t)tmp.size();
+      peak[slot] = pk;
+      for (const Op& o : tmp) ops.push_back(o.code);
+    }
+  const size_t tab_bytes = 3 * off.size() * 4;
+  const size_t bytes = tab_bytes + 4 * std::max<size_t>(1, ops.size());
+  RH_CUDA(cudaMallocAsync(&S->dops, bytes, st));
+  std::vector<char> stage(bytes, 0);
+  memcpy(stage.data(), off.data(), off.size() * 4);
+  memcpy(stage.data() + off.size() * 4, cnt.data(), cnt.size() * 4);
+  memcpy(stage.data() + 2 * off.size() * 4, peak.data(), peak.size() * 4);
+  if (!ops.empty()) memcpy(stage.data() + tab_bytes, ops.data(), ops.size() * 4);
+  RH_CUDA(cudaMemcpyAsync(S->dops, stage.data(), bytes, cudaMemcpyHostToDevice, st));
+  RH_CUDA(cudaStreamSynchronize(st));  // the staging buffer dies here
+  char* B = static_cast<char*>(S->dops);
+  S->dv.tab_off = reinterpret_cast<const int32_t*>(B);
+  S->dv.tab_cnt = reinterpret_cast<const int32_t*>(B + off.size() * 4);
+  S->dv.tab_peak = reinterpret_cast<const int32_t*>(B + 2 * off.size() * 4);
+  S->dv.ops = reinterpret_cast<const uint32_t*>(B + tab_bytes);
+  (void)ctx;
+  return RH_OK;
 }
 
 }  // namespace rh
@@ -759,9 +936,9 @@ int rh_search_create(rh_ctx* ctx, const rh_search_desc* desc, rh_search** out, v
     return RH_OK;
   }
   // ---- device memory
-  static int max_blocks_per_sm = -1;  // cached occupancy of the table kernel
+  static int max_blocks_per_sm = -1;  // cached occupancy of the combine kernel
   if (max_blocks_per_sm < 0)
-    RH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_blocks_per_sm, table_kernel<0>,
+    RH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_blocks_per_sm, combine_kernel,
                                                           kEvalThreads, 0));
   S->eval_blocks = ctx->num_sms * std::max(1, max_blocks_per_sm);
   size_t bytes = 0;
@@ -808,7 +985,8 @@ int rh_search_create(rh_ctx* ctx, const rh_search_desc* desc, rh_search** out, v
                o_base = take(8 * (size_t)d.n_micro_batches),
                o_bb = take(8 * (size_t)S->eval_blocks), o_bi = take(8 * (size_t)S->eval_blocks),
                o_rtab = take(8 * (size_t)S->n_rt), o_pinfo = take(16 * (size_t)S->n_pairs),
-               o_tasks = take(sizeof(PhaseTask) * (size_t)NL);
+               o_rl = take(8 * 96 * (size_t)S->n_pairs),
+               o_tasks = take(sizeof(PipeTask) * (size_t)NL);
   // stream-ordered pool: after the first re-plan the memory is reused, not
   // mapped again (the pool keeps what it has; see rh_ctx::pool_ready)
   if (!ctx->pool_ready) {
@@ -842,7 +1020,7 @@ int rh_search_create(rh_ctx* ctx, const rh_search_desc* desc, rh_search** out, v
   v.ldoff = I(o_ldoff); v.lboff = I(o_lboff); v.lnb = I(o_lnb);
   v.lbase = LL(o_lbase); v.lnv = LL(o_lnv); v.lnu = LL(o_lnu);
   v.lpair = LL(o_lpair); v.lrt = LL(o_lrt);
-  v.rtab = Dp(o_rtab); v.pinfo = Dp(o_pinfo); v.tasks = B + o_tasks;
+  v.rtab = Dp(o_rtab); v.pinfo = Dp(o_pinfo); v.tasks = B + o_tasks; v.rl = Dp(o_rl);
   v.blk_node = I(o_bnode); v.blk_rank = I(o_brank); v.blk_members = I(o_bmem);
   v.blk_moff = I(o_bmoff); v.blk_speed = Dp(o_bspeed);
   v.quad = reinterpret_cast<int64_t*>(B + o_quad);
@@ -857,6 +1035,10 @@ int rh_search_create(rh_ctx* ctx, const rh_search_desc* desc, rh_search** out, v
   RH_CHECK_LAUNCH(ctx);
   prep_kernel<<<(NL * 32 + 127) / 128, 128, 0, st>>>(a);
   RH_CHECK_LAUNCH(ctx);
+  if (int rc = build_op_lists(ctx, S, st)) {
+    rh_search_destroy(S);
+    return rc;
+  }
   RH_CUDA(cudaStreamSynchronize(st));
   *out = S;
   return RH_OK;
@@ -866,6 +1048,7 @@ int rh_search_destroy(rh_search* S) {
   if (!S) return RH_OK;
   // back to the pool, ordered after the latest work issued on the search
   if (S->dmem) cudaFreeAsync(S->dmem, S->last_stream);
+  if (S->dops) cudaFreeAsync(S->dops, S->last_stream);
   delete S;
   return RH_OK;
 }
@@ -892,30 +1075,57 @@ int rh_search_eval(rh_ctx* ctx, rh_search* S, int64_t begin, int64_t end, double
   S->last_stream = st;
   SearchArgs a = make_args(S);
   const long long n = end - begin;
-  // phase 1 tasks: (layout, partition variant) pairs overlapping the range
-  std::vector<PhaseTask> tk;
-  long long n_tasks = 0;
-  for (int li = 0; li < (int)S->lT.size(); ++li) {
-    const long long lb = S->lbase[li], le = lb + S->lnv[li] * S->lnu[li];
-    if (le <= begin || lb >= end) continue;
-    const int v_lo = (int)((std::max<long long>(begin, lb) - lb) / S->lnu[li]);
-    const int v_hi = (int)((std::min<long long>(end, le) - 1 - lb) / S->lnu[li]);
-    int pw = 1;
-    while (pw < S->lP[li]) pw <<= 1;
-    const int R = 32 / pw, nb = (S->lD[li] + R - 1) / R;
-    tk.push_back({li, v_lo, n_tasks});
-    n_tasks += (long long)(v_hi - v_lo + 1) * 8 * nb;
+  // phase 1 tasks: (layout, partition variant range) overlapping [begin, end),
+  // grouped by P (one pipe_kernel launch per stage count: its shared memory
+  // holds P stage slots per thread)
+  std::vector<PipeTask> tk;
+  struct Group {
+    int P;
+    size_t first, count;
+    long long n_pipes, n_rows;
+  };
+  std::vector<Group> groups;
+  for (int P = 1; P <= 32; ++P) {
+    Group g{P, tk.size(), 0, 0, 0};
+    for (int li = 0; li < (int)S->lT.size(); ++li) {
+      if (S->lP[li] != P) continue;
+      const long long lb = S->lbase[li], le = lb + S->lnv[li] * S->lnu[li];
+      if (le <= begin || lb >= end) continue;
+      const int v_lo = (int)((std::max<long long>(begin, lb) - lb) / S->lnu[li]);
+      const int v_hi = (int)((std::min<long long>(end, le) - 1 - lb) / S->lnu[li]);
+      tk.push_back({li, v_lo, g.n_pipes, g.n_rows});
+      g.n_pipes += (long long)(v_hi - v_lo + 1) * 8 * S->lD[li];
+      g.n_rows += v_hi - v_lo + 1;
+    }
+    g.count = tk.size() - g.first;
+    if (g.count) groups.push_back(g);
   }
-  RH_CUDA(cudaMemcpyAsync(S->dv.tasks, tk.data(), sizeof(PhaseTask) * tk.size(),
+  RH_CUDA(cudaMemcpyAsync(S->dv.tasks, tk.data(), sizeof(PipeTask) * tk.size(),
                           cudaMemcpyHostToDevice, st));
-  const int tblocks = (int)std::min<long long>(S->eval_blocks, (n_tasks + 7) / 8);
-  if (S->d.schedule == RH_SCHED_ZBH)
-    table_kernel<1><<<tblocks, kEvalThreads, 0, st>>>(
-        a, reinterpret_cast<const PhaseTask*>(S->dv.tasks), (int)tk.size(), n_tasks);
-  else
-    table_kernel<0><<<tblocks, kEvalThreads, 0, st>>>(
-        a, reinterpret_cast<const PhaseTask*>(S->dv.tasks), (int)tk.size(), n_tasks);
-  RH_CHECK_LAUNCH(ctx);
+  const bool zbh = S->d.schedule == RH_SCHED_ZBH;
+  void* kern = zbh ? (void*)pipe_kernel<1> : (void*)pipe_kernel<0>;
+  for (const Group& g : groups) {
+    const size_t smem = (size_t)(zbh ? 3 : 2) * g.P * kPipeThreads * sizeof(double);
+    // (the pipe kernel strides its state by kPipeThreads)
+    if (int e = ensure_smem(kern, smem)) return e;
+    int occ = 0;
+    RH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kPipeThreads, smem));
+    const long long want = (g.n_pipes + kPipeThreads - 1) / kPipeThreads;
+    const int blocks = (int)std::max<long long>(
+        1, std::min<long long>(want, (long long)ctx->num_sms * std::max(1, occ) * 8));
+    const PipeTask* tp = reinterpret_cast<const PipeTask*>(S->dv.tasks) + g.first;
+    int n_tk = (int)g.count;
+    {
+      const long long n_rl = g.n_rows * g.P;
+      rl_kernel<<<(unsigned)((n_rl + 255) / 256), 256, 0, st>>>(a, tp, n_tk, g.P, g.n_rows);
+      RH_CHECK_LAUNCH(ctx);
+    }
+    long long n_pipes = g.n_pipes;
+    int P = g.P;
+    void* args[] = {&a, &tp, &n_tk, &n_pipes, &P};
+    RH_CUDA(cudaLaunchKernel(kern, dim3(blocks), dim3(kPipeThreads), args, smem, st));
+    RH_CHECK_LAUNCH(ctx);
+  }
   const int blocks = (int)std::min<long long>(S->eval_blocks, (n + kEvalThreads - 1) / kEvalThreads);
   combine_kernel<<<blocks, kEvalThreads, 0, st>>>(a, begin, end, scores);
   RH_CHECK_LAUNCH(ctx);
