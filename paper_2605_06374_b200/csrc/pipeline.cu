@@ -312,40 +312,11 @@ __device__ __forceinline__ void walk_table(const WalkArgs<P>& a, const unsigned 
   }
 }
 
-// The chunk of stage s at DAG level t for MM micro-batches (inverse of the
-// wavefront.cuh closed forms): kind (0 none) and micro-batch j.  Evaluated
-// on compile-time constants inside walk_static, so it folds away.
-__host__ __device__ constexpr int op_at(int P, int MM, int zbh, int t, int s, int& j) {
-  const int w = (P - 1 - s) < MM ? (P - 1 - s) : MM;
-  const int k = t - s;
-  if (k >= 0 && k <= w && k < MM) {
-    j = k;
-    return kOpF;
-  }
-  if (k > 2 * w && (k & 1) == 0 && k / 2 > w && k / 2 < MM) {
-    j = k / 2;
-    return kOpF;
-  }
-  const int kb = t - (2 * P - 1 - s);
-  if (kb >= 0 && (kb & 1) == 0 && kb / 2 < MM) {
-    j = kb / 2;
-    return kOpB;
-  }
-  if (zbh) {
-    const int kw = t - (2 * P - s) - 2 * (MM - w);
-    if (kw >= 0 && (kw & 1) == 0 && kw / 2 < w) {
-      j = kw / 2;
-      return kOpW;
-    }
-    const int tail = (w > 0 ? 2 * P - s + 2 * MM - 2 : 2 * P - 1 - s + 2 * (MM - 1));
-    const int jt = t - tail + w - 1;
-    if (jt >= w && jt < MM) {
-      j = jt;
-      return kOpW;
-    }
-  }
-  j = 0;
-  return 0;
+// The chunk of stage s at DAG level t for MM micro-batches (ChainLevels::at,
+// the inverse of the wavefront.cuh closed forms).  Evaluated on compile-time
+// constants inside walk_static, so it folds away.
+__host__ __device__ __forceinline__ int op_at(int P, int MM, int zbh, int t, int s, int& j) {
+  return ChainLevels{s, P, MM, (P - 1 - s) < MM ? (P - 1 - s) : MM}.at(t, zbh != 0, j);
 }
 
 // Upper bound on the DAG levels of an MM-micro-batch replica (levels past the
@@ -395,7 +366,7 @@ __device__ __forceinline__ bool walk_static_dispatch(const WalkArgs<P>& a, int m
 }
 
 template <int P, int ZBH, int DETECT>
-__global__ void __launch_bounds__(kSmallThreads, kSmallMinBlocks) pass_small_kernel(const PassParams p) {
+__global__ void __launch_bounds__(kSmallThreads, ZBH ? 4 : kSmallMinBlocks) pass_small_kernel(const PassParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x, nt = blockDim.x;
   const int D = p.sh.dp, M = p.sh.micro_batches, T = p.sh.tp;

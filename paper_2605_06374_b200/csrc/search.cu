@@ -755,42 +755,33 @@ static int build_op_lists(rh_ctx* ctx, rh_search* S, cudaStream_t st) {
   std::vector<int32_t> off(33 * (size_t)stride, 0), cnt(33 * (size_t)stride, 0),
       peak(33 * (size_t)stride, 0);
   std::vector<uint32_t> ops;
-  struct Op {
-    int level, s;
-    uint32_t code;
-  };
-  std::vector<Op> tmp;
   for (int P = 1; P <= 32; ++P)
     for (int md = 0; md <= M; ++md) {
       const size_t slot = (size_t)P * stride + md;
       if (!need[slot]) continue;
-      tmp.clear();
-      for (int s2 = 0; s2 < P; ++s2) {
-        const ChainLevels lv{s2, P, md, std::min(P - 1 - s2, md)};
-        const uint32_t depF = s2 > 0 ? 1u : 0u, depB = s2 < P - 1 ? 2u : 0u;
-        for (int j = 0; j < md; ++j) {
-          tmp.push_back({lv.F(j), s2,
-                         (uint32_t)s2 | (kOpF << 6) | (depF << 8) | ((uint32_t)j << 10)});
-          tmp.push_back({lv.B(j), s2,
-                         (uint32_t)s2 | (kOpB << 6) | (depB << 8) | ((uint32_t)j << 10)});
-          if (zbh)
-            tmp.push_back({lv.W(j), s2, (uint32_t)s2 | (kOpW << 6) | ((uint32_t)j << 10)});
-        }
-      }
-      std::sort(tmp.begin(), tmp.end(), [](const Op& x, const Op& y) {
-        return x.level != y.level ? x.level < y.level : x.s > y.s;
-      });
+      // emit in (level ascending, stage descending) order straight from the
+      // closed forms; live counts give the capacity peak
+      off[slot] = (int32_t)ops.size();
+      int t_end = 0;
+      for (int s2 = 0; s2 < P; ++s2)
+        t_end = std::max(t_end, ChainLevels{s2, P, md, std::min(P - 1 - s2, md)}.end(zbh));
       std::vector<int> live(P, 0);
       int pk = 0;
-      for (const Op& o : tmp) {
-        const unsigned kind = (o.code >> 6) & 3u;
-        if (kind == kOpF) pk = std::max(pk, ++live[o.s]);
-        if (kind == kOpB) --live[o.s];
-      }
-      off[slot] = (int32_t)ops.size();
-      cnt[slot] = (int32_t)tmp.size();
+      for (int t = 0; t < t_end; ++t)
+        for (int s2 = P - 1; s2 >= 0; --s2) {
+          int j = 0;
+          const unsigned kind =
+              (unsigned)ChainLevels{s2, P, md, std::min(P - 1 - s2, md)}.at(t, zbh, j);
+          if (!kind) continue;
+          uint32_t dep = 0;
+          if (kind == kOpF && s2 > 0) dep = 1;
+          if (kind == kOpB && s2 < P - 1) dep = 2;
+          ops.push_back((uint32_t)s2 | (kind << 6) | (dep << 8) | ((uint32_t)j << 10));
+          if (kind == kOpF) pk = std::max(pk, ++live[s2]);
+          if (kind == kOpB) --live[s2];
+        }
+      cnt[slot] = (int32_t)ops.size() - off[slot];
       peak[slot] = pk;
-      for (const Op& o : tmp) ops.push_back(o.code);
     }
   const size_t tab_bytes = 3 * off.size() * 4;
   const size_t bytes = tab_bytes + 4 * std::max<size_t>(1, ops.size());

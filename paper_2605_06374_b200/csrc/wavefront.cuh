@@ -52,6 +52,43 @@ struct ChainLevels {
     if (j < w) return 2 * P - s + 2 * (m - w + j);
     return (w > 0 ? 2 * P - s + 2 * m - 2 : 2 * P - 1 - s + 2 * (m - 1)) + (j - w + 1);
   }
+  // Inverse: the chunk of this chain at level t -- kind 1 F, 2 B/BW, 3 W (ZBH),
+  // 0 none -- and its micro-batch j.  A chain holds at most one chunk per level.
+  __host__ __device__ __forceinline__ int at(int t, bool zbh, int& j) const {
+    const int k = t - s;
+    if (k >= 0 && k <= w && k < m) {
+      j = k;
+      return 1;
+    }
+    if (k > 2 * w && (k & 1) == 0 && k / 2 < m) {
+      j = k / 2;
+      return 1;
+    }
+    const int kb = t - (2 * P - 1 - s);
+    if (kb >= 0 && (kb & 1) == 0 && kb / 2 < m) {
+      j = kb / 2;
+      return 2;
+    }
+    if (zbh) {
+      const int kw = t - (2 * P - s) - 2 * (m - w);
+      if (kw >= 0 && (kw & 1) == 0 && kw / 2 < w) {
+        j = kw / 2;
+        return 3;
+      }
+      const int tail = w > 0 ? 2 * P - s + 2 * m - 2 : 2 * P - 1 - s + 2 * (m - 1);
+      const int jt = t - tail + w - 1;
+      if (jt >= w && jt < m) {
+        j = jt;
+        return 3;
+      }
+    }
+    j = 0;
+    return 0;
+  }
+  // one past the last level of the chain
+  __host__ __device__ __forceinline__ int end(bool zbh) const {
+    return m == 0 ? 0 : 1 + (zbh ? W(m - 1) : B(m - 1));
+  }
 };
 
 template <int ZBH>
