@@ -15,15 +15,17 @@
 //           stage_cost/measured (detector.py:127-158), measured = max over
 //           the group's member device times (float4 loads).
 //
-// Mapping (B200): one replica pipeline = `pw` lanes (pw = next_pow2(P) <= 32,
-// lane s = stage s), so a warp runs 32/pw pipelines; all D pipelines of an
-// iteration sit in one CTA and reduce the makespan through shared memory.
-// Each lane walks its stage's 1F1B/ZBH chain in order; a chunk whose data
-// predecessor lives on a neighbouring stage waits until that lane has
-// published the finish time in shared memory (dynamic wavefront, one
-// __syncwarp per step).  The canonical DAG is acyclic, so the chain head of
-// the earliest unprocessed vertex is always ready and the loop terminates.
-// All fp64 ops use explicit _rn intrinsics: no FMA contraction anywhere.
+// Two mappings (launch_pass picks one per launch):
+//   pass_small_kernel (P <= 4, D <= 128): one THREAD per replica pipeline,
+//     all stage state in registers, chunks in DAG-level order (fully unrolled
+//     for small micro-batch counts, level table otherwise); see below.
+//   pass_kernel (P <= 32): one replica pipeline = `pw` lanes (pw =
+//     next_pow2(P), lane s = stage s); each lane walks its chain with the
+//     branch-free static level walk of wavefront.cuh, neighbours exchange the
+//     last F / B finish by warp shuffle.
+// In both, all D pipelines of an iteration sit in one CTA and reduce the
+// makespan through shared memory.  All fp64 ops use explicit _rn
+// intrinsics: no FMA contraction anywhere.
 #include <algorithm>
 #include <type_traits>
 
