@@ -12,9 +12,9 @@ validation, and the median/MAD change-point state machine.
            inputs resident in HBM, L2 flushed (256 MiB write) before every
            step, each step timed with CUDA events on the launching stream;
   e2e    = the same metric through the reference-facing C-ABI call
-           rh_detector_pass_host with pinned host buffers (H2D + kernels +
-           D2H inside the timed region);
-  roofline of the dominant kernel (pass_kernel<1F1B,detect>);
+           rh_detector_pass_host_packed with pinned host buffers in the packed
+           wire form (H2D + kernels + D2H inside the timed region);
+  roofline of the dominant kernel (pass_small_kernel<P=4,1F1B,detect>);
   cpu_baseline = the C oracle restatement of the reference on the host cores.
 Multi-GPU (torchrun): each rank processes its own trace (weak scaling, no
 data-path collective); the step time is the max over ranks.
@@ -290,7 +290,9 @@ def run_ours(args, world, rank, local):
 
 
 def run_e2e(tr, p, args, dev):
-    """rh_detector_pass_host with pinned host buffers; H2D + kernels + D2H timed."""
+    """rh_detector_pass_host_packed with pinned host buffers in the packed wire
+    form (uint16 document lengths, uint8 documents per micro-batch, int32
+    per-iteration document offsets); H2D + kernels + D2H timed."""
     import torch
 
     from paper_2605_06374_b200 import _lib
@@ -299,9 +301,11 @@ def run_e2e(tr, p, args, dev):
     pin = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).pin_memory()
     segs = tr.known
     cat = lambda name, dt: pin(np.concatenate([getattr(s, name) for s in segs]), dt)
+    pk = tr.packed()
     h = {
-        "seg": pin(tr.seg, np.int32), "mb_off": pin(tr.mb_off, np.int32),
-        "doc_len": pin(tr.doc_len, np.int32), "dt": pin(tr.device_time, np.float32),
+        "seg": pin(tr.seg, np.int32), "iter_doc": pin(pk["iter_doc"], np.int32),
+        "mb_docs": pin(pk["mb_docs"], np.uint8), "doc_len": pin(pk["doc_len"], np.uint16),
+        "dt": pin(tr.device_time, np.float32),
         "obs": pin(tr.observed, np.float64), "reset": pin(tr.reset, np.uint8),
         "layers": cat("layers", np.int32), "mb_start": cat("mb_start", np.int32),
         "speed": cat("speed", np.float64), "hf": cat("hop_fwd", np.float64),
@@ -320,8 +324,9 @@ def run_e2e(tr, p, args, dev):
     seg_c = _lib.Segments(len(segs), h["layers"].data_ptr(), h["mb_start"].data_ptr(),
                           h["speed"].data_ptr(), h["hf"].data_ptr(), h["hb"].data_ptr(),
                           h["ar"].data_ptr(), h["loff"].data_ptr(), h["lr"].data_ptr())
-    tr_c = _lib.Trace(n, h["seg"].data_ptr(), h["mb_off"].data_ptr(), h["doc_len"].data_ptr(),
-                      h["dt"].data_ptr(), h["obs"].data_ptr())
+    tr_c = _lib.TracePacked(n, h["seg"].data_ptr(), h["iter_doc"].data_ptr(),
+                            h["mb_docs"].data_ptr(), h["doc_len"].data_ptr(),
+                            h["dt"].data_ptr(), h["obs"].data_ptr())
     out_c = _lib.PassOut(o["ms"].data_ptr(), o["st"].data_ptr(), None, o["fl"].data_ptr(),
                          o["sv"].data_ptr())
     max_mb = int(max(np.diff(s.mb_start).max() for s in segs))
@@ -332,11 +337,11 @@ def run_e2e(tr, p, args, dev):
     stream = torch.cuda.current_stream(dev)
 
     def call():
-        _lib.check(lib.rh_detector_pass_host(
+        _lib.check(lib.rh_detector_pass_host_packed(
             ctx, C.byref(shape), C.byref(p.model_c), C.byref(seg_c), C.byref(tr_c), 1.25,
             C.byref(p.screen_params), 0, None, h["reset"].data_ptr(), C.byref(out_c),
             o["oc"].data_ptr(), C.byref(series_len), stream.cuda_stream),
-            "rh_detector_pass_host")
+            "rh_detector_pass_host_packed")
 
     for _ in range(max(1, args.warmup)):
         call()

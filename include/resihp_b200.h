@@ -256,6 +256,35 @@ int rh_detector_pass_host(rh_ctx* ctx, const rh_pipe_shape* shape,
                           const rh_pass_out* out, uint8_t* outcome,
                           int64_t* series_len_out, void* stream);
 
+/*
+ * Packed wire form of a trace for the host-buffer pass (the same data as
+ * rh_trace, ~40 % fewer bytes over PCIe).  pack_sequences bins hold at most
+ * `token_budget` tokens (workload.py:52-80), so a document length fits 16 bits
+ * whenever token_budget <= 65535; a micro-batch holds at most 255 documents.
+ *   iter_doc[i] .. iter_doc[i+1]   documents of iteration i (int32, < 2^31)
+ *   mb_docs[i*M + j]               documents in micro-batch j of iteration i
+ *   doc_len[k]                     length of document k
+ * The device rebuilds the int32 CSR chunk by chunk while later chunks cross
+ * PCIe, then runs exactly the rh_detector_pass_host pipeline.
+ */
+typedef struct rh_trace_packed {
+  int64_t n_iter;
+  const int32_t* seg;          /* [n_iter] segment id; NULL = segment 0 */
+  const int32_t* iter_doc;     /* [n_iter + 1]                          */
+  const uint8_t* mb_docs;      /* [n_iter * M]                          */
+  const uint16_t* doc_len;     /* [iter_doc[n_iter]]                    */
+  const float* device_time;    /* [n_iter][D][P][T]                     */
+  const double* observed;      /* [n_iter]                              */
+} rh_trace_packed;
+
+int rh_detector_pass_host_packed(rh_ctx* ctx, const rh_pipe_shape* shape,
+                                 const rh_cost_model* model, const rh_segments* segs,
+                                 const rh_trace_packed* trace, double threshold,
+                                 const rh_screen_params* screen, int64_t series_len,
+                                 const double* hist, const uint8_t* reset,
+                                 const rh_pass_out* out, uint8_t* outcome,
+                                 int64_t* series_len_out, void* stream);
+
 /* -------------------------------------------- general DAG critical path */
 /*
  * critical_path (pipeline.py:259-292) on an arbitrary DAG given in CSR by

@@ -67,6 +67,11 @@ class Trace(C.Structure):
                 ("device_time", _p), ("observed", _p)]
 
 
+class TracePacked(C.Structure):
+    _fields_ = [("n_iter", C.c_int64), ("seg", _p), ("iter_doc", _p), ("mb_docs", _p),
+                ("doc_len", _p), ("device_time", _p), ("observed", _p)]
+
+
 class PassOut(C.Structure):
     _fields_ = [("makespan", _p), ("status", _p), ("stage_cost", _p),
                 ("stage_flag", _p), ("severity", _p)]
@@ -103,6 +108,11 @@ _SIGS = {
                                C.POINTER(Segments), C.POINTER(Trace), C.c_double,
                                C.POINTER(ScreenParams), C.c_int64, _p, _p, C.POINTER(PassOut),
                                _p, C.POINTER(C.c_int64), _p], C.c_int),
+    "rh_detector_pass_host_packed": ([_p, C.POINTER(PipeShape), C.POINTER(CostModelC),
+                                      C.POINTER(Segments), C.POINTER(TracePacked), C.c_double,
+                                      C.POINTER(ScreenParams), C.c_int64, _p, _p,
+                                      C.POINTER(PassOut), _p, C.POINTER(C.c_int64), _p],
+                                     C.c_int),
     "rh_pack_sequences": ([C.c_int64, _p, C.c_int32, C.c_int64, _p, _p, C.POINTER(C.c_int64),
                            C.POINTER(C.c_int64)], C.c_int),
     "rh_repartition_batch": ([_p, C.c_int32, _p, _p, _p, _p, _p, _p, _p], C.c_int),

@@ -161,9 +161,12 @@ int rh_ctx_destroy(rh_ctx* ctx) {
   for (cudaEvent_t e : ctx->chunk_ev)
     if (e) cudaEventDestroy(e);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+  if (ctx->side_stream) cudaStreamDestroy(ctx->side_stream);
+  if (ctx->side_ev) cudaEventDestroy(ctx->side_ev);
   for (auto& t : ctx->sched) cudaFree(t.dev);
   if (ctx->prep.done) cudaEventDestroy(ctx->prep.done);
   if (ctx->prep.consumed) cudaEventDestroy(ctx->prep.consumed);
+  if (ctx->host_graph.exec) cudaGraphExecDestroy(ctx->host_graph.exec);
   delete ctx;
   return RH_OK;
 }

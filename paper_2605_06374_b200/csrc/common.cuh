@@ -27,6 +27,9 @@ struct rh_ctx {
   static constexpr int kChunkEvents = 8;
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t chunk_ev[kChunkEvents] = {};
+  // side stream of the host pass (rh_screen_prepare while the trace streams in)
+  cudaStream_t side_stream = nullptr;
+  cudaEvent_t side_ev = nullptr;
   // per-(pp, schedule, max micro-batches) op-order tables of the
   // thread-per-replica pass kernel, built and uploaded on first use
   struct SchedTable {
@@ -37,6 +40,12 @@ struct rh_ctx {
   std::mutex sched_mu;
   // the device's default memory pool keeps freed memory (re-plan searches)
   bool pool_ready = false;
+  // rh_detector_pass_host*: the captured pass for the last argument key
+  struct HostGraph {
+    std::vector<uint64_t> key;
+    cudaGraphExec_t exec = nullptr;
+    bool failed = false;
+  } host_graph;
   // the last rh_screen_prepare: its arguments and completion event
   struct ScreenPrep {
     bool valid = false;

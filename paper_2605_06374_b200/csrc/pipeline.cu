@@ -714,12 +714,7 @@ int launch_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
     // the region holds the staged documents, later the base costs
     const size_t region = std::max<size_t>(16 * 1024, (size_t)threads * p.mmax * 8);
     p.doc_stage = (int)(region / 4);
-    {
-      const char* e1 = getenv("RH_STATIC_MAX");
-      const char* e2 = getenv("RH_STATIC_DIV_MAX");
-      p.static_max = e1 ? atoi(e1) : kStaticMaxMB;
-      p.static_div_max = e2 ? atoi(e2) : kStaticMaxMB;
-    }
+    p.static_max = p.static_div_max = kStaticMaxMB;
     const size_t smem = p.region_off + region;
     if (smem <= ctx->smem_optin && smem <= 56 * 1024) {
       const bool zbh = sh->schedule == RH_SCHED_ZBH;
@@ -764,6 +759,46 @@ int launch_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
 }
 
 // ------------------------------------------------------------------ host I/O
+
+// Packed trace -> int32 CSR for iterations [i0, i0 + gridDim.x): one block per
+// iteration scans its micro-batch document counts (absolute offsets from
+// iter_doc) and widens its document lengths.
+constexpr int kExpandThreads = 128;
+
+__global__ void __launch_bounds__(kExpandThreads) expand_kernel(
+    int64_t i0, int64_t n, int M, const int32_t* __restrict__ iter_doc,
+    const uint8_t* __restrict__ mb_docs, const uint16_t* __restrict__ doc16,
+    int32_t* __restrict__ off, int32_t* __restrict__ doc) {
+  __shared__ int s_w[kExpandThreads / 32];
+  const int64_t i = i0 + blockIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int carry = iter_doc[i];
+  for (int j0 = 0; j0 < M; j0 += kExpandThreads) {
+    const int j = j0 + threadIdx.x;
+    const int c = j < M ? (int)mb_docs[i * M + j] : 0;
+    int x = c;  // inclusive block scan
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_w[wid] = x;
+    __syncthreads();
+    int pre = 0, tot = 0;
+    for (int w = 0; w < kExpandThreads / 32; ++w) {
+      if (w < wid) pre += s_w[w];
+      tot += s_w[w];
+    }
+    if (j < M) off[i * M + j] = carry + pre + x - c;
+    carry += tot;
+    __syncthreads();
+  }
+  // the end offset of this iteration's last micro-batch (the next iteration's
+  // block writes the same value as its start)
+  if (threadIdx.x == 0) off[(i + 1) * M] = iter_doc[i + 1];
+  const int32_t d0 = iter_doc[i], d1 = iter_doc[i + 1];
+  for (int32_t k = d0 + threadIdx.x; k < d1; k += kExpandThreads) doc[k] = doc16[k];
+}
+
 namespace {
 struct Carver {
   char* base;
@@ -778,19 +813,40 @@ struct Carver {
 };
 }  // namespace
 
-int detect_host(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
-                const rh_segments* sg, const rh_trace* tr, double thr,
-                const rh_screen_params* screen, int64_t series_len, const double* hist,
-                const uint8_t* reset, const rh_pass_out* out, uint8_t* outcome,
-                int64_t* series_len_out, cudaStream_t stream) {
-  if (!ctx || !sh || !sg || !tr || !out || !tr->mb_off) {
+// Chunks of the host pass: H2D of chunk k+1 overlaps the kernels of chunk k.
+// (each extra chunk costs a handful of DMA setups; 4 measured best on B200)
+static int host_chunks(int64_t n) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(4, n / 1024));
+}
+
+// Host-buffer Detector pass over an int32 trace (tr) or a packed one (pk):
+// enqueues copies, kernels and read-backs on `stream` (+ the copy stream).
+int enqueue_host_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
+                const rh_segments* sg, const rh_trace* tr_in, const rh_trace_packed* pk,
+                double thr, const rh_screen_params* screen, int64_t series_len,
+                const double* hist, const uint8_t* reset, const rh_pass_out* out,
+                uint8_t* outcome, int64_t* series_len_out, cudaStream_t stream) {
+  if (!ctx || !sh || !sg || !out || (!tr_in && !pk) || (tr_in && !tr_in->mb_off) ||
+      (pk && (!pk->iter_doc || !pk->mb_docs || !pk->doc_len))) {
     set_error("detect_host: NULL argument");
     return RH_E_INVALID;
   }
   const int P = sh->pp, D = sh->dp, T = sh->tp, M = sh->micro_batches;
+  // the int32 view of the trace (its CSR arrays are rebuilt on the device
+  // when the trace is packed)
+  rh_trace tv{};
+  if (pk) {
+    tv.n_iter = pk->n_iter;
+    tv.seg = pk->seg;
+    tv.device_time = pk->device_time;
+    tv.observed = pk->observed;
+  } else {
+    tv = *tr_in;
+  }
+  const rh_trace* tr = &tv;
   const int64_t n = tr->n_iter, G = (int64_t)D * P, S = sg->n_seg;
   if (n == 0) return RH_OK;
-  const int64_t n_docs = tr->mb_off[n * M];
+  const int64_t n_docs = pk ? pk->iter_doc[n] : tr->mb_off[n * M];
   const int64_t n_links = sg->link_off ? sg->link_off[S] : 0;
   size_t need = 0;
   {
@@ -815,6 +871,11 @@ int detect_host(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
     c.take<uint8_t>(n);
     c.take<uint8_t>(n);
     c.take<int64_t>(1);
+    if (pk) {
+      c.take<int32_t>(n + 1);
+      c.take<uint8_t>(n * M);
+      c.take<uint16_t>(n_docs);
+    }
     need = c.off + 256;
   }
   void* ws = nullptr;
@@ -847,6 +908,9 @@ int detect_host(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
   uint8_t* d_reset = c.take<uint8_t>(n);
   uint8_t* d_outcome = c.take<uint8_t>(n);
   int64_t* d_len = c.take<int64_t>(1);
+  int32_t* d_idoc = pk ? c.take<int32_t>(n + 1) : nullptr;
+  uint8_t* d_cnt = pk ? c.take<uint8_t>(n * M) : nullptr;
+  uint16_t* d_doc16 = pk ? c.take<uint16_t>(n_docs) : nullptr;
   auto cp = [&](void* dst, const void* src, size_t bytes, cudaMemcpyKind kind,
                 cudaStream_t st) -> int {
     if (!src || !bytes) return RH_OK;
@@ -880,11 +944,24 @@ int detect_host(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
   }
   if ((rc = cp(d_hist, hist, 8 * h, H2D, stream))) return rc;
   if (screen && reset && (rc = cp(d_reset, reset, n, H2D, stream))) return rc;
-  // chunked pipeline: chunk k+1 crosses PCIe on the copy stream while chunk k
-  // is processed (and its results copied back) on the caller's stream
+  // the screen's inputs are tiny: copy them first and start its input-only
+  // half (rh_screen_prepare) on the side stream while the trace streams in
+  if ((rc = cp(d_obs, tr->observed, 8 * n, H2D, stream))) return rc;
   if (!ctx->copy_stream)
     RH_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
-  const int n_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(4, n / 1024));
+  if (!ctx->side_stream)
+    RH_CUDA(cudaStreamCreateWithFlags(&ctx->side_stream, cudaStreamNonBlocking));
+  if (!ctx->side_ev) RH_CUDA(cudaEventCreateWithFlags(&ctx->side_ev, cudaEventDisableTiming));
+  if (screen) {
+    RH_CUDA(cudaEventRecord(ctx->side_ev, stream));
+    RH_CUDA(cudaStreamWaitEvent(ctx->side_stream, ctx->side_ev, 0));
+    if ((rc = rh_screen_prepare(ctx, screen, series_len, d_hist, n, d_obs,
+                                reset ? d_reset : nullptr, ctx->side_stream)))
+      return rc;
+  }
+  // chunked pipeline: chunk k+1 crosses PCIe on the copy stream while chunk k
+  // is processed (and its results copied back) on the caller's stream
+  const int n_chunks = host_chunks(n);
   for (int k = 0; k < n_chunks; ++k)
     if (!ctx->chunk_ev[k])
       RH_CUDA(cudaEventCreateWithFlags(&ctx->chunk_ev[k], cudaEventDisableTiming));
@@ -894,15 +971,27 @@ int detect_host(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
   cudaStream_t cs = ctx->copy_stream;
   for (int k = 0; k < n_chunks; ++k) {
     const int64_t i0 = n * k / n_chunks, i1 = n * (k + 1) / n_chunks, ni = i1 - i0;
-    const int64_t o0 = tr->mb_off[i0 * M], o1 = tr->mb_off[i1 * M];
+    const int64_t o0 = pk ? pk->iter_doc[i0] : tr->mb_off[i0 * M];
+    const int64_t o1 = pk ? pk->iter_doc[i1] : tr->mb_off[i1 * M];
     if ((rc = cp(d_seg ? d_seg + i0 : nullptr, tr->seg ? tr->seg + i0 : nullptr, 4 * ni, H2D, cs)) ||
-        (rc = cp(d_off + i0 * M, tr->mb_off + i0 * M, 4 * (ni * M + 1), H2D, cs)) ||
-        (rc = cp(d_doc + o0, tr->doc_len + o0, 4 * (o1 - o0), H2D, cs)) ||
-        (rc = cp(d_dt + i0 * G * T, tr->device_time + i0 * G * T, 4 * ni * G * T, H2D, cs)) ||
-        (rc = cp(d_obs + i0, tr->observed + i0, 8 * ni, H2D, cs)))
+        (rc = cp(d_dt + i0 * G * T, tr->device_time + i0 * G * T, 4 * ni * G * T, H2D, cs)))
       return rc;
+    if (pk) {
+      if ((rc = cp(d_idoc + i0, pk->iter_doc + i0, 4 * (ni + 1), H2D, cs)) ||
+          (rc = cp(d_cnt + i0 * M, pk->mb_docs + i0 * M, ni * M, H2D, cs)) ||
+          (rc = cp(d_doc16 + o0, pk->doc_len + o0, 2 * (o1 - o0), H2D, cs)))
+        return rc;
+    } else if ((rc = cp(d_off + i0 * M, tr->mb_off + i0 * M, 4 * (ni * M + 1), H2D, cs)) ||
+               (rc = cp(d_doc + o0, tr->doc_len + o0, 4 * (o1 - o0), H2D, cs))) {
+      return rc;
+    }
     RH_CUDA(cudaEventRecord(ctx->chunk_ev[k], cs));
     RH_CUDA(cudaStreamWaitEvent(stream, ctx->chunk_ev[k], 0));
+    if (pk) {  // rebuild this chunk's int32 CSR
+      expand_kernel<<<(unsigned)ni, kExpandThreads, 0, stream>>>(i0, n, M, d_idoc, d_cnt,
+                                                                 d_doc16, d_off, d_doc);
+      RH_CHECK_LAUNCH(ctx);
+    }
     rh_trace ct = *tr;
     ct.n_iter = ni;
     ct.seg = d_seg ? d_seg + i0 : nullptr;
@@ -934,6 +1023,104 @@ int detect_host(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
     if (series_len_out)
       RH_CUDA(cudaMemcpyAsync(series_len_out, d_len, sizeof(int64_t), D2H, stream));
   }
+  return RH_OK;
+}
+
+// Everything that shapes the enqueued work of a host pass: the graph key.
+// Buffer CONTENTS are not part of it (memcpy nodes read them at replay), but
+// the chunk boundaries' document offsets are, because they size the copies.
+static std::vector<uint64_t> host_pass_key(const rh_pipe_shape* sh, const rh_cost_model* m,
+                                           const rh_segments* sg, const rh_trace* tr,
+                                           const rh_trace_packed* pk, double thr,
+                                           const rh_screen_params* screen, int64_t series_len,
+                                           const double* hist, const uint8_t* reset,
+                                           const rh_pass_out* out, uint8_t* outcome,
+                                           int64_t* series_len_out, cudaStream_t stream) {
+  std::vector<uint64_t> k;
+  auto raw = [&](const void* p, size_t n) {
+    const size_t w = (n + 7) / 8;
+    const size_t at = k.size();
+    k.resize(at + w, 0);
+    memcpy(k.data() + at, p, n);
+  };
+  raw(sh, sizeof(*sh));
+  raw(m, sizeof(*m));
+  raw(sg, sizeof(*sg));
+  raw(out, sizeof(*out));
+  if (tr) raw(tr, sizeof(*tr));
+  if (pk) raw(pk, sizeof(*pk));
+  if (screen) raw(screen, sizeof(*screen));
+  raw(&thr, sizeof(thr));
+  k.push_back((uint64_t)series_len);
+  k.push_back((uint64_t)(uintptr_t)hist);
+  k.push_back((uint64_t)(uintptr_t)reset);
+  k.push_back((uint64_t)(uintptr_t)outcome);
+  k.push_back((uint64_t)(uintptr_t)series_len_out);
+  k.push_back((uint64_t)(uintptr_t)stream);
+  k.push_back(pk ? 1 : 0);
+  k.push_back(screen ? 1 : 0);
+  const int64_t n = pk ? pk->n_iter : tr->n_iter;
+  const int M = sh->micro_batches;
+  k.push_back(sg->link_off ? (uint64_t)sg->link_off[sg->n_seg] : 0);
+  const int n_chunks = host_chunks(n);
+  for (int c = 0; c <= n_chunks; ++c) {
+    const int64_t i = n * c / n_chunks;
+    k.push_back((uint64_t)(pk ? pk->iter_doc[i] : tr->mb_off[i * M]));
+  }
+  return k;
+}
+
+// The host pass replays a CUDA graph: the first call with a given key runs
+// directly (sizing every workspace and table), the second captures and
+// instantiates it, later calls are one cudaGraphLaunch -- instead of ~60
+// copy / event / launch API calls.  A failed capture just runs directly.
+int detect_host(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
+                const rh_segments* sg, const rh_trace* tr, const rh_trace_packed* pk,
+                double thr, const rh_screen_params* screen, int64_t series_len,
+                const double* hist, const uint8_t* reset, const rh_pass_out* out,
+                uint8_t* outcome, int64_t* series_len_out, cudaStream_t stream) {
+  if (!ctx || !sh || !sg || !out || (!tr && !pk) || (tr && !tr->mb_off) ||
+      (pk && (!pk->iter_doc || !pk->mb_docs || !pk->doc_len))) {
+    set_error("detect_host: NULL argument");
+    return RH_E_INVALID;
+  }
+  if ((pk ? pk->n_iter : tr->n_iter) == 0) return RH_OK;
+  auto& g = ctx->host_graph;
+  std::vector<uint64_t> key = host_pass_key(sh, m, sg, tr, pk, thr, screen, series_len, hist,
+                                            reset, out, outcome, series_len_out, stream);
+  const bool same = key == g.key;
+  if (same && g.exec) {
+    RH_CUDA(cudaGraphLaunch(g.exec, stream));
+    RH_CUDA(cudaStreamSynchronize(stream));
+    return RH_OK;
+  }
+  if (!same) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    g.exec = nullptr;
+    g.key = std::move(key);
+    g.failed = false;
+  } else if (!g.failed && !getenv("RH_NO_GRAPH")) {
+    cudaGraph_t graph = nullptr;
+    if (cudaStreamBeginCapture(stream, cudaStreamCaptureModeRelaxed) == cudaSuccess) {
+      const int rc = enqueue_host_pass(ctx, sh, m, sg, tr, pk, thr, screen, series_len, hist,
+                                       reset, out, outcome, series_len_out, stream);
+      const cudaError_t e = cudaStreamEndCapture(stream, &graph);
+      if (rc == RH_OK && e == cudaSuccess && graph &&
+          cudaGraphInstantiate(&g.exec, graph, 0) == cudaSuccess) {
+        cudaGraphDestroy(graph);
+        RH_CUDA(cudaGraphLaunch(g.exec, stream));
+        RH_CUDA(cudaStreamSynchronize(stream));
+        return RH_OK;
+      }
+      if (graph) cudaGraphDestroy(graph);
+      g.exec = nullptr;
+    }
+    cudaGetLastError();  // clear a capture failure; run directly below
+    g.failed = true;
+  }
+  if (int rc = enqueue_host_pass(ctx, sh, m, sg, tr, pk, thr, screen, series_len, hist, reset,
+                                 out, outcome, series_len_out, stream))
+    return rc;
   RH_CUDA(cudaStreamSynchronize(stream));
   return RH_OK;
 }
@@ -960,8 +1147,21 @@ int rh_detector_pass_host(rh_ctx* ctx, const rh_pipe_shape* shape, const rh_cost
                           const rh_screen_params* screen, int64_t series_len,
                           const double* hist, const uint8_t* reset, const rh_pass_out* out,
                           uint8_t* outcome, int64_t* series_len_out, void* stream) {
-  return rh::detect_host(ctx, shape, model, segs, trace, threshold, screen, series_len, hist,
-                         reset, out, outcome, series_len_out, rh::as_stream(stream));
+  return rh::detect_host(ctx, shape, model, segs, trace, nullptr, threshold, screen,
+                         series_len, hist, reset, out, outcome, series_len_out,
+                         rh::as_stream(stream));
+}
+
+int rh_detector_pass_host_packed(rh_ctx* ctx, const rh_pipe_shape* shape,
+                                 const rh_cost_model* model, const rh_segments* segs,
+                                 const rh_trace_packed* trace, double threshold,
+                                 const rh_screen_params* screen, int64_t series_len,
+                                 const double* hist, const uint8_t* reset,
+                                 const rh_pass_out* out, uint8_t* outcome,
+                                 int64_t* series_len_out, void* stream) {
+  return rh::detect_host(ctx, shape, model, segs, nullptr, trace, threshold, screen,
+                         series_len, hist, reset, out, outcome, series_len_out,
+                         rh::as_stream(stream));
 }
 
 }  // extern "C"

@@ -495,8 +495,12 @@ extern "C" int rh_screen_prepare(rh_ctx* ctx, const rh_screen_params* params,
   ctx->prep.valid = false;
   if (n == 0) return RH_OK;
   cudaStream_t st = as_stream(stream);
-  // the previous rh_screen may still read the slot-2 results
-  if (ctx->prep.consumed_recorded) RH_CUDA(cudaStreamWaitEvent(st, ctx->prep.consumed, 0));
+  // the previous rh_screen may still read the slot-2 results (inside a graph
+  // capture the fork from the capturing stream already orders us after it)
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  RH_CUDA(cudaStreamIsCapturing(st, &cap));
+  if (ctx->prep.consumed_recorded && cap == cudaStreamCaptureStatusNone)
+    RH_CUDA(cudaStreamWaitEvent(st, ctx->prep.consumed, 0));
   ScreenArgs a;
   fill_inputs(a, params, series_len, hist, n, observed, reset);
   if (int rc = launch_prepare(ctx, a, st)) return rc;

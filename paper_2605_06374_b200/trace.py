@@ -118,6 +118,23 @@ class DetectorTrace:
             "out_flag_severity": 5.0 * G,
         }
 
+    def packed(self) -> dict:
+        """The packed wire form (rh_trace_packed): per-iteration document
+        offsets (int32), documents per micro-batch (uint8) and document
+        lengths (uint16).  Raises ValueError when the trace does not fit it."""
+        n, M = self.n_iter, self.M
+        off = np.asarray(self.mb_off, dtype=np.int64)
+        counts = np.diff(off)
+        if counts.size and (counts.max() > 255 or counts.min() < 0):
+            raise ValueError("packed trace: a micro-batch holds more than 255 documents")
+        if self.doc_len.size and (self.doc_len.max() > 65535 or self.doc_len.min() < 0):
+            raise ValueError("packed trace: a document is longer than 65535 tokens")
+        return {
+            "iter_doc": np.ascontiguousarray(off[::M][:n + 1], dtype=np.int32),
+            "mb_docs": np.ascontiguousarray(counts, dtype=np.uint8),
+            "doc_len": np.ascontiguousarray(self.doc_len, dtype=np.uint16),
+        }
+
     def attach_measurements(self, stage_cost_actual: np.ndarray, observed: np.ndarray,
                             noise: float = 0.01, seed: int = 1) -> None:
         """device_time from the ground-truth stage costs (harness.py:424-427):

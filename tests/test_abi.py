@@ -38,6 +38,7 @@ STRUCTS = {
     "rh_pipe_shape": _lib.PipeShape,
     "rh_segments": _lib.Segments,
     "rh_trace": _lib.Trace,
+    "rh_trace_packed": _lib.TracePacked,
     "rh_pass_out": _lib.PassOut,
     "rh_screen_params": _lib.ScreenParams,
     "rh_migration_desc": _lib.MigrationDesc,

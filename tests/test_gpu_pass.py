@@ -179,3 +179,101 @@ def test_screen_prepare_protocol(seed, oracle, cuda_device):
         for oc, ln in outs:
             np.testing.assert_array_equal(oc.cpu().numpy(), ooc)
             assert int(ln.item()) == oln
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_detector_pass_host_packed(seed, oracle, cuda_device):
+    """rh_detector_pass_host_packed (uint16 docs, uint8 counts, device-side CSR
+    rebuild per chunk) == oracle, including chunk boundaries and empty
+    micro-batches."""
+    import ctypes as C
+
+    from paper_2605_06374_b200 import _lib
+    from paper_2605_06374_b200.tables import pipe_shape
+    from paper_2605_06374_b200.workload import cost_model_c
+    from tests.oracle_bind import HostSegments
+
+    tr = with_measurements(random_trace(400 + seed, n_iter=2600 + 911 * seed, n_seg=3,
+                                        pp=int(2 + seed * 2)), oracle, noise=0.02, seed=seed)
+    tr.reset[::500] = 1
+    pk = tr.packed()
+    segs = HostSegments(tr.known)
+    n, G = tr.n_iter, tr.cfg.dp * tr.cfg.pp
+    keep = [np.ascontiguousarray(a) for a in (tr.seg, tr.device_time.astype(np.float32),
+                                               tr.observed, tr.reset)]
+    seg, dt, obs, rst = keep
+    ms, st = np.zeros(n), np.zeros(n, np.uint8)
+    fl, sv = np.zeros(n * G, np.uint8), np.zeros(n * G, np.float32)
+    oc, ln = np.zeros(n, np.uint8), C.c_int64()
+    trc = _lib.TracePacked(n, seg.ctypes.data, pk["iter_doc"].ctypes.data,
+                           pk["mb_docs"].ctypes.data, pk["doc_len"].ctypes.data,
+                           dt.ctypes.data, obs.ctypes.data)
+    out = _lib.PassOut(ms.ctypes.data, st.ctypes.data, None, fl.ctypes.data, sv.ctypes.data)
+    shape = pipe_shape(tr.cfg, tr.M, tr.N, has_allreduce=tr.has_allreduce, max_mb=segs.max_mb)
+    sp = _lib.ScreenParams(20, 1, 3.0)
+    lib = _lib.load_library()
+    _lib.check(lib.rh_detector_pass_host_packed(
+        _lib.context(), C.byref(shape), C.byref(cost_model_c(tr.model)), C.byref(segs.c),
+        C.byref(trc), 1.25, C.byref(sp), 0, None, rst.ctypes.data, C.byref(out),
+        oc.ctypes.data, C.byref(ln), None), "rh_detector_pass_host_packed")
+    oms, ost, _, ofl, osv = oracle.detect(tr)
+    ooc, oln = oracle.screen(tr.observed, ost, reset=tr.reset)
+    np.testing.assert_array_equal(st, ost)
+    np.testing.assert_array_equal(_bits(ms), _bits(oms))
+    np.testing.assert_array_equal(fl, ofl.reshape(-1))
+    np.testing.assert_array_equal(sv.view(np.uint32), osv.reshape(-1).view(np.uint32))
+    np.testing.assert_array_equal(oc, ooc)
+    assert ln.value == oln
+
+
+def test_detector_pass_host_graph_replay(oracle, cuda_device):
+    """Repeated host passes on the same buffers run direct, then capture a CUDA
+    graph, then replay it: each call must see the CURRENT buffer contents."""
+    import ctypes as C
+
+    from paper_2605_06374_b200 import _lib
+    from paper_2605_06374_b200.tables import pipe_shape
+    from paper_2605_06374_b200.workload import cost_model_c
+    from tests.oracle_bind import HostSegments
+
+    tr = with_measurements(random_trace(777, n_iter=4100, n_seg=2, pp=3), oracle, noise=0.02,
+                           seed=7)
+    tr.reset[::900] = 1
+    pk = tr.packed()
+    segs = HostSegments(tr.known)
+    n, G = tr.n_iter, tr.cfg.dp * tr.cfg.pp
+    seg = np.ascontiguousarray(tr.seg)
+    dt = np.ascontiguousarray(tr.device_time.astype(np.float32))
+    obs = np.ascontiguousarray(tr.observed.copy())
+    rst = np.ascontiguousarray(tr.reset)
+    ms, st = np.zeros(n), np.zeros(n, np.uint8)
+    fl, sv = np.zeros(n * G, np.uint8), np.zeros(n * G, np.float32)
+    oc, ln = np.zeros(n, np.uint8), C.c_int64()
+    trc = _lib.TracePacked(n, seg.ctypes.data, pk["iter_doc"].ctypes.data,
+                           pk["mb_docs"].ctypes.data, pk["doc_len"].ctypes.data,
+                           dt.ctypes.data, obs.ctypes.data)
+    out = _lib.PassOut(ms.ctypes.data, st.ctypes.data, None, fl.ctypes.data, sv.ctypes.data)
+    shape = pipe_shape(tr.cfg, tr.M, tr.N, has_allreduce=tr.has_allreduce, max_mb=segs.max_mb)
+    sp = _lib.ScreenParams(20, 1, 3.0)
+    lib, ctx = _lib.load_library(), _lib.context()
+    model = cost_model_c(tr.model)
+    base_obs, base_dt = obs.copy(), dt.copy()
+    rng = np.random.default_rng(5)
+    for call in range(4):
+        # new measurements in place (same pointers): 1.0x, then perturbed
+        scale = 1.0 if call == 0 else float(rng.uniform(0.8, 1.6))
+        obs[:] = base_obs * scale
+        dt[:] = base_dt * np.float32(scale)
+        _lib.check(lib.rh_detector_pass_host_packed(
+            ctx, C.byref(shape), C.byref(model), C.byref(segs.c), C.byref(trc), 1.25,
+            C.byref(sp), 0, None, rst.ctypes.data, C.byref(out), oc.ctypes.data, C.byref(ln),
+            None), "rh_detector_pass_host_packed")
+        tr.observed, tr.device_time = obs.copy(), dt.copy().reshape(tr.device_time.shape)
+        oms, ost, _, ofl, osv = oracle.detect(tr)
+        ooc, oln = oracle.screen(obs, ost, reset=rst)
+        np.testing.assert_array_equal(st, ost)
+        np.testing.assert_array_equal(_bits(ms), _bits(oms))
+        np.testing.assert_array_equal(fl, ofl.reshape(-1))
+        np.testing.assert_array_equal(sv.view(np.uint32), osv.reshape(-1).view(np.uint32))
+        np.testing.assert_array_equal(oc, ooc)
+        assert ln.value == oln

@@ -226,3 +226,23 @@ def test_detector_trace_golden(oracle, k):
         assert alarms == it["alarms"], (i, oc[i], it["alarms"])
     # final series length (reset after a confirmation happens outside observe)
     assert (0 if its[-1]["reset_after"] else ln) == its[-1]["series_len"]
+
+
+def test_packed_trace_roundtrip():
+    """DetectorTrace.packed(): the wire form decodes back to the int32 CSR."""
+    from tests.helpers import random_trace
+
+    for seed in range(4):
+        tr = random_trace(900 + seed, n_iter=57)
+        pk = tr.packed()
+        n, M = tr.n_iter, tr.M
+        assert pk["iter_doc"].dtype == np.int32 and pk["iter_doc"].shape == (n + 1,)
+        assert pk["mb_docs"].dtype == np.uint8 and pk["mb_docs"].shape == (n * M,)
+        assert pk["doc_len"].dtype == np.uint16
+        off = np.concatenate([[0], np.cumsum(pk["mb_docs"].astype(np.int64))])
+        np.testing.assert_array_equal(off, tr.mb_off)
+        np.testing.assert_array_equal(pk["iter_doc"], tr.mb_off[::M])
+        np.testing.assert_array_equal(pk["doc_len"].astype(np.int32), tr.doc_len)
+    tr.doc_len[0] = 70000
+    with pytest.raises(ValueError):
+        tr.packed()
