@@ -153,9 +153,29 @@ struct WindowTest {
   bool skip, cand, refill_len;  // refill_len: series still at most `window` long
 };
 
+// Round-0 pop decision of iteration j from its prepared verdict bits and
+// status (the filter / validation logic of outcome_of, without the outcome).
+__device__ __forceinline__ unsigned pop0_of(unsigned c0, unsigned stb, int fe) {
+  const bool cand = c0 & 1u, refill = !cand && fe && (c0 & 2u);
+  if (!(cand || refill)) return 0u;
+  if (fe && !(stb & RH_IT_ESCALATE)) return cand ? 1u : 0u;
+  return (stb & (RH_IT_STAGE_FLAG | RH_IT_LINK_FLAG)) ? 0u : 1u;
+}
+
+// state byte of iteration j in the previous round: bit 0 popped, bit 1
+// changed.  from_c0: that round is round 0, rebuilt on the fly from the
+// prepared verdicts (changed == popped, since round 0 starts from kept = all).
+__device__ __forceinline__ unsigned prev_state(const ScreenArgs& a, const uint8_t* cur,
+                                               bool first_round, bool from_c0, int64_t j) {
+  if (first_round) return 0u;
+  if (from_c0) return pop0_of(__ldg(a.c0 + j), __ldg(a.st + j), a.fe) * 3u;
+  return (unsigned)__ldcg(cur + j);
+}
+
 __device__ __forceinline__ WindowTest window_test(const ScreenArgs& a, int64_t i, int r, double x,
                                                   const double* ob, const uint8_t* cur,
-                                                  bool first_round, WarpScratch& ws) {
+                                                  bool first_round, WarpScratch& ws,
+                                                  bool from_c0 = false) {
   const int lane = threadIdx.x & 31;
   const int w = a.w;
   const int64_t first = r >= 0 ? r : 0;
@@ -165,7 +185,7 @@ __device__ __forceinline__ WindowTest window_test(const ScreenArgs& a, int64_t i
   for (int64_t hi = i; hi > first && found < w; hi -= 32) {
     const int64_t j = hi - 32 + lane;
     const bool in = j >= first;
-    const unsigned sv = in ? (first_round ? 0u : (unsigned)__ldcg(cur + j)) : 1u;
+    const unsigned sv = in ? prev_state(a, cur, first_round, from_c0, j) : 1u;
     const bool kept = !(sv & 1u);
     const unsigned km = __ballot_sync(0xffffffffu, kept);
     const unsigned cm = __ballot_sync(0xffffffffu, (sv & 2u) != 0u);
@@ -322,8 +342,9 @@ __global__ void __launch_bounds__(kScreenThreads) screen_kernel(const ScreenArgs
       unsigned stb, old;
       unsigned pop;
       if (round == 0) {
-        // verdicts of round 0 came from round0_kernel; cache what later
-        // rounds need
+        // First cooperative round = Jacobi round 1, reading round 0's state on
+        // the fly from the prepared verdicts (no barrier for round 0 itself).
+        // Cache what later rounds need.
         x = a.obs[i];
         stb = a.st[i];
         r = a.R[i];
@@ -332,14 +353,18 @@ __global__ void __launch_bounds__(kScreenThreads) screen_kernel(const ScreenArgs
           const int64_t j = i - 32 + lane;
           s_ob[wid][k][lane] = j >= 0 ? a.obs[j] : 0.0;
         }
-        uint8_t oc;
-        pop = outcome_of(c0 & 1u, (c0 & 2u) != 0u, stb, a.fe, oc);
+        __syncwarp();
+        uint8_t oc0;
+        old = outcome_of(c0 & 1u, (c0 & 2u) != 0u, stb, a.fe, oc0);
+        const WindowTest t = window_test(a, i, r, x, cached ? s_ob[wid][k] : nullptr, cur, false,
+                                         s_ws[wid], true);
+        uint8_t oc = oc0;
+        pop = old;
+        if (!t.skip) pop = outcome_of(t.cand, t.refill_len, stb, a.fe, oc);
         if (lane == 0) {
           a.outcome[i] = oc;
           if (cached) s_it[wid][k] = IterCache{x, r, (uint8_t)stb, 0};
         }
-        __syncwarp();
-        old = 0;
       } else {
         if (cached) {
           const IterCache c = s_it[wid][k];
