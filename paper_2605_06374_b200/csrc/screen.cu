@@ -175,7 +175,7 @@ __device__ __forceinline__ unsigned prev_state(const ScreenArgs& a, const uint8_
 __device__ __forceinline__ WindowTest window_test(const ScreenArgs& a, int64_t i, int r, double x,
                                                   const double* ob, const uint8_t* cur,
                                                   bool first_round, WarpScratch& ws,
-                                                  bool from_c0 = false) {
+                                                  bool from_c0 = false, int sv0 = -1) {
   const int lane = threadIdx.x & 31;
   const int w = a.w;
   const int64_t first = r >= 0 ? r : 0;
@@ -185,7 +185,10 @@ __device__ __forceinline__ WindowTest window_test(const ScreenArgs& a, int64_t i
   for (int64_t hi = i; hi > first && found < w; hi -= 32) {
     const int64_t j = hi - 32 + lane;
     const bool in = j >= first;
-    const unsigned sv = in ? prev_state(a, cur, first_round, from_c0, j) : 1u;
+    // sv0: this lane's state byte of the first chunk, preloaded by the caller
+    const unsigned sv = !in ? 1u
+                            : (hi == i && sv0 >= 0 ? (unsigned)sv0
+                                                   : prev_state(a, cur, first_round, from_c0, j));
     const bool kept = !(sv & 1u);
     const unsigned km = __ballot_sync(0xffffffffu, kept);
     const unsigned cm = __ballot_sync(0xffffffffu, (sv & 2u) != 0u);
@@ -295,6 +298,13 @@ struct IterCache {
   uint8_t pop;
 };
 
+struct ScreenSmem {
+  WarpScratch ws[kScreenWarps];
+  double ob[kScreenWarps][kCache][32];
+  IterCache it[kScreenWarps][kCache];
+  unsigned cnt;
+};
+
 #ifdef RH_SCREEN_TRACE
 // debug build only (tools/screen_trace.py): per round, block 0's timestamps
 // around the barrier and the slowest block's compute time
@@ -316,10 +326,14 @@ extern "C" int rh_debug_screen_trace(unsigned long long* t, unsigned long long* 
 #endif
 
 __global__ void __launch_bounds__(kScreenThreads) screen_kernel(const ScreenArgs a) {
-  __shared__ WarpScratch s_ws[kScreenWarps];
-  __shared__ double s_ob[kScreenWarps][kCache][32];
-  __shared__ IterCache s_it[kScreenWarps][kCache];
-  __shared__ unsigned s_cnt;
+  // dynamic shared memory (ScreenSmem): per-warp scratch, the 32 preceding
+  // observations and the constants of each cached iteration
+  extern __shared__ __align__(16) unsigned char screen_smem[];
+  ScreenSmem& sm = *reinterpret_cast<ScreenSmem*>(screen_smem);
+  WarpScratch* s_ws = sm.ws;
+  auto& s_ob = sm.ob;
+  auto& s_it = sm.it;
+  unsigned& s_cnt = sm.cnt;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t gw = (int64_t)blockIdx.x * kScreenWarps + wid;
   const int64_t n_warps = (int64_t)gridDim.x * kScreenWarps;
@@ -334,9 +348,7 @@ __global__ void __launch_bounds__(kScreenThreads) screen_kernel(const ScreenArgs
     const unsigned long long t_start = gtimer();
 #endif
     unsigned changes = 0;
-    int k = 0;
-    for (int64_t i = gw; i < a.n; i += n_warps, ++k) {
-      const bool cached = k < kCache;
+    auto process = [&](int64_t i, int k, bool cached, int sv0) {
       int r;
       double x;
       unsigned stb, old;
@@ -357,7 +369,7 @@ __global__ void __launch_bounds__(kScreenThreads) screen_kernel(const ScreenArgs
         uint8_t oc0;
         old = outcome_of(c0 & 1u, (c0 & 2u) != 0u, stb, a.fe, oc0);
         const WindowTest t = window_test(a, i, r, x, cached ? s_ob[wid][k] : nullptr, cur, false,
-                                         s_ws[wid], true);
+                                         s_ws[wid], true, sv0);
         uint8_t oc = oc0;
         pop = old;
         if (!t.skip) pop = outcome_of(t.cand, t.refill_len, stb, a.fe, oc);
@@ -379,7 +391,7 @@ __global__ void __launch_bounds__(kScreenThreads) screen_kernel(const ScreenArgs
           old = __ldcg(cur + i) & 1u;
         }
         const WindowTest t = window_test(a, i, r, x, cached ? s_ob[wid][k] : nullptr, cur, false,
-                                         s_ws[wid]);
+                                         s_ws[wid], false, sv0);
         if (t.skip) {
           pop = old;
         } else {
@@ -394,7 +406,24 @@ __global__ void __launch_bounds__(kScreenThreads) screen_kernel(const ScreenArgs
         if (cached) s_it[wid][k].pop = (uint8_t)pop;
       }
       changes += changed;
+    };
+    // the first window chunk of every cached iteration is loaded up front, so
+    // those round trips overlap instead of queueing behind each other
+    int pre[kCache];
+#pragma unroll
+    for (int k = 0; k < kCache; ++k) {
+      const int64_t i = gw + k * n_warps, j = i - 32 + lane;
+      pre[k] = -1;
+      if (i < a.n && j >= 0)
+        pre[k] = (int)(round == 0 ? pop0_of(__ldg(a.c0 + j), __ldg(a.st + j), a.fe) * 3u
+                                  : (unsigned)__ldcg(cur + j));
     }
+#pragma unroll
+    for (int k = 0; k < kCache; ++k) {
+      const int64_t i = gw + k * n_warps;
+      if (i < a.n) process(i, k, true, pre[k]);
+    }
+    for (int64_t i = gw + kCache * n_warps; i < a.n; i += n_warps) process(i, kCache, false, -1);
     if (lane == 0 && changes) atomicAdd(&s_cnt, changes);
     // the next round's counter was last read before this round began
     if (blockIdx.x == 0 && threadIdx.x == 0) a.cnt[(round + 1) % 3] = 0;
@@ -571,9 +600,12 @@ extern "C" int rh_screen(rh_ctx* ctx, const rh_screen_params* params, int64_t se
     return RH_OK;
   }
   static int occ = -1;  // cached occupancy of the cooperative kernel
-  if (occ < 0)
+  if (occ < 0) {
+    RH_CUDA(cudaFuncSetAttribute((void*)screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(ScreenSmem)));
     RH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (void*)screen_kernel,
-                                                          kScreenThreads, 0));
+                                                          kScreenThreads, sizeof(ScreenSmem)));
+  }
   if (occ < 1) {
     set_error("rh_screen: kernel does not fit on an SM");
     return RH_E_SHAPE;
@@ -617,7 +649,7 @@ extern "C" int rh_screen(rh_ctx* ctx, const rh_screen_params* params, int64_t se
   RH_CUDA(cudaMemsetAsync(base, 0, ctrl, st));
   void* kargs[] = {&a};
   RH_CUDA(cudaLaunchCooperativeKernel((void*)screen_kernel, dim3(blocks), dim3(kScreenThreads),
-                                      kargs, 0, st));
+                                      kargs, sizeof(ScreenSmem), st));
   RH_CHECK_LAUNCH(ctx);
   if (!ctx->prep.consumed)
     RH_CUDA(cudaEventCreateWithFlags(&ctx->prep.consumed, cudaEventDisableTiming));
