@@ -369,14 +369,14 @@ def run_scheduler(args, world, rank, local, names=("C3", "C4", "C5")):
     import torch
 
     from paper_2605_06374_b200.replan_scenarios import replan_problem
-    from paper_2605_06374_b200.search import ReplanSearch, distributed_best, shard_range
+    from paper_2605_06374_b200.search import ReplanSearch, distributed_best
 
     dev = torch.device("cuda", local)
     out = {}
     for name in names:
         st, cfg, mbs, inputs = replan_problem(name)
         s = ReplanSearch(inputs, dev)
-        a, b = shard_range(s.size, rank, world)
+        a, b = s.shard(rank, world)
         s.eval_async(a, b)  # warm-up (module load, caches)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -435,6 +435,13 @@ int rh_search_destroy(rh_search* search);
 /* total number of candidates / layouts */
 int64_t rh_search_size(const rh_search* search);
 int32_t rh_search_layouts(const rh_search* search);
+/* Cost-balanced contiguous shard of [0, size) for `rank` of `world` (HOST):
+ * boundaries fall between (layout, partition variant) blocks of candidates,
+ * weighted by each block's evaluation work (its replica-pipeline table plus
+ * the per-candidate combination), so that no table row is computed twice and
+ * ranks finish together.  The union over ranks is [0, size). */
+int rh_search_shard(const rh_search* search, int32_t rank, int32_t world, int64_t* begin,
+                    int64_t* end);
 /* Score candidates [begin, end) and min-loc them.  best_score/best_index are
  * DEVICE scalars (+inf / -1 when nothing is feasible); scores (optional,
  * device, [end-begin]) receives every candidate's score (+inf infeasible). */

@@ -1045,6 +1045,53 @@ int rh_search_destroy(rh_search* S) {
 }
 
 int64_t rh_search_size(const rh_search* S) { return S ? S->total : 0; }
+
+int rh_search_shard(const rh_search* S, int32_t rank, int32_t world, int64_t* begin,
+                    int64_t* end) {
+  if (!S || world < 1 || rank < 0 || rank >= world || !begin || !end) {
+    set_error("rh_search_shard: invalid arguments");
+    return RH_E_INVALID;
+  }
+  // work of one (layout, v) block: 8*D pipelines of ~c*P*(M/D) chunks each
+  // (~c*P*M*8 chunk steps) plus nu candidates combining D table entries
+  // (one combination step ~ 1/8 of a chunk step, measured on B200)
+  const int c = S->d.schedule == RH_SCHED_ZBH ? 3 : 2;
+  const double M = (double)S->d.n_micro_batches;
+  double total = 0.0;
+  for (size_t li = 0; li < S->lT.size(); ++li)
+    total += (double)S->lnv[li] *
+             (8.0 * c * S->lP[li] * M + 0.125 * (double)S->lnu[li] * S->lD[li]);
+  const double lo = total * rank / world, hi = total * (rank + 1) / world;
+  // block k belongs to the rank whose cost interval holds its cumulative midpoint
+  int64_t b = -1, e = -1;
+  double acc = 0.0;
+  for (size_t li = 0; li < S->lT.size(); ++li) {
+    const double w = 8.0 * c * S->lP[li] * M + 0.125 * (double)S->lnu[li] * S->lD[li];
+    for (long long v = 0; v < S->lnv[li]; ++v) {
+      const double mid = acc + 0.5 * w;
+      acc += w;
+      if (mid < lo) continue;
+      if (mid >= hi && rank < world - 1) break;
+      const int64_t first = S->lbase[li] + v * S->lnu[li];
+      if (b < 0) b = first;
+      e = first + S->lnu[li];
+    }
+  }
+  if (b < 0) {  // an empty shard: place it where the cost boundary falls
+    b = e = 0;
+    double acc2 = 0.0;
+    for (size_t li = 0; li < S->lT.size() && acc2 < lo; ++li) {
+      const double w = 8.0 * c * S->lP[li] * M + 0.125 * (double)S->lnu[li] * S->lD[li];
+      for (long long v = 0; v < S->lnv[li] && acc2 + 0.5 * w < lo; ++v) {
+        acc2 += w;
+        b = e = S->lbase[li] + (v + 1) * S->lnu[li];
+      }
+    }
+  }
+  *begin = b;
+  *end = e;
+  return RH_OK;
+}
 int32_t rh_search_layouts(const rh_search* S) { return S ? (int32_t)S->lT.size() : 0; }
 
 int rh_search_eval(rh_ctx* ctx, rh_search* S, int64_t begin, int64_t end, double* best_score,

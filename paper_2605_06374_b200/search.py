@@ -51,6 +51,8 @@ _SIGS = {
                          C.c_int),
     "rh_search_destroy": ([C.c_void_p], C.c_int),
     "rh_search_size": ([C.c_void_p], C.c_int64),
+    "rh_search_shard": ([C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_int64),
+                         C.POINTER(C.c_int64)], C.c_int),
     "rh_search_layouts": ([C.c_void_p], C.c_int32),
     "rh_search_eval": ([C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p,
                         C.c_void_p, C.c_void_p], C.c_int),
@@ -190,6 +192,14 @@ class ReplanSearch:
         except Exception:
             pass
 
+    def shard(self, rank: int, world: int) -> tuple[int, int]:
+        """Cost-balanced contiguous shard of the candidate range for `rank`
+        (rh_search_shard: boundaries between (layout, partition) blocks)."""
+        b, e = C.c_int64(), C.c_int64()
+        _lib.check(self.lib.rh_search_shard(self.handle, int(rank), int(world), C.byref(b),
+                                            C.byref(e)), "rh_search_shard")
+        return int(b.value), int(e.value)
+
     def eval_async(self, begin: int = 0, end: int | None = None, scores=None):
         """Launch scoring of [begin, end); results stay on the device."""
         end = self.size if end is None else int(end)
@@ -270,8 +280,12 @@ def distributed_best(search: ReplanSearch, group=None, begin: int = 0,
     if not dist.is_available() or not dist.is_initialized():
         return search.best(begin, end)
     r, w = dist.get_rank(group), dist.get_world_size(group)
-    a, b = shard_range(end - begin, r, w)
-    best, idx = search.eval_async(begin + a, begin + b)
+    if begin == 0 and end == search.size:
+        a, b = search.shard(r, w)  # cost-balanced over the whole space
+    else:
+        a, b = shard_range(end - begin, r, w)
+        a, b = begin + a, begin + b
+    best, idx = search.eval_async(a, b)
     if dist.get_backend(group) == "nccl":
         import torch
 

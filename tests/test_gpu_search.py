@@ -87,3 +87,23 @@ def test_random_problems(seed, oracle, cuda_device):
     fin = np.isfinite(c)
     np.testing.assert_array_equal(bits(g[fin]), bits(c[fin]))
     assert gpu.best(a, b) == cpu.best(a, b)
+
+
+@pytest.mark.parametrize("k", range(4))
+def test_cost_balanced_shards(k, cuda_device):
+    """rh_search_shard: for any world size the shards tile [0, size) in rank
+    order without gaps or overlap, boundaries fall on (layout, partition)
+    blocks, and the minimum of the per-shard winners is the global winner."""
+    from paper_2605_06374_b200.search import ReplanSearch, lexicographic_min
+
+    case = load("search")["cases"][k]
+    *_, inputs = search_problem(case)
+    gpu = ReplanSearch(inputs)
+    full = gpu.best()
+    for world in (1, 2, 3, 4, 7, 8):
+        shards = [gpu.shard(r, world) for r in range(world)]
+        assert shards[0][0] == 0 and shards[-1][1] == gpu.size
+        for (a0, b0), (a1, b1) in zip(shards, shards[1:]):
+            assert b0 == a1 and a0 <= b0
+        per = [gpu.best(a, b) for a, b in shards if b > a]
+        assert lexicographic_min(per) == full
