@@ -40,6 +40,8 @@ struct rh_search {
   std::vector<int32_t> link_nodes;
   std::vector<double> link_factor;
   std::vector<int32_t> cur_groups, cur_partition;
+  // prep results read back once (rh_search_decode is then host-only)
+  std::vector<int32_t> h_gblk, h_repart, h_pstart;
   // layouts
   std::vector<int32_t> lT, lD, lP, lgoff, lpoff, ldoff, lboff, lnb;
   std::vector<long long> lbase, lnv, lnu, lpair, lrt;
@@ -736,8 +738,15 @@ static int build_op_lists(rh_ctx* ctx, rh_search* S, cudaStream_t st) {
   const int NL = (int)S->lT.size(), M = S->d.n_micro_batches;
   const int stride = M + 2;
   const bool zbh = S->d.schedule == RH_SCHED_ZBH;
-  std::vector<int32_t> pst(S->n_rep + NL);
+  std::vector<int32_t>& pst = S->h_pstart;
+  pst.resize(S->n_rep + NL);
+  S->h_gblk.resize(S->n_groups);
+  S->h_repart.resize(S->n_stage);
   RH_CUDA(cudaMemcpyAsync(pst.data(), S->dv.pstart, 4 * pst.size(), cudaMemcpyDeviceToHost, st));
+  RH_CUDA(cudaMemcpyAsync(S->h_gblk.data(), S->dv.gblk, 4 * S->n_groups, cudaMemcpyDeviceToHost,
+                          st));
+  RH_CUDA(cudaMemcpyAsync(S->h_repart.data(), S->dv.repart, 4 * S->n_stage,
+                          cudaMemcpyDeviceToHost, st));
   RH_CUDA(cudaStreamSynchronize(st));
   std::vector<char> need(33 * (size_t)stride, 0);
   for (int li = 0; li < NL; ++li) {
@@ -759,27 +768,47 @@ static int build_op_lists(rh_ctx* ctx, rh_search* S, cudaStream_t st) {
     for (int md = 0; md <= M; ++md) {
       const size_t slot = (size_t)P * stride + md;
       if (!need[slot]) continue;
-      // emit in (level ascending, stage descending) order straight from the
-      // closed forms; live counts give the capacity peak
+      // counting sort by DAG level of the forward closed forms; stages are
+      // visited in descending order, so each level lists them descending
       off[slot] = (int32_t)ops.size();
       int t_end = 0;
       for (int s2 = 0; s2 < P; ++s2)
         t_end = std::max(t_end, ChainLevels{s2, P, md, std::min(P - 1 - s2, md)}.end(zbh));
+      std::vector<int32_t> lvl_start(t_end + 1, 0);
+      const int kinds = zbh ? 3 : 2;
+      for (int s2 = 0; s2 < P; ++s2) {
+        const ChainLevels lv{s2, P, md, std::min(P - 1 - s2, md)};
+        for (int j = 0; j < md; ++j) {
+          ++lvl_start[lv.F(j) + 1];
+          ++lvl_start[lv.B(j) + 1];
+          if (zbh) ++lvl_start[lv.W(j) + 1];
+        }
+      }
+      for (int t = 0; t < t_end; ++t) lvl_start[t + 1] += lvl_start[t];
+      const size_t base_op = ops.size();
+      ops.resize(base_op + (size_t)kinds * P * md);
+      for (int s2 = P - 1; s2 >= 0; --s2) {
+        const ChainLevels lv{s2, P, md, std::min(P - 1 - s2, md)};
+        const uint32_t depF = s2 > 0 ? 1u : 0u, depB = s2 < P - 1 ? 2u : 0u;
+        for (int j = 0; j < md; ++j) {
+          ops[base_op + lvl_start[lv.F(j)]++] =
+              (uint32_t)s2 | (kOpF << 6) | (depF << 8) | ((uint32_t)j << 10);
+          ops[base_op + lvl_start[lv.B(j)]++] =
+              (uint32_t)s2 | (kOpB << 6) | (depB << 8) | ((uint32_t)j << 10);
+          if (zbh)
+            ops[base_op + lvl_start[lv.W(j)]++] =
+                (uint32_t)s2 | (kOpW << 6) | ((uint32_t)j << 10);
+        }
+      }
+      // capacity peak: forward chunks in flight on any stage
       std::vector<int> live(P, 0);
       int pk = 0;
-      for (int t = 0; t < t_end; ++t)
-        for (int s2 = P - 1; s2 >= 0; --s2) {
-          int j = 0;
-          const unsigned kind =
-              (unsigned)ChainLevels{s2, P, md, std::min(P - 1 - s2, md)}.at(t, zbh, j);
-          if (!kind) continue;
-          uint32_t dep = 0;
-          if (kind == kOpF && s2 > 0) dep = 1;
-          if (kind == kOpB && s2 < P - 1) dep = 2;
-          ops.push_back((uint32_t)s2 | (kind << 6) | (dep << 8) | ((uint32_t)j << 10));
-          if (kind == kOpF) pk = std::max(pk, ++live[s2]);
-          if (kind == kOpB) --live[s2];
-        }
+      for (size_t e = base_op; e < ops.size(); ++e) {
+        const int s2 = ops[e] & 63u;
+        const unsigned kind = (ops[e] >> 6) & 3u;
+        if (kind == kOpF) pk = std::max(pk, ++live[s2]);
+        if (kind == kOpB) --live[s2];
+      }
       cnt[slot] = (int32_t)ops.size() - off[slot];
       peak[slot] = pk;
     }
@@ -1193,11 +1222,9 @@ int rh_search_decode(rh_ctx* ctx, rh_search* S, int64_t index, rh_candidate* out
   out->layout = li;
   out->partition_variant = vv;
   out->count_variant = uu;
-  std::vector<int32_t> gblk(D * P), rep(P), pst(D + 1);
-  RH_CUDA(cudaMemcpy(gblk.data(), S->dv.gblk + S->lgoff[li], 4 * D * P, cudaMemcpyDeviceToHost));
-  RH_CUDA(cudaMemcpy(rep.data(), S->dv.repart + S->lpoff[li], 4 * P, cudaMemcpyDeviceToHost));
-  RH_CUDA(cudaMemcpy(pst.data(), S->dv.pstart + S->ldoff[li] + li, 4 * (D + 1),
-                     cudaMemcpyDeviceToHost));
+  const int32_t* gblk = S->h_gblk.data() + S->lgoff[li];
+  const int32_t* rep = S->h_repart.data() + S->lpoff[li];
+  const int32_t* pst = S->h_pstart.data() + S->ldoff[li] + li;
   const rh_search_desc& d = S->d;
   std::vector<int> part(P), cnt(D);
   int psrc = -1, pdst = -1, csrc = -1, cdst = -1;

@@ -231,7 +231,7 @@ class ReplanSearch:
         _lib.check(self.lib.rh_search_decode(self.ctx, self.handle, int(index), C.byref(c),
                                              groups.ctypes.data, part.ctypes.data,
                                              cnt.ctypes.data), "rh_search_decode")
-        g = [tuple(int(x) for x in groups[k * c.tp:(k + 1) * c.tp]) for k in range(c.dp * c.pp)]
+        g = list(map(tuple, groups[:c.dp * c.pp * c.tp].reshape(-1, c.tp).tolist()))
         return CandidatePlan(int(c.index), c.tp, c.dp, c.pp, part[:c.pp].tolist(),
                              cnt[:c.dp].tolist(), g, c.partition_variant, c.count_variant,
                              bool(c.feasible))
