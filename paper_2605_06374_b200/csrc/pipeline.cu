@@ -237,21 +237,76 @@ constexpr int kSmallThreads = 128;
 #endif
 constexpr int kSmallMinBlocks = RH_SMALL_MIN_BLOCKS;  // CTAs per SM the register budget targets
 
-// Copy n ints global -> shared with U independent loads in flight per thread.
-template <int U>
-__device__ __forceinline__ void stage_ints(int32_t* dst, const int32_t* src, int n) {
-  for (int q0 = threadIdx.x; q0 < n; q0 += U * blockDim.x) {
-    int32_t v[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int q = q0 + u * blockDim.x;
-      v[u] = q < n ? __ldg(src + q) : 0;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int q = q0 + u * blockDim.x;
-      if (q < n) dst[q] = v[u];
-    }
+// ---- TMA bulk staging (cp.async.bulk + mbarrier, sm_90+ / sm_100a)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // visible to the TMA unit
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+        "selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Stage n ints at src into shared memory: the 16-byte-aligned interior by
+// one TMA bulk copy (issued by thread 0, completing on `bar`), the ragged
+// head / tail words by plain loads -- nothing outside [src, src+n) is read.
+// `dst_base` is 16-byte aligned with 16 spare bytes; the returned pointer is
+// dst_base shifted by src's misalignment so the interior lines up.  Returns
+// the bytes the TMA will deliver (for the barrier's expect_tx).
+struct StagePlan {
+  int32_t* dst;
+  int head, tail;      // words loaded by threads at the front / back
+  unsigned tx_bytes;   // bytes delivered by the bulk copy
+};
+__device__ __forceinline__ StagePlan stage_plan(unsigned char* dst_base, const int32_t* src,
+                                                int n) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(src);
+  StagePlan sp;
+  sp.dst = reinterpret_cast<int32_t*>(dst_base + (a & 15));
+  const uintptr_t a16 = (a + 15) & ~uintptr_t(15), b = a + 4 * (uintptr_t)n,
+                  b16 = b & ~uintptr_t(15);
+  if (b16 > a16) {
+    sp.head = (int)((a16 - a) / 4);
+    sp.tail = (int)((b - b16) / 4);
+    sp.tx_bytes = (unsigned)(b16 - a16);
+  } else {  // too short for a bulk copy: threads load everything
+    sp.head = n;
+    sp.tail = 0;
+    sp.tx_bytes = 0;
+  }
+  return sp;
+}
+__device__ __forceinline__ void stage_issue(const StagePlan& sp, const int32_t* src,
+                                            uint64_t* bar) {
+  if (sp.tx_bytes) bulk_g2s(sp.dst + sp.head, src + sp.head, sp.tx_bytes, bar);
+}
+__device__ __forceinline__ void stage_edges(const StagePlan& sp, const int32_t* src, int n) {
+  for (int q = threadIdx.x; q < sp.head + sp.tail; q += blockDim.x) {
+    const int k = q < sp.head ? q : n - sp.tail + (q - sp.head);
+    sp.dst[k] = __ldg(src + k);
   }
 }
 
@@ -382,19 +437,38 @@ __global__ void __launch_bounds__(kSmallThreads, ZBH ? 4 : kSmallMinBlocks) pass
   unsigned* it_st = reinterpret_cast<unsigned*>(it_ms + p.ipb);
   const int it_bytes = ((p.ipb * 12 + 15) / 16) * 16;
   unsigned long long* s_q = reinterpret_cast<unsigned long long*>(smem_raw + it_bytes);
-  int32_t* s_off = reinterpret_cast<int32_t*>(s_q + p.ipb * M);
+  // offsets region: 16-B aligned with 16 spare bytes (TMA alignment shift)
+  int32_t* s_off_raw = reinterpret_cast<int32_t*>(
+      smem_raw + ((it_bytes + 8 * (size_t)p.ipb * M + 15) & ~size_t(15)));
   double* base_t = reinterpret_cast<double*>(smem_raw + p.region_off);
-  int32_t* s_doc = reinterpret_cast<int32_t*>(base_t);
+  __shared__ uint64_t s_bar;
   if (tid < p.ipb) {
     it_ms[tid] = 0.0;
     it_st[tid] = 0u;
   }
-  // ---- everything that does not depend on shared memory is issued first,
-  // so its latency hides behind the offset / document staging
+  // ---- staging by TMA: thread 0 arms the barrier and issues the bulk
+  // copies of the offsets and (when they fit) the documents; the per-thread
+  // loads below run meanwhile
   const int seg = on && p.tr.seg ? __ldg(p.tr.seg + it) : 0;
   const int n_mb = n_it * M;
-  stage_ints<8>(s_off, p.tr.mb_off + it0 * M, n_mb + 1);
-  for (int q = tid; q < n_mb; q += nt) s_q[q] = 0ull;
+  const int32_t* g_off = p.tr.mb_off + it0 * M;
+  const int32_t d_lo = __ldg(g_off), d_hi = __ldg(g_off + n_mb);
+  const int n_doc = d_hi - d_lo;
+  const bool staged = n_doc <= p.doc_stage;
+  const StagePlan so = stage_plan(reinterpret_cast<unsigned char*>(s_off_raw), g_off, n_mb + 1);
+  const StagePlan sd = staged ? stage_plan(reinterpret_cast<unsigned char*>(base_t),
+                                           p.tr.doc_len + d_lo, n_doc)
+                              : StagePlan{nullptr, 0, 0, 0u};
+  if (tid == 0) {
+    mbar_init(&s_bar, 1);
+    mbar_arrive_expect_tx(&s_bar, so.tx_bytes + sd.tx_bytes);
+    stage_issue(so, g_off, &s_bar);
+    if (staged) stage_issue(sd, p.tr.doc_len + d_lo, &s_bar);
+  }
+  stage_edges(so, g_off, n_mb + 1);
+  if (staged) stage_edges(sd, p.tr.doc_len + d_lo, n_doc);
+  int32_t* s_off = so.dst;
+  int32_t* s_doc = sd.dst;
   int m0 = 0, md = 0;
   double rlF[P], rlB[P], rlW[P], sp[P], hf[P], hb[P], fin[P], ssum[P];
   float meas[P];
@@ -435,49 +509,24 @@ __global__ void __launch_bounds__(kSmallThreads, ZBH ? 4 : kSmallMinBlocks) pass
       meas[s] = mx;
     }
   }
-  __syncthreads();
-  const int32_t d_lo = s_off[0];
-  const int n_doc = s_off[n_mb] - d_lo;
-  if (n_doc <= p.doc_stage) {
-    stage_ints<8>(s_doc, p.tr.doc_len + d_lo, n_doc);
-    __syncthreads();
-    // document-parallel segmented sum of l^2
-    const int per = (n_doc + nt - 1) / nt;
-    const int k0 = min(n_doc, tid * per), k1 = min(n_doc, k0 + per);
-    if (k0 < k1) {
-      int lo = 0, hi = n_mb;  // last micro-batch starting at or before k0
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (s_off[mid] - d_lo <= k0)
-          lo = mid;
-        else
-          hi = mid;
-      }
-      int mb = lo, next = s_off[mb + 1] - d_lo;
-      unsigned long long acc = 0;
-      for (int k = k0; k < k1; ++k) {
-        if (k >= next) {
-          atomicAdd(s_q + mb, acc);
-          acc = 0;
-          do {
-            ++mb;
-            next = s_off[mb + 1] - d_lo;
-          } while (next <= k);
-        }
+  mbar_wait(&s_bar, 0);  // the bulk copies have landed
+  __syncthreads();       // ... and so have the threads' edge words
+  // quadratic loads, one thread per micro-batch (no atomics)
+  for (int mb = tid; mb < n_mb; mb += nt) {
+    const int32_t k0 = s_off[mb] - d_lo, k1 = s_off[mb + 1] - d_lo;
+    unsigned long long q = 0;
+    if (staged) {
+      for (int32_t k = k0; k < k1; ++k) {
         const long long l = s_doc[k];
-        acc += (unsigned long long)(l * l);
-      }
-      atomicAdd(s_q + mb, acc);
-    }
-  } else {  // too many documents to stage: one thread per micro-batch
-    for (int mb = tid; mb < n_mb; mb += nt) {
-      unsigned long long q = 0;
-      for (int32_t k = s_off[mb]; k < s_off[mb + 1]; ++k) {
-        const long long l = __ldg(p.tr.doc_len + k);
         q += (unsigned long long)(l * l);
       }
-      s_q[mb] = q;
+    } else {  // too many documents to stage: straight from global memory
+      for (int32_t k = k0; k < k1; ++k) {
+        const long long l = __ldg(p.tr.doc_len + d_lo + k);
+        q += (unsigned long long)(l * l);
+      }
     }
+    s_q[mb] = q;
   }
   __syncthreads();  // sums complete; the document buffer is dead from here
   if (md > p.mmax) md = -1;
@@ -709,11 +758,15 @@ int launch_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
     const int threads = p.ipb * D;
     // j is stored in 14 bits of a level word
     const int it_bytes = ((p.ipb * 12 + 15) / 16) * 16;
-    const size_t head = it_bytes + 8 * (size_t)p.ipb * M + 4 * (size_t)(p.ipb * M + 1);
+    // [it_ms|it_st] [q: ipb*M int64] [off: 16 + 4*(ipb*M+1)] [docs -> base costs]
+    const size_t off_base = (it_bytes + 8 * (size_t)p.ipb * M + 15) & ~size_t(15);
+    const size_t head = off_base + 16 + 4 * (size_t)(p.ipb * M + 1);
     p.region_off = (int)((head + 15) & ~size_t(15));
-    // the region holds the staged documents, later the base costs
-    const size_t region = std::max<size_t>(16 * 1024, (size_t)threads * p.mmax * 8);
-    p.doc_stage = (int)(region / 4);
+    // the region holds the staged documents (+16 B for the TMA alignment
+    // shift), later the base costs
+    const size_t region =
+        std::max<size_t>(16 * 1024 + 16, (size_t)kSmallThreads * p.mmax * 8);
+    p.doc_stage = (int)((region - 16) / 4);
     p.static_max = p.static_div_max = kStaticMaxMB;
     const size_t smem = p.region_off + region;
     if (smem <= ctx->smem_optin && smem <= 56 * 1024) {
