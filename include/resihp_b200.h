@@ -136,6 +136,12 @@ int rh_ctx_destroy(rh_ctx* ctx);
 /* number of kernel launches issued through this context (for bench.py) */
 int64_t rh_ctx_launches(const rh_ctx* ctx);
 
+/* Device self-test of the exact division used on the hot path (a hoisted
+ * correctly rounded reciprocal + Markstein correction, with __ddiv_rn outside
+ * a safe range): counts the bit mismatches against __ddiv_rn over n seeded
+ * random (a, b) pairs.  Synchronous; 0 is the only acceptable result. */
+int rh_selftest_division(rh_ctx* ctx, int64_t n, uint64_t seed, int64_t* mismatches);
+
 /* ------------------------------------------------------- cost model rows */
 /* quad_load (workload.py:83-85) for n micro-batches given a CSR of docs. */
 int rh_quad_load(rh_ctx* ctx, int64_t n_mb, const int32_t* mb_off,

@@ -7,6 +7,7 @@
 #include <unordered_map>
 
 #include "common.cuh"
+#include "wavefront.cuh"
 
 namespace {
 thread_local char g_err[1024] = "";
@@ -117,11 +118,65 @@ __global__ void validate_kernel(int64_t n, const double* __restrict__ meas,
   sev[i] = s;
 }
 
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+
+// div_recip (hoisted-reciprocal division) against __ddiv_rn over regimes of
+// divisors: random in (0, 1], k / 2^m fractions (TP-subgroup speeds), random
+// severities, all-ones mantissas, 1 - ulp, and wide exponents for both.
+__global__ void selftest_div_kernel(int64_t n, uint64_t seed, unsigned long long* bad) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint64_t h1 = splitmix64(seed ^ (uint64_t)i), h2 = splitmix64(h1 ^ 0x5bd1e995ull);
+    const uint64_t mant_a = h1 & 0xfffffffffffffull, mant_b = h2 & 0xfffffffffffffull;
+    const int ea = (int)((h1 >> 52) % 200) - 120;  // a in [2^-120, 2^80)
+    double a = __longlong_as_double((long long)(((uint64_t)(1023 + ea) << 52) | mant_a));
+    double b;
+    switch ((h2 >> 52) & 7) {
+      case 0: b = __longlong_as_double((long long)((1022ull << 52) | mant_b)); break;  // [0.5,1)
+      case 1: b = (double)(1 + (h2 >> 56) % 8) / 8.0; break;                          // k/8
+      case 2: b = 0.3 + 0.4 * (double)(mant_b >> 20) / (double)(1ull << 32); break;     // severity
+      case 3: b = __longlong_as_double((long long)(((uint64_t)(1023 - (int)((h2 >> 56) % 30)) << 52) |
+                                                   0xfffffffffffffull)); break;     // all-ones
+      case 4: b = 1.0 - 0x1p-53 * (double)(1 + (h2 >> 60)); break;                   // 1 - k ulp
+      case 5: b = __longlong_as_double((long long)(((uint64_t)(1023 - (int)((h2 >> 56) % 90)) << 52) |
+                                                   mant_b)); break;  // [2^-89, 2)
+      case 6: b = 1.0; break;
+      default: b = (double)(1 + (h2 >> 56) % 7) / 7.0; a = b * (double)(1 + (h1 >> 60)); break;
+    }
+    const double q1 = div_recip(a, b, recip_of(b));
+    const double q2 = __ddiv_rn(a, b);
+    if (__double_as_longlong(q1) != __double_as_longlong(q2)) atomicAdd(bad, 1ull);
+  }
+}
+
 }  // namespace rh
 
 using namespace rh;
 
 extern "C" {
+
+int rh_selftest_division(rh_ctx* ctx, int64_t n, uint64_t seed, int64_t* mismatches) {
+  if (!ctx || n < 0 || !mismatches) {
+    set_error("rh_selftest_division: invalid arguments");
+    return RH_E_INVALID;
+  }
+  unsigned long long* d = nullptr;
+  RH_CUDA(cudaMalloc(&d, sizeof(unsigned long long)));
+  RH_CUDA(cudaMemset(d, 0, sizeof(unsigned long long)));
+  selftest_div_kernel<<<ctx->num_sms * 8, 256>>>(n, seed, d);
+  cudaError_t e = cudaGetLastError();
+  unsigned long long h = 0;
+  if (e == cudaSuccess) e = cudaMemcpy(&h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) return cuda_fail(e, "rh_selftest_division");
+  *mismatches = (int64_t)h;
+  return RH_OK;
+}
 
 int rh_abi_version(void) { return RH_ABI_VERSION; }
 

@@ -29,6 +29,8 @@
 #include <algorithm>
 #include <type_traits>
 
+#include <math_constants.h>
+
 #include "common.cuh"
 #include "wavefront.cuh"
 
@@ -52,7 +54,7 @@ struct PassParams {
   const int32_t* sched_peak;        // [mmax+1] peak in-flight forward chunks on any stage
   int region_off;            // smem offset of the document / base-cost region
   int doc_stage;             // documents that fit in that region
-  int static_max, static_div_max;  // largest counts walked by the unrolled code
+  int static_max;  // largest micro-batch count walked by the unrolled code
 };
 
 // MAXT = launch bound: 256 for the common case (more registers per lane),
@@ -322,6 +324,7 @@ struct WalkArgs {
   const double (&rlB)[P];
   const double (&rlW)[P];
   const double (&sp)[P];
+  const double (&inv)[P];  // recip_of(sp): exact division by div_recip
   const double (&hf)[P];
   const double (&hb)[P];
   double (&fin)[P];
@@ -330,11 +333,13 @@ struct WalkArgs {
 
 // One chunk of stage s: c = (rl * base_j) [/ speed], start = max(chain
 // finish, dependency finish + hop), finish = start + c (pipeline.py:275-291).
-template <bool DIV>
+template <bool SAFE>
 __device__ __forceinline__ double chunk(double& fin, double& ssum, double rl, double b,
-                                        double sp, double dep) {
-  double c = __dmul_rn(rl, b);
-  if (DIV && sp != 1.0) c = div_slow(c, sp);  // out of line: keeps the unrolled walks small
+                                        double sp, double inv, double dep) {
+  // (rl * b) / sp exactly as __ddiv_rn; SAFE: the walk's operand ranges were
+  // checked up front, otherwise every division is __ddiv_rn itself
+  const double a = __dmul_rn(rl, b);
+  const double c = SAFE ? div_fast(a, sp, inv) : __ddiv_rn(a, sp);
   const double st = fin > dep ? fin : dep;
   fin = __dadd_rn(st, c);
   ssum = __dadd_rn(ssum, c);
@@ -343,7 +348,7 @@ __device__ __forceinline__ double chunk(double& fin, double& ssum, double rl, do
 
 // Dynamic walk over the level table: one 64-bit word per level, 16 bits per
 // stage (0 idle, else kind | j << 2); stages in descending order.
-template <int P, bool DIV>
+template <int P, int ZBH, bool SAFE>
 __device__ __forceinline__ void walk_table(const WalkArgs<P>& a, const unsigned long long* lv,
                                            const unsigned long long* lv_end) {
   double lastF[P], lastB[P];
@@ -359,9 +364,9 @@ __device__ __forceinline__ void walk_table(const WalkArgs<P>& a, const unsigned 
       const bool isF = kind == kOpF, isB = kind == kOpB;
       const double dF = s > 0 ? __dadd_rn(lastF[s > 0 ? s - 1 : 0], a.hf[s]) : 0.0;
       const double dB = s < P - 1 ? __dadd_rn(lastB[s < P - 1 ? s + 1 : 0], a.hb[s]) : 0.0;
-      const double nf = chunk<DIV>(a.fin[s], a.ssum[s],
-                                   isF ? a.rlF[s] : (isB ? a.rlB[s] : a.rlW[s]),
-                                   a.bt[(code >> 2) * kSmallThreads], a.sp[s],
+      const double nf = chunk<SAFE>(a.fin[s], a.ssum[s],
+                                   isF ? a.rlF[s] : (isB || !ZBH ? a.rlB[s] : a.rlW[s]),
+                                   a.bt[(code >> 2) * kSmallThreads], a.sp[s], a.inv[s],
                                    isF ? dF : (isB ? dB : 0.0));
       lastF[s] = isF ? nf : lastF[s];
       lastB[s] = isB ? nf : lastB[s];
@@ -382,7 +387,7 @@ __host__ __device__ constexpr int n_levels(int P, int MM) { return 2 * P + 3 * M
 
 // Fully unrolled walk for a compile-time micro-batch count: every op, its
 // kind and j are constants, so a chunk is ~8 instructions with no dispatch.
-template <int P, int ZBH, int MM, bool DIV>
+template <int P, int ZBH, int MM>
 __device__ __forceinline__ void walk_static(const WalkArgs<P>& a) {
   double lastF[P], lastB[P];
 #pragma unroll
@@ -396,12 +401,15 @@ __device__ __forceinline__ void walk_static(const WalkArgs<P>& a) {
       const int kind = op_at(P, MM, ZBH, t, s, j);
       if (kind == kOpF) {
         const double dep = s > 0 ? __dadd_rn(lastF[s > 0 ? s - 1 : 0], a.hf[s]) : 0.0;
-        lastF[s] = chunk<DIV>(a.fin[s], a.ssum[s], a.rlF[s], a.bt[j * kSmallThreads], a.sp[s], dep);
+        lastF[s] = chunk<true>(a.fin[s], a.ssum[s], a.rlF[s], a.bt[j * kSmallThreads], a.sp[s],
+                         a.inv[s], dep);
       } else if (kind == kOpB) {
         const double dep = s < P - 1 ? __dadd_rn(lastB[s < P - 1 ? s + 1 : 0], a.hb[s]) : 0.0;
-        lastB[s] = chunk<DIV>(a.fin[s], a.ssum[s], a.rlB[s], a.bt[j * kSmallThreads], a.sp[s], dep);
+        lastB[s] = chunk<true>(a.fin[s], a.ssum[s], a.rlB[s], a.bt[j * kSmallThreads], a.sp[s],
+                         a.inv[s], dep);
       } else if (kind == kOpW) {
-        chunk<DIV>(a.fin[s], a.ssum[s], a.rlW[s], a.bt[j * kSmallThreads], a.sp[s], 0.0);
+        chunk<true>(a.fin[s], a.ssum[s], a.rlW[s], a.bt[j * kSmallThreads], a.sp[s], a.inv[s],
+                    0.0);
       }
     }
   }
@@ -409,16 +417,16 @@ __device__ __forceinline__ void walk_static(const WalkArgs<P>& a) {
 
 constexpr int kStaticMaxMB = 12;  // replicas with <= 12 micro-batches
 
-template <int P, int ZBH, bool DIV, int MM = 1>
+template <int P, int ZBH, int MM = 1>
 __device__ __forceinline__ bool walk_static_dispatch(const WalkArgs<P>& a, int mm) {
   if constexpr (MM > kStaticMaxMB) {
     return false;
   } else {
     if (mm == MM) {
-      walk_static<P, ZBH, MM, DIV>(a);
+      walk_static<P, ZBH, MM>(a);
       return true;
     }
-    return walk_static_dispatch<P, ZBH, DIV, MM + 1>(a, mm);
+    return walk_static_dispatch<P, ZBH, MM + 1>(a, mm);
   }
 }
 
@@ -530,12 +538,16 @@ __global__ void __launch_bounds__(kSmallThreads, ZBH ? 4 : kSmallMinBlocks) pass
   }
   __syncthreads();  // sums complete; the document buffer is dead from here
   if (md > p.mmax) md = -1;
+  double b_lo = CUDART_INF, b_hi = 0.0;  // base-cost range (non-zero minimum)
   if (md > 0) {
     const double lin = __dmul_rn(p.m.alpha, (double)p.sh.token_budget);
     const unsigned long long* q = s_q + li * M + m0;
-    for (int j = 0; j < md; ++j)
-      base_t[j * kSmallThreads + tid] =
-          __dadd_rn(lin, __dmul_rn(p.m.beta, (double)(long long)q[j]));
+    for (int j = 0; j < md; ++j) {
+      const double b = __dadd_rn(lin, __dmul_rn(p.m.beta, (double)(long long)q[j]));
+      base_t[j * kSmallThreads + tid] = b;
+      b_hi = fmax(b_hi, b);
+      if (b > 0.0) b_lo = fmin(b_lo, b);
+    }
   }
   const int m = md > 0 ? md : 0;
   bool stopped = false;
@@ -553,20 +565,32 @@ __global__ void __launch_bounds__(kSmallThreads, ZBH ? 4 : kSmallMinBlocks) pass
   // schedule, so its peak per micro-batch count is precomputed
   const bool over = p.sh.capacity > 0 && mm > 0 && __ldg(p.sched_peak + mm) > p.sh.capacity;
   const double* bt = base_t + tid;
-  bool unit = true;  // x / 1.0 == x exactly: healthy replicas never divide
+  // exact division by a hoisted reciprocal when every numerator rl * b of the
+  // walk and every divisor are in range (always, in practice); otherwise the
+  // table walk divides with __ddiv_rn
+  double inv[P];
+  bool safe = true;
+  double r_lo = CUDART_INF, r_hi = 0.0;
 #pragma unroll
-  for (int s = 0; s < P; ++s) unit = unit && sp[s] == 1.0;
-  WalkArgs<P> wa{bt, rlF, rlB, rlW, sp, hf, hb, fin, ssum};
+  for (int s = 0; s < P; ++s) {
+    inv[s] = recip_of(sp[s]);
+    safe = safe && inv[s] != 0.0;
+    const double rs[3] = {rlF[s], rlB[s], ZBH ? rlW[s] : rlB[s]};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      r_hi = fmax(r_hi, rs[k]);
+      if (rs[k] > 0.0) r_lo = fmin(r_lo, rs[k]);
+    }
+  }
+  safe = safe && div_range_ok(r_lo * b_lo, r_hi * b_hi);
+  WalkArgs<P> wa{bt, rlF, rlB, rlW, sp, inv, hf, hb, fin, ssum};
   if (mm > 0) {
     const unsigned long long* l0 = p.sched + __ldg(p.sched_off + mm);
     const unsigned long long* l1 = p.sched + __ldg(p.sched_off + mm + 1);
-    if (unit) {
-      if (mm > p.static_max || !walk_static_dispatch<P, ZBH, false>(wa, mm))
-        walk_table<P, false>(wa, l0, l1);
-    } else {
-      if (mm > p.static_div_max || !walk_static_dispatch<P, ZBH, true>(wa, mm))
-        walk_table<P, true>(wa, l0, l1);
-    }
+    if (!safe)
+      walk_table<P, ZBH, false>(wa, l0, l1);
+    else if (mm > p.static_max || !walk_static_dispatch<P, ZBH>(wa, mm))
+      walk_table<P, ZBH, true>(wa, l0, l1);
   }
   __syncthreads();  // iteration slots initialised before the reductions
   // ---- replica makespan, validation, iteration reductions
@@ -767,7 +791,7 @@ int launch_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
     const size_t region =
         std::max<size_t>(16 * 1024 + 16, (size_t)kSmallThreads * p.mmax * 8);
     p.doc_stage = (int)((region - 16) / 4);
-    p.static_max = p.static_div_max = kStaticMaxMB;
+    p.static_max = kStaticMaxMB;
     const size_t smem = p.region_off + region;
     if (smem <= ctx->smem_optin && smem <= 56 * 1024) {
       const bool zbh = sh->schedule == RH_SCHED_ZBH;

@@ -53,6 +53,7 @@ struct rh_search {
   void* dmem = nullptr;
   size_t dbytes = 0;
   cudaStream_t last_stream = nullptr;  // stream of the latest create / eval
+  int div_safe = 0;  // see SearchArgs::div_safe
   struct Dev {
     int32_t *lT, *lD, *lP, *lgoff, *lpoff, *ldoff, *lboff, *lnb;
     long long *lbase, *lnv, *lnu, *lpair, *lrt;
@@ -63,6 +64,9 @@ struct rh_search {
     double* blk_speed;
     int32_t *gblk, *gnode;
     double *gspeed, *ghop;
+    // per-group tables of the pipe kernel, TRANSPOSED to [s][d] so the lanes
+    // of a warp (consecutive replicas) read consecutive addresses
+    double *tspeed, *tinv, *thop;
     double *ring, *sspeed;
     int32_t* repart;
     double* rspeed;
@@ -95,6 +99,7 @@ struct SearchArgs {
   int amort;
   int cur_T, cur_D, cur_P, T0;
   double r_bw;     // ratio_b + ratio_w (1F1B's fused BW chunk)
+  int div_safe;    // every chunk's (numerator, speed) is in div_fast's exact range
   int tab_stride;  // op-list index: slot = P * tab_stride + md
   rh_search::Dev v;
 };
@@ -286,18 +291,25 @@ __global__ void prep_kernel(SearchArgs a) {
       const int g = taken + __popc(m & ((1u << lane) - 1u));
       a.v.gblk[goff + g] = boff + b;
       // slowest * |group| / nominal_tp (cluster.py:155-169)
-      a.v.gspeed[goff + g] = __ddiv_rn(__dmul_rn(a.v.blk_speed[boff + b], (double)T),
-                                       (double)a.T0);
+      const double gsp = __ddiv_rn(__dmul_rn(a.v.blk_speed[boff + b], (double)T),
+                                   (double)a.T0);
+      a.v.gspeed[goff + g] = gsp;
       a.v.gnode[goff + g] = a.v.blk_node[boff + b];
     }
     taken += __popc(m);
   }
   __syncwarp();
-  // hop weights on stage boundaries (same in both directions: T == T)
+  // hop weights on stage boundaries (same in both directions: T == T);
+  // transposed copies for the pipe kernel
   for (int g = lane; g < K; g += 32) {
-    const int s = g % P;
-    a.v.ghop[goff + g] = s < P - 1 ? hop_cost(a, a.v.gnode[goff + g], a.v.gnode[goff + g + 1], T)
-                                   : 0.0;
+    const int s = g % P, d = g / P;
+    const double h = s < P - 1 ? hop_cost(a, a.v.gnode[goff + g], a.v.gnode[goff + g + 1], T)
+                               : 0.0;
+    a.v.ghop[goff + g] = h;
+    a.v.thop[goff + s * D + d] = h;
+    const double gsp = a.v.gspeed[goff + g];
+    a.v.tspeed[goff + s * D + d] = gsp;
+    a.v.tinv[goff + s * D + d] = recip_of(gsp);
   }
   // per stage: all-reduce ring bandwidth (comm.py:87-107), min speed
   for (int s = lane; s < P; s += 32) {
@@ -510,15 +522,17 @@ __global__ void __launch_bounds__(kPipeThreads) pipe_kernel(SearchArgs a, const 
         if (ZBH) pipe_smem[fN + q * kPipeThreads + tid] = 0.0;
       }
       const double* bs = a.v.base + start;
-      const double* sp_d = a.v.gspeed + goff + d * P;
-      const double* hop_d = a.v.ghop + goff + d * P;
+      // [s][d] tables: element (d, s) at s * D
+      const double* sp_d = a.v.tspeed + goff + d;
+      const double* inv_d = a.v.tinv + goff + d;
+      const double* hop_d = a.v.thop + goff + d;
       const double* rlt = a.v.rl + pair * 3LL * 32 - 32;  // indexed by kind * 32 + s
       const uint32_t* opp = a.v.ops + e0;
       // software pipeline: op codes two ahead, their global operands one ahead,
       // so only the shared-memory state chain is serial
       struct Operands {
         unsigned op;
-        double rl, b, sp, hop;
+        double rl, b, sp, inv, hop;
       };
       auto fetch = [&](unsigned op) {
         Operands o;
@@ -527,8 +541,9 @@ __global__ void __launch_bounds__(kPipeThreads) pipe_kernel(SearchArgs a, const 
         const unsigned kind = (op >> 6) & 3u, dk = (op >> 8) & 3u;
         o.rl = __ldg(rlt + kind * 32 + st);
         o.b = __ldg(bs + (op >> 10));
-        o.sp = __ldg(sp_d + st);
-        o.hop = dk ? __ldg(hop_d + st - (dk == 1 ? 1 : 0)) : 0.0;
+        o.sp = __ldg(sp_d + st * D);
+        o.inv = __ldg(inv_d + st * D);
+        o.hop = dk ? __ldg(hop_d + (st - (dk == 1 ? 1 : 0)) * D) : 0.0;
         return o;
       };
       unsigned op2 = ne > 1 ? __ldg(opp + 1) : 0u;
@@ -540,8 +555,11 @@ __global__ void __launch_bounds__(kPipeThreads) pipe_kernel(SearchArgs a, const 
         op2 = op3;
         const int st = o.op & 63u;
         const unsigned kind = (o.op >> 6) & 3u, dk = (o.op >> 8) & 3u;
+        // (rl * b) / sp exactly as __ddiv_rn: unit speeds skip it (uniform
+        // branch), others use the hoisted reciprocal when the host proved the
+        // ranges safe for the whole search
         double c = __dmul_rn(o.rl, o.b);
-        if (o.sp != 1.0) c = div_slow(c, o.sp);  // out of line: unit speeds skip it
+        if (o.sp != 1.0) c = a.div_safe ? div_fast(c, o.sp, o.inv) : div_slow(c, o.sp);
         const int self = st * kPipeThreads + tid;
         double dep = 0.0;
         if (dk) {
@@ -721,6 +739,7 @@ static SearchArgs make_args(const rh_search* S) {
   a.cur_P = d.cur_pp;
   a.T0 = d.nominal_tp > 0 ? d.nominal_tp : 1;
   a.r_bw = d.model.ratio_b + d.model.ratio_w;
+  a.div_safe = S->div_safe;
   a.tab_stride = d.n_micro_batches + 2;
   a.v = S->dv;
   return a;
@@ -955,6 +974,31 @@ int rh_search_create(rh_ctx* ctx, const rh_search_desc* desc, rh_search** out, v
     *out = S;
     return RH_OK;
   }
+  {  // ranges of every numerator ((ratio * L) * base) and divisor (group speed)
+    double q_lo = HUGE_VAL, q_hi = 0.0;
+    for (int j = 0; j < d.n_micro_batches; ++j) {
+      const double b = d.model.alpha * d.token_budget + d.model.beta * (double)desc->quad[j];
+      q_hi = std::max(q_hi, b);
+      if (b > 0.0) q_lo = std::min(q_lo, b);
+    }
+    const double ratios[4] = {d.model.ratio_f, d.model.ratio_b, d.model.ratio_w,
+                              d.model.ratio_b + d.model.ratio_w};
+    double r_lo = HUGE_VAL, r_hi = 0.0;
+    for (double r : ratios) {
+      r_hi = std::max(r_hi, r * d.total_layers);
+      if (r > 0.0) r_lo = std::min(r_lo, r);  // times at least one layer
+    }
+    double s_lo = HUGE_VAL, s_hi = 0.0;
+    const double T0 = d.nominal_tp > 0 ? d.nominal_tp : 1;
+    for (double v : S->blk_speed) {
+      s_lo = std::min(s_lo, v * 1.0 / T0);
+      s_hi = std::max(s_hi, v * 32.0 / T0);
+    }
+    // margins of 2^10 absorb the rounding of these host estimates
+    const bool nums = q_hi * r_hi <= 0x1p890 && (q_hi * r_hi == 0.0 || q_lo * r_lo >= 0x1p-890);
+    const bool dens = S->blk_speed.empty() || (s_lo >= 0x1p-90 && s_hi <= 0x1p90);
+    S->div_safe = nums && dens ? 1 : 0;
+  }
   // ---- device memory
   static int max_blocks_per_sm = -1;  // cached occupancy of the combine kernel
   if (max_blocks_per_sm < 0)
@@ -999,6 +1043,8 @@ int rh_search_create(rh_ctx* ctx, const rh_search_desc* desc, rh_search** out, v
   const size_t up_bytes = bytes;  // everything uploaded sits in front
   const size_t o_gblk = take(4 * S->n_groups), o_gnode = take(4 * S->n_groups),
                o_gspeed = take(8 * S->n_groups), o_ghop = take(8 * S->n_groups),
+               o_tspeed = take(8 * S->n_groups), o_tinv = take(8 * S->n_groups),
+               o_thop = take(8 * S->n_groups),
                o_ring = take(8 * S->n_stage), o_sspeed = take(8 * S->n_stage),
                o_repart = take(4 * S->n_stage), o_rspeed = take(8 * S->n_rep),
                o_pstart = take(4 * (S->n_rep + NL)), o_same = take(4 * NL),
@@ -1047,6 +1093,7 @@ int rh_search_create(rh_ctx* ctx, const rh_search_desc* desc, rh_search** out, v
   v.link_nodes = I(o_ln); v.link_factor = Dp(o_lf); v.cur_groups = I(o_cg);
   v.cur_partition = I(o_cp);
   v.gblk = I(o_gblk); v.gnode = I(o_gnode); v.gspeed = Dp(o_gspeed); v.ghop = Dp(o_ghop);
+  v.tspeed = Dp(o_tspeed); v.tinv = Dp(o_tinv); v.thop = Dp(o_thop);
   v.ring = Dp(o_ring); v.sspeed = Dp(o_sspeed); v.repart = I(o_repart);
   v.rspeed = Dp(o_rspeed); v.pstart = I(o_pstart); v.same = I(o_same); v.base = Dp(o_base);
   v.blk_best = Dp(o_bb); v.blk_idx = LL(o_bi);

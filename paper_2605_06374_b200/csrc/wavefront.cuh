@@ -41,6 +41,42 @@ namespace rh {
 // over it rather than an always-executed predicated sequence.
 __device__ __noinline__ inline double div_slow(double a, double b) { return __ddiv_rn(a, b); }
 
+// Correctly rounded a / b with a hoisted reciprocal y = __drcp_rn(b)
+// (Markstein): q = RN(a*y), r = a - b*q exactly (FMA), RN(q + r*y) = RN(a/b)
+// whenever nothing under- or overflows.  Outside a conservative range it
+// defers to __ddiv_rn, so the result always equals __ddiv_rn(a, b)
+// (rh_selftest_division checks this on the device).  With b == 1, y == 1:
+// q = a, r = 0 and the result is a -- unit speeds cost 3 flops, no branch.
+// Safe range: a == 0 or |a| in [2^-900, 2^900], b in [2^-100, 2^100] -- then
+// a/b, the residual and r*y are all normal.  recip_of returns 0 for an
+// out-of-range b, which sends every division by it to __ddiv_rn.
+__device__ __forceinline__ double div_recip(double a, double b, double y) {
+  const double q = __dmul_rn(a, y);
+  const double r = __fma_rn(-b, q, a);
+  const double res = __fma_rn(r, y, q);
+  const double aa = fabs(a);
+  if (!((aa >= 0x1p-900 && aa <= 0x1p900) || a == 0.0) || y == 0.0) return div_slow(a, b);
+  return res;
+}
+
+// div_recip without the per-call range test, for callers that checked the
+// operand ranges once for a whole walk (see div_range_ok).
+__device__ __forceinline__ double div_fast(double a, double b, double y) {
+  const double q = __dmul_rn(a, y);
+  return __fma_rn(__fma_rn(-b, q, a), y, q);
+}
+
+// every numerator of a walk lies in [lo, hi] (lo = smallest non-zero one):
+// div_fast is then exact for divisors with recip_of(b) != 0
+__device__ __forceinline__ bool div_range_ok(double lo, double hi) {
+  return !(hi > 0x1p900) && (hi == 0.0 || lo >= 0x1p-900);
+}
+
+__device__ __forceinline__ double recip_of(double b) {
+  if (!(b >= 0x1p-100 && b <= 0x1p100)) return 0.0;
+  return b == 1.0 ? 1.0 : __drcp_rn(b);
+}
+
 struct ChainLevels {
   int s, P, m, w;
   __host__ __device__ __forceinline__ int F(int j) const {
@@ -97,7 +133,7 @@ __device__ __forceinline__ void chain_walk(int s, int P, int pw, int md, int w, 
                                            double rlW, double sp, double hopf, double hopb,
                                            int cap, int /*mmax*/, double& fin, double& ssum,
                                            bool& over, bool& /*hung*/) {
-  const bool unit = sp == 1.0;  // x / 1.0 == x exactly: skip the division
+  const double inv = recip_of(sp);  // exact division by div_recip
   const ChainLevels lv{s, P, n_chain > 0 ? md : 0, w};
   int jf = 0, jb = 0, jw = 0, live = 0;
   int LF = lv.F(0), LB = lv.B(0), LW = ZBH ? lv.W(0) : INT_MAX;
@@ -107,8 +143,8 @@ __device__ __forceinline__ void chain_walk(int s, int P, int pw, int md, int w, 
   const bool getF = s > 0, getB = s < P - 1;
   double lastF = 0.0, lastB = 0.0;
   // Branch-free step: F-, B- and idle lanes of a warp execute the same
-  // instruction stream (selects instead of divergent paths); only the rare
-  // non-unit-speed division is a real branch.
+  // instruction stream (selects instead of divergent paths; division by the
+  // stage speed is the branch-free div_recip).
   const int jmax = lv.m > 0 ? lv.m - 1 : 0;
   for (int t = 0; t < T; ++t) {
     const double nF = __shfl_up_sync(0xffffffffu, lastF, 1, pw);
@@ -120,8 +156,7 @@ __device__ __forceinline__ void chain_walk(int s, int P, int pw, int md, int w, 
     const double dep = doF ? dF : (doB ? dB : 0.0);
     const double rl = doF ? rlF : (doB ? rlB : rlW);
     const int j = min(doF ? jf : (doB ? jb : jw), jmax);
-    double c = __dmul_rn(rl, base[j]);
-    if (!unit && act) c = div_slow(c, sp);
+    const double c = div_recip(__dmul_rn(rl, base[j]), sp, inv);
     const double st = fin > dep ? fin : dep;  // max (no NaNs on this path)
     const double nf = __dadd_rn(st, c);
     fin = act ? nf : fin;

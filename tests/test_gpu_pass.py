@@ -277,3 +277,16 @@ def test_detector_pass_host_graph_replay(oracle, cuda_device):
         np.testing.assert_array_equal(sv.view(np.uint32), osv.reshape(-1).view(np.uint32))
         np.testing.assert_array_equal(oc, ooc)
         assert ln.value == oln
+
+
+def test_division_selftest(cuda_device):
+    """The hot path's hoisted-reciprocal division equals __ddiv_rn bit for bit
+    (2^28 seeded pairs over divisor regimes, on the device)."""
+    import ctypes as C
+
+    from paper_2605_06374_b200 import _lib
+
+    bad = C.c_int64(-1)
+    _lib.check(_lib.load_library().rh_selftest_division(_lib.context(), 1 << 28, 12345,
+                                                        C.byref(bad)), "rh_selftest_division")
+    assert bad.value == 0
