@@ -473,6 +473,9 @@ __global__ void __launch_bounds__(kSmallThreads, ZBH ? 4 : kSmallMinBlocks) pass
     stage_issue(so, g_off, &s_bar);
     if (staged) stage_issue(sd, p.tr.doc_len + d_lo, &s_bar);
   }
+  // nobody may poll the barrier before thread 0 has initialised it (the word
+  // may still hold a previous CTA's state)
+  __syncthreads();
   stage_edges(so, g_off, n_mb + 1);
   if (staged) stage_edges(sd, p.tr.doc_len + d_lo, n_doc);
   int32_t* s_off = so.dst;
@@ -524,7 +527,12 @@ __global__ void __launch_bounds__(kSmallThreads, ZBH ? 4 : kSmallMinBlocks) pass
     const int32_t k0 = s_off[mb] - d_lo, k1 = s_off[mb + 1] - d_lo;
     unsigned long long q = 0;
     if (staged) {
-      for (int32_t k = k0; k < k1; ++k) {
+      int32_t k = k0;
+      for (; k + 1 < k1; k += 2) {  // two documents per step
+        const long long l0 = s_doc[k], l1 = s_doc[k + 1];
+        q += (unsigned long long)(l0 * l0) + (unsigned long long)(l1 * l1);
+      }
+      if (k < k1) {
         const long long l = s_doc[k];
         q += (unsigned long long)(l * l);
       }
@@ -538,6 +546,11 @@ __global__ void __launch_bounds__(kSmallThreads, ZBH ? 4 : kSmallMinBlocks) pass
   }
   __syncthreads();  // sums complete; the document buffer is dead from here
   if (md > p.mmax) md = -1;
+  // division by a unit speed is exact for any numerator (div_fast(a, 1, 1)
+  // == a): only replicas with a slower stage need the operand-range check
+  bool all_unit = true;
+#pragma unroll
+  for (int s = 0; s < P; ++s) all_unit = all_unit && sp[s] == 1.0;
   double b_lo = CUDART_INF, b_hi = 0.0;  // base-cost range (non-zero minimum)
   if (md > 0) {
     const double lin = __dmul_rn(p.m.alpha, (double)p.sh.token_budget);
@@ -545,8 +558,10 @@ __global__ void __launch_bounds__(kSmallThreads, ZBH ? 4 : kSmallMinBlocks) pass
     for (int j = 0; j < md; ++j) {
       const double b = __dadd_rn(lin, __dmul_rn(p.m.beta, (double)(long long)q[j]));
       base_t[j * kSmallThreads + tid] = b;
-      b_hi = fmax(b_hi, b);
-      if (b > 0.0) b_lo = fmin(b_lo, b);
+      if (!all_unit) {
+        b_hi = fmax(b_hi, b);
+        if (b > 0.0) b_lo = fmin(b_lo, b);
+      }
     }
   }
   const int m = md > 0 ? md : 0;
@@ -570,19 +585,22 @@ __global__ void __launch_bounds__(kSmallThreads, ZBH ? 4 : kSmallMinBlocks) pass
   // table walk divides with __ddiv_rn
   double inv[P];
   bool safe = true;
-  double r_lo = CUDART_INF, r_hi = 0.0;
 #pragma unroll
-  for (int s = 0; s < P; ++s) {
-    inv[s] = recip_of(sp[s]);
-    safe = safe && inv[s] != 0.0;
-    const double rs[3] = {rlF[s], rlB[s], ZBH ? rlW[s] : rlB[s]};
+  for (int s = 0; s < P; ++s) inv[s] = sp[s] == 1.0 ? 1.0 : recip_of(sp[s]);
+  if (!all_unit) {
+    double r_lo = CUDART_INF, r_hi = 0.0;
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      r_hi = fmax(r_hi, rs[k]);
-      if (rs[k] > 0.0) r_lo = fmin(r_lo, rs[k]);
+    for (int s = 0; s < P; ++s) {
+      safe = safe && inv[s] != 0.0;
+      const double rs[3] = {rlF[s], rlB[s], ZBH ? rlW[s] : rlB[s]};
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        r_hi = fmax(r_hi, rs[k]);
+        if (rs[k] > 0.0) r_lo = fmin(r_lo, rs[k]);
+      }
     }
+    safe = safe && div_range_ok(r_lo * b_lo, r_hi * b_hi);
   }
-  safe = safe && div_range_ok(r_lo * b_lo, r_hi * b_hi);
   WalkArgs<P> wa{bt, rlF, rlB, rlW, sp, inv, hf, hb, fin, ssum};
   if (mm > 0) {
     const unsigned long long* l0 = p.sched + __ldg(p.sched_off + mm);
