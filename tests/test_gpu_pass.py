@@ -290,3 +290,54 @@ def test_division_selftest(cuda_device):
     _lib.check(_lib.load_library().rh_selftest_division(_lib.context(), 1 << 28, 12345,
                                                         C.byref(bad)), "rh_selftest_division")
     assert bad.value == 0
+
+
+@pytest.mark.parametrize("n_iter", [800, 2500])
+def test_c2_scenario_matches_oracle(n_iter, oracle, cuda_device):
+    """The headline configuration itself (bench.py's C2 trace: 256 GPUs,
+    TP4 x DP16 x PP4, 128 micro-batches, fail-stop / fail-slow / link phases,
+    resets) through DetectorPass -- detect + screen -- vs the oracle."""
+    from paper_2605_06374_b200.detect_pass import DetectorPass
+    from paper_2605_06374_b200.scenarios import c2_trace
+
+    tr = c2_trace(n_iter, seed=3)
+    ms, st, sc = oracle.pipeline(tr, view="actual")
+    tr.attach_measurements(sc, ms, seed=3)
+    p = DetectorPass(tr, keep_stage_cost=True)
+    p.run()
+    r = p.results()
+    oms, ost, osc, ofl, osv = oracle.detect(tr)
+    np.testing.assert_array_equal(r["status"], ost)
+    np.testing.assert_array_equal(_bits(r["makespan"]), _bits(oms))
+    np.testing.assert_array_equal(_bits(r["stage_cost"]), _bits(osc))
+    np.testing.assert_array_equal(r["stage_flag"], ofl)
+    np.testing.assert_array_equal(r["severity"].view(np.uint32), osv.view(np.uint32))
+    ooc, oln = oracle.screen(tr.observed, ost, reset=tr.reset)
+    np.testing.assert_array_equal(r["outcome"], ooc)
+    assert r["series_len"] == oln
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_wide_replica_shapes_match_oracle(seed, oracle, cuda_device):
+    """Shapes the small random traces do not reach: 8..128 replicas, up to 384
+    micro-batches (micro-batch counts past the unrolled walks' 12), long
+    documents (the unstaged-document fallback), slow stages (division)."""
+    from paper_2605_06374_b200.detect_pass import DetectorPass
+
+    rng = np.random.default_rng(500 + seed)
+    dp = int(rng.choice([8, 16, 32, 64, 128]))
+    pp = int(rng.integers(1, 5))
+    M = int(rng.integers(dp, 3 * dp + 1)) if seed % 3 else int(rng.integers(dp, 384 + 1))
+    mean = 4.0 if seed % 4 == 0 else 7.0  # short documents: many per micro-batch
+    tr = with_measurements(random_trace(700 + seed, n_iter=int(rng.integers(40, 200)), dp=dp,
+                                        pp=pp, M=M, mean=mean, sigma=1.0), oracle, noise=0.02,
+                           seed=seed)
+    p = DetectorPass(tr, keep_stage_cost=True)
+    p.detect()
+    r = p.results()
+    oms, ost, osc, ofl, osv = oracle.detect(tr)
+    np.testing.assert_array_equal(r["status"], ost)
+    np.testing.assert_array_equal(_bits(r["makespan"]), _bits(oms))
+    np.testing.assert_array_equal(_bits(r["stage_cost"]), _bits(osc))
+    np.testing.assert_array_equal(r["stage_flag"], ofl)
+    np.testing.assert_array_equal(r["severity"].view(np.uint32), osv.view(np.uint32))
