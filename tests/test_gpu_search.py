@@ -107,3 +107,33 @@ def test_cost_balanced_shards(k, cuda_device):
             assert b0 == a1 and a0 <= b0
         per = [gpu.best(a, b) for a, b in shards if b > a]
         assert lexicographic_min(per) == full
+
+
+@pytest.mark.parametrize("name", ["C3", "C4", "C5"])
+def test_benchmarked_spaces_sampled(name, oracle, cuda_device):
+    """The benchmarked re-plan spaces themselves (bench.py's C3/C4/C5): every
+    score in sampled ranges -- the first candidates, every layout's first
+    block, and the block around the GPU winner -- equals the oracle's bit for
+    bit, the range winners agree, and the winner decodes identically."""
+    import os
+
+    from paper_2605_06374_b200.replan_scenarios import replan_problem
+    from paper_2605_06374_b200.search import ReplanSearch
+
+    *_, inputs = replan_problem(name)
+    gpu = ReplanSearch(inputs)
+    cpu = oracle.search(inputs)
+    assert gpu.size == cpu.size
+    best, bidx = gpu.best()
+    threads = os.cpu_count() or 1
+    ranges = [(0, 256), (max(0, bidx - 128), min(gpu.size, bidx + 128))]
+    rng = np.random.default_rng(len(name))
+    ranges += [(int(a), int(a) + 64) for a in rng.integers(0, gpu.size - 64, 6)]
+    for a, b in ranges:
+        g = gpu.scores(a, b)
+        cb, ci, c = cpu.best(a, b, threads=threads, with_scores=True)
+        np.testing.assert_array_equal(np.isinf(g), np.isinf(c))
+        fin = np.isfinite(c)
+        np.testing.assert_array_equal(bits(g[fin]), bits(c[fin]))
+        assert gpu.best(a, b) == (cb, ci)
+    assert gpu.decode(bidx) == cpu.decode(bidx)
