@@ -222,6 +222,7 @@ int rh_ctx_destroy(rh_ctx* ctx) {
   if (ctx->prep.done) cudaEventDestroy(ctx->prep.done);
   if (ctx->prep.consumed) cudaEventDestroy(ctx->prep.consumed);
   if (ctx->host_graph.exec) cudaGraphExecDestroy(ctx->host_graph.exec);
+  if (ctx->screen_ctrl) cudaFree(ctx->screen_ctrl);
   delete ctx;
   return RH_OK;
 }

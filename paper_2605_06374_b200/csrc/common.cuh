@@ -38,6 +38,8 @@ struct rh_ctx {
   };
   std::vector<SchedTable> sched;
   std::mutex sched_mu;
+  // rh_screen's cooperative-kernel control words (zero between launches)
+  void* screen_ctrl = nullptr;
   // the device's default memory pool keeps freed memory (re-plan searches)
   bool pool_ready = false;
   // rh_detector_pass_host*: the captured pass for the last argument key

@@ -63,9 +63,12 @@ struct ScreenArgs {
   int32_t* bres;                   // [n/128] last reset inside each scan block
   uint8_t* state;                  // [2][n] bit0 popped, bit1 changed in that round
   uint8_t* c0;                     // [n] round-0 verdicts (round0_kernel)
-  unsigned* cnt;                   // [3] changes per round (rotating)
-  unsigned* bar;                   // [2] barrier count, generation
-  unsigned long long* kept_total;  // [2] kept count, block ticket
+  // control words (rh_ctx::screen_ctrl): zero when a launch starts, and the
+  // launch leaves them zero again (no memset per call; graph-replay safe)
+  unsigned* cnt;             // [3] changes per round (rotating)
+  unsigned long long* kcnt;  // [3] kept entries since the last reset, per round
+  unsigned* bar;             // [2] barrier count, generation
+  unsigned* ticket;          // [1] blocks finished
 };
 
 __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
@@ -302,6 +305,7 @@ struct ScreenSmem {
   WarpScratch ws[kScreenWarps];
   double ob[kScreenWarps][kCache][32];
   IterCache it[kScreenWarps][kCache];
+  unsigned long long kcnt;
   unsigned cnt;
 };
 
@@ -334,6 +338,10 @@ __global__ void __launch_bounds__(kScreenThreads) screen_kernel(const ScreenArgs
   auto& s_ob = sm.ob;
   auto& s_it = sm.it;
   unsigned& s_cnt = sm.cnt;
+  unsigned long long& s_kcnt = sm.kcnt;
+  // the series length at the end counts kept entries from the last reset on
+  const int32_t r_last = __ldg(a.R + (a.n - 1));
+  const int64_t first_last = r_last >= 0 ? r_last : 0;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t gw = (int64_t)blockIdx.x * kScreenWarps + wid;
   const int64_t n_warps = (int64_t)gridDim.x * kScreenWarps;
@@ -342,12 +350,15 @@ __global__ void __launch_bounds__(kScreenThreads) screen_kernel(const ScreenArgs
   for (;; ++round) {
     const uint8_t* cur = a.state + (size_t)(round & 1) * a.n;
     uint8_t* nxt = a.state + (size_t)((round + 1) & 1) * a.n;
-    if (threadIdx.x == 0) s_cnt = 0;
+    if (threadIdx.x == 0) {
+      s_cnt = 0;
+      s_kcnt = 0;
+    }
     __syncthreads();
 #ifdef RH_SCREEN_TRACE
     const unsigned long long t_start = gtimer();
 #endif
-    unsigned changes = 0;
+    unsigned changes = 0, kept = 0;
     auto process = [&](int64_t i, int k, bool cached, int sv0) {
       int r;
       double x;
@@ -406,6 +417,7 @@ __global__ void __launch_bounds__(kScreenThreads) screen_kernel(const ScreenArgs
         if (cached) s_it[wid][k].pop = (uint8_t)pop;
       }
       changes += changed;
+      kept += (!pop && i >= first_last) ? 1u : 0u;
     };
     // the first window chunk of every cached iteration is loaded up front, so
     // those round trips overlap instead of queueing behind each other
@@ -425,10 +437,15 @@ __global__ void __launch_bounds__(kScreenThreads) screen_kernel(const ScreenArgs
     }
     for (int64_t i = gw + kCache * n_warps; i < a.n; i += n_warps) process(i, kCache, false, -1);
     if (lane == 0 && changes) atomicAdd(&s_cnt, changes);
-    // the next round's counter was last read before this round began
-    if (blockIdx.x == 0 && threadIdx.x == 0) a.cnt[(round + 1) % 3] = 0;
+    if (lane == 0 && kept) atomicAdd(&s_kcnt, (unsigned long long)kept);
+    // the next round's counters were last read before this round began
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      a.cnt[(round + 1) % 3] = 0;
+      a.kcnt[(round + 1) % 3] = 0;
+    }
     __syncthreads();
     if (threadIdx.x == 0 && s_cnt) atomicAdd(a.cnt + round % 3, s_cnt);
+    if (threadIdx.x == 0 && s_kcnt) atomicAdd(a.kcnt + round % 3, s_kcnt);
 #ifdef RH_SCREEN_TRACE
     const unsigned long long t_arrive = gtimer();
     if (threadIdx.x == 0 && round < 32) atomicMax(&g_trace_slow[round], t_arrive - t_start);
@@ -444,25 +461,20 @@ __global__ void __launch_bounds__(kScreenThreads) screen_kernel(const ScreenArgs
 #endif
     if (__ldcg(a.cnt + round % 3) == 0) break;  // fixpoint: nothing changed
   }
-  // final series length: kept entries since the last reset (+ history)
-  if (a.len_out) {
-    const int32_t r_last = __ldcg(a.R + (a.n - 1));
-    const int64_t first = r_last >= 0 ? r_last : 0;
-    const uint8_t* fin = a.state + (size_t)((round + 1) & 1) * a.n;  // written last
-    unsigned long long k = 0;
-    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    for (int64_t i = first + tid; i < a.n; i += (int64_t)gridDim.x * blockDim.x)
-      k += (__ldcg(fin + i) & 1u) ? 0 : 1;
-    for (int o = 16; o > 0; o >>= 1) k += __shfl_xor_sync(0xffffffffu, k, o);
-    if (lane == 0 && k) atomicAdd(a.kept_total, k);
+  // final series length: kept entries since the last reset (+ history), as
+  // counted in the round that changed nothing
+  if (threadIdx.x == 0) {
+    const unsigned long long total = __ldcg(a.kcnt + round % 3);
+    if (blockIdx.x == 0 && a.len_out)
+      *a.len_out = r_last >= 0 ? (int64_t)total : a.len0 + (int64_t)total;
+    // the last block out leaves the control words zero for the next launch
     __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const unsigned long long ticket = atomicAdd(a.kept_total + 1, 1ull);
-      if (ticket == gridDim.x - 1) {
-        const unsigned long long total = atomicAdd(a.kept_total, 0ull);
-        *a.len_out = r_last >= 0 ? (int64_t)total : a.len0 + (int64_t)total;
+    if (atomicAdd(a.ticket, 1u) == gridDim.x - 1) {
+      for (int q = 0; q < 3; ++q) {
+        a.cnt[q] = 0;
+        a.kcnt[q] = 0;
       }
+      *a.ticket = 0;
     }
   }
 }
@@ -628,25 +640,20 @@ extern "C" int rh_screen(rh_ctx* ctx, const rh_screen_params* params, int64_t se
   } else if (int rc = launch_prepare(ctx, a, st)) {
     return rc;
   }
-  size_t bytes = 0;
-  auto take = [&](size_t n_bytes) {
-    const size_t o = bytes;
-    bytes = (bytes + n_bytes + 255) & ~size_t(255);
-    return o;
-  };
-  // the control words first: one memset clears them all
-  const size_t oBar = take(sizeof(unsigned) * 2), oCnt = take(sizeof(unsigned) * 3);
-  const size_t oKept = take(sizeof(unsigned long long) * 2);
-  const size_t ctrl = bytes;
-  const size_t oSt = take(2 * (size_t)n);
+  // control words: a dedicated per-context block, zeroed once (the kernel
+  // leaves it zero); kept-state: the slot-1 workspace
+  if (!ctx->screen_ctrl) {
+    RH_CUDA(cudaMalloc(&ctx->screen_ctrl, 256));
+    RH_CUDA(cudaMemset(ctx->screen_ctrl, 0, 256));
+  }
+  char* cb = static_cast<char*>(ctx->screen_ctrl);
+  a.kcnt = reinterpret_cast<unsigned long long*>(cb);       // 24 B
+  a.cnt = reinterpret_cast<unsigned*>(cb + 32);             // 12 B
+  a.bar = reinterpret_cast<unsigned*>(cb + 64);             // 8 B
+  a.ticket = reinterpret_cast<unsigned*>(cb + 96);          // 4 B
   void* ws = nullptr;
-  if (int rc = workspace(ctx, bytes, &ws, 1)) return rc;
-  char* base = static_cast<char*>(ws);
-  a.bar = reinterpret_cast<unsigned*>(base + oBar);
-  a.cnt = reinterpret_cast<unsigned*>(base + oCnt);
-  a.kept_total = reinterpret_cast<unsigned long long*>(base + oKept);
-  a.state = reinterpret_cast<uint8_t*>(base + oSt);
-  RH_CUDA(cudaMemsetAsync(base, 0, ctrl, st));
+  if (int rc = workspace(ctx, 2 * (size_t)n + 256, &ws, 1)) return rc;
+  a.state = static_cast<uint8_t*>(ws);
   void* kargs[] = {&a};
   RH_CUDA(cudaLaunchCooperativeKernel((void*)screen_kernel, dim3(blocks), dim3(kScreenThreads),
                                       kargs, sizeof(ScreenSmem), st));
