@@ -55,7 +55,48 @@ struct PassParams {
   int region_off;            // smem offset of the document / base-cost region
   int doc_stage;             // documents that fit in that region
   int static_max;  // largest micro-batch count walked by the unrolled code
+  // lane kernel only: level table (lane_table), NULL = closed-form walk
+  const uint16_t* ltab;
+  const int32_t *ltab_off, *ltab_nlev, *ltab_peak;  // [mmax+1] each
 };
+
+// Lane walk driven by a host-built level table (lane_table): for the
+// replica's micro-batch count mm, codes[t * P + s] is stage s's chunk at DAG
+// level t (0 idle, else kind | j << 2).  Same arithmetic and exchange as
+// chain_walk, without the closed-form level bookkeeping.
+template <int ZBH>
+__device__ __forceinline__ void chain_walk_table(int s, int P, int pw, int mm,
+                                                 const uint16_t* codes, int n_lev,
+                                                 const double* base, double rlF, double rlB,
+                                                 double rlW, double sp, double hopf,
+                                                 double hopb, double& fin, double& ssum) {
+  const bool unit = sp == 1.0;
+  const double inv = unit ? 1.0 : recip_of(sp);
+  const int T = __reduce_max_sync(0xffffffffu, mm > 0 ? n_lev : 0);
+  const double hF = s > 0 ? hopf : 0.0, hB = s < P - 1 ? hopb : 0.0;
+  const bool getF = s > 0, getB = s < P - 1;
+  const bool mine = mm > 0 && s < P;
+  double lastF = 0.0, lastB = 0.0;
+  for (int t = 0; t < T; ++t) {
+    const double nF = __shfl_up_sync(0xffffffffu, lastF, 1, pw);
+    const double nB = __shfl_down_sync(0xffffffffu, lastB, 1, pw);
+    const unsigned code = (mine && t < n_lev) ? (unsigned)__ldg(codes + t * P + s) : 0u;
+    const unsigned kind = code & 3u;
+    const bool doF = kind == 1u, doB = kind == 2u, act = kind != 0u;
+    const double dF = getF ? __dadd_rn(nF, hF) : 0.0;
+    const double dB = getB ? __dadd_rn(nB, hB) : 0.0;
+    const double dep = doF ? dF : (doB ? dB : 0.0);
+    const double rl = doF ? rlF : (doB || !ZBH ? rlB : rlW);
+    double c = __dmul_rn(rl, base[code >> 2]);
+    if (!unit) c = div_recip(c, sp, inv);
+    const double st = fin > dep ? fin : dep;  // max (no NaNs on this path)
+    const double nf = __dadd_rn(st, c);
+    fin = act ? nf : fin;
+    ssum = act ? __dadd_rn(ssum, c) : ssum;
+    lastF = doF ? nf : lastF;
+    lastB = doB ? nf : lastB;
+  }
+}
 
 // MAXT = launch bound: 256 for the common case (more registers per lane),
 // 1024 when one iteration needs D*pw > 256 lanes.
@@ -139,8 +180,17 @@ __global__ void __launch_bounds__(MAXT) pass_kernel(const PassParams p) {
   // ---------------------------------------------------------- wavefront
   double fin = 0.0, ssum = 0.0;
   bool over = false, hung = false;
-  chain_walk<ZBH>(s, P, p.pw, md, w, n_chain, gbase, rlF, rlB, rlW, sp, hopf, hopb,
-                  p.sh.capacity, p.mmax, fin, ssum, over, hung);
+  if (p.ltab) {  // level table: codes per (level, stage), peak in-flight per count
+    const int mm = n_chain > 0 ? md : 0;
+    const int mi = mm > 0 ? mm : 0;
+    chain_walk_table<ZBH>(s, P, p.pw, mm, p.ltab + __ldg(p.ltab_off + mi),
+                          __ldg(p.ltab_nlev + mi), gbase, rlF, rlB, rlW, sp, hopf, hopb, fin,
+                          ssum);
+    over = p.sh.capacity > 0 && mm > 0 && __ldg(p.ltab_peak + mi) > p.sh.capacity;
+  } else {
+    chain_walk<ZBH>(s, P, p.pw, md, w, n_chain, gbase, rlF, rlB, rlW, sp, hopf, hopb,
+                    p.sh.capacity, p.mmax, fin, ssum, over, hung);
+  }
 
   // ------------------------------------------------------ reductions
   double gmax = fin;
@@ -739,6 +789,76 @@ static int sched_table(rh_ctx* ctx, int P, int zbh, int mmax,
   return RH_OK;
 }
 
+// Level table of the lane kernel for (P, schedule, mmax): for every count
+// mm = 0..mmax, uint16 codes [level][stage] (0 idle, else kind | j << 2), the
+// level count and the peak in-flight forward chunks on any stage.  Device
+// layout [off | nlev | peak: (mmax+1) int32 each, padded to 16 B][codes].
+// Built once per context; returns ok = false when it would be too large.
+static int lane_table(rh_ctx* ctx, int P, int zbh, int mmax, const uint16_t** codes,
+                      const int32_t** off, const int32_t** nlev, const int32_t** peak,
+                      bool* ok) {
+  const size_t head = ((3 * (size_t)(mmax + 1) * 4) + 15) & ~size_t(15);
+  auto view = [&](void* dev) {
+    const int32_t* b = static_cast<const int32_t*>(dev);
+    *off = b;
+    *nlev = b + (mmax + 1);
+    *peak = b + 2 * (mmax + 1);
+    *codes = reinterpret_cast<const uint16_t*>(static_cast<const char*>(dev) + head);
+  };
+  std::lock_guard<std::mutex> lock(ctx->sched_mu);
+  const int key_p = 1000 + P;  // distinct from sched_table's entries
+  for (const auto& t : ctx->sched)
+    if (t.pp == key_p && t.zbh == zbh && t.mmax == mmax) {
+      view(t.dev);
+      *ok = true;
+      return RH_OK;
+    }
+  // size first: levels(mm) <= 2P + 3mm per count
+  size_t words = 0;
+  for (int mm = 1; mm <= mmax; ++mm) words += (size_t)(2 * P + 3 * mm + 2) * P;
+  if (words * 2 > (64u << 20) || mmax >= (1 << 14)) {
+    *ok = false;
+    return RH_OK;
+  }
+  std::vector<int32_t> o(mmax + 1, 0), nl(mmax + 1, 0), pk(mmax + 1, 0);
+  std::vector<uint16_t> v;
+  for (int mm = 1; mm <= mmax; ++mm) {
+    o[mm] = (int32_t)v.size();
+    int t_end = 0;
+    for (int s2 = 0; s2 < P; ++s2)
+      t_end = std::max(t_end, ChainLevels{s2, P, mm, std::min(P - 1 - s2, mm)}.end(zbh));
+    v.resize(v.size() + (size_t)t_end * P, 0);
+    std::vector<int> live(P, 0);
+    int peak_mm = 0;
+    for (int s2 = 0; s2 < P; ++s2) {
+      const ChainLevels lv{s2, P, mm, std::min(P - 1 - s2, mm)};
+      for (int t = 0; t < t_end; ++t) {
+        int j = 0;
+        const int kind = lv.at(t, zbh, j);
+        if (!kind) continue;
+        v[o[mm] + (size_t)t * P + s2] = (uint16_t)(kind | (j << 2));
+        if (kind == kOpF) peak_mm = std::max(peak_mm, ++live[s2]);
+        if (kind == kOpB) --live[s2];
+      }
+    }
+    nl[mm] = t_end;
+    pk[mm] = peak_mm;
+  }
+  const size_t bytes = head + 2 * std::max<size_t>(1, v.size());
+  std::vector<char> stage(bytes, 0);
+  memcpy(stage.data(), o.data(), 4 * o.size());
+  memcpy(stage.data() + 4 * (mmax + 1), nl.data(), 4 * nl.size());
+  memcpy(stage.data() + 8 * (mmax + 1), pk.data(), 4 * pk.size());
+  if (!v.empty()) memcpy(stage.data() + head, v.data(), 2 * v.size());
+  void* dev = nullptr;
+  RH_CUDA(cudaMalloc(&dev, bytes));
+  RH_CUDA(cudaMemcpy(dev, stage.data(), bytes, cudaMemcpyHostToDevice));
+  ctx->sched.push_back({key_p, zbh, mmax, dev});
+  view(dev);
+  *ok = true;
+  return RH_OK;
+}
+
 template <int ZBH, int DETECT>
 static void* small_kernel(int P) {
   switch (P) {
@@ -813,6 +933,7 @@ int launch_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
         std::max<size_t>(16 * 1024 + 16, (size_t)kSmallThreads * p.mmax * 8);
     p.doc_stage = (int)((region - 16) / 4);
     p.static_max = kStaticMaxMB;
+    p.ltab = nullptr;
     const size_t smem = p.region_off + region;
     if (smem <= ctx->smem_optin && smem <= 56 * 1024) {
       const bool zbh = sh->schedule == RH_SCHED_ZBH;
@@ -830,6 +951,13 @@ int launch_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
   }
   p.ipb = std::max(1, 256 / p.lpi);
   const int threads = ((p.ipb * p.lpi + 31) / 32) * 32;
+  {
+    bool ok = false;
+    if (int e = lane_table(ctx, P, sh->schedule == RH_SCHED_ZBH, p.mmax, &p.ltab, &p.ltab_off,
+                           &p.ltab_nlev, &p.ltab_peak, &ok))
+      return e;
+    if (!ok) p.ltab = nullptr;
+  }
   const int it_bytes = ((p.ipb * 12 + 15) / 16) * 16;
   const size_t smem = it_bytes + (size_t)(threads / p.pw) * p.mmax * 8;
   if (smem > ctx->smem_optin) {
