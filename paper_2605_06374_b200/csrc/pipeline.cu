@@ -265,24 +265,26 @@ __global__ void __launch_bounds__(MAXT) pass_kernel(const PassParams p) {
 // ---------------------------------------------------------------------------
 // Small-P variant (P <= 4, D <= 128): one THREAD per replica pipeline.
 //
-// Op order.  The thread executes its replica's chunks in a precomputed order
-// (sched_table): sorted by DAG level (wavefront.cuh closed forms), and inside
-// a level by DESCENDING stage.  With every stage's state in registers (P is a
-// template parameter, the stage switch is unrolled) the dependencies then
-// read straight from the neighbours' registers:
+// Op order.  The thread executes its replica's chunks in DAG-level order
+// (wavefront.cuh closed forms), inside a level by DESCENDING stage: fully
+// unrolled at compile time for small micro-batch counts (walk_static), else
+// from a level table (sched_table).  With every stage's state in registers
+// (P is a template parameter) the dependencies then read straight from the
+// neighbours' registers:
 //   * F(s,j) needs F(s-1,j) (one level earlier); stage s-1's next F may sit
 //     on the same level as F(s,j), but in descending order it runs after;
 //   * B(s,j) needs B(s+1,j) (one level earlier); B levels of neighbouring
 //     stages have opposite parity, so no B of stage s+1 shares its level.
 // That is exactly the level-synchronous wavefront, without per-level tests.
-// Replicas with equal micro-batch counts share one op list, so in a warp the
-// op fetch is a broadcast and the stage switch is uniform.
 //
-// Quadratic loads.  The CTA stages its micro-batch offsets and documents in
-// shared memory and sums l^2 document-parallel (contiguous doc ranges per
-// thread, segment boundaries flushed with shared 64-bit atomics), then each
-// thread turns its replica's sums into base costs stored [j][thread]
-// (conflict-free reads in the op loop), aliasing the dead document buffer.
+// Quadratic loads.  Thread 0 stages the CTA's micro-batch offsets and
+// documents into shared memory with TMA bulk copies (cp.async.bulk completing
+// on an mbarrier); l^2 is summed one thread per micro-batch; each thread then
+// turns its replica's sums into base costs stored [j][thread] (conflict-free
+// reads in the walk), aliasing the dead document buffer.
+//
+// Division by a stage speed: exact hoisted-reciprocal form (div_fast) after a
+// once-per-replica operand-range check (wavefront.cuh).
 constexpr int kSmallThreads = 128;
 #ifndef RH_SMALL_MIN_BLOCKS
 #define RH_SMALL_MIN_BLOCKS 5

@@ -17,10 +17,12 @@
 // layout (cluster.py:175-208) on a healthy cluster.
 //
 // GPU work: one warp per layout prepares group speeds/nodes, hop weights,
-// all-reduce ring bandwidths, repartition and proportional split; one warp
-// per candidate evaluates the canonical chunk-DAG makespan replica by
-// replica with the shared wavefront (wavefront.cuh), adds the amortised
-// reconfiguration surcharge and keeps a lexicographic (score, index) min.
+// all-reduce ring bandwidths, repartition and proportional split
+// (prep_kernel); one thread per (layout, partition variant, range case,
+// replica) walks that replica pipeline's op list (pipe_kernel, the replica
+// table); one thread per candidate combines the table exactly, adds the
+// amortised reconfiguration surcharge and keeps a lexicographic (score,
+// index) min (combine_kernel, minloc_kernel).
 #include <algorithm>
 #include <cmath>
 #include <cstring>
