@@ -230,6 +230,11 @@ __global__ void __launch_bounds__(MAXT) pass_kernel(const PassParams p) {
       atomic_max_nonneg(it_ms + li, msd);
     }
     if (flag) bits |= RH_IT_STAGE_FLAG;
+    if (DETECT && p.sg.link_off) {  // exercised-link ratios, split over the lanes
+      const int32_t q0 = __ldg(p.sg.link_off + seg), q1 = __ldg(p.sg.link_off + seg + 1);
+      for (int32_t q = q0 + within; q < q1; q += p.lpi)
+        if (__ldg(p.sg.link_ratio + q) > p.thr) bits |= RH_IT_LINK_FLAG;
+    }
     if (bits) atomicOr(it_st + li, bits);
   }
   __syncthreads();
@@ -252,10 +257,6 @@ __global__ void __launch_bounds__(MAXT) pass_kernel(const PassParams p) {
     if (DETECT && !dead) {
       const double obs = __ldg(p.tr.observed + it);
       if (ms <= 0.0 || obs > __dmul_rn(p.thr, ms)) st |= RH_IT_ESCALATE;
-      if (p.sg.link_off) {
-        for (int32_t q = p.sg.link_off[seg]; q < p.sg.link_off[seg + 1]; ++q)
-          if (__ldg(p.sg.link_ratio + q) > p.thr) st |= RH_IT_LINK_FLAG;
-      }
     }
     p.out.makespan[it] = ms;
     p.out.status[it] = (uint8_t)st;
