@@ -359,6 +359,45 @@ def run_e2e(tr, p, args, dev):
     return {"step_s": step, "h2d": int(h2d), "d2h": int(d2h)}
 
 
+def run_trace_r(args, dev, n_iter=10_000):
+    """SURVEY §8(d)'s Detector roofline trace R -- the C5 shape (4096 GPUs,
+    TP8 x DP32 x PP16, 80 layers, 512 micro-batches) -- on a bounded sample of
+    n_iter iterations (R itself is 10^5; its Python generation alone takes
+    ~40 s).  The sample is ~0.3 GB, larger than L2, so no flush is needed."""
+    import torch
+
+    from paper_2605_06374_b200.detect_pass import DetectorPass, synthesize_measurements
+    from paper_2605_06374_b200.scenarios import c2_trace
+
+    tr = c2_trace(n_iter, seed=0, tp=8, dp=32, pp=16, layers=80, M=512)
+    synthesize_measurements(tr, seed=0)
+    p = DetectorPass(tr, dev)
+    for _ in range(args.warmup):
+        p.run()
+    torch.cuda.synchronize()
+    steps = max(3, min(args.steps, 20))
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
+    stream = torch.cuda.current_stream(dev)
+    for k in range(steps):
+        ev[k][0].record(stream)
+        p.detect()
+        ev[k][1].record(stream)
+        p.screen()
+        ev[k][2].record(stream)
+    torch.cuda.synchronize()
+    det = sum(e[0].elapsed_time(e[1]) for e in ev) / steps
+    scr = sum(e[1].elapsed_time(e[2]) for e in ev) / steps
+    nbytes = algorithmic_bytes(tr)
+    peak, _ = _peaks()
+    dev_n = 8 * 32 * 16
+    return {"workload": "C5 shape (4096 GPUs, TP8xDP32xPP16, 80 layers, 512 micro-batches), "
+                        f"{n_iter}-iteration sample of SURVEY trace R",
+            "device_samples_per_s": n_iter * dev_n / ((det + scr) * 1e-3),
+            "detect_ms": det, "screen_ms": scr, "algorithmic_bytes": nbytes,
+            "achieved_gbs": nbytes / (det * 1e-3) / 1e9, "frac_of_hbm": nbytes / (det * 1e-3) / 1e9 / peak,
+            "kernel": "pass_kernel<1F1B,detect> (lane per stage, P=16)"}
+
+
 def run_scheduler(args, world, rank, local, names=("C3", "C4", "C5")):
     """Re-plan search (BASELINE configs[2..4]): candidates/s and re-plan latency.
 
@@ -448,6 +487,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-scheduler", action="store_true")
+    ap.add_argument("--no-trace-r", action="store_true", help="skip the C5-shape trace R sample")
     ap.add_argument("--scheduler-only", default="", help="comma list of C3,C4,C5: only these")
     args = ap.parse_args()
     if args.warmup < 3:
@@ -465,6 +505,10 @@ def main():
             print(json.dumps({"scheduler": res}), flush=True)
         return
     line, tr = run_ours(args, world, rank, local)
+    if world == 1 and not args.no_trace_r:
+        import torch
+
+        line["trace_R"] = run_trace_r(args, torch.device("cuda", local))
     if not args.no_scheduler:
         line["scheduler"] = run_scheduler(args, world, rank, local)
     if rank == 0:
