@@ -483,56 +483,129 @@ __device__ __forceinline__ bool walk_static_dispatch(const WalkArgs<P>& a, int m
   }
 }
 
+// Shared-memory layout of the thread-per-replica kernels:
+//   [it_ms | it_st][q: ipb*M int64][off: 16 + 4*(ipb*M+1)][documents -> base costs]
+struct CtaStage {
+  double* it_ms;
+  unsigned* it_st;
+  unsigned long long* s_q;
+  double* base_t;
+  int n_it, n_mb;
+};
+
+__device__ __forceinline__ CtaStage cta_layout(const PassParams& p, unsigned char* smem_raw) {
+  CtaStage c;
+  const int M = p.sh.micro_batches;
+  c.it_ms = reinterpret_cast<double*>(smem_raw);
+  c.it_st = reinterpret_cast<unsigned*>(c.it_ms + p.ipb);
+  const int it_bytes = ((p.ipb * 12 + 15) / 16) * 16;
+  c.s_q = reinterpret_cast<unsigned long long*>(smem_raw + it_bytes);
+  c.base_t = reinterpret_cast<double*>(smem_raw + p.region_off);
+  const int64_t it0 = (int64_t)blockIdx.x * p.ipb;
+  c.n_it = (int)min((int64_t)p.ipb, p.tr.n_iter - it0);
+  c.n_mb = c.n_it * M;
+  return c;
+}
+
+// Phase A of the CTA staging: thread 0 arms the mbarrier and issues the TMA
+// bulk copies of the offsets and (when they fit) the documents; everybody
+// loads the ragged edges.  Per-thread loads issued between stage_begin and
+// stage_finish overlap the copies.
+struct StageState {
+  StagePlan so, sd;
+  const int32_t* g_off;
+  int32_t d_lo;
+  int n_doc;
+  bool staged;
+};
+
+__device__ __forceinline__ StageState stage_begin(const PassParams& p, unsigned char* smem_raw,
+                                                  const CtaStage& c, uint64_t* bar) {
+  const int M = p.sh.micro_batches;
+  const int it_bytes = ((p.ipb * 12 + 15) / 16) * 16;
+  int32_t* s_off_raw = reinterpret_cast<int32_t*>(
+      smem_raw + ((it_bytes + 8 * (size_t)p.ipb * M + 15) & ~size_t(15)));
+  StageState g;
+  const int64_t it0 = (int64_t)blockIdx.x * p.ipb;
+  g.g_off = p.tr.mb_off + it0 * M;
+  g.d_lo = __ldg(g.g_off);
+  g.n_doc = __ldg(g.g_off + c.n_mb) - g.d_lo;
+  g.staged = g.n_doc <= p.doc_stage;
+  g.so = stage_plan(reinterpret_cast<unsigned char*>(s_off_raw), g.g_off, c.n_mb + 1);
+  g.sd = g.staged ? stage_plan(reinterpret_cast<unsigned char*>(c.base_t), p.tr.doc_len + g.d_lo,
+                               g.n_doc)
+                  : StagePlan{nullptr, 0, 0, 0u};
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    mbar_arrive_expect_tx(bar, g.so.tx_bytes + g.sd.tx_bytes);
+    stage_issue(g.so, g.g_off, bar);
+    if (g.staged) stage_issue(g.sd, p.tr.doc_len + g.d_lo, bar);
+  }
+  // nobody may poll the barrier before thread 0 has initialised it (the word
+  // may still hold a previous CTA's state)
+  __syncthreads();
+  stage_edges(g.so, g.g_off, c.n_mb + 1);
+  if (g.staged) stage_edges(g.sd, p.tr.doc_len + g.d_lo, g.n_doc);
+  return g;
+}
+
+// Phase B: wait for the copies, then Q_j = sum l^2, one thread per
+// micro-batch, into s_q; the document buffer is dead afterwards.
+__device__ __forceinline__ void stage_finish(const PassParams& p, const CtaStage& c,
+                                             const StageState& g, uint64_t* bar) {
+  mbar_wait(bar, 0);  // the bulk copies have landed
+  __syncthreads();    // ... and so have the threads' edge words
+  const int32_t* s_off = g.so.dst;
+  const int32_t* s_doc = g.sd.dst;
+  for (int mb = threadIdx.x; mb < c.n_mb; mb += blockDim.x) {
+    const int32_t k0 = s_off[mb] - g.d_lo, k1 = s_off[mb + 1] - g.d_lo;
+    unsigned long long q = 0;
+    if (g.staged) {
+      // packed bins hold few documents (C2: 2.4 on average, at most 4): the
+      // first four are summed branch-free with predicated loads
+      const int32_t nd = k1 - k0;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const long long l = t < nd ? s_doc[k0 + t] : 0;
+        q += (unsigned long long)(l * l);
+      }
+      for (int32_t k = k0 + 4; k < k1; ++k) {
+        const long long l = s_doc[k];
+        q += (unsigned long long)(l * l);
+      }
+    } else {  // too many documents to stage: straight from global memory
+      for (int32_t k = k0; k < k1; ++k) {
+        const long long l = __ldg(p.tr.doc_len + g.d_lo + k);
+        q += (unsigned long long)(l * l);
+      }
+    }
+    c.s_q[mb] = q;
+  }
+  __syncthreads();  // sums complete; the document buffer is dead from here
+}
+
 template <int P, int ZBH, int DETECT>
 __global__ void __launch_bounds__(kSmallThreads, ZBH ? 4 : kSmallMinBlocks) pass_small_kernel(const PassParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x, nt = blockDim.x;
   const int D = p.sh.dp, M = p.sh.micro_batches, T = p.sh.tp;
   const int li = tid / D, d = tid - li * D;
-  const int64_t it0 = (int64_t)blockIdx.x * p.ipb;
-  const int64_t it = it0 + li;
-  const int n_it = (int)min((int64_t)p.ipb, p.tr.n_iter - it0);
+  const int64_t it = (int64_t)blockIdx.x * p.ipb + li;
+  const CtaStage cs = cta_layout(p, smem_raw);
+  double* it_ms = cs.it_ms;
+  unsigned* it_st = cs.it_st;
+  unsigned long long* s_q = cs.s_q;
+  double* base_t = cs.base_t;
+  const int n_it = cs.n_it;
   const bool on = li < n_it;
-  // layout: it_ms[ipb] it_st[ipb] | q[ipb*M] int64 | off[ipb*M+1] | docs / base
-  double* it_ms = reinterpret_cast<double*>(smem_raw);
-  unsigned* it_st = reinterpret_cast<unsigned*>(it_ms + p.ipb);
-  const int it_bytes = ((p.ipb * 12 + 15) / 16) * 16;
-  unsigned long long* s_q = reinterpret_cast<unsigned long long*>(smem_raw + it_bytes);
-  // offsets region: 16-B aligned with 16 spare bytes (TMA alignment shift)
-  int32_t* s_off_raw = reinterpret_cast<int32_t*>(
-      smem_raw + ((it_bytes + 8 * (size_t)p.ipb * M + 15) & ~size_t(15)));
-  double* base_t = reinterpret_cast<double*>(smem_raw + p.region_off);
   __shared__ uint64_t s_bar;
   if (tid < p.ipb) {
     it_ms[tid] = 0.0;
     it_st[tid] = 0u;
   }
-  // ---- staging by TMA: thread 0 arms the barrier and issues the bulk
-  // copies of the offsets and (when they fit) the documents; the per-thread
-  // loads below run meanwhile
+  // ---- staging by TMA; the per-thread loads below run meanwhile
   const int seg = on && p.tr.seg ? __ldg(p.tr.seg + it) : 0;
-  const int n_mb = n_it * M;
-  const int32_t* g_off = p.tr.mb_off + it0 * M;
-  const int32_t d_lo = __ldg(g_off), d_hi = __ldg(g_off + n_mb);
-  const int n_doc = d_hi - d_lo;
-  const bool staged = n_doc <= p.doc_stage;
-  const StagePlan so = stage_plan(reinterpret_cast<unsigned char*>(s_off_raw), g_off, n_mb + 1);
-  const StagePlan sd = staged ? stage_plan(reinterpret_cast<unsigned char*>(base_t),
-                                           p.tr.doc_len + d_lo, n_doc)
-                              : StagePlan{nullptr, 0, 0, 0u};
-  if (tid == 0) {
-    mbar_init(&s_bar, 1);
-    mbar_arrive_expect_tx(&s_bar, so.tx_bytes + sd.tx_bytes);
-    stage_issue(so, g_off, &s_bar);
-    if (staged) stage_issue(sd, p.tr.doc_len + d_lo, &s_bar);
-  }
-  // nobody may poll the barrier before thread 0 has initialised it (the word
-  // may still hold a previous CTA's state)
-  __syncthreads();
-  stage_edges(so, g_off, n_mb + 1);
-  if (staged) stage_edges(sd, p.tr.doc_len + d_lo, n_doc);
-  int32_t* s_off = so.dst;
-  int32_t* s_doc = sd.dst;
+  const StageState sg_state = stage_begin(p, smem_raw, cs, &s_bar);
   int m0 = 0, md = 0;
   double rlF[P], rlB[P], rlW[P], sp[P], hf[P], hb[P], fin[P], ssum[P];
   float meas[P];
@@ -573,34 +646,7 @@ __global__ void __launch_bounds__(kSmallThreads, ZBH ? 4 : kSmallMinBlocks) pass
       meas[s] = mx;
     }
   }
-  mbar_wait(&s_bar, 0);  // the bulk copies have landed
-  __syncthreads();       // ... and so have the threads' edge words
-  // quadratic loads, one thread per micro-batch (no atomics)
-  for (int mb = tid; mb < n_mb; mb += nt) {
-    const int32_t k0 = s_off[mb] - d_lo, k1 = s_off[mb + 1] - d_lo;
-    unsigned long long q = 0;
-    if (staged) {
-      // packed bins hold few documents (C2: 2.4 on average, at most 4): the
-      // first four are summed branch-free with predicated loads
-      const int32_t nd = k1 - k0;
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const long long l = t < nd ? s_doc[k0 + t] : 0;
-        q += (unsigned long long)(l * l);
-      }
-      for (int32_t k = k0 + 4; k < k1; ++k) {
-        const long long l = s_doc[k];
-        q += (unsigned long long)(l * l);
-      }
-    } else {  // too many documents to stage: straight from global memory
-      for (int32_t k = k0; k < k1; ++k) {
-        const long long l = __ldg(p.tr.doc_len + d_lo + k);
-        q += (unsigned long long)(l * l);
-      }
-    }
-    s_q[mb] = q;
-  }
-  __syncthreads();  // sums complete; the document buffer is dead from here
+  stage_finish(p, cs, sg_state, &s_bar);
   if (md > p.mmax) md = -1;
   // division by a unit speed is exact for any numerator (div_fast(a, 1, 1)
   // == a): only replicas with a slower stage need the operand-range check
