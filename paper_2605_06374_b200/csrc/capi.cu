@@ -223,6 +223,11 @@ int rh_ctx_destroy(rh_ctx* ctx) {
   if (ctx->prep.consumed) cudaEventDestroy(ctx->prep.consumed);
   if (ctx->host_graph.exec) cudaGraphExecDestroy(ctx->host_graph.exec);
   if (ctx->screen_ctrl) cudaFree(ctx->screen_ctrl);
+  for (int q = 0; q < rh_ctx::kAuxStreams; ++q) {
+    if (ctx->aux_stream[q]) cudaStreamDestroy(ctx->aux_stream[q]);
+    if (ctx->aux_ev[q]) cudaEventDestroy(ctx->aux_ev[q]);
+  }
+  if (ctx->aux_fork) cudaEventDestroy(ctx->aux_fork);
   delete ctx;
   return RH_OK;
 }

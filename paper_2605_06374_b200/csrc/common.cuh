@@ -38,6 +38,11 @@ struct rh_ctx {
   };
   std::vector<SchedTable> sched;
   std::mutex sched_mu;
+  // concurrent per-P launches of the search's table stage (fork / join)
+  static constexpr int kAuxStreams = 4;
+  cudaStream_t aux_stream[kAuxStreams] = {};
+  cudaEvent_t aux_ev[kAuxStreams] = {};
+  cudaEvent_t aux_fork = nullptr;
   // rh_screen's cooperative-kernel control words (zero between launches)
   void* screen_ctrl = nullptr;
   // the device's default memory pool keeps freed memory (re-plan searches)

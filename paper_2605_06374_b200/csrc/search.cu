@@ -594,7 +594,9 @@ __global__ void __launch_bounds__(kPipeThreads) pipe_kernel(SearchArgs a, const 
 
 // ---- phase 2: every candidate from the table (thread per candidate) -------
 __global__ void __launch_bounds__(kEvalThreads) combine_kernel(SearchArgs a, long long begin,
-                                                              long long end, double* scores) {
+                                                              long long end, long long sbegin,
+                                                              double* scores, double* out_best,
+                                                              long long* out_idx) {
   __shared__ double s_best[kEvalThreads / 32];
   __shared__ long long s_idx[kEvalThreads / 32];
   double best = CUDART_INF;
@@ -638,7 +640,7 @@ __global__ void __launch_bounds__(kEvalThreads) combine_kernel(SearchArgs a, lon
       if (ar >= 0.0) ms = __dadd_rn(ms, ar);
       score = __dadd_rn(ms, sur);
     }
-    if (scores) scores[idx - begin] = score;
+    if (scores) scores[idx - sbegin] = score;
     if (lex_less(score, idx, best, best_i)) {
       best = score;
       best_i = idx;
@@ -665,8 +667,8 @@ __global__ void __launch_bounds__(kEvalThreads) combine_kernel(SearchArgs a, lon
         b = s_best[q];
         bi = s_idx[q];
       }
-    a.v.blk_best[blockIdx.x] = b;
-    a.v.blk_idx[blockIdx.x] = bi;
+    out_best[blockIdx.x] = b;
+    out_idx[blockIdx.x] = bi;
   }
 }
 
@@ -1051,7 +1053,7 @@ int rh_search_create(rh_ctx* ctx, const rh_search_desc* desc, rh_search** out, v
                o_repart = take(4 * S->n_stage), o_rspeed = take(8 * S->n_rep),
                o_pstart = take(4 * (S->n_rep + NL)), o_same = take(4 * NL),
                o_base = take(8 * (size_t)d.n_micro_batches),
-               o_bb = take(8 * (size_t)S->eval_blocks), o_bi = take(8 * (size_t)S->eval_blocks),
+               o_bb = take(8 * (size_t)S->eval_blocks * NL), o_bi = take(8 * (size_t)S->eval_blocks * NL),
                o_rtab = take(8 * (size_t)S->n_rt), o_pinfo = take(16 * (size_t)S->n_pairs),
                o_rl = take(8 * 96 * (size_t)S->n_pairs),
                o_tasks = take(sizeof(PipeTask) * (size_t)NL);
@@ -1220,7 +1222,23 @@ int rh_search_eval(rh_ctx* ctx, rh_search* S, int64_t begin, int64_t end, double
                           cudaMemcpyHostToDevice, st));
   const bool zbh = S->d.schedule == RH_SCHED_ZBH;
   void* kern = zbh ? (void*)pipe_kernel<1> : (void*)pipe_kernel<0>;
+  // the per-P launches write disjoint table rows: run them concurrently on the
+  // context's auxiliary streams (fork / join by events on `st`) so one
+  // launch's last wave overlaps the next launch instead of idling SMs
+  constexpr int kAux = rh_ctx::kAuxStreams;
+  for (int q = 0; q < kAux; ++q) {
+    if (!ctx->aux_stream[q])
+      RH_CUDA(cudaStreamCreateWithFlags(&ctx->aux_stream[q], cudaStreamNonBlocking));
+    if (!ctx->aux_ev[q]) RH_CUDA(cudaEventCreateWithFlags(&ctx->aux_ev[q], cudaEventDisableTiming));
+  }
+  if (!ctx->aux_fork) RH_CUDA(cudaEventCreateWithFlags(&ctx->aux_fork, cudaEventDisableTiming));
+  RH_CUDA(cudaEventRecord(ctx->aux_fork, st));
+  const int n_used = std::min<int>(kAux, (int)groups.size());
+  for (int q = 0; q < n_used; ++q) RH_CUDA(cudaStreamWaitEvent(ctx->aux_stream[q], ctx->aux_fork, 0));
+  int gi = 0;
+  long long n_blk = 0;  // block results written so far (contiguous)
   for (const Group& g : groups) {
+    cudaStream_t gs = ctx->aux_stream[gi++ % kAux];
     const size_t smem = (size_t)(zbh ? 3 : 2) * g.P * kPipeThreads * sizeof(double);
     // (the pipe kernel strides its state by kPipeThreads)
     if (int e = ensure_smem(kern, smem)) return e;
@@ -1233,19 +1251,33 @@ int rh_search_eval(rh_ctx* ctx, rh_search* S, int64_t begin, int64_t end, double
     int n_tk = (int)g.count;
     {
       const long long n_rl = g.n_rows * g.P;
-      rl_kernel<<<(unsigned)((n_rl + 255) / 256), 256, 0, st>>>(a, tp, n_tk, g.P, g.n_rows);
+      rl_kernel<<<(unsigned)((n_rl + 255) / 256), 256, 0, gs>>>(a, tp, n_tk, g.P, g.n_rows);
       RH_CHECK_LAUNCH(ctx);
     }
     long long n_pipes = g.n_pipes;
     int P = g.P;
     void* args[] = {&a, &tp, &n_tk, &n_pipes, &P};
-    RH_CUDA(cudaLaunchKernel(kern, dim3(blocks), dim3(kPipeThreads), args, smem, st));
+    RH_CUDA(cudaLaunchKernel(kern, dim3(blocks), dim3(kPipeThreads), args, smem, gs));
     RH_CHECK_LAUNCH(ctx);
+    // this group's candidates, layout by layout, right behind its table rows
+    for (size_t q = g.first; q < g.first + g.count; ++q) {
+      const int li = tk[q].layout;
+      const long long lo = std::max<long long>(begin, S->lbase[li]);
+      const long long hi = std::min<long long>(end, S->lbase[li] + S->lnv[li] * S->lnu[li]);
+      if (lo >= hi) continue;
+      const int cb = (int)std::min<long long>(S->eval_blocks, (hi - lo + kEvalThreads - 1) / kEvalThreads);
+      combine_kernel<<<cb, kEvalThreads, 0, gs>>>(a, lo, hi, begin, scores, S->dv.blk_best + n_blk,
+                                                 S->dv.blk_idx + n_blk);
+      RH_CHECK_LAUNCH(ctx);
+      n_blk += cb;
+    }
   }
-  const int blocks = (int)std::min<long long>(S->eval_blocks, (n + kEvalThreads - 1) / kEvalThreads);
-  combine_kernel<<<blocks, kEvalThreads, 0, st>>>(a, begin, end, scores);
-  RH_CHECK_LAUNCH(ctx);
-  minloc_kernel<<<1, 1024, 0, st>>>(S->dv.blk_best, S->dv.blk_idx, blocks, best_score,
+  for (int q = 0; q < n_used; ++q) {
+    RH_CUDA(cudaEventRecord(ctx->aux_ev[q], ctx->aux_stream[q]));
+    RH_CUDA(cudaStreamWaitEvent(st, ctx->aux_ev[q], 0));
+  }
+  (void)n;
+  minloc_kernel<<<1, 1024, 0, st>>>(S->dv.blk_best, S->dv.blk_idx, (int)n_blk, best_score,
                                     best_index);
   RH_CHECK_LAUNCH(ctx);
   return RH_OK;
