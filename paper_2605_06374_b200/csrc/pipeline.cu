@@ -584,6 +584,27 @@ __device__ __forceinline__ void stage_finish(const PassParams& p, const CtaStage
   __syncthreads();  // sums complete; the document buffer is dead from here
 }
 
+#ifdef RH_DETECT_TRACE
+// debug build only (tools/detect_trace.py): per CTA, warp 0's globaltimer at
+// the phase boundaries of pass_small_kernel, and the SM it ran on
+__device__ unsigned long long g_dtrace[4096 * 8];
+__device__ __forceinline__ void dmark(int k) {
+  if (threadIdx.x == 0 && blockIdx.x < 4096) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_dtrace[blockIdx.x * 8 + k] = t;
+    if (k == 0) {
+      unsigned sm;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+      g_dtrace[blockIdx.x * 8 + 7] = sm;
+    }
+  }
+}
+#define RH_DMARK(k) dmark(k)
+#else
+#define RH_DMARK(k) ((void)0)
+#endif
+
 template <int P, int ZBH, int DETECT>
 __global__ void __launch_bounds__(kSmallThreads, ZBH ? 4 : kSmallMinBlocks) pass_small_kernel(const PassParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -599,6 +620,7 @@ __global__ void __launch_bounds__(kSmallThreads, ZBH ? 4 : kSmallMinBlocks) pass
   const int n_it = cs.n_it;
   const bool on = li < n_it;
   __shared__ uint64_t s_bar;
+  RH_DMARK(0);
   if (tid < p.ipb) {
     it_ms[tid] = 0.0;
     it_st[tid] = 0u;
@@ -646,7 +668,9 @@ __global__ void __launch_bounds__(kSmallThreads, ZBH ? 4 : kSmallMinBlocks) pass
       meas[s] = mx;
     }
   }
+  RH_DMARK(1);
   stage_finish(p, cs, sg_state, &s_bar);
+  RH_DMARK(2);
   if (md > p.mmax) md = -1;
   // division by a unit speed is exact for any numerator (div_fast(a, 1, 1)
   // == a): only replicas with a slower stage need the operand-range check
@@ -704,6 +728,7 @@ __global__ void __launch_bounds__(kSmallThreads, ZBH ? 4 : kSmallMinBlocks) pass
     safe = safe && div_range_ok(r_lo * b_lo, r_hi * b_hi);
   }
   WalkArgs<P> wa{bt, rlF, rlB, rlW, sp, inv, hf, hb, fin, ssum};
+  RH_DMARK(3);
   if (mm > 0) {
     const unsigned long long* l0 = p.sched + __ldg(p.sched_off + mm);
     const unsigned long long* l1 = p.sched + __ldg(p.sched_off + mm + 1);
@@ -712,7 +737,9 @@ __global__ void __launch_bounds__(kSmallThreads, ZBH ? 4 : kSmallMinBlocks) pass
     else if (mm > p.static_max || !walk_static_dispatch<P, ZBH>(wa, mm))
       walk_table<P, ZBH, true>(wa, l0, l1);
   }
+  RH_DMARK(4);
   __syncthreads();  // iteration slots initialised before the reductions
+  RH_DMARK(5);
   // ---- replica makespan, validation, iteration reductions
   uint8_t flag[P];
   float sev[P];
@@ -771,6 +798,7 @@ __global__ void __launch_bounds__(kSmallThreads, ZBH ? 4 : kSmallMinBlocks) pass
     p.out.makespan[it] = ms;
     p.out.status[it] = (uint8_t)st;
   }
+  RH_DMARK(6);
 }
 
 // Level table for (P, schedule, mmax): for every micro-batch count
@@ -981,7 +1009,11 @@ int launch_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
     const size_t region =
         std::max<size_t>(16 * 1024 + 16, (size_t)kSmallThreads * p.mmax * 8);
     p.doc_stage = (int)((region - 16) / 4);
+#ifdef RH_STATIC_MAX_MB
+    p.static_max = RH_STATIC_MAX_MB;  // A/B builds: 0 = always the level-table walk
+#else
     p.static_max = kStaticMaxMB;
+#endif
     p.ltab = nullptr;
     const size_t smem = p.region_off + region;
     if (smem <= ctx->smem_optin && smem <= 56 * 1024) {
@@ -1440,3 +1472,9 @@ int rh_detector_pass_host_packed(rh_ctx* ctx, const rh_pipe_shape* shape,
 }
 
 }  // extern "C"
+
+#ifdef RH_DETECT_TRACE
+extern "C" int rh_debug_detect_trace(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, rh::g_dtrace, sizeof(rh::g_dtrace)) == cudaSuccess ? 0 : 1;
+}
+#endif
