@@ -65,29 +65,42 @@ struct ScreenArgs {
   uint8_t* c0;                     // [n] round-0 verdicts (round0_kernel)
   // control words (rh_ctx::screen_ctrl): zero when a launch starts, and the
   // launch leaves them zero again (no memset per call; graph-replay safe)
-  unsigned* cnt;             // [3] changes per round (rotating)
+  unsigned* cnt;             // [3] barrier words per round (rotating): arrivals + changed blocks << 16
   unsigned long long* kcnt;  // [3] kept entries since the last reset, per round
-  unsigned* bar;             // [2] barrier count, generation
+  unsigned* bar;             // [2] unused (reserved)
   unsigned* ticket;          // [1] blocks finished
 };
 
-__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
+// Grid barrier of Jacobi round `round`, carrying the round's "anything
+// changed" bit: thread 0 of every block adds 1 (+ 1 << 16 when the block
+// changed a decision) to the round's word with release semantics and polls it
+// with acquire loads until every block has arrived.  One fire-and-forget
+// atomic and one polling round trip per block; the poll's value is the
+// round's verdict, so no separate counter read follows.  Words rotate over
+// three rounds: the word of round r + 1 was last polled before barrier r - 1
+// and is zeroed by block 0 before it arrives at barrier r.
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ bool grid_barrier_any(unsigned* words, int round, unsigned nblocks,
+                                                 bool changed, unsigned* s_any) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    volatile unsigned* gen = bar + 1;
-    const unsigned g = *gen;
-    __threadfence();
-    if (atomicAdd(bar, 1u) == nblocks - 1) {
-      atomicExch(bar, 0u);
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
-    } else {
-      while (*gen == g) {
-      }
-    }
-    __threadfence();
+    unsigned* w = words + round % 3;
+    red_release_add(w, 1u + (changed ? 0x10000u : 0u));
+    unsigned v;
+    do {
+      v = ld_acquire(w);
+    } while ((v & 0xffffu) < nblocks);
+    *s_any = v >> 16;
   }
   __syncthreads();
+  return *s_any != 0;
 }
 
 // statistics.median of the w values in a[] (shared memory, warp-visible):
@@ -338,6 +351,7 @@ __global__ void __launch_bounds__(kScreenThreads) screen_kernel(const ScreenArgs
   auto& s_ob = sm.ob;
   auto& s_it = sm.it;
   unsigned& s_cnt = sm.cnt;
+  __shared__ unsigned s_any;
   unsigned long long& s_kcnt = sm.kcnt;
   // the series length at the end counts kept entries from the last reset on
   const int32_t r_last = __ldg(a.R + (a.n - 1));
@@ -444,22 +458,21 @@ __global__ void __launch_bounds__(kScreenThreads) screen_kernel(const ScreenArgs
       a.kcnt[(round + 1) % 3] = 0;
     }
     __syncthreads();
-    if (threadIdx.x == 0 && s_cnt) atomicAdd(a.cnt + round % 3, s_cnt);
     if (threadIdx.x == 0 && s_kcnt) atomicAdd(a.kcnt + round % 3, s_kcnt);
 #ifdef RH_SCREEN_TRACE
     const unsigned long long t_arrive = gtimer();
     if (threadIdx.x == 0 && round < 32) atomicMax(&g_trace_slow[round], t_arrive - t_start);
 #endif
-    grid_barrier(a.bar, gridDim.x);
+    const bool any = grid_barrier_any(a.cnt, round, gridDim.x, s_cnt != 0, &s_any);
 #ifdef RH_SCREEN_TRACE
     if (blockIdx.x == 0 && threadIdx.x == 0 && round < 32) {
       g_trace_t[3 * round] = t_start;
       g_trace_t[3 * round + 1] = t_arrive;
       g_trace_t[3 * round + 2] = gtimer();
-      g_trace_chg[round] = __ldcg(a.cnt + round % 3);
+      g_trace_chg[round] = __ldcg(a.cnt + round % 3) >> 16;
     }
 #endif
-    if (__ldcg(a.cnt + round % 3) == 0) break;  // fixpoint: nothing changed
+    if (!any) break;  // fixpoint: nothing changed
   }
   // final series length: kept entries since the last reset (+ history), as
   // counted in the round that changed nothing
