@@ -434,7 +434,7 @@ __device__ __forceinline__ int layer_of(const SearchArgs& a, const int32_t* rep,
 
 constexpr int kPipeThreads = 128;
 
-template <int ZBH>
+template <int ZBH, bool SAFE>
 __global__ void __launch_bounds__(kPipeThreads) pipe_kernel(SearchArgs a, const PipeTask* tk,
                                                            int n_tk, long long n_pipes, int P) {
   extern __shared__ double pipe_smem[];
@@ -531,7 +531,12 @@ __global__ void __launch_bounds__(kPipeThreads) pipe_kernel(SearchArgs a, const 
       const double* rlt = a.v.rl + pair * 3LL * 32 - 32;  // indexed by kind * 32 + s
       const uint32_t* opp = a.v.ops + e0;
       // software pipeline: op codes two ahead, their global operands one ahead,
-      // so only the shared-memory state chain is serial
+      // so only the shared-memory state chain is serial.  The loop body is
+      // branch-free: the prefetch indices clamp to the last op (a harmless
+      // re-fetch), an op without a data predecessor reads a valid dummy slot
+      // and selects 0, and the division is always the exact hoisted-reciprocal
+      // form (unit speeds: inv == 1 gives c unchanged) when the host proved the
+      // search's operand ranges safe.
       struct Operands {
         unsigned op;
         double rl, b, sp, inv, hop;
@@ -541,34 +546,35 @@ __global__ void __launch_bounds__(kPipeThreads) pipe_kernel(SearchArgs a, const 
         o.op = op;
         const int st = op & 63u;
         const unsigned kind = (op >> 6) & 3u, dk = (op >> 8) & 3u;
-        o.rl = __ldg(rlt + kind * 32 + st);
-        o.b = __ldg(bs + (op >> 10));
-        o.sp = __ldg(sp_d + st * D);
-        o.inv = __ldg(inv_d + st * D);
-        o.hop = dk ? __ldg(hop_d + (st - (dk == 1 ? 1 : 0)) * D) : 0.0;
+        const int so = st * D;  // [s][d] tables: element (d, s) at s * D
+        o.rl = __ldg(rlt + (int)(kind * 32 + st));
+        o.b = __ldg(bs + (int)(op >> 10));
+        o.sp = __ldg(sp_d + so);
+        o.inv = __ldg(inv_d + so);
+        o.hop = __ldg(hop_d + (dk == 1 ? so - D : so));
         return o;
       };
-      unsigned op2 = ne > 1 ? __ldg(opp + 1) : 0u;
-      Operands nx = ne > 0 ? fetch(__ldg(opp)) : Operands{};
+      const int last = ne - 1;
+      unsigned op2 = 0u;
+      Operands nx{};
+      if (ne > 0) {  // real op codes only (kind >= 1): every fetch stays in its tables
+        op2 = __ldg(opp + min(1, last));
+        nx = fetch(__ldg(opp));
+      }
       for (int e = 0; e < ne; ++e) {
         const Operands o = nx;
-        const unsigned op3 = e + 2 < ne ? __ldg(opp + e + 2) : 0u;
-        if (e + 1 < ne) nx = fetch(op2);
+        const unsigned op3 = __ldg(opp + min(e + 2, last));
+        nx = fetch(op2);
         op2 = op3;
         const int st = o.op & 63u;
         const unsigned kind = (o.op >> 6) & 3u, dk = (o.op >> 8) & 3u;
-        // (rl * b) / sp exactly as __ddiv_rn: unit speeds skip it (uniform
-        // branch), others use the hoisted reciprocal when the host proved the
-        // ranges safe for the whole search
         double c = __dmul_rn(o.rl, o.b);
-        if (o.sp != 1.0) c = a.div_safe ? div_fast(c, o.sp, o.inv) : div_slow(c, o.sp);
+        if (SAFE) c = div_fast(c, o.sp, o.inv);
+        else if (o.sp != 1.0) c = div_slow(c, o.sp);
         const int self = st * kPipeThreads + tid;
-        double dep = 0.0;
-        if (dk) {
-          // F: last F of stage-1 (+ hop s-1 -> s); B: last B of stage+1 (+ hop s)
-          const int src = dk == 1 ? self - kPipeThreads : fB + self + kPipeThreads;
-          dep = __dadd_rn(pipe_smem[src], o.hop);
-        }
+        // F: last F of stage-1 (+ hop s-1 -> s); B: last B of stage+1 (+ hop s)
+        const int src = dk == 1 ? self - kPipeThreads : (dk ? fB + self + kPipeThreads : self);
+        const double dep = dk ? __dadd_rn(pipe_smem[src], o.hop) : 0.0;
         double fin;
         if (ZBH) {
           fin = pipe_smem[fN + self];
@@ -577,8 +583,12 @@ __global__ void __launch_bounds__(kPipeThreads) pipe_kernel(SearchArgs a, const 
           fin = x > y ? x : y;
         }
         const double nf = __dadd_rn(fin > dep ? fin : dep, c);
-        if (ZBH) pipe_smem[fN + self] = nf;
-        if (kind != kOpW) pipe_smem[(kind == kOpF ? 0 : fB) + self] = nf;
+        if (ZBH) {
+          pipe_smem[fN + self] = nf;
+          if (kind != kOpW) pipe_smem[(kind == kOpF ? 0 : fB) + self] = nf;
+        } else {
+          pipe_smem[(kind == kOpF ? 0 : fB) + self] = nf;  // 1F1B: F or BW only
+        }
       }
       double gm = 0.0;
       for (int q = 0; q < P; ++q) {
@@ -1221,7 +1231,8 @@ int rh_search_eval(rh_ctx* ctx, rh_search* S, int64_t begin, int64_t end, double
   RH_CUDA(cudaMemcpyAsync(S->dv.tasks, tk.data(), sizeof(PipeTask) * tk.size(),
                           cudaMemcpyHostToDevice, st));
   const bool zbh = S->d.schedule == RH_SCHED_ZBH;
-  void* kern = zbh ? (void*)pipe_kernel<1> : (void*)pipe_kernel<0>;
+  void* kern = zbh ? (S->div_safe ? (void*)pipe_kernel<1, true> : (void*)pipe_kernel<1, false>)
+                  : (S->div_safe ? (void*)pipe_kernel<0, true> : (void*)pipe_kernel<0, false>);
   // the per-P launches write disjoint table rows: run them concurrently on the
   // context's auxiliary streams (fork / join by events on `st`) so one
   // launch's last wave overlaps the next launch instead of idling SMs
