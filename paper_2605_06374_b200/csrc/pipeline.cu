@@ -681,7 +681,10 @@ __global__ void __launch_bounds__(kSmallThreads, ZBH ? 4 : kSmallMinBlocks) pass
   if (md > 0) {
     const double lin = __dmul_rn(p.m.alpha, (double)p.sh.token_budget);
     const unsigned long long* q = s_q + li * M + m0;
-    for (int j = 0; j < md; ++j) {
+    // rotated start: neighbouring replicas' runs are md words apart, so
+    // reading them in step would hit the same banks
+    int j = d % md;
+    for (int k = 0; k < md; ++k, j = j + 1 == md ? 0 : j + 1) {
       const double b = __dadd_rn(lin, __dmul_rn(p.m.beta, (double)(long long)q[j]));
       base_t[j * kSmallThreads + tid] = b;
       if (!all_unit) {
