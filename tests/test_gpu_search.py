@@ -137,3 +137,39 @@ def test_benchmarked_spaces_sampled(name, oracle, cuda_device):
         np.testing.assert_array_equal(bits(g[fin]), bits(c[fin]))
         assert gpu.best(a, b) == (cb, ci)
     assert gpu.decode(bidx) == cpu.decode(bidx)
+
+
+@pytest.mark.parametrize("alpha,beta", [(1e-300, 1e-310), (1e270, 1e262)])
+def test_extreme_cost_model_exact_division(alpha, beta, oracle, cuda_device):
+    """Numerators outside the hoisted-reciprocal range: the search must fall back
+    to correctly rounded division everywhere and still match the oracle bit for bit."""
+    from paper_2605_06374_b200.cluster import (FailureEvent, ParallelismConfig, apply_failures,
+                                               build_cluster)
+    from paper_2605_06374_b200.comm import CommSpec
+    from paper_2605_06374_b200.search import ReplanSearch, build_desc
+    from paper_2605_06374_b200.trace import synth_iterations
+    from paper_2605_06374_b200.workload import CostModel, MicroBatch
+
+    T, D, P = 4, 4, 4
+    cfg = ParallelismConfig(T, D, P, "1f1b", [10, 10, 10, 10])
+    st = build_cluster(T * D * P // 8, 8, cfg, 300.0 * 2**30, 25.0 * 2**30)
+    st = apply_failures(st, [FailureEvent("fail_slow_compute", 0.0, device=5, severity=0.4),
+                             FailureEvent("fail_slow_compute", 0.0, device=40, severity=0.7)],
+                        0.0)
+    M = 3 * D
+    off, docs = synth_iterations(1, M, 4096, 7.2, 0.8, 7)
+    mbs = [MicroBatch(j, tuple(int(x) for x in docs[off[j]:off[j + 1]]), 4096) for j in range(M)]
+    inputs = build_desc(st, cfg, mbs, CostModel(alpha, beta), CommSpec(), capacity=0,
+                        quad=[sum(x * x for x in mb.doc_lengths) for mb in mbs],
+                        min_utilization=0.85)
+    gpu = ReplanSearch(inputs)
+    cpu = oracle.search(inputs)
+    assert gpu.size == cpu.size
+    b = min(gpu.size, 4000)
+    g = gpu.scores(0, b)
+    _, _, c = cpu.best(0, b, with_scores=True)
+    np.testing.assert_array_equal(np.isinf(g), np.isinf(c))
+    fin = np.isfinite(c)
+    assert fin.any()
+    np.testing.assert_array_equal(bits(g[fin]), bits(c[fin]))
+    assert gpu.best(0, b) == cpu.best(0, b)
