@@ -341,3 +341,22 @@ def test_wide_replica_shapes_match_oracle(seed, oracle, cuda_device):
     np.testing.assert_array_equal(_bits(r["stage_cost"]), _bits(osc))
     np.testing.assert_array_equal(r["stage_flag"], ofl)
     np.testing.assert_array_equal(r["severity"].view(np.uint32), osv.view(np.uint32))
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_extreme_cost_model_matches_oracle(seed, oracle, cuda_device):
+    """Base costs far outside the hoisted-reciprocal range (tiny and huge cost
+    models): the walks fall back to correctly rounded division, bit-exact."""
+    from paper_2605_06374_b200.detect_pass import DetectorPass
+    from paper_2605_06374_b200.workload import CostModel
+
+    tr = random_trace(900 + seed, n_iter=20, pp=[2, 4, 6, 12][seed % 4])
+    alpha, beta = ((1e-300, 1e-310), (1e270, 1e262))[seed % 2]
+    tr.model = CostModel(alpha=alpha, beta=beta, chunk_ratios=tr.model.chunk_ratios)
+    p = DetectorPass(tr)
+    for view in ("known", "actual"):
+        ms, st, sc = p.pipeline(view)
+        oms, ost, osc = oracle.pipeline(tr, view=view)
+        np.testing.assert_array_equal(st.cpu().numpy(), ost)
+        np.testing.assert_array_equal(_bits(ms.cpu().numpy()), _bits(oms))
+        np.testing.assert_array_equal(_bits(sc.cpu().numpy()), _bits(osc))
