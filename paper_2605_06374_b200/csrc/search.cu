@@ -434,6 +434,104 @@ __device__ __forceinline__ int layer_of(const SearchArgs& a, const int32_t* rep,
 
 constexpr int kPipeThreads = 128;
 
+// One replica pipeline of the search, identified by its id g within a P
+// group: its layout, partition variant, range case and replica, its
+// micro-batch range, and whether it is evaluated at all.  With `info` set the
+// caller also writes the per-(layout, v) all-reduce vertex and amortised
+// reconfiguration surcharge.
+struct PipeId {
+  int li, D, vv, cs, d, goff, start, md;
+  long long pair;
+  bool feas_v, valid;
+};
+
+__device__ __forceinline__ PipeId pipe_id(const SearchArgs& a, const PipeTask* tk, int n_tk,
+                                          int P, long long g, bool info) {
+  int lo = 0, hi = n_tk - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (tk[mid].pipe_base <= g) lo = mid;
+    else hi = mid - 1;
+  }
+  const int li = tk[lo].layout;
+  const int D = a.v.lD[li];
+  const long long local = g - tk[lo].pipe_base;
+  const int vv = tk[lo].v_lo + (int)(local / (8 * D));
+  const int rr = (int)(local % (8 * D));
+  const int cs = rr / D, d = rr % D;
+  const int goff = a.v.lgoff[li], poff = a.v.lpoff[li];
+  const int32_t* rep = a.v.repart + poff;
+  const int32_t* pst = a.v.pstart + a.v.ldoff[li] + li;
+  int psrc = -1, pdst = -1;
+  if (vv >= 2) {
+    const int m = vv - 2, r = m % (P - 1);
+    psrc = m / (P - 1);
+    pdst = r < psrc ? r : r + 1;
+  }
+  const bool feas_v = !(psrc >= 0 && rep[psrc] - 1 < a.min_layers);
+  const long long pair = a.v.lpair[li] + vv;
+  if (info && cs == 0 && d == 0) {
+    // per (layout, v): all-reduce vertex (pipeline.py:356-372) and the
+    // amortised reconfiguration surcharge (scheduler.py:562-593)
+    const bool has_ar = a.has_comm && D > 1;
+    double ar = 0.0;
+    if (has_ar)
+      for (int q = 0; q < P; ++q) {
+        const double nbytes = __dmul_rn((double)layer_of(a, rep, P, vv, psrc, pdst, q), a.lb);
+        ar = fmax(ar, __ddiv_rn(__dmul_rn(__dmul_rn(2.0, nbytes), (double)(D - 1)),
+                                __dmul_rn((double)D, a.v.ring[poff + q])));
+      }
+    const bool same_layout = a.v.same[li] != 0;
+    const bool sameP = P == a.cur_P;
+    bool changed = false;
+    long long moved = 0;
+    for (int q = 0; q < P && sameP; ++q) {
+      const int lq = layer_of(a, rep, P, vv, psrc, pdst, q);
+      const int old = a.v.cur_partition[q];
+      if (lq != old) changed = true;
+      if (lq > old) moved += lq - old;
+    }
+    double reshard = 0.0;
+    if (!same_layout)
+      for (int dd = 0; dd < D; ++dd)
+        for (int q = 0; q < P; ++q)
+          reshard = __dadd_rn(reshard,
+                              __dmul_rn((double)layer_of(a, rep, P, vv, psrc, pdst, q), a.lb));
+    double sur = 0.0;
+    if (!same_layout || changed) {
+      const double transfer = __ddiv_rn(__dadd_rn(__dmul_rn((double)moved, a.lb), reshard),
+                                        a.worst_inter);
+      sur = __ddiv_rn(__dadd_rn(a.rebuild_s, transfer), (double)max(1, a.amort));
+    }
+    a.v.pinfo[2 * pair] = has_ar ? ar : -1.0;  // -1: no all-reduce vertex
+    a.v.pinfo[2 * pair + 1] = feas_v ? sur : CUDART_INF;
+  }
+  int start = 0, md = 0;
+  bool valid = true;
+  if (cs == 0) {
+    const int base = a.M / D, extra = a.M % D;
+    start = d * base + min(d, extra);
+    md = base + (d < extra ? 1 : 0);
+  } else {
+    start = pst[d] + kDs[cs];
+    md = pst[d + 1] + kDe[cs] - start;
+    valid = start >= 0 && md >= 0 && start + md <= a.M;
+  }
+  PipeId id;
+  id.li = li;
+  id.D = D;
+  id.vv = vv;
+  id.cs = cs;
+  id.d = d;
+  id.goff = goff;
+  id.start = start;
+  id.md = md;
+  id.pair = pair;
+  id.feas_v = feas_v;
+  id.valid = valid;
+  return id;
+}
+
 template <int ZBH, bool SAFE>
 __global__ void __launch_bounds__(kPipeThreads) pipe_kernel(SearchArgs a, const PipeTask* tk,
                                                            int n_tk, long long n_pipes, int P) {
@@ -441,76 +539,11 @@ __global__ void __launch_bounds__(kPipeThreads) pipe_kernel(SearchArgs a, const 
   const int tid = threadIdx.x, nt = blockDim.x;
   for (long long g = (long long)blockIdx.x * nt + tid; g < n_pipes;
        g += (long long)gridDim.x * nt) {
-    int lo = 0, hi = n_tk - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (tk[mid].pipe_base <= g) lo = mid;
-      else hi = mid - 1;
-    }
-    const int li = tk[lo].layout;
-    const int D = a.v.lD[li];
-    const long long local = g - tk[lo].pipe_base;
-    const int vv = tk[lo].v_lo + (int)(local / (8 * D));
-    const int rr = (int)(local % (8 * D));
-    const int cs = rr / D, d = rr % D;
-    const int goff = a.v.lgoff[li], poff = a.v.lpoff[li];
-    const int32_t* rep = a.v.repart + poff;
-    const int32_t* pst = a.v.pstart + a.v.ldoff[li] + li;
-    int psrc = -1, pdst = -1;
-    if (vv >= 2) {
-      const int m = vv - 2, r = m % (P - 1);
-      psrc = m / (P - 1);
-      pdst = r < psrc ? r : r + 1;
-    }
-    const bool feas_v = !(psrc >= 0 && rep[psrc] - 1 < a.min_layers);
-    const long long pair = a.v.lpair[li] + vv;
-    if (cs == 0 && d == 0) {
-      // per (layout, v): all-reduce vertex (pipeline.py:356-372) and the
-      // amortised reconfiguration surcharge (scheduler.py:562-593)
-      const bool has_ar = a.has_comm && D > 1;
-      double ar = 0.0;
-      if (has_ar)
-        for (int q = 0; q < P; ++q) {
-          const double nbytes = __dmul_rn((double)layer_of(a, rep, P, vv, psrc, pdst, q), a.lb);
-          ar = fmax(ar, __ddiv_rn(__dmul_rn(__dmul_rn(2.0, nbytes), (double)(D - 1)),
-                                  __dmul_rn((double)D, a.v.ring[poff + q])));
-        }
-      const bool same_layout = a.v.same[li] != 0;
-      const bool sameP = P == a.cur_P;
-      bool changed = false;
-      long long moved = 0;
-      for (int q = 0; q < P && sameP; ++q) {
-        const int lq = layer_of(a, rep, P, vv, psrc, pdst, q);
-        const int old = a.v.cur_partition[q];
-        if (lq != old) changed = true;
-        if (lq > old) moved += lq - old;
-      }
-      double reshard = 0.0;
-      if (!same_layout)
-        for (int dd = 0; dd < D; ++dd)
-          for (int q = 0; q < P; ++q)
-            reshard = __dadd_rn(reshard,
-                                __dmul_rn((double)layer_of(a, rep, P, vv, psrc, pdst, q), a.lb));
-      double sur = 0.0;
-      if (!same_layout || changed) {
-        const double transfer = __ddiv_rn(__dadd_rn(__dmul_rn((double)moved, a.lb), reshard),
-                                          a.worst_inter);
-        sur = __ddiv_rn(__dadd_rn(a.rebuild_s, transfer), (double)max(1, a.amort));
-      }
-      a.v.pinfo[2 * pair] = has_ar ? ar : -1.0;  // -1: no all-reduce vertex
-      a.v.pinfo[2 * pair + 1] = feas_v ? sur : CUDART_INF;
-    }
-    int start = 0, md = 0;
-    bool valid = true;
-    if (cs == 0) {
-      const int base = a.M / D, extra = a.M % D;
-      start = d * base + min(d, extra);
-      md = base + (d < extra ? 1 : 0);
-    } else {
-      start = pst[d] + kDs[cs];
-      md = pst[d + 1] + kDe[cs] - start;
-      valid = start >= 0 && md >= 0 && start + md <= a.M;
-    }
+    const PipeId id = pipe_id(a, tk, n_tk, P, g, true);
+    const int li = id.li, D = id.D, vv = id.vv, cs = id.cs, d = id.d, goff = id.goff;
+    const int start = id.start, md = id.md;
+    const long long pair = id.pair;
+    const bool feas_v = id.feas_v, valid = id.valid;
     double res = CUDART_INF;
     if (feas_v && valid) {
       const int slot = P * a.tab_stride + md;
