@@ -54,6 +54,7 @@ struct PassParams {
   const int32_t* sched_peak;        // [mmax+1] peak in-flight forward chunks on any stage
   int region_off;            // smem offset of the document / base-cost region
   int doc_stage;             // documents that fit in that region
+  int pf_stride;             // resident CTA slots: CTA b prefetches CTA b + pf_stride (0: off)
   int static_max;  // largest micro-batch count walked by the unrolled code
   // lane kernel only: level table (lane_table), NULL = closed-form walk
   const uint16_t* ltab;
@@ -315,6 +316,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
         : "=r"(done)
         : "r"(smem_u32(bar)), "r"(phase)
         : "memory");
+}
+// L2 prefetch of [p, p + bytes), trimmed inward to 16-byte alignment (a hint:
+// nothing outside the range is touched)
+__device__ __forceinline__ void prefetch_l2(const void* p, size_t bytes) {
+  const uintptr_t a = (reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15);
+  const uintptr_t b = (reinterpret_cast<uintptr_t>(p) + bytes) & ~uintptr_t(15);
+  if (b > a)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((unsigned)(b - a))
+                 : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
                                          uint64_t* bar) {
@@ -608,7 +618,7 @@ __device__ __forceinline__ void dmark(int k) {
 template <int P, int ZBH, int DETECT>
 __global__ void __launch_bounds__(kSmallThreads, ZBH ? 4 : kSmallMinBlocks) pass_small_kernel(const PassParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int tid = threadIdx.x, nt = blockDim.x;
+  const int tid = threadIdx.x;
   const int D = p.sh.dp, M = p.sh.micro_batches, T = p.sh.tp;
   const int li = tid / D, d = tid - li * D;
   const int64_t it = (int64_t)blockIdx.x * p.ipb + li;
@@ -627,6 +637,19 @@ __global__ void __launch_bounds__(kSmallThreads, ZBH ? 4 : kSmallMinBlocks) pass
   }
   // ---- staging by TMA; the per-thread loads below run meanwhile
   const int seg = on && p.tr.seg ? __ldg(p.tr.seg + it) : 0;
+  // the CTA that will run in this slot's next wave: its inputs are pulled into
+  // L2 now, while this wave is latency-bound and HBM is mostly idle
+  const int64_t nb = (int64_t)blockIdx.x + p.pf_stride;
+  const bool pf = tid == 0 && p.pf_stride > 0 && nb < gridDim.x;
+  int64_t pf_it = 0;
+  int pf_nmb = 0;
+  int32_t pf_lo = 0, pf_hi = 0;
+  if (pf) {
+    pf_it = nb * p.ipb;
+    pf_nmb = (int)min((int64_t)p.ipb, p.tr.n_iter - pf_it) * M;
+    pf_lo = __ldg(p.tr.mb_off + pf_it * M);
+    pf_hi = __ldg(p.tr.mb_off + pf_it * M + pf_nmb);
+  }
   const StageState sg_state = stage_begin(p, smem_raw, cs, &s_bar);
   int m0 = 0, md = 0;
   double rlF[P], rlB[P], rlW[P], sp[P], hf[P], hb[P], fin[P], ssum[P];
@@ -669,6 +692,12 @@ __global__ void __launch_bounds__(kSmallThreads, ZBH ? 4 : kSmallMinBlocks) pass
     }
   }
   RH_DMARK(1);
+  if (pf) {
+    prefetch_l2(p.tr.mb_off + pf_it * M, 4 * (size_t)(pf_nmb + 1));
+    prefetch_l2(p.tr.doc_len + pf_lo, 4 * (size_t)(pf_hi - pf_lo));
+    if (DETECT)
+      prefetch_l2(p.tr.device_time + pf_it * D * P * T, 4 * (size_t)(pf_nmb / M) * D * P * T);
+  }
   stage_finish(p, cs, sg_state, &s_bar);
   RH_DMARK(2);
   if (md > p.mmax) md = -1;
@@ -1027,6 +1056,11 @@ int launch_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
       void* kern = zbh ? (detect ? small_kernel<1, 1>(P) : small_kernel<1, 0>(P))
                        : (detect ? small_kernel<0, 1>(P) : small_kernel<0, 0>(P));
       if (int e = ensure_smem(kern, smem)) return e;
+      {
+        int occ = 0;
+        RH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
+        p.pf_stride = getenv("RH_NO_L2_PREFETCH") ? 0 : occ * ctx->num_sms;
+      }
       void* args[] = {&p};
       RH_CUDA(cudaLaunchKernel(kern, dim3((unsigned)blocks), dim3(threads), args, smem, stream));
       RH_CHECK_LAUNCH(ctx);
