@@ -552,9 +552,12 @@ __device__ __forceinline__ void walk_steady(const WalkArgs<P>& a, int m) {
 
 constexpr int kStaticMaxMB = 12;  // replicas with <= 12 micro-batches
 
+// 1F1B replicas with m >= P take walk_steady, so the 1F1B kernels carry
+// unrolled walks only for m < P (less code competing for the instruction
+// cache); the level table covers the rest.
 template <int P, int ZBH, int MM = 1>
 __device__ __forceinline__ bool walk_static_dispatch(const WalkArgs<P>& a, int mm) {
-  if constexpr (MM > kStaticMaxMB) {
+  if constexpr (MM > (ZBH ? kStaticMaxMB : P - 1)) {
     return false;
   } else {
     if (mm == MM) {
