@@ -17,8 +17,9 @@
 //
 // Two mappings (launch_pass picks one per launch):
 //   pass_small_kernel (P <= 4, D <= 128): one THREAD per replica pipeline,
-//     all stage state in registers, chunks in DAG-level order (fully unrolled
-//     for small micro-batch counts, level table otherwise); see below.
+//     all stage state in registers, chunks in DAG-level order (steady-state
+//     loop walk for 1F1B, fully unrolled for small micro-batch counts, level
+//     table otherwise); see below.
 //   pass_kernel (P <= 32): one replica pipeline = `pw` lanes (pw =
 //     next_pow2(P), lane s = stage s); each lane walks its chain with the
 //     branch-free static level walk of wavefront.cuh, neighbours exchange the
@@ -269,9 +270,11 @@ __global__ void __launch_bounds__(MAXT) pass_kernel(const PassParams p) {
 // Small-P variant (P <= 4, D <= 128): one THREAD per replica pipeline.
 //
 // Op order.  The thread executes its replica's chunks in DAG-level order
-// (wavefront.cuh closed forms), inside a level by DESCENDING stage: fully
-// unrolled at compile time for small micro-batch counts (walk_static), else
-// from a level table (sched_table).  With every stage's state in registers
+// (wavefront.cuh closed forms), inside a level by DESCENDING stage: for
+// 1F1B with m >= P an unrolled warm-up and cool-down around a loop over the
+// steady F/B level pairs (walk_steady); for smaller m (and ZBH up to 12)
+// fully unrolled at compile time (walk_static); otherwise from a level table
+// (sched_table).  With every stage's state in registers
 // (P is a template parameter) the dependencies then read straight from the
 // neighbours' registers:
 //   * F(s,j) needs F(s-1,j) (one level earlier); stage s-1's next F may sit
@@ -284,7 +287,9 @@ __global__ void __launch_bounds__(MAXT) pass_kernel(const PassParams p) {
 // documents into shared memory with TMA bulk copies (cp.async.bulk completing
 // on an mbarrier); l^2 is summed one thread per micro-batch; each thread then
 // turns its replica's sums into base costs stored [j][thread] (conflict-free
-// reads in the walk), aliasing the dead document buffer.
+// reads in the walk), aliasing the dead document buffer.  Thread 0 also
+// prefetches into L2 the inputs of the CTA that takes over its slot in the
+// next wave (cp.async.bulk.prefetch.L2).
 //
 // Division by a stage speed: exact hoisted-reciprocal form (div_fast) after a
 // once-per-replica operand-range check (wavefront.cuh).
