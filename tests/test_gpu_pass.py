@@ -360,3 +360,30 @@ def test_extreme_cost_model_matches_oracle(seed, oracle, cuda_device):
         np.testing.assert_array_equal(st.cpu().numpy(), ost)
         np.testing.assert_array_equal(_bits(ms.cpu().numpy()), _bits(oms))
         np.testing.assert_array_equal(_bits(sc.cpu().numpy()), _bits(osc))
+
+
+@pytest.mark.parametrize("pp", [1, 2, 3, 4])
+def test_steady_walk_boundaries_match_oracle(pp, oracle, cuda_device):
+    """1F1B replicas at and around the steady-state walk's boundary (m = P-1, P,
+    P+1, 2P, and long runs): warm-up, steady loop and cool-down reproduce the
+    level-ordered walk bit for bit, with stage-cost sums and capacity checks."""
+    from paper_2605_06374_b200.detect_pass import DetectorPass
+
+    for m in sorted({max(1, pp - 1), pp, pp + 1, 2 * pp, 13, 37}):
+        dp = 4
+        tr = with_measurements(random_trace(1200 + 10 * pp + m, n_iter=12, pp=pp, dp=dp,
+                                            M=m * dp, schedule="1f1b", n_seg=1),
+                               oracle, noise=0.02, seed=m)
+        p = DetectorPass(tr, keep_stage_cost=True)
+        p.detect()
+        r = p.results()
+        oms, ost, osc, ofl, osv = oracle.detect(tr)
+        np.testing.assert_array_equal(r["status"], ost)
+        np.testing.assert_array_equal(_bits(r["makespan"]), _bits(oms))
+        np.testing.assert_array_equal(_bits(r["stage_cost"]), _bits(osc))
+        np.testing.assert_array_equal(r["stage_flag"], ofl)
+        for cap in (1, pp, pp + 2):
+            ms, st, _ = p.pipeline("actual", capacity=cap)
+            oms2, ost2, _ = oracle.pipeline(tr, view="actual", capacity=cap)
+            np.testing.assert_array_equal(st.cpu().numpy(), ost2)
+            np.testing.assert_array_equal(_bits(ms.cpu().numpy()), _bits(oms2))

@@ -32,7 +32,17 @@ from paper_2605_06374_b200 import _lib  # noqa: E402
 from paper_2605_06374_b200.detect_pass import DetectorPass  # noqa: E402
 
 dev = torch.device("cuda", 0)
-tr = bench.build_trace(0, bench.N_ITER, use_oracle=False)
+shape = next((a for a in sys.argv[1:] if a in ("C1", "C5")), None)
+if shape:  # another BASELINE shape (tools/detect_shapes.py's parameters), 4000 iterations
+    from paper_2605_06374_b200.detect_pass import synthesize_measurements
+    from paper_2605_06374_b200.scenarios import c2_trace
+
+    kw = {"C1": dict(tp=4, dp=4, pp=2, layers=32, M=16),
+          "C5": dict(tp=8, dp=32, pp=16, layers=80, M=512)}[shape]
+    tr = c2_trace(4000, seed=0, **kw)
+    synthesize_measurements(tr, seed=0)
+else:
+    tr = bench.build_trace(0, bench.N_ITER, use_oracle=False)
 p = DetectorPass(tr, dev)
 fn = _lib.load_library().rh_debug_screen_trace
 t = (C.c_ulonglong * 96)()
