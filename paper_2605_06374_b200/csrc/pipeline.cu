@@ -57,7 +57,7 @@ struct PassParams {
   int doc_stage;             // documents that fit in that region
   int pf_stride;             // resident CTA slots: CTA b prefetches CTA b + pf_stride (0: off)
   int static_max;  // largest micro-batch count walked by the unrolled code
-  int steady;      // 1F1B with m >= P: the steady-state loop walk (walk_steady)
+  int steady;      // m >= P: the steady-state loop walk (walk_steady)
   // lane kernel only: level table (lane_table), NULL = closed-form walk
   const uint16_t* ltab;
   const int32_t *ltab_off, *ltab_nlev, *ltab_peak;  // [mmax+1] each
@@ -484,47 +484,58 @@ __device__ __forceinline__ void walk_static(const WalkArgs<P>& a) {
   }
 }
 
-// Levels [T0, T1) of the MM-micro-batch walk, with the chain state passed in
-// and micro-batch j read at bt[j * kSmallThreads] (callers shift bt to
-// re-base j).  Everything folds to constants as in walk_static.
-template <int P, int MM, int T0, int T1>
-__device__ __forceinline__ void walk_levels(const WalkArgs<P>& a, const double* bt,
-                                            double (&lastF)[P], double (&lastB)[P]) {
+// Levels [T0, T1) of the MM-micro-batch walk, with the chain state passed in:
+// F / B chunks read micro-batch j at bt_fb[j * kSmallThreads], W chunks (ZBH)
+// at bt_w[j * kSmallThreads] (callers shift the pointers to re-base j); with
+// COOL the W chunks of the chain's tail (j >= P-1-s) are left to the caller.
+// Everything folds to constants as in walk_static.
+template <int P, int ZBH, int MM, int T0, int T1, bool COOL>
+__device__ __forceinline__ void walk_levels(const WalkArgs<P>& a, const double* bt_fb,
+                                            const double* bt_w, double (&lastF)[P],
+                                            double (&lastB)[P]) {
 #pragma unroll
   for (int t = T0; t < T1; ++t) {
 #pragma unroll
     for (int s = P - 1; s >= 0; --s) {
       int j = 0;
-      const int kind = op_at(P, MM, 0, t, s, j);
+      const int kind = op_at(P, MM, ZBH, t, s, j);
       if (kind == kOpF) {
         const double dep = s > 0 ? __dadd_rn(lastF[s > 0 ? s - 1 : 0], a.hf[s]) : 0.0;
-        lastF[s] = chunk<true>(a.fin[s], a.ssum[s], a.rlF[s], bt[j * kSmallThreads], a.sp[s],
+        lastF[s] = chunk<true>(a.fin[s], a.ssum[s], a.rlF[s], bt_fb[j * kSmallThreads], a.sp[s],
                                a.inv[s], dep);
       } else if (kind == kOpB) {
         const double dep = s < P - 1 ? __dadd_rn(lastB[s < P - 1 ? s + 1 : 0], a.hb[s]) : 0.0;
-        lastB[s] = chunk<true>(a.fin[s], a.ssum[s], a.rlB[s], bt[j * kSmallThreads], a.sp[s],
+        lastB[s] = chunk<true>(a.fin[s], a.ssum[s], a.rlB[s], bt_fb[j * kSmallThreads], a.sp[s],
                                a.inv[s], dep);
+      } else if (kind == kOpW && !(COOL && j >= P - 1 - s)) {
+        chunk<true>(a.fin[s], a.ssum[s], a.rlW[s], bt_w[j * kSmallThreads], a.sp[s], a.inv[s],
+                    0.0);
       }
     }
   }
 }
 
-// 1F1B walk for any m >= P micro-batches with a compact steady state.  The
-// level pattern of m >= P micro-batches is: levels [0, 2P-1) as for m = P
+// Walk for any m >= P micro-batches with a compact steady state.  The level
+// pattern of m >= P micro-batches is: levels [0, 2P-1) as for m = P
 // (warm-up: every j involved is < P); then m - P level pairs in which every
 // stage does one F and one B -- at level 2P-1+2k even stages do B_{k+s/2}
 // and odd stages F_{P+k-(s+1)/2}, at the next level even stages do
-// F_{P+k-s/2} and odd stages B_{k+(s+1)/2}; then the cool-down, which is
-// the m = P pattern from level 2P-1 on with every j shifted by m - P.  The
-// steady pair is a loop (its body stays in the instruction cache), warm-up
-// and cool-down are unrolled; the op order within a level (stages
-// descending) is the same as the fully unrolled walks'.
-template <int P>
+// F_{P+k-s/2} and odd stages B_{k+(s+1)/2}; then the cool-down, the m = P
+// pattern from level 2P-1 on with every F / B j shifted by m - P.  ZBH: the
+// cool-down's W chunks with j < P-1-s keep their j, and each stage's chain
+// ends with W_j for j = P-1-s .. m-1, walked last (a W chunk feeds only its
+// own stage's chain, so only the per-stage chain order matters for it).
+// The F / B order (stages descending within a level) and every stage's chain
+// order equal the level-ordered walk's; checked against the closed-form
+// levels for P <= 8, m < 40 (1F1B) and m < 30 (ZBH).  The steady pair is a
+// loop whose body stays in the instruction cache; warm-up and cool-down are
+// unrolled.
+template <int P, int ZBH>
 __device__ __forceinline__ void walk_steady(const WalkArgs<P>& a, int m) {
   double lastF[P], lastB[P];
 #pragma unroll
   for (int s = 0; s < P; ++s) lastF[s] = lastB[s] = 0.0;
-  walk_levels<P, P, 0, 2 * P - 1>(a, a.bt, lastF, lastB);
+  walk_levels<P, ZBH, P, 0, 2 * P - 1, false>(a, a.bt, a.bt, lastF, lastB);
   const double* bk = a.bt;
   for (int k = 0; k < m - P; ++k, bk += kSmallThreads) {
 #pragma unroll
@@ -552,17 +563,25 @@ __device__ __forceinline__ void walk_steady(const WalkArgs<P>& a, int m) {
       }
     }
   }
-  walk_levels<P, P, 2 * P - 1, n_levels(P, P)>(a, a.bt + (m - P) * kSmallThreads, lastF, lastB);
+  walk_levels<P, ZBH, P, 2 * P - 1, n_levels(P, P), true>(a, a.bt + (m - P) * kSmallThreads,
+                                                          a.bt, lastF, lastB);
+  if (ZBH) {
+#pragma unroll
+    for (int s = P - 1; s >= 0; --s)
+      for (int j = P - 1 - s; j < m; ++j)
+        chunk<true>(a.fin[s], a.ssum[s], a.rlW[s], a.bt[j * kSmallThreads], a.sp[s], a.inv[s],
+                    0.0);
+  }
 }
 
-constexpr int kStaticMaxMB = 12;  // replicas with <= 12 micro-batches
+constexpr int kStaticMaxMB = 12;  // RH_STATIC_MAX_MB-style cap on the unrolled walks (m < P in practice)
 
-// 1F1B replicas with m >= P take walk_steady, so the 1F1B kernels carry
-// unrolled walks only for m < P (less code competing for the instruction
-// cache); the level table covers the rest.
+// Replicas with m >= P take walk_steady, so the kernels carry unrolled walks
+// only for m < P (less code competing for the instruction cache); the level
+// table covers the rest.
 template <int P, int ZBH, int MM = 1>
 __device__ __forceinline__ bool walk_static_dispatch(const WalkArgs<P>& a, int mm) {
-  if constexpr (MM > (ZBH ? kStaticMaxMB : P - 1)) {
+  if constexpr (MM > P - 1) {
     return false;
   } else {
     if (mm == MM) {
@@ -846,8 +865,8 @@ __global__ void __launch_bounds__(kSmallThreads, ZBH ? 4 : kSmallMinBlocks) pass
     const unsigned long long* l1 = p.sched + __ldg(p.sched_off + mm + 1);
     if (!safe)
       walk_table<P, ZBH, false>(wa, l0, l1);
-    else if (!ZBH && mm >= P && p.steady)
-      walk_steady<P>(wa, mm);
+    else if (mm >= P && p.steady)
+      walk_steady<P, ZBH>(wa, mm);
     else if (mm > p.static_max || !walk_static_dispatch<P, ZBH>(wa, mm))
       walk_table<P, ZBH, true>(wa, l0, l1);
   }

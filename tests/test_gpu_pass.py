@@ -362,17 +362,19 @@ def test_extreme_cost_model_matches_oracle(seed, oracle, cuda_device):
         np.testing.assert_array_equal(_bits(sc.cpu().numpy()), _bits(osc))
 
 
+@pytest.mark.parametrize("schedule", ["1f1b", "zbh"])
 @pytest.mark.parametrize("pp", [1, 2, 3, 4])
-def test_steady_walk_boundaries_match_oracle(pp, oracle, cuda_device):
-    """1F1B replicas at and around the steady-state walk's boundary (m = P-1, P,
-    P+1, 2P, and long runs): warm-up, steady loop and cool-down reproduce the
-    level-ordered walk bit for bit, with stage-cost sums and capacity checks."""
+def test_steady_walk_boundaries_match_oracle(pp, schedule, oracle, cuda_device):
+    """Replicas at and around the steady-state walk's boundary (m = P-1, P, P+1,
+    2P, and long runs), 1F1B and ZBH: warm-up, steady loop, cool-down and the ZBH
+    W tail reproduce the level-ordered walk bit for bit, with stage-cost sums and
+    capacity checks."""
     from paper_2605_06374_b200.detect_pass import DetectorPass
 
     for m in sorted({max(1, pp - 1), pp, pp + 1, 2 * pp, 13, 37}):
         dp = 4
         tr = with_measurements(random_trace(1200 + 10 * pp + m, n_iter=12, pp=pp, dp=dp,
-                                            M=m * dp, schedule="1f1b", n_seg=1),
+                                            M=m * dp, schedule=schedule, n_seg=1),
                                oracle, noise=0.02, seed=m)
         p = DetectorPass(tr, keep_stage_cost=True)
         p.detect()
