@@ -1415,20 +1415,26 @@ int enqueue_host_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model*
   RH_CUDA(cudaEventRecord(ctx->chunk_ev[0], stream));
   RH_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->chunk_ev[0], 0));
   cudaStream_t cs = ctx->copy_stream;
+  // the per-iteration index arrays (segment ids, micro-batch offsets or the
+  // packed counts) are small: one copy each up front; only the bulky
+  // device times and documents are chunked (fewer, larger DMA transfers)
+  if ((rc = cp(d_seg, tr->seg, 4 * n, H2D, cs))) return rc;
+  if (pk) {
+    if ((rc = cp(d_idoc, pk->iter_doc, 4 * (n + 1), H2D, cs)) ||
+        (rc = cp(d_cnt, pk->mb_docs, n * M, H2D, cs)))
+      return rc;
+  } else if ((rc = cp(d_off, tr->mb_off, 4 * (n * M + 1), H2D, cs))) {
+    return rc;
+  }
   for (int k = 0; k < n_chunks; ++k) {
     const int64_t i0 = n * k / n_chunks, i1 = n * (k + 1) / n_chunks, ni = i1 - i0;
     const int64_t o0 = pk ? pk->iter_doc[i0] : tr->mb_off[i0 * M];
     const int64_t o1 = pk ? pk->iter_doc[i1] : tr->mb_off[i1 * M];
-    if ((rc = cp(d_seg ? d_seg + i0 : nullptr, tr->seg ? tr->seg + i0 : nullptr, 4 * ni, H2D, cs)) ||
-        (rc = cp(d_dt + i0 * G * T, tr->device_time + i0 * G * T, 4 * ni * G * T, H2D, cs)))
+    if ((rc = cp(d_dt + i0 * G * T, tr->device_time + i0 * G * T, 4 * ni * G * T, H2D, cs)))
       return rc;
     if (pk) {
-      if ((rc = cp(d_idoc + i0, pk->iter_doc + i0, 4 * (ni + 1), H2D, cs)) ||
-          (rc = cp(d_cnt + i0 * M, pk->mb_docs + i0 * M, ni * M, H2D, cs)) ||
-          (rc = cp(d_doc16 + o0, pk->doc_len + o0, 2 * (o1 - o0), H2D, cs)))
-        return rc;
-    } else if ((rc = cp(d_off + i0 * M, tr->mb_off + i0 * M, 4 * (ni * M + 1), H2D, cs)) ||
-               (rc = cp(d_doc + o0, tr->doc_len + o0, 4 * (o1 - o0), H2D, cs))) {
+      if ((rc = cp(d_doc16 + o0, pk->doc_len + o0, 2 * (o1 - o0), H2D, cs))) return rc;
+    } else if ((rc = cp(d_doc + o0, tr->doc_len + o0, 4 * (o1 - o0), H2D, cs))) {
       return rc;
     }
     RH_CUDA(cudaEventRecord(ctx->chunk_ev[k], cs));
