@@ -293,7 +293,10 @@ __global__ void __launch_bounds__(MAXT) pass_kernel(const PassParams p) {
 //
 // Division by a stage speed: exact hoisted-reciprocal form (div_fast) after a
 // once-per-replica operand-range check (wavefront.cuh).
-constexpr int kSmallThreads = 128;
+#ifndef RH_SMALL_THREADS
+#define RH_SMALL_THREADS 128
+#endif
+constexpr int kSmallThreads = RH_SMALL_THREADS;
 #ifndef RH_SMALL_MIN_BLOCKS
 #define RH_SMALL_MIN_BLOCKS 5
 #endif
@@ -1140,7 +1143,7 @@ int launch_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
     // the region holds the staged documents (+16 B for the TMA alignment
     // shift), later the base costs
     const size_t region =
-        std::max<size_t>(16 * 1024 + 16, (size_t)kSmallThreads * p.mmax * 8);
+        std::max<size_t>(128 * (size_t)kSmallThreads + 16, (size_t)kSmallThreads * p.mmax * 8);
     p.doc_stage = (int)((region - 16) / 4);
 #ifdef RH_STATIC_MAX_MB
     p.static_max = RH_STATIC_MAX_MB;  // A/B builds: 0 = always the level-table walk
