@@ -301,6 +301,9 @@ constexpr int kSmallThreads = RH_SMALL_THREADS;
 #define RH_SMALL_MIN_BLOCKS 5
 #endif
 constexpr int kSmallMinBlocks = RH_SMALL_MIN_BLOCKS;  // CTAs per SM the register budget targets
+// narrow CTA width, used when dp <= kSmallNarrow (min blocks scale up to keep
+// the per-thread register budget of the wide kernel)
+constexpr int kSmallNarrow = kSmallThreads / 2;
 
 // ---- TMA bulk staging (cp.async.bulk + mbarrier, sm_90+ / sm_100a)
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -389,9 +392,10 @@ __device__ __forceinline__ void stage_edges(const StagePlan& sp, const int32_t* 
 enum : unsigned { kOpF = 1, kOpB = 2, kOpW = 3 };
 
 // Register state of one replica's walk (references into the kernel's arrays).
-template <int P>
+template <int P, int TW>
 struct WalkArgs {
-  const double* bt;  // base costs of this thread: bt[j * kSmallThreads]
+  static constexpr int kStride = TW;  // CTA width: base costs live [j][thread]
+  const double* bt;  // base costs of this thread: bt[j * kStride]
   const double (&rlF)[P];
   const double (&rlB)[P];
   const double (&rlW)[P];
@@ -420,8 +424,8 @@ __device__ __forceinline__ double chunk(double& fin, double& ssum, double rl, do
 
 // Dynamic walk over the level table: one 64-bit word per level, 16 bits per
 // stage (0 idle, else kind | j << 2); stages in descending order.
-template <int P, int ZBH, bool SAFE>
-__device__ __forceinline__ void walk_table(const WalkArgs<P>& a, const unsigned long long* lv,
+template <int P, int ZBH, bool SAFE, class WA>
+__device__ __forceinline__ void walk_table(const WA& a, const unsigned long long* lv,
                                            const unsigned long long* lv_end) {
   double lastF[P], lastB[P];
 #pragma unroll
@@ -438,7 +442,7 @@ __device__ __forceinline__ void walk_table(const WalkArgs<P>& a, const unsigned 
       const double dB = s < P - 1 ? __dadd_rn(lastB[s < P - 1 ? s + 1 : 0], a.hb[s]) : 0.0;
       const double nf = chunk<SAFE>(a.fin[s], a.ssum[s],
                                    isF ? a.rlF[s] : (isB || !ZBH ? a.rlB[s] : a.rlW[s]),
-                                   a.bt[(code >> 2) * kSmallThreads], a.sp[s], a.inv[s],
+                                   a.bt[(code >> 2) * WA::kStride], a.sp[s], a.inv[s],
                                    isF ? dF : (isB ? dB : 0.0));
       lastF[s] = isF ? nf : lastF[s];
       lastB[s] = isB ? nf : lastB[s];
@@ -459,8 +463,8 @@ __host__ __device__ constexpr int n_levels(int P, int MM) { return 2 * P + 3 * M
 
 // Fully unrolled walk for a compile-time micro-batch count: every op, its
 // kind and j are constants, so a chunk is ~8 instructions with no dispatch.
-template <int P, int ZBH, int MM>
-__device__ __forceinline__ void walk_static(const WalkArgs<P>& a) {
+template <int P, int ZBH, int MM, class WA>
+__device__ __forceinline__ void walk_static(const WA& a) {
   double lastF[P], lastB[P];
 #pragma unroll
   for (int s = 0; s < P; ++s) lastF[s] = lastB[s] = 0.0;
@@ -473,14 +477,14 @@ __device__ __forceinline__ void walk_static(const WalkArgs<P>& a) {
       const int kind = op_at(P, MM, ZBH, t, s, j);
       if (kind == kOpF) {
         const double dep = s > 0 ? __dadd_rn(lastF[s > 0 ? s - 1 : 0], a.hf[s]) : 0.0;
-        lastF[s] = chunk<true>(a.fin[s], a.ssum[s], a.rlF[s], a.bt[j * kSmallThreads], a.sp[s],
+        lastF[s] = chunk<true>(a.fin[s], a.ssum[s], a.rlF[s], a.bt[j * WA::kStride], a.sp[s],
                          a.inv[s], dep);
       } else if (kind == kOpB) {
         const double dep = s < P - 1 ? __dadd_rn(lastB[s < P - 1 ? s + 1 : 0], a.hb[s]) : 0.0;
-        lastB[s] = chunk<true>(a.fin[s], a.ssum[s], a.rlB[s], a.bt[j * kSmallThreads], a.sp[s],
+        lastB[s] = chunk<true>(a.fin[s], a.ssum[s], a.rlB[s], a.bt[j * WA::kStride], a.sp[s],
                          a.inv[s], dep);
       } else if (kind == kOpW) {
-        chunk<true>(a.fin[s], a.ssum[s], a.rlW[s], a.bt[j * kSmallThreads], a.sp[s], a.inv[s],
+        chunk<true>(a.fin[s], a.ssum[s], a.rlW[s], a.bt[j * WA::kStride], a.sp[s], a.inv[s],
                     0.0);
       }
     }
@@ -488,12 +492,12 @@ __device__ __forceinline__ void walk_static(const WalkArgs<P>& a) {
 }
 
 // Levels [T0, T1) of the MM-micro-batch walk, with the chain state passed in:
-// F / B chunks read micro-batch j at bt_fb[j * kSmallThreads], W chunks (ZBH)
-// at bt_w[j * kSmallThreads] (callers shift the pointers to re-base j); with
+// F / B chunks read micro-batch j at bt_fb[j * WA::kStride], W chunks (ZBH)
+// at bt_w[j * WA::kStride] (callers shift the pointers to re-base j); with
 // COOL the W chunks of the chain's tail (j >= P-1-s) are left to the caller.
 // Everything folds to constants as in walk_static.
-template <int P, int ZBH, int MM, int T0, int T1, bool COOL>
-__device__ __forceinline__ void walk_levels(const WalkArgs<P>& a, const double* bt_fb,
+template <int P, int ZBH, int MM, int T0, int T1, bool COOL, class WA>
+__device__ __forceinline__ void walk_levels(const WA& a, const double* bt_fb,
                                             const double* bt_w, double (&lastF)[P],
                                             double (&lastB)[P]) {
 #pragma unroll
@@ -504,14 +508,14 @@ __device__ __forceinline__ void walk_levels(const WalkArgs<P>& a, const double* 
       const int kind = op_at(P, MM, ZBH, t, s, j);
       if (kind == kOpF) {
         const double dep = s > 0 ? __dadd_rn(lastF[s > 0 ? s - 1 : 0], a.hf[s]) : 0.0;
-        lastF[s] = chunk<true>(a.fin[s], a.ssum[s], a.rlF[s], bt_fb[j * kSmallThreads], a.sp[s],
+        lastF[s] = chunk<true>(a.fin[s], a.ssum[s], a.rlF[s], bt_fb[j * WA::kStride], a.sp[s],
                                a.inv[s], dep);
       } else if (kind == kOpB) {
         const double dep = s < P - 1 ? __dadd_rn(lastB[s < P - 1 ? s + 1 : 0], a.hb[s]) : 0.0;
-        lastB[s] = chunk<true>(a.fin[s], a.ssum[s], a.rlB[s], bt_fb[j * kSmallThreads], a.sp[s],
+        lastB[s] = chunk<true>(a.fin[s], a.ssum[s], a.rlB[s], bt_fb[j * WA::kStride], a.sp[s],
                                a.inv[s], dep);
       } else if (kind == kOpW && !(COOL && j >= P - 1 - s)) {
-        chunk<true>(a.fin[s], a.ssum[s], a.rlW[s], bt_w[j * kSmallThreads], a.sp[s], a.inv[s],
+        chunk<true>(a.fin[s], a.ssum[s], a.rlW[s], bt_w[j * WA::kStride], a.sp[s], a.inv[s],
                     0.0);
       }
     }
@@ -533,46 +537,46 @@ __device__ __forceinline__ void walk_levels(const WalkArgs<P>& a, const double* 
 // levels for P <= 8, m < 40 (1F1B) and m < 30 (ZBH).  The steady pair is a
 // loop whose body stays in the instruction cache; warm-up and cool-down are
 // unrolled.
-template <int P, int ZBH>
-__device__ __forceinline__ void walk_steady(const WalkArgs<P>& a, int m) {
+template <int P, int ZBH, class WA>
+__device__ __forceinline__ void walk_steady(const WA& a, int m) {
   double lastF[P], lastB[P];
 #pragma unroll
   for (int s = 0; s < P; ++s) lastF[s] = lastB[s] = 0.0;
   walk_levels<P, ZBH, P, 0, 2 * P - 1, false>(a, a.bt, a.bt, lastF, lastB);
   const double* bk = a.bt;
-  for (int k = 0; k < m - P; ++k, bk += kSmallThreads) {
+  for (int k = 0; k < m - P; ++k, bk += WA::kStride) {
 #pragma unroll
     for (int s = P - 1; s >= 0; --s) {  // level 2P-1+2k
       if (s % 2 == 0) {
         const double dep = s < P - 1 ? __dadd_rn(lastB[s < P - 1 ? s + 1 : 0], a.hb[s]) : 0.0;
-        lastB[s] = chunk<true>(a.fin[s], a.ssum[s], a.rlB[s], bk[(s / 2) * kSmallThreads],
+        lastB[s] = chunk<true>(a.fin[s], a.ssum[s], a.rlB[s], bk[(s / 2) * WA::kStride],
                                a.sp[s], a.inv[s], dep);
       } else {
         const double dep = __dadd_rn(lastF[s > 0 ? s - 1 : 0], a.hf[s]);
         lastF[s] = chunk<true>(a.fin[s], a.ssum[s], a.rlF[s],
-                               bk[(P - (s + 1) / 2) * kSmallThreads], a.sp[s], a.inv[s], dep);
+                               bk[(P - (s + 1) / 2) * WA::kStride], a.sp[s], a.inv[s], dep);
       }
     }
 #pragma unroll
     for (int s = P - 1; s >= 0; --s) {  // level 2P+2k
       if (s % 2 == 0) {
         const double dep = s > 0 ? __dadd_rn(lastF[s > 0 ? s - 1 : 0], a.hf[s]) : 0.0;
-        lastF[s] = chunk<true>(a.fin[s], a.ssum[s], a.rlF[s], bk[(P - s / 2) * kSmallThreads],
+        lastF[s] = chunk<true>(a.fin[s], a.ssum[s], a.rlF[s], bk[(P - s / 2) * WA::kStride],
                                a.sp[s], a.inv[s], dep);
       } else {
         const double dep = s < P - 1 ? __dadd_rn(lastB[s < P - 1 ? s + 1 : 0], a.hb[s]) : 0.0;
         lastB[s] = chunk<true>(a.fin[s], a.ssum[s], a.rlB[s],
-                               bk[((s + 1) / 2) * kSmallThreads], a.sp[s], a.inv[s], dep);
+                               bk[((s + 1) / 2) * WA::kStride], a.sp[s], a.inv[s], dep);
       }
     }
   }
-  walk_levels<P, ZBH, P, 2 * P - 1, n_levels(P, P), true>(a, a.bt + (m - P) * kSmallThreads,
+  walk_levels<P, ZBH, P, 2 * P - 1, n_levels(P, P), true>(a, a.bt + (m - P) * WA::kStride,
                                                           a.bt, lastF, lastB);
   if (ZBH) {
 #pragma unroll
     for (int s = P - 1; s >= 0; --s)
       for (int j = P - 1 - s; j < m; ++j)
-        chunk<true>(a.fin[s], a.ssum[s], a.rlW[s], a.bt[j * kSmallThreads], a.sp[s], a.inv[s],
+        chunk<true>(a.fin[s], a.ssum[s], a.rlW[s], a.bt[j * WA::kStride], a.sp[s], a.inv[s],
                     0.0);
   }
 }
@@ -582,8 +586,8 @@ constexpr int kStaticMaxMB = 12;  // RH_STATIC_MAX_MB-style cap on the unrolled 
 // Replicas with m >= P take walk_steady, so the kernels carry unrolled walks
 // only for m < P (less code competing for the instruction cache); the level
 // table covers the rest.
-template <int P, int ZBH, int MM = 1>
-__device__ __forceinline__ bool walk_static_dispatch(const WalkArgs<P>& a, int mm) {
+template <int P, int ZBH, int MM = 1, class WA>
+__device__ __forceinline__ bool walk_static_dispatch(const WA& a, int mm) {
   if constexpr (MM > P - 1) {
     return false;
   } else {
@@ -717,8 +721,8 @@ __device__ __forceinline__ void dmark(int k) {
 #define RH_DMARK(k) ((void)0)
 #endif
 
-template <int P, int ZBH, int DETECT>
-__global__ void __launch_bounds__(kSmallThreads, ZBH ? 4 : kSmallMinBlocks) pass_small_kernel(const PassParams p) {
+template <int P, int ZBH, int DETECT, int TW>
+__global__ void __launch_bounds__(TW, (ZBH ? 4 : kSmallMinBlocks) * (kSmallThreads / TW)) pass_small_kernel(const PassParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x;
   const int D = p.sh.dp, M = p.sh.micro_batches, T = p.sh.tp;
@@ -817,7 +821,7 @@ __global__ void __launch_bounds__(kSmallThreads, ZBH ? 4 : kSmallMinBlocks) pass
     int j = d % md;
     for (int k = 0; k < md; ++k, j = j + 1 == md ? 0 : j + 1) {
       const double b = __dadd_rn(lin, __dmul_rn(p.m.beta, (double)(long long)q[j]));
-      base_t[j * kSmallThreads + tid] = b;
+      base_t[j * TW + tid] = b;
       if (!all_unit) {
         b_hi = fmax(b_hi, b);
         if (b > 0.0) b_lo = fmin(b_lo, b);
@@ -861,7 +865,7 @@ __global__ void __launch_bounds__(kSmallThreads, ZBH ? 4 : kSmallMinBlocks) pass
     }
     safe = safe && div_range_ok(r_lo * b_lo, r_hi * b_hi);
   }
-  WalkArgs<P> wa{bt, rlF, rlB, rlW, sp, inv, hf, hb, fin, ssum};
+  WalkArgs<P, TW> wa{bt, rlF, rlB, rlW, sp, inv, hf, hb, fin, ssum};
   RH_DMARK(3);
   if (mm > 0) {
     const unsigned long long* l0 = p.sched + __ldg(p.sched_off + mm);
@@ -1072,14 +1076,20 @@ static int lane_table(rh_ctx* ctx, int P, int zbh, int mmax, const uint16_t** co
   return RH_OK;
 }
 
-template <int ZBH, int DETECT>
-static void* small_kernel(int P) {
+template <int ZBH, int DETECT, int TW>
+static void* small_kernel_w(int P) {
   switch (P) {
-    case 1: return (void*)pass_small_kernel<1, ZBH, DETECT>;
-    case 2: return (void*)pass_small_kernel<2, ZBH, DETECT>;
-    case 3: return (void*)pass_small_kernel<3, ZBH, DETECT>;
-    default: return (void*)pass_small_kernel<4, ZBH, DETECT>;
+    case 1: return (void*)pass_small_kernel<1, ZBH, DETECT, TW>;
+    case 2: return (void*)pass_small_kernel<2, ZBH, DETECT, TW>;
+    case 3: return (void*)pass_small_kernel<3, ZBH, DETECT, TW>;
+    default: return (void*)pass_small_kernel<4, ZBH, DETECT, TW>;
   }
+}
+
+template <int ZBH, int DETECT>
+static void* small_kernel(int P, int tw) {
+  return tw == kSmallNarrow ? small_kernel_w<ZBH, DETECT, kSmallNarrow>(P)
+                            : small_kernel_w<ZBH, DETECT, kSmallThreads>(P);
 }
 
 static int next_pow2(int x) {
@@ -1132,7 +1142,10 @@ int launch_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
   p.vec4 = (sh->tp % 4 == 0) && ((reinterpret_cast<uintptr_t>(tr->device_time) & 15) == 0);
   if (P <= 4 && D <= kSmallThreads && p.mmax < 16384 && !getenv("RH_FORCE_LANE_KERNEL")) {
     // thread-per-replica kernel for short pipelines
-    p.ipb = std::max(1, kSmallThreads / D);
+    // narrow CTAs when a replica set fits: twice the CTAs per SM at the same
+    // register budget, so more of them overlap their setup latency
+    const int tw = (D <= kSmallNarrow && !getenv("RH_SMALL_WIDE")) ? kSmallNarrow : kSmallThreads;
+    p.ipb = std::max(1, tw / D);
     const int threads = p.ipb * D;
     // j is stored in 14 bits of a level word
     const int it_bytes = ((p.ipb * 12 + 15) / 16) * 16;
@@ -1143,7 +1156,7 @@ int launch_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
     // the region holds the staged documents (+16 B for the TMA alignment
     // shift), later the base costs
     const size_t region =
-        std::max<size_t>(128 * (size_t)kSmallThreads + 16, (size_t)kSmallThreads * p.mmax * 8);
+        std::max<size_t>(128 * (size_t)tw + 16, (size_t)tw * p.mmax * 8);
     p.doc_stage = (int)((region - 16) / 4);
 #ifdef RH_STATIC_MAX_MB
     p.static_max = RH_STATIC_MAX_MB;  // A/B builds: 0 = always the level-table walk
@@ -1158,8 +1171,8 @@ int launch_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
       if (int e = sched_table(ctx, P, zbh, p.mmax, &p.sched, &p.sched_off, &p.sched_peak))
         return e;
       const int64_t blocks = (tr->n_iter + p.ipb - 1) / p.ipb;
-      void* kern = zbh ? (detect ? small_kernel<1, 1>(P) : small_kernel<1, 0>(P))
-                       : (detect ? small_kernel<0, 1>(P) : small_kernel<0, 0>(P));
+      void* kern = zbh ? (detect ? small_kernel<1, 1>(P, tw) : small_kernel<1, 0>(P, tw))
+                       : (detect ? small_kernel<0, 1>(P, tw) : small_kernel<0, 0>(P, tw));
       if (int e = ensure_smem(kern, smem)) return e;
       {
         int occ = 0;
