@@ -389,3 +389,29 @@ def test_steady_walk_boundaries_match_oracle(pp, schedule, oracle, cuda_device):
             oms2, ost2, _ = oracle.pipeline(tr, view="actual", capacity=cap)
             np.testing.assert_array_equal(st.cpu().numpy(), ost2)
             np.testing.assert_array_equal(_bits(ms.cpu().numpy()), _bits(oms2))
+
+
+@pytest.mark.parametrize("dp", [3, 16, 48, 64])
+def test_cta_width_variants_match_oracle(dp, oracle, cuda_device, monkeypatch):
+    """The thread-per-replica kernel runs 64-thread CTAs for dp <= 64 and
+    128-thread CTAs otherwise (`RH_SMALL_WIDE=1` forces 128). Both widths must
+    give the oracle's bits: dp = 48 leaves a 64-wide CTA partly empty (one
+    iteration of 48 replicas), dp = 3 packs 21 iterations per CTA."""
+    from paper_2605_06374_b200.detect_pass import DetectorPass
+
+    tr = with_measurements(random_trace(900 + dp, n_iter=150, dp=dp, pp=4, schedule="1f1b",
+                                        M=2 * dp + 1), oracle, noise=0.02, seed=dp)
+    oms, ost, osc, ofl, osv = oracle.detect(tr)
+    for wide in (False, True):
+        if wide:
+            monkeypatch.setenv("RH_SMALL_WIDE", "1")
+        else:
+            monkeypatch.delenv("RH_SMALL_WIDE", raising=False)
+        p = DetectorPass(tr, keep_stage_cost=True)
+        p.detect()
+        r = p.results()
+        np.testing.assert_array_equal(r["status"], ost)
+        np.testing.assert_array_equal(_bits(r["makespan"]), _bits(oms))
+        np.testing.assert_array_equal(_bits(r["stage_cost"]), _bits(osc))
+        np.testing.assert_array_equal(r["stage_flag"], ofl)
+        np.testing.assert_array_equal(r["severity"].view(np.uint32), osv.view(np.uint32))
