@@ -40,9 +40,15 @@
 namespace rh {
 
 constexpr int kScanThreads = 128;  // reset_scan_kernel block (= bres granularity)
-constexpr int kScreenThreads = 512;
+#ifndef RH_SCREEN_THREADS
+#define RH_SCREEN_THREADS 512
+#endif
+#ifndef RH_SCREEN_BPS
+#define RH_SCREEN_BPS 2
+#endif
+constexpr int kScreenThreads = RH_SCREEN_THREADS;  // A/B builds may override both
 constexpr int kScreenWarps = kScreenThreads / 32;
-constexpr int kScreenBlocksPerSm = 2;
+constexpr int kScreenBlocksPerSm = RH_SCREEN_BPS;
 constexpr int kMaxWindow = 64;
 
 struct ScreenArgs {
