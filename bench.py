@@ -124,18 +124,24 @@ def dist_init():
 
 
 def build_trace(rank: int, n_iter: int, use_oracle: bool):
+    """The C2 trace.  use_oracle (the reference arm): documents packed by the
+    oracle's literal FFD and measurements from the oracle's DAG, so that
+    process never loads the product library (checked by
+    tests/test_bench_contract.py)."""
     from paper_2605_06374_b200.scenarios import c2_trace
 
-    tr = c2_trace(n_iter, seed=rank)
     if use_oracle:
         from tests.oracle_bind import Oracle
 
-        ms, st, sc = Oracle().pipeline(tr, view="actual")
+        o = Oracle()
+        tr = c2_trace(n_iter, seed=rank, packer=o.pack_sequences)
+        ms, st, sc = o.pipeline(tr, view="actual")
         tr.attach_measurements(sc, ms, seed=rank)
-    else:
-        from paper_2605_06374_b200.detect_pass import synthesize_measurements
+        return tr
+    from paper_2605_06374_b200.detect_pass import synthesize_measurements
 
-        synthesize_measurements(tr, seed=rank)
+    tr = c2_trace(n_iter, seed=rank)
+    synthesize_measurements(tr, seed=rank)
     return tr
 
 

@@ -17,6 +17,25 @@
  *     functions are asynchronous on that stream unless documented otherwise;
  *   - arithmetic on every decision-carrying quantity is IEEE fp64 with the
  *     reference's evaluation order and no FMA contraction.
+ *
+ * Threading contract
+ *   - An rh_ctx belongs to one device; every entry point makes that device
+ *     current for the call and restores the caller's current device.
+ *   - A context may be used from several host threads.  Scratch memory is
+ *     per (context, stream): calls on distinct streams never share scratch,
+ *     so they may run concurrently; calls on one stream are stream-ordered.
+ *     Scratch only grows; a grown buffer is retired (not freed) until
+ *     rh_ctx_destroy, so work already queued never sees freed memory, and
+ *     growth is refused (RH_E_INVALID) inside a stream capture — run a call
+ *     once outside the capture before capturing it.
+ *   - rh_screen_prepare / rh_screen: one pending prepare per context (the
+ *     next rh_screen with the same arguments consumes it).
+ *   - An rh_search handle may be evaluated from several streams: each eval
+ *     waits for the handle's previous create / eval.  No call ever
+ *     synchronises the device, and the device's default memory pool is not
+ *     modified (searches allocate from a private pool).
+ *   - rh_detector_pass_host*: synchronous; the context replays one captured
+ *     graph per argument key (serialise calls that share a context).
  */
 #ifndef RESIHP_B200_H
 #define RESIHP_B200_H

@@ -24,6 +24,66 @@ int64_t orc_quad_load(int32_t n_docs, const int32_t* docs) {
   return q;
 }
 
+static int cmp_desc_i32(const void* a, const void* b) {
+  const int32_t x = *(const int32_t*)a, y = *(const int32_t*)b;
+  return (x < y) - (x > y);
+}
+
+/* workload.py:52-80
+ *   for l in sorted(lengths, reverse=True):
+ *       for i, space in enumerate(remaining):
+ *           if l <= space: bins[i].append(l); remaining[i] -= l; break
+ *       else: bins.append([l]); remaining.append(token_budget - l)
+ *   padding document = residual space, when > 0                            */
+int orc_pack_sequences(int64_t n_docs, const int32_t* lengths, int32_t budget, int64_t max_bins,
+                       int32_t* mb_off, int32_t* doc_len, int64_t* n_bins, int64_t* n_entries) {
+  int32_t* v = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n_docs > 0 ? n_docs : 1));
+  int64_t* rem = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n_docs > 0 ? n_docs : 1));
+  int64_t* bin_of = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n_docs > 0 ? n_docs : 1));
+  int64_t nb = 0, i, b;
+  for (i = 0; i < n_docs; ++i) {
+    if (lengths[i] <= 0 || lengths[i] > budget) {
+      free(v);
+      free(rem);
+      free(bin_of);
+      return -1;
+    }
+    v[i] = lengths[i];
+  }
+  qsort(v, (size_t)n_docs, sizeof(int32_t), cmp_desc_i32);
+  for (i = 0; i < n_docs; ++i) {
+    for (b = 0; b < nb; ++b)
+      if (v[i] <= rem[b]) break;
+    if (b == nb) rem[nb++] = budget;
+    rem[b] -= v[i];
+    bin_of[i] = b;
+  }
+  const int64_t keep = (max_bins >= 0 && max_bins < nb) ? max_bins : nb;
+  /* documents of bin b in insertion order (= the sorted order), then padding */
+  int64_t* start = (int64_t*)calloc((size_t)(nb + 1), sizeof(int64_t));
+  for (i = 0; i < n_docs; ++i) ++start[bin_of[i] + 1];
+  for (b = 0; b < nb; ++b) start[b + 1] += start[b] + (rem[b] > 0 ? 1 : 0);
+  if (doc_len) {
+    int64_t* fill = (int64_t*)malloc(sizeof(int64_t) * (size_t)(nb > 0 ? nb : 1));
+    for (b = 0; b < nb; ++b) fill[b] = start[b];
+    for (i = 0; i < n_docs; ++i)
+      if (bin_of[i] < keep) doc_len[fill[bin_of[i]]++] = v[i];
+    for (b = 0; b < keep; ++b)
+      if (rem[b] > 0) doc_len[fill[b]] = (int32_t)rem[b];
+    free(fill);
+  }
+  if (mb_off)
+    for (b = 0; b <= keep; ++b) mb_off[b] = (int32_t)start[b];
+  const int64_t e = start[keep];
+  free(start);
+  *n_bins = keep;
+  *n_entries = e;
+  free(v);
+  free(rem);
+  free(bin_of);
+  return 0;
+}
+
 /* workload.py:46-49  ratio(BW) = B + W */
 static double ratio_of(const rh_cost_model* m, int kind) {
   switch (kind) {

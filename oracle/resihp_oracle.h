@@ -26,6 +26,13 @@ extern "C" {
 
 /* workload.py:83-85 */
 int64_t orc_quad_load(int32_t n_docs, const int32_t* docs);
+/* workload.py:52-80 pack_sequences, literally (sort descending, first fit by
+ * scanning the bins in creation order, residual appended as padding), keeping
+ * the first max_bins bins (harness.py:251-252; max_bins < 0 = all).  Same
+ * contract as rh_pack_sequences: mb_off / doc_len may be NULL to size the
+ * output.  Returns -1 for a length <= 0 or > budget. */
+int orc_pack_sequences(int64_t n_docs, const int32_t* lengths, int32_t budget, int64_t max_bins,
+                       int32_t* mb_off, int32_t* doc_len, int64_t* n_bins, int64_t* n_entries);
 /* workload.py:88-98; kind 0=F 1=B 2=W 3=BW.  Returns 0 and sets *bad when
  * speed <= 0 (the reference raises ValueError). */
 double orc_chunk_time(const rh_cost_model* m, int kind, int64_t quad,

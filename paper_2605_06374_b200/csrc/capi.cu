@@ -22,34 +22,52 @@ void set_error(const char* fmt, ...) {
   va_end(ap);
 }
 
-int workspace(rh_ctx* ctx, size_t bytes, void** out, int slot) {
-  if (bytes > ctx->ws_bytes[slot]) {
-    if (ctx->ws[slot]) {
-      RH_CUDA(cudaDeviceSynchronize());
-      RH_CUDA(cudaFree(ctx->ws[slot]));
-      ctx->ws[slot] = nullptr;
-      ctx->ws_bytes[slot] = 0;
-    }
-    size_t want = bytes + bytes / 4 + (1u << 20);
-    cudaError_t e = cudaMalloc(&ctx->ws[slot], want);
-    if (e != cudaSuccess) {
-      set_error("workspace of %zu bytes: %s", want, cudaGetErrorString(e));
-      return RH_E_NOMEM;
-    }
-    ctx->ws_bytes[slot] = want;
+int workspace(rh_ctx* ctx, size_t bytes, void** out, int slot, cudaStream_t stream, bool zero) {
+  std::lock_guard<std::mutex> lock(ctx->ws_mu);
+  rh_ctx::Workspace* w = nullptr;
+  for (auto& x : ctx->ws)
+    if (x.slot == slot && x.stream == stream) w = &x;
+  if (w && w->bytes >= bytes) {
+    *out = w->p;
+    return RH_OK;
   }
-  *out = ctx->ws[slot];
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  RH_CUDA(cudaStreamIsCapturing(stream, &cap));
+  if (cap != cudaStreamCaptureStatusNone) {
+    set_error("workspace growth to %zu bytes inside a stream capture: run the call once "
+              "outside the capture first", bytes);
+    return RH_E_INVALID;
+  }
+  const size_t want = bytes + bytes / 4 + (1u << 20);
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, want);
+  if (e != cudaSuccess) {
+    set_error("workspace of %zu bytes: %s", want, cudaGetErrorString(e));
+    return RH_E_NOMEM;
+  }
+  if (zero) RH_CUDA(cudaMemsetAsync(p, 0, want, stream));
+  if (w) {  // queued work or a captured graph may still use the old buffer
+    ctx->ws_retired.push_back(w->p);
+    w->p = p;
+    w->bytes = want;
+  } else {
+    ctx->ws.push_back({slot, stream, p, want});
+  }
+  ++ctx->ws_epoch;
+  *out = p;
   return RH_OK;
 }
 
-int ensure_smem(const void* kernel, size_t bytes) {
+int ensure_smem(const rh_ctx* ctx, const void* kernel, size_t bytes) {
   static std::mutex mu;
-  static std::unordered_map<const void*, size_t> granted;
+  static std::unordered_map<const void*, size_t> granted[64];  // per device ordinal
+  if (bytes <= 48 * 1024) return RH_OK;  // the default limit
   std::lock_guard<std::mutex> lock(mu);
-  auto it = granted.find(kernel);
-  if (it != granted.end() && it->second >= bytes) return RH_OK;
+  auto& g = granted[ctx->device & 63];
+  auto it = g.find(kernel);
+  if (it != g.end() && it->second >= bytes) return RH_OK;
   RH_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-  granted[kernel] = bytes;
+  g[kernel] = bytes;
   return RH_OK;
 }
 
@@ -165,6 +183,7 @@ int rh_selftest_division(rh_ctx* ctx, int64_t n, uint64_t seed, int64_t* mismatc
     set_error("rh_selftest_division: invalid arguments");
     return RH_E_INVALID;
   }
+  DeviceGuard guard(ctx);
   unsigned long long* d = nullptr;
   RH_CUDA(cudaMalloc(&d, sizeof(unsigned long long)));
   RH_CUDA(cudaMemset(d, 0, sizeof(unsigned long long)));
@@ -193,7 +212,7 @@ int rh_ctx_create(int device, rh_ctx** out) {
     set_error("rh_ctx_create: device %d out of range (%d devices)", device, n);
     return RH_E_INVALID;
   }
-  RH_CUDA(cudaSetDevice(device));
+  // the caller's current device is left as it was
   cudaDeviceProp prop;
   RH_CUDA(cudaGetDeviceProperties(&prop, device));
   if (prop.major != 10) {
@@ -211,8 +230,11 @@ int rh_ctx_create(int device, rh_ctx** out) {
 
 int rh_ctx_destroy(rh_ctx* ctx) {
   if (!ctx) return RH_OK;
-  for (void* w : ctx->ws)
-    if (w) cudaFree(w);
+  DeviceGuard guard(ctx);
+  cudaDeviceSynchronize();  // nothing queued may still use the context's memory
+  for (auto& w : ctx->ws)
+    if (w.p) cudaFree(w.p);
+  for (void* p : ctx->ws_retired) cudaFree(p);
   for (cudaEvent_t e : ctx->chunk_ev)
     if (e) cudaEventDestroy(e);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
@@ -222,12 +244,12 @@ int rh_ctx_destroy(rh_ctx* ctx) {
   if (ctx->prep.done) cudaEventDestroy(ctx->prep.done);
   if (ctx->prep.consumed) cudaEventDestroy(ctx->prep.consumed);
   if (ctx->host_graph.exec) cudaGraphExecDestroy(ctx->host_graph.exec);
-  if (ctx->screen_ctrl) cudaFree(ctx->screen_ctrl);
   for (int q = 0; q < rh_ctx::kAuxStreams; ++q) {
     if (ctx->aux_stream[q]) cudaStreamDestroy(ctx->aux_stream[q]);
     if (ctx->aux_ev[q]) cudaEventDestroy(ctx->aux_ev[q]);
   }
   if (ctx->aux_fork) cudaEventDestroy(ctx->aux_fork);
+  if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
   delete ctx;
   return RH_OK;
 }
@@ -241,6 +263,7 @@ int rh_quad_load(rh_ctx* ctx, int64_t n_mb, const int32_t* mb_off,
     return RH_E_INVALID;
   }
   if (n_mb == 0) return RH_OK;
+  DeviceGuard guard(ctx);
   int th = 256;
   quad_load_kernel<<<(unsigned)((n_mb + th - 1) / th), th, 0, as_stream(stream)>>>(
       n_mb, mb_off, doc_len, quad_out);
@@ -257,6 +280,7 @@ int rh_chunk_time(rh_ctx* ctx, const rh_cost_model* model, int64_t n,
     return RH_E_INVALID;
   }
   if (n == 0) return RH_OK;
+  DeviceGuard guard(ctx);
   int th = 256;
   chunk_time_kernel<<<(unsigned)((n + th - 1) / th), th, 0, as_stream(stream)>>>(
       *model, n, quad, budget, kind, layers, speed, t_out, bad_out);
@@ -271,6 +295,7 @@ int rh_validate(rh_ctx* ctx, int64_t n, const double* measured, const double* ex
     return RH_E_INVALID;
   }
   if (n == 0) return RH_OK;
+  DeviceGuard guard(ctx);
   int th = 256;
   validate_kernel<<<(unsigned)((n + th - 1) / th), th, 0, as_stream(stream)>>>(
       n, measured, expected, threshold, flag, severity);

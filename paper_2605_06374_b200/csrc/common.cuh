@@ -18,11 +18,28 @@ struct rh_ctx {
   int num_sms = 148;
   size_t smem_optin = 0;
   std::atomic<int64_t> launches{0};
-  // grow-only device workspaces: slot 0 = host-buffer staging,
-  // slot 1 = kernel scratch (screen, general DAG), slot 2 = rh_screen_prepare
-  // results (reset indices, round-0 verdicts); never aliased
-  void* ws[3] = {nullptr, nullptr, nullptr};
-  size_t ws_bytes[3] = {0, 0, 0};
+  // grow-only device workspaces, one per (slot, stream) so calls on distinct
+  // streams never share scratch: slot 0 = host-buffer staging, slot 1 =
+  // kernel scratch (screen kept-state, general DAG), slot 2 = rh_screen_prepare
+  // results (reset indices, round-0 verdicts), slot 3 = the screen's
+  // cooperative-kernel control words (zeroed on allocation; kernels leave
+  // them zero).  A grown buffer is retired, never freed on the call path
+  // (work still queued or a captured graph may reference it); retired
+  // buffers are freed by rh_ctx_destroy.  ws_epoch counts reallocations and
+  // is part of the host-pass graph key.
+  struct Workspace {
+    int slot;
+    cudaStream_t stream;
+    void* p;
+    size_t bytes;
+  };
+  std::vector<Workspace> ws;
+  std::vector<void*> ws_retired;
+  uint64_t ws_epoch = 0;
+  std::mutex ws_mu;
+  // cached occupancies (per context, hence per device)
+  int screen_occ = -1;
+  int combine_occ = -1;
   // host-buffer entry points: copy stream + per-chunk events (lazily made)
   static constexpr int kChunkEvents = 8;
   cudaStream_t copy_stream = nullptr;
@@ -43,10 +60,11 @@ struct rh_ctx {
   cudaStream_t aux_stream[kAuxStreams] = {};
   cudaEvent_t aux_ev[kAuxStreams] = {};
   cudaEvent_t aux_fork = nullptr;
-  // rh_screen's cooperative-kernel control words (zero between launches)
-  void* screen_ctrl = nullptr;
-  // the device's default memory pool keeps freed memory (re-plan searches)
-  bool pool_ready = false;
+  std::mutex search_mu;  // serialises the enqueue of search evals (shared aux streams)
+  // private stream-ordered pool of the re-plan searches (keeps what it has,
+  // so a re-plan reuses memory instead of mapping it; the device's default
+  // pool is left untouched)
+  cudaMemPool_t pool = nullptr;
   // rh_detector_pass_host*: the captured pass for the last argument key
   struct HostGraph {
     std::vector<uint64_t> key;
@@ -60,11 +78,13 @@ struct rh_ctx {
     double kappa = 0.0;
     int64_t series_len = 0, n = 0;
     const void *hist = nullptr, *observed = nullptr, *reset = nullptr;
+    void* buf = nullptr;  // the slot-2 buffer holding the results
     cudaEvent_t done = nullptr;
     // recorded after each rh_screen: the slot-2 results are free again
     cudaEvent_t consumed = nullptr;
     bool consumed_recorded = false;
   } prep;
+  std::mutex prep_mu;  // guards prep (one pending prepare per context)
 };
 
 namespace rh {
@@ -89,13 +109,33 @@ inline int cuda_fail(cudaError_t e, const char* what) {
     (ctx)->launches.fetch_add(1, std::memory_order_relaxed);        \
   } while (0)
 
-// Grow the context workspace to at least `bytes` (stream-ordered free of the
-// old buffer is not needed: callers synchronise before growth).
-int workspace(rh_ctx* ctx, size_t bytes, void** out, int slot);
+// The (slot, stream) workspace of at least `bytes` (see rh_ctx::ws).  Growth
+// inside a stream capture is refused (a captured graph must not depend on a
+// reallocation); zero = memset a newly allocated buffer on `stream`.
+int workspace(rh_ctx* ctx, size_t bytes, void** out, int slot, cudaStream_t stream,
+              bool zero = false);
+
+// Makes ctx's device current for the lifetime of the guard and restores the
+// caller's device afterwards (every entry point that touches the device).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(const rh_ctx* ctx) {
+    if (ctx && cudaGetDevice(&prev) == cudaSuccess && prev != ctx->device)
+      cudaSetDevice(ctx->device);
+    else
+      prev = -1;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
 
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) only when a kernel needs
-// more than it was last granted (the call costs microseconds per launch)
-int ensure_smem(const void* kernel, size_t bytes);
+// more than it was last granted on the context's device (the attribute is per
+// device; the call costs microseconds per launch)
+int ensure_smem(const rh_ctx* ctx, const void* kernel, size_t bytes);
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 

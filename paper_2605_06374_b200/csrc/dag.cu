@@ -115,9 +115,10 @@ extern "C" int rh_dag_critical_path(rh_ctx* ctx, int32_t n_vertices, const doubl
     set_error("rh_dag_critical_path: invalid arguments");
     return RH_E_INVALID;
   }
+  DeviceGuard guard(ctx);
   void* ws = nullptr;
   const size_t per = ((size_t)n_vertices * sizeof(int32_t) + 255) & ~size_t(255);
-  int rc = workspace(ctx, 3 * per + 256, &ws, 1);
+  int rc = workspace(ctx, 3 * per + 256, &ws, 1, as_stream(stream));
   if (rc) return rc;
   int32_t* indeg = static_cast<int32_t*>(ws);
   int32_t* fa = reinterpret_cast<int32_t*>(static_cast<char*>(ws) + per);

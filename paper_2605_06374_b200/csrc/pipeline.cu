@@ -1113,6 +1113,7 @@ int launch_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
     return RH_E_INVALID;
   }
   if (tr->n_iter == 0) return RH_OK;
+  DeviceGuard guard(ctx);
   if (!tr->mb_off || !tr->doc_len || !sg->layers || !sg->mb_start || !sg->speed ||
       !sg->hop_fwd || !sg->hop_bwd || (sh->has_allreduce && D > 1 && !sg->allreduce) ||
       (detect && (!tr->device_time || !tr->observed))) {
@@ -1173,7 +1174,7 @@ int launch_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
       const int64_t blocks = (tr->n_iter + p.ipb - 1) / p.ipb;
       void* kern = zbh ? (detect ? small_kernel<1, 1>(P, tw) : small_kernel<1, 0>(P, tw))
                        : (detect ? small_kernel<0, 1>(P, tw) : small_kernel<0, 0>(P, tw));
-      if (int e = ensure_smem(kern, smem)) return e;
+      if (int e = ensure_smem(ctx, kern, smem)) return e;
       {
         int occ = 0;
         RH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
@@ -1214,7 +1215,7 @@ int launch_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
   else
     kern = detect ? (big ? pass_kernel<0, 1, 1024> : pass_kernel<0, 1, 256>)
                   : (big ? pass_kernel<0, 0, 1024> : pass_kernel<0, 0, 256>);
-  if (int e = ensure_smem((const void*)kern, smem)) return e;
+  if (int e = ensure_smem(ctx, (const void*)kern, smem)) return e;
   kern<<<(unsigned)blocks, threads, smem, stream>>>(p);
   RH_CHECK_LAUNCH(ctx);
   return RH_OK;
@@ -1289,8 +1290,9 @@ int enqueue_host_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model*
                 const double* hist, const uint8_t* reset, const rh_pass_out* out,
                 uint8_t* outcome, int64_t* series_len_out, cudaStream_t stream) {
   if (!ctx || !sh || !sg || !out || (!tr_in && !pk) || (tr_in && !tr_in->mb_off) ||
-      (pk && (!pk->iter_doc || !pk->mb_docs || !pk->doc_len))) {
-    set_error("detect_host: NULL argument");
+      (pk && (!pk->iter_doc || !pk->mb_docs || !pk->doc_len)) ||
+      (screen && series_len > 0 && !hist)) {
+    set_error("detect_host: NULL argument (or series_len > 0 without hist)");
     return RH_E_INVALID;
   }
   const int P = sh->pp, D = sh->dp, T = sh->tp, M = sh->micro_batches;
@@ -1341,7 +1343,7 @@ int enqueue_host_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model*
     need = c.off + 256;
   }
   void* ws = nullptr;
-  int rc = workspace(ctx, need, &ws, 0);
+  int rc = workspace(ctx, need, &ws, 0, stream);
   if (rc) return rc;
   Carver c{static_cast<char*>(ws)};
   // device buffers: every trace array lands at its own offsets, so the
@@ -1552,10 +1554,21 @@ int detect_host(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
     set_error("detect_host: NULL argument");
     return RH_E_INVALID;
   }
+  if (screen && series_len > 0 && !hist) {
+    set_error("detect_host: series_len = %lld but hist is NULL", (long long)series_len);
+    return RH_E_INVALID;
+  }
   if ((pk ? pk->n_iter : tr->n_iter) == 0) return RH_OK;
+  DeviceGuard guard(ctx);
   auto& g = ctx->host_graph;
   std::vector<uint64_t> key = host_pass_key(sh, m, sg, tr, pk, thr, screen, series_len, hist,
                                             reset, out, outcome, series_len_out, stream);
+  // the captured graph bakes in workspace pointers: any reallocation since
+  // (by this or another call on the context) invalidates it
+  {
+    std::lock_guard<std::mutex> lock(ctx->ws_mu);
+    key.push_back(ctx->ws_epoch);
+  }
   const bool same = key == g.key;
   if (same && g.exec) {
     RH_CUDA(cudaGraphLaunch(g.exec, stream));

@@ -69,12 +69,13 @@ struct ScreenArgs {
   int32_t* bres;                   // [n/128] last reset inside each scan block
   uint8_t* state;                  // [2][n] bit0 popped, bit1 changed in that round
   uint8_t* c0;                     // [n] round-0 verdicts (round0_kernel)
-  // control words (rh_ctx::screen_ctrl): zero when a launch starts, and the
+  // control words (workspace slot 3 of the stream): zero when a launch starts, and the
   // launch leaves them zero again (no memset per call; graph-replay safe)
   unsigned* cnt;             // [3] barrier words per round (rotating): arrivals + changed blocks << 16
   unsigned long long* kcnt;  // [3] kept entries since the last reset, per round
   unsigned* bar;             // [2] unused (reserved)
   unsigned* ticket;          // [1] blocks finished
+  void* prep_buf;            // host side: the slot-2 buffer launch_prepare filled
 };
 
 // Grid barrier of Jacobi round `round`, carrying the round's "anything
@@ -553,7 +554,8 @@ void fill_inputs(ScreenArgs& a, const rh_screen_params* params, int64_t series_l
 int launch_prepare(rh_ctx* ctx, ScreenArgs& a, cudaStream_t st) {
   const PrepLayout L(a.n);
   void* ws = nullptr;
-  if (int rc = workspace(ctx, L.bytes, &ws, 2)) return rc;
+  if (int rc = workspace(ctx, L.bytes, &ws, 2, st)) return rc;
+  a.prep_buf = ws;
   char* base = static_cast<char*>(ws);
   a.R = reinterpret_cast<int32_t*>(base + L.oR);
   a.bres = reinterpret_cast<int32_t*>(base + L.oRes);
@@ -577,6 +579,8 @@ extern "C" int rh_screen_prepare(rh_ctx* ctx, const rh_screen_params* params,
                                  int64_t series_len, const double* hist, int64_t n,
                                  const double* observed, const uint8_t* reset, void* stream) {
   if (int rc = check_screen_args(ctx, params, series_len, hist, n, observed)) return rc;
+  DeviceGuard guard(ctx);
+  std::lock_guard<std::mutex> lock(ctx->prep_mu);
   ctx->prep.valid = false;
   if (n == 0) return RH_OK;
   cudaStream_t st = as_stream(stream);
@@ -600,6 +604,7 @@ extern "C" int rh_screen_prepare(rh_ctx* ctx, const rh_screen_params* params,
   pr.hist = hist;
   pr.observed = observed;
   pr.reset = reset;
+  pr.buf = a.prep_buf;
   pr.valid = true;
   return RH_OK;
 }
@@ -614,6 +619,8 @@ extern "C" int rh_screen(rh_ctx* ctx, const rh_screen_params* params, int64_t se
     return RH_E_INVALID;
   }
   cudaStream_t st = as_stream(stream);
+  DeviceGuard guard(ctx);
+  std::lock_guard<std::mutex> lock(ctx->prep_mu);
   const auto& pr = ctx->prep;
   const bool prepared = pr.valid && pr.window == params->window &&
                         pr.filter_enabled == params->filter_enabled && pr.kappa == params->kappa &&
@@ -630,7 +637,7 @@ extern "C" int rh_screen(rh_ctx* ctx, const rh_screen_params* params, int64_t se
                               cudaMemcpyHostToDevice, st));
     return RH_OK;
   }
-  static int occ = -1;  // cached occupancy of the cooperative kernel
+  int& occ = ctx->screen_occ;  // cached occupancy of the cooperative kernel
   if (occ < 0) {
     RH_CUDA(cudaFuncSetAttribute((void*)screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sizeof(ScreenSmem)));
@@ -652,26 +659,24 @@ extern "C" int rh_screen(rh_ctx* ctx, const rh_screen_params* params, int64_t se
   a.len_out = series_len_out;
   if (prepared) {
     const PrepLayout L(n);
-    char* pbase = static_cast<char*>(ctx->ws[2]);
+    char* pbase = static_cast<char*>(pr.buf);
     a.R = reinterpret_cast<int32_t*>(pbase + L.oR);
     a.bres = reinterpret_cast<int32_t*>(pbase + L.oRes);
     a.c0 = reinterpret_cast<uint8_t*>(pbase + L.oC0);
   } else if (int rc = launch_prepare(ctx, a, st)) {
     return rc;
   }
-  // control words: a dedicated per-context block, zeroed once (the kernel
-  // leaves it zero); kept-state: the slot-1 workspace
-  if (!ctx->screen_ctrl) {
-    RH_CUDA(cudaMalloc(&ctx->screen_ctrl, 256));
-    RH_CUDA(cudaMemset(ctx->screen_ctrl, 0, 256));
-  }
-  char* cb = static_cast<char*>(ctx->screen_ctrl);
+  // control words: a dedicated per-stream block, zeroed on allocation (the
+  // kernel leaves it zero); kept-state: the slot-1 workspace
+  void* ctrl = nullptr;
+  if (int rc = workspace(ctx, 256, &ctrl, 3, st, /*zero=*/true)) return rc;
+  char* cb = static_cast<char*>(ctrl);
   a.kcnt = reinterpret_cast<unsigned long long*>(cb);       // 24 B
   a.cnt = reinterpret_cast<unsigned*>(cb + 32);             // 12 B
   a.bar = reinterpret_cast<unsigned*>(cb + 64);             // 8 B
   a.ticket = reinterpret_cast<unsigned*>(cb + 96);          // 4 B
   void* ws = nullptr;
-  if (int rc = workspace(ctx, 2 * (size_t)n + 256, &ws, 1)) return rc;
+  if (int rc = workspace(ctx, 2 * (size_t)n + 256, &ws, 1, st)) return rc;
   a.state = static_cast<uint8_t*>(ws);
   void* kargs[] = {&a};
   RH_CUDA(cudaLaunchCooperativeKernel((void*)screen_kernel, dim3(blocks), dim3(kScreenThreads),

@@ -55,6 +55,9 @@ struct rh_search {
   void* dmem = nullptr;
   size_t dbytes = 0;
   cudaStream_t last_stream = nullptr;  // stream of the latest create / eval
+  // recorded after the latest create / eval: a later eval on another stream
+  // waits for it (the task list and block results are per search)
+  cudaEvent_t done_ev = nullptr;
   int div_safe = 0;  // see SearchArgs::div_safe
   struct Dev {
     int32_t *lT, *lD, *lP, *lgoff, *lpoff, *ldoff, *lboff, *lnb;
@@ -880,7 +883,7 @@ static int build_op_lists(rh_ctx* ctx, rh_search* S, cudaStream_t st) {
     }
   const size_t tab_bytes = 3 * off.size() * 4;
   const size_t bytes = tab_bytes + 4 * std::max<size_t>(1, ops.size());
-  RH_CUDA(cudaMallocAsync(&S->dops, bytes, st));
+  RH_CUDA(cudaMallocFromPoolAsync(&S->dops, bytes, ctx->pool, st));
   std::vector<char> stage(bytes, 0);
   memcpy(stage.data(), off.data(), off.size() * 4);
   memcpy(stage.data() + off.size() * 4, cnt.data(), cnt.size() * 4);
@@ -913,6 +916,7 @@ int rh_search_create(rh_ctx* ctx, const rh_search_desc* desc, rh_search** out, v
     return RH_E_INVALID;
   }
   cudaStream_t st = as_stream(stream);
+  DeviceGuard guard(ctx);
   rh_search* S = new rh_search();
   S->d = *desc;
   const rh_search_desc& d = *desc;
@@ -1047,7 +1051,7 @@ int rh_search_create(rh_ctx* ctx, const rh_search_desc* desc, rh_search** out, v
     S->div_safe = nums && dens ? 1 : 0;
   }
   // ---- device memory
-  static int max_blocks_per_sm = -1;  // cached occupancy of the combine kernel
+  int& max_blocks_per_sm = ctx->combine_occ;  // cached occupancy of the combine kernel
   if (max_blocks_per_sm < 0)
     RH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_blocks_per_sm, combine_kernel,
                                                           kEvalThreads, 0));
@@ -1100,16 +1104,18 @@ int rh_search_create(rh_ctx* ctx, const rh_search_desc* desc, rh_search** out, v
                o_rtab = take(8 * (size_t)S->n_rt), o_pinfo = take(16 * (size_t)S->n_pairs),
                o_rl = take(8 * 96 * (size_t)S->n_pairs),
                o_tasks = take(sizeof(PipeTask) * (size_t)NL);
-  // stream-ordered pool: after the first re-plan the memory is reused, not
-  // mapped again (the pool keeps what it has; see rh_ctx::pool_ready)
-  if (!ctx->pool_ready) {
-    cudaMemPool_t pool;
-    RH_CUDA(cudaDeviceGetDefaultMemPool(&pool, ctx->device));
+  // private stream-ordered pool: after the first re-plan the memory is
+  // reused, not mapped again (the device's default pool is not touched)
+  if (!ctx->pool) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = ctx->device;
+    RH_CUDA(cudaMemPoolCreate(&ctx->pool, &props));
     uint64_t keep = ~0ull;
-    RH_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
-    ctx->pool_ready = true;
+    RH_CUDA(cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrReleaseThreshold, &keep));
   }
-  cudaError_t e = cudaMallocAsync(&S->dmem, bytes, st);
+  cudaError_t e = cudaMallocFromPoolAsync(&S->dmem, bytes, ctx->pool, st);
   if (e != cudaSuccess) {
     delete S;
     set_error("rh_search_create: %zu bytes: %s", bytes, cudaGetErrorString(e));
@@ -1153,6 +1159,8 @@ int rh_search_create(rh_ctx* ctx, const rh_search_desc* desc, rh_search** out, v
     rh_search_destroy(S);
     return rc;
   }
+  RH_CUDA(cudaEventCreateWithFlags(&S->done_ev, cudaEventDisableTiming));
+  RH_CUDA(cudaEventRecord(S->done_ev, st));
   RH_CUDA(cudaStreamSynchronize(st));
   *out = S;
   return RH_OK;
@@ -1163,6 +1171,7 @@ int rh_search_destroy(rh_search* S) {
   // back to the pool, ordered after the latest work issued on the search
   if (S->dmem) cudaFreeAsync(S->dmem, S->last_stream);
   if (S->dops) cudaFreeAsync(S->dops, S->last_stream);
+  if (S->done_ev) cudaEventDestroy(S->done_ev);
   delete S;
   return RH_OK;
 }
@@ -1226,6 +1235,12 @@ int rh_search_eval(rh_ctx* ctx, rh_search* S, int64_t begin, int64_t end, double
     return RH_E_INVALID;
   }
   cudaStream_t st = as_stream(stream);
+  DeviceGuard guard(ctx);
+  // the context's auxiliary streams and fork / join events are shared
+  std::lock_guard<std::mutex> lock(ctx->search_mu);
+  // the previous eval (maybe on another stream) still reads this search's
+  // task list and block results
+  if (S->done_ev) RH_CUDA(cudaStreamWaitEvent(st, S->done_ev, 0));
   if (begin == end) {
     const double inf = std::numeric_limits<double>::infinity();
     const int64_t none = -1;
@@ -1285,7 +1300,7 @@ int rh_search_eval(rh_ctx* ctx, rh_search* S, int64_t begin, int64_t end, double
     cudaStream_t gs = ctx->aux_stream[gi++ % kAux];
     const size_t smem = (size_t)(zbh ? 3 : 2) * g.P * kPipeThreads * sizeof(double);
     // (the pipe kernel strides its state by kPipeThreads)
-    if (int e = ensure_smem(kern, smem)) return e;
+    if (int e = ensure_smem(ctx, kern, smem)) return e;
     int occ = 0;
     RH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kPipeThreads, smem));
     const long long want = (g.n_pipes + kPipeThreads - 1) / kPipeThreads;
@@ -1324,6 +1339,7 @@ int rh_search_eval(rh_ctx* ctx, rh_search* S, int64_t begin, int64_t end, double
   minloc_kernel<<<1, 1024, 0, st>>>(S->dv.blk_best, S->dv.blk_idx, (int)n_blk, best_score,
                                     best_index);
   RH_CHECK_LAUNCH(ctx);
+  RH_CUDA(cudaEventRecord(S->done_ev, st));
   return RH_OK;
 }
 
@@ -1333,6 +1349,7 @@ int rh_search_decode(rh_ctx* ctx, rh_search* S, int64_t index, rh_candidate* out
     set_error("rh_search_decode: index out of range");
     return RH_E_INVALID;
   }
+  DeviceGuard guard(ctx);
   const int NL = (int)S->lT.size();
   int li = (int)(std::upper_bound(S->lbase.begin(), S->lbase.end(), (long long)index) -
                  S->lbase.begin()) - 1;
@@ -1471,6 +1488,7 @@ int rh_repartition_batch(rh_ctx* ctx, int32_t n, const int32_t* off, const doubl
     return RH_E_INVALID;
   }
   if (!n) return RH_OK;
+  DeviceGuard guard(ctx);
   repartition_batch_kernel<<<(n * 32 + 127) / 128, 128, 0, as_stream(stream)>>>(
       n, off, speeds, total_layers, min_layers, out, err);
   RH_CHECK_LAUNCH(ctx);
@@ -1485,6 +1503,7 @@ int rh_proportional_split_batch(rh_ctx* ctx, int32_t n, const int32_t* off,
     return RH_E_INVALID;
   }
   if (!n) return RH_OK;
+  DeviceGuard guard(ctx);
   proportional_batch_kernel<<<(n + 127) / 128, 128, 0, as_stream(stream)>>>(n, off, weights,
                                                                            totals, counts, err);
   RH_CHECK_LAUNCH(ctx);
@@ -1499,6 +1518,7 @@ int rh_select_subgroup_batch(rh_ctx* ctx, int32_t n, const int32_t* off, const d
     return RH_E_INVALID;
   }
   if (!n) return RH_OK;
+  DeviceGuard guard(ctx);
   subgroup_batch_kernel<<<(n + 127) / 128, 128, 0, as_stream(stream)>>>(n, off, speeds, ids,
                                                                        degree_mask, ranked, best_k);
   RH_CHECK_LAUNCH(ctx);

@@ -42,7 +42,7 @@ def _proportional(total: int, weights: list[float]) -> list[int]:
 
 
 def c2_trace(n_iter: int = 10_000, seed: int = 0, *, tp=4, dp=16, pp=4, layers=40, M=128,
-             N=4096, mean=7.2, sigma=0.8) -> DetectorTrace:
+             N=4096, mean=7.2, sigma=0.8, packer=None) -> DetectorTrace:
     cfg = ParallelismConfig(tp=tp, dp=dp, pp=pp, layer_partition=[layers // pp] * pp)
     n_dev = tp * dp * pp
     nodes = -(-n_dev // 8)
@@ -100,7 +100,7 @@ def c2_trace(n_iter: int = 10_000, seed: int = 0, *, tp=4, dp=16, pp=4, layers=4
         seg[start:] = k
         if phases[k][5] and start < n_iter:
             reset[start] = 1
-    mb_off, doc_len = synth_iterations(n_iter, M, N, mean, sigma, seed)
+    mb_off, doc_len = synth_iterations(n_iter, M, N, mean, sigma, seed, packer=packer)
     tr = DetectorTrace(cfg=cfg, model=model, M=M, N=N, has_allreduce=dp > 1, seg=seg,
                        mb_off=mb_off, doc_len=doc_len, known=known, actual=actual, reset=reset,
                        group_size=np.asarray(sizes, dtype=np.int64))

@@ -61,14 +61,20 @@ def draw_documents(rng: np.random.Generator, target_tokens: int, budget: int, me
     return np.concatenate(out)
 
 
-def synth_iterations(n_iter: int, M: int, N: int, mean: float, sigma: float, seed: int):
-    """Packed micro-batches of n_iter iterations -> (mb_off[n*M+1], doc_len)."""
+def synth_iterations(n_iter: int, M: int, N: int, mean: float, sigma: float, seed: int,
+                     packer=None):
+    """Packed micro-batches of n_iter iterations -> (mb_off[n*M+1], doc_len).
+
+    `packer(lengths, budget, max_bins) -> (off, docs)` defaults to the native
+    pack_ffd; bench.py's reference arm passes the oracle's literal FFD so that
+    process never loads the product library."""
+    packer = packer or pack_ffd
     rng = np.random.default_rng([seed, 0])
     offs, docs = [np.zeros(1, np.int64)], []
     base = 0
     for _ in range(n_iter):
         lengths = draw_documents(rng, M * N, N, mean, sigma)
-        off, d = pack_ffd(lengths, N, M)
+        off, d = packer(lengths, N, M)
         if len(off) - 1 < M:
             raise ValueError("workload produced fewer than M micro-batches")
         offs.append(off[1:].astype(np.int64) + base)

@@ -55,6 +55,9 @@ class Oracle:
         self.lib = C.CDLL(str(ORACLE_LIB))
         p = C.c_void_p
         L = self.lib
+        L.orc_pack_sequences.argtypes = [C.c_int64, p, C.c_int32, C.c_int64, p, p,
+                                         C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+        L.orc_pack_sequences.restype = C.c_int
         L.orc_quad_load.argtypes = [C.c_int32, p]
         L.orc_quad_load.restype = C.c_int64
         L.orc_chunk_time.argtypes = [C.POINTER(_lib.CostModelC), C.c_int, C.c_int64, C.c_int32,
@@ -137,6 +140,20 @@ class Oracle:
                         a(trace.device_time, np.float32) if detect else None,
                         a(trace.observed, np.float64) if detect else None)
         return tr, keep
+
+    def pack_sequences(self, lengths, budget, max_bins=-1):
+        """workload.py:52-80 (literal FFD) -> (mb_off, doc_len), the
+        rh_pack_sequences contract: a drop-in `packer` for synth_iterations."""
+        v = np.ascontiguousarray(lengths, dtype=np.int32)
+        nb, ne = C.c_int64(), C.c_int64()
+        if self.lib.orc_pack_sequences(len(v), _ptr(v), int(budget), int(max_bins), None, None,
+                                       C.byref(nb), C.byref(ne)):
+            raise ValueError("orc_pack_sequences: document length outside [1, budget]")
+        off = np.zeros(nb.value + 1, np.int32)
+        docs = np.zeros(max(ne.value, 1), np.int32)
+        self.lib.orc_pack_sequences(len(v), _ptr(v), int(budget), int(max_bins), _ptr(off),
+                                    _ptr(docs), C.byref(nb), C.byref(ne))
+        return off, docs[:ne.value]
 
     def pipeline(self, trace, view="known", capacity=None, threads=0):
         segs = HostSegments(trace.known if view == "known" else trace.actual)

@@ -279,6 +279,113 @@ def test_detector_pass_host_graph_replay(oracle, cuda_device):
         assert ln.value == oln
 
 
+def test_host_pass_graph_survives_workspace_growth(oracle, cuda_device):
+    """replay the captured host pass after OTHER calls on the
+    same context grew the shared scratch (a longer screen on the same stream,
+    a large general DAG): the graph must not replay into retired buffers --
+    the pass is re-captured and still equals the oracle."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2605_06374_b200 import _lib
+    from paper_2605_06374_b200.detector import _screen
+    from paper_2605_06374_b200.tables import pipe_shape
+    from paper_2605_06374_b200.workload import cost_model_c
+    from tests.oracle_bind import HostSegments
+
+    tr = with_measurements(random_trace(4242, n_iter=3000, n_seg=2, pp=3), oracle, noise=0.02,
+                           seed=3)
+    tr.reset[::700] = 1
+    pk = tr.packed()
+    segs = HostSegments(tr.known)
+    n, G = tr.n_iter, tr.cfg.dp * tr.cfg.pp
+    seg = np.ascontiguousarray(tr.seg)
+    dt = np.ascontiguousarray(tr.device_time.astype(np.float32))
+    obs = np.ascontiguousarray(tr.observed)
+    rst = np.ascontiguousarray(tr.reset)
+    ms, st = np.zeros(n), np.zeros(n, np.uint8)
+    fl, sv = np.zeros(n * G, np.uint8), np.zeros(n * G, np.float32)
+    oc, ln = np.zeros(n, np.uint8), C.c_int64()
+    trc = _lib.TracePacked(n, seg.ctypes.data, pk["iter_doc"].ctypes.data,
+                           pk["mb_docs"].ctypes.data, pk["doc_len"].ctypes.data,
+                           dt.ctypes.data, obs.ctypes.data)
+    out = _lib.PassOut(ms.ctypes.data, st.ctypes.data, None, fl.ctypes.data, sv.ctypes.data)
+    shape = pipe_shape(tr.cfg, tr.M, tr.N, has_allreduce=tr.has_allreduce, max_mb=segs.max_mb)
+    sp = _lib.ScreenParams(20, 1, 3.0)
+    lib, ctx = _lib.load_library(), _lib.context()
+    model = cost_model_c(tr.model)
+    oms, ost, _, ofl, osv = oracle.detect(tr)
+    ooc, oln = oracle.screen(obs, ost, reset=rst)
+
+    def host_pass():
+        ms[:] = 0
+        oc[:] = 0
+        _lib.check(lib.rh_detector_pass_host_packed(
+            ctx, C.byref(shape), C.byref(model), C.byref(segs.c), C.byref(trc), 1.25,
+            C.byref(sp), 0, None, rst.ctypes.data, C.byref(out), oc.ctypes.data, C.byref(ln),
+            None), "rh_detector_pass_host_packed")
+        np.testing.assert_array_equal(st, ost)
+        np.testing.assert_array_equal(_bits(ms), _bits(oms))
+        np.testing.assert_array_equal(oc, ooc)
+        assert ln.value == oln
+
+    rng = np.random.default_rng(9)
+    for grow in range(3):
+        host_pass()
+        host_pass()  # captured here (or replayed)
+        # grow the legacy stream's screen scratch: a much longer series
+        m = 60_000 * (grow + 2)
+        big = 10.0 + rng.standard_normal(m)
+        bst = np.zeros(m, np.uint8)
+        with torch.cuda.stream(torch.cuda.default_stream()):
+            oc_big, _ = _screen(0, [], big, bst, 20, 3.0, True, reset=None)
+        ooc_big, _ = oracle.screen(big, bst)
+        np.testing.assert_array_equal(oc_big, ooc_big)
+        torch.cuda.synchronize()
+        host_pass()  # must not replay into the retired buffers
+    torch.cuda.synchronize()
+
+
+def test_two_streams_concurrent_screens(oracle, cuda_device):
+    """Per-stream scratch: rh_screen enqueued on two streams of one context
+    back to back (no synchronisation between the calls, so the kernels may
+    overlap) equals the oracle on both."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2605_06374_b200 import _lib
+
+    lib, ctx = _lib.load_library(), _lib.context()
+    rng = np.random.default_rng(11)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    params = _lib.ScreenParams(20, 1, 3.0)
+    cases = []
+    for k in range(2):
+        n = 50_000 + 7_777 * k
+        base = 10.0 + rng.standard_normal(n) * 0.5
+        obs = np.where(rng.random(n) < 0.1, base * 2.0, base)
+        stt = (rng.random(n) < 0.2).astype(np.uint8)
+        cases.append(dict(obs=obs, st=stt, t_obs=torch.as_tensor(obs).to(dev),
+                          t_st=torch.as_tensor(stt).to(dev), hist=torch.zeros(1, dtype=torch.float64, device=dev),
+                          out=torch.empty(n, dtype=torch.uint8, device=dev),
+                          ln=torch.empty(1, dtype=torch.int64, device=dev)))
+    torch.cuda.synchronize()
+    for rep in range(3):
+        for c, s in zip(cases, streams):
+            _lib.check(lib.rh_screen(ctx, C.byref(params), 0, c["hist"].data_ptr(), len(c["obs"]),
+                                     c["t_obs"].data_ptr(), c["t_st"].data_ptr(), None,
+                                     c["out"].data_ptr(), c["ln"].data_ptr(), s.cuda_stream),
+                       "rh_screen")
+        torch.cuda.synchronize()
+        for c in cases:
+            ooc, oln = oracle.screen(c["obs"], c["st"])
+            np.testing.assert_array_equal(c["out"].cpu().numpy(), ooc)
+            assert int(c["ln"].item()) == oln
+
+
 def test_division_selftest(cuda_device):
     """The hot path's hoisted-reciprocal division equals __ddiv_rn bit for bit
     (2^28 seeded pairs over divisor regimes, on the device)."""

@@ -30,6 +30,17 @@ def test_chunk_time_golden(oracle):
         assert bits(got) == bits(t), (docs, kind, layers, speed)
 
 
+def test_oracle_ffd_pack_golden(oracle):
+    """The oracle's literal FFD (bench.py's reference arm packs with it) equals
+    the reference's pack_sequences on every golden packing."""
+    for docs, budget, bins in load("workload")["pack"]:
+        off, flat = oracle.pack_sequences(np.asarray(docs, np.int32), budget)
+        got = [list(map(int, flat[off[i]:off[i + 1]])) for i in range(len(off) - 1)]
+        assert got == bins
+    with pytest.raises(ValueError):
+        oracle.pack_sequences(np.array([5000]), 4096)
+
+
 def test_native_ffd_pack_golden():
     for docs, budget, bins in load("workload")["pack"]:
         off, flat = pack_ffd(np.asarray(docs, np.int32), budget)
