@@ -1,0 +1,419 @@
+// pass_wide_kernel: the thread-per-replica Detector pass for long 1F1B
+// pipelines (5 <= P <= 16, D <= 64) -- SURVEY §8(d)'s trace R and the C3-C5
+// shapes -- where a lane per stage (pass_kernel) idles half its DAG levels
+// and pays ~45 instructions of level bookkeeping per lane per level.
+//
+// One THREAD walks one replica pipeline: the chain state (last finish, last
+// F finish and cost sum of every stage) lives in registers, and the chunks
+// are visited in a topological order that is a pair of short loops with the
+// stage index unrolled at compile time:
+//
+//   warm-up triangle, for j = 0..P-1, stages ascending:
+//       F_j(s)                        if j <= P-1-s and j < m
+//   main loop, for i = 0..m-1, stages descending:
+//       B_i(s)                        (dependency B_i(s+1): same i, done)
+//       F_{P-s+i}(s)                  if P-s+i < m  (dependency
+//                                     F_{P-s+i}(s-1): previous i, not yet
+//                                     overwritten -- s-1 comes later)
+//
+// Each stage's chunks come out in its 1F1B chain order (warm-up Fs, then
+// (B_i, F_{w+1+i}) pairs, then the B tail -- pipeline.py:92-126) and every
+// chunk after its DAG predecessors, so starts, finishes and chain-order cost
+// sums equal the level-ordered walk's bit for bit (any topological order of
+// Eq. 2's max/+ relaxation gives the same values).  The loop bodies are a
+// few hundred instructions (the unrolled 512-chunk walk streamed 480 KB of
+// SASS through a 32 KB instruction cache).
+//
+// Shared memory per CTA (~26 KB for C5: 8 CTAs / SM): base costs [j][thread],
+// the iteration's ratio * layers, and one region that first holds the TMA-
+// staged offsets + documents and then the hop weights [stage][thread].
+// Speeds are read from global memory only on the stages some replica of the
+// warp runs slow (a warp-uniform branch; x / 1.0 == x exactly otherwise).
+#include "walks.cuh"
+
+namespace rh {
+
+// ld.volatile.shared at a 32-bit shared address plus a compile-time offset
+// (folded into the instruction): never cached in a register by the compiler,
+// so the per-stage constants cost a load per use instead of pinning ~100
+// registers across the walk.
+template <int OFF>
+__device__ __forceinline__ double lds_at(uint32_t a) {
+  double v;
+  asm volatile("ld.volatile.shared.f64 %0, [%1+%2];" : "=d"(v) : "r"(a), "n"(OFF));
+  return v;
+}
+__device__ __forceinline__ double lds_rt(uint32_t a) {
+  double v;
+  asm volatile("ld.volatile.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+
+// One replica's walk state: shared addresses of its base costs [j][TW], its
+// iteration's ratio * layers [rlF: P][rlB: P], its hop weights and speed
+// reciprocals [s][TW]; the chain state in registers.
+template <int P, int TW, bool EXACT>
+struct WideWalk {
+  uint32_t bt, rl, hf, hb, inv;  // shared addresses (this thread's column)
+  const double* gsp;             // this (segment, replica)'s stage speeds
+  unsigned slow;  // warp-uniform: bit s = some replica of the warp runs stage s slow
+  double fin[P], lastF[P], ssum[P];
+
+  // c = (rl * b) / speed exactly as __ddiv_rn (the hoisted-reciprocal form
+  // after the kernel's operand-range check; EXACT: out-of-range operands,
+  // __ddiv_rn out of line), skipped on unit-speed stages (x / 1.0 == x)
+  template <int S>
+  __device__ __forceinline__ double cost(double rl_, double b_) const {
+    const double x = __dmul_rn(rl_, b_);
+    if (slow & (1u << S)) {  // warp-uniform branch
+      const double sp = __ldg(gsp + S);
+      if (EXACT) return div_slow(x, sp);
+      return div_fast(x, sp, lds_at<S * TW * 8>(inv));
+    }
+    return x;
+  }
+  // start = max(chain finish, dependency finish + hop); finish = start + c;
+  // cost sum in chain order (pipeline.py:275-291, 446-453)
+  template <int S>
+  __device__ __forceinline__ double step(double c, double dep) {
+    const double st = fin[S] > dep ? fin[S] : dep;
+    fin[S] = __dadd_rn(st, c);
+    ssum[S] = __dadd_rn(ssum[S], c);
+    return fin[S];
+  }
+  // warm-up triangle slot: F_j(S) if j <= P-1-S and j < m (stages ascending)
+  template <int S>
+  __device__ __forceinline__ void tri(int j, int m, double bj) {
+    if (j <= P - 1 - S && j < m) {
+      const double dep = S > 0 ? __dadd_rn(lastF[S > 0 ? S - 1 : 0], lds_at<S * TW * 8>(hf)) : 0.0;
+      lastF[S] = step<S>(cost<S>(lds_at<S * 8>(rl), bj), dep);
+    }
+  }
+  // main-loop slot (stages descending): B_i(S), then F_{P-S+i}(S) if it exists
+  template <int S>
+  __device__ __forceinline__ void pair(int i, int m, double bi, double& nB) {
+    const double depB = S < P - 1 ? __dadd_rn(nB, lds_at<S * TW * 8>(hb)) : 0.0;
+    nB = step<S>(cost<S>(lds_at<(P + S) * 8>(rl), bi), depB);
+    if (i < m - P + S) {
+      const double bF = lds_rt(bt + (uint32_t)((P - S + i) * TW * 8));
+      const double dep = S > 0 ? __dadd_rn(lastF[S > 0 ? S - 1 : 0], lds_at<S * TW * 8>(hf)) : 0.0;
+      lastF[S] = step<S>(cost<S>(lds_at<S * 8>(rl), bF), dep);
+    }
+  }
+  template <int... I>
+  __device__ __forceinline__ void tri_all(int j, int m, double bj, std::integer_sequence<int, I...>) {
+    (tri<I>(j, m, bj), ...);  // S = 0, 1, ..., P-1
+  }
+  template <int... I>
+  __device__ __forceinline__ void pair_all(int i, int m, double bi,
+                                           std::integer_sequence<int, I...>) {
+    double nB = 0.0;  // B_i of the stage above
+    (pair<P - 1 - I>(i, m, bi, nB), ...);  // S = P-1, ..., 0
+  }
+  // (Tried: K groups of stages skewed by one loop step each, so a step holds
+  // K independent dependency chains -- bit-exact, but the per-group validity
+  // and slow-stage branches kept the compiler from interleaving them: trace R
+  // 463 -> 520 us per 10^4 iterations; branch-free division on top: 624 us.)
+  __device__ __forceinline__ void walk(int m) {
+#pragma unroll 1
+    for (int j = 0; j < P; ++j)
+      tri_all(j, m, lds_rt(bt + (uint32_t)((j < m ? j : 0) * TW * 8)),
+              std::make_integer_sequence<int, P>());
+#pragma unroll 1
+    for (int i = 0; i < m; ++i)
+      pair_all(i, m, lds_rt(bt + (uint32_t)(i * TW * 8)), std::make_integer_sequence<int, P>());
+  }
+};
+
+// CTAs per SM the register budget targets: the loop-carried chain state is
+// 3P doubles (finish, last F finish, cost sum per stage), so long pipelines
+// trade occupancy for registers (P = 16: 168 registers, 6 CTAs = 12 warps).
+constexpr int wide_min_blocks(int P) { return P <= 10 ? 8 : (P <= 12 ? 7 : 6); }
+
+template <int P, int DETECT>
+__global__ void __launch_bounds__(kWideThreads, wide_min_blocks(P)) pass_wide_kernel(const PassParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int TW = kWideThreads;
+  const int tid = threadIdx.x;
+  const int D = p.sh.dp, M = p.sh.micro_batches, T = p.sh.tp;
+  const int li = tid / D, d = tid - li * D;
+  const int64_t it0 = (int64_t)blockIdx.x * p.ipb;
+  const int64_t it = it0 + li;
+  const int n_it = (int)min((int64_t)p.ipb, p.tr.n_iter - it0);
+  const bool on = li < n_it;
+  double* it_ms = reinterpret_cast<double*>(smem_raw);
+  unsigned* it_st = reinterpret_cast<unsigned*>(it_ms + p.ipb);
+  double* base_t = reinterpret_cast<double*>(smem_raw + p.w_base);
+  double* s_rl = reinterpret_cast<double*>(smem_raw + p.w_rl);
+  double* s_hf = reinterpret_cast<double*>(smem_raw + p.w_union);
+  double* s_hb = s_hf + P * TW;
+  double* s_inv = s_hb + P * TW;
+  __shared__ uint64_t s_bar;
+  if (tid < p.ipb) {
+    it_ms[tid] = 0.0;
+    it_st[tid] = 0u;
+  }
+  // ---- TMA staging of the CTA's micro-batch offsets and documents
+  const int n_mb = n_it * M;
+  const int32_t* g_off = p.tr.mb_off + it0 * M;
+  const int32_t d_lo = __ldg(g_off), n_doc = __ldg(g_off + n_mb) - d_lo;
+  const bool staged = n_doc <= p.doc_stage;
+  const StagePlan so = stage_plan(smem_raw + p.w_union, g_off, n_mb + 1);
+  const StagePlan sd = staged ? stage_plan(smem_raw + p.w_docs, p.tr.doc_len + d_lo, n_doc)
+                              : StagePlan{nullptr, 0, 0, 0u};
+  if (tid == 0) {
+    mbar_init(&s_bar, 1);
+    mbar_arrive_expect_tx(&s_bar, so.tx_bytes + sd.tx_bytes);
+    stage_issue(so, g_off, &s_bar);
+    if (staged) stage_issue(sd, p.tr.doc_len + d_lo, &s_bar);
+    if (DETECT)  // reduced after the walk: pull the rows into L2 now
+      prefetch_l2(p.tr.device_time + it0 * D * P * T, 4 * (size_t)n_it * D * P * T);
+    const int64_t nb = (int64_t)blockIdx.x + p.pf_stride;
+    if (p.pf_stride > 0 && nb < gridDim.x) {  // the next wave's inputs
+      const int64_t pf_it = nb * p.ipb;
+      const int pf_nmb = (int)min((int64_t)p.ipb, p.tr.n_iter - pf_it) * M;
+      const int32_t lo = __ldg(p.tr.mb_off + pf_it * M);
+      const int32_t hi = __ldg(p.tr.mb_off + pf_it * M + pf_nmb);
+      prefetch_l2(p.tr.mb_off + pf_it * M, 4 * (size_t)(pf_nmb + 1));
+      prefetch_l2(p.tr.doc_len + lo, 4 * (size_t)(hi - lo));
+    }
+  }
+  __syncthreads();  // the barrier is initialised before anybody polls it
+  stage_edges(so, g_off, n_mb + 1);
+  if (staged) stage_edges(sd, p.tr.doc_len + d_lo, n_doc);
+  // ---- per-replica inputs (overlap the copies)
+  const int seg = on && p.tr.seg ? __ldg(p.tr.seg + it) : 0;
+  int m0 = 0, md = 0;
+  if (on) {
+    const int32_t* ms = p.sg.mb_start + (int64_t)seg * (D + 1);
+    m0 = __ldg(ms + d);
+    md = __ldg(ms + d + 1) - m0;
+  }
+  if (on)  // the iteration's ratio * layers (the same for all its replicas)
+    for (int s = d; s < P; s += D) {
+      const double L = (double)__ldg(p.sg.layers + (int64_t)seg * P + s);
+      s_rl[li * 2 * P + s] = __dmul_rn(p.m.ratio_f, L);
+      s_rl[li * 2 * P + P + s] = __dmul_rn(__dadd_rn(p.m.ratio_b, p.m.ratio_w), L);
+    }
+  const double* gsp = p.sg.speed + ((int64_t)seg * D + d) * P;
+  double hf[P], hb[P];
+  bool stopped = false, safe = true;
+  unsigned slow = 0;
+#pragma unroll
+  for (int s = 0; s < P; ++s) {
+    const int64_t gs = ((int64_t)seg * D + d) * P + s;
+    double sp = 1.0;
+    hf[s] = hb[s] = 0.0;
+    if (on) {
+      sp = __ldg(gsp + s);
+      if (s > 0) hf[s] = __ldg(p.sg.hop_fwd + gs - 1);
+      if (s < P - 1) hb[s] = __ldg(p.sg.hop_bwd + gs);
+    }
+    if (sp != 1.0) {
+      slow |= 1u << s;
+      safe = safe && sp >= 0x1p-100 && sp <= 0x1p100;  // recip_of(sp) != 0
+    }
+    stopped = stopped || sp <= 0.0;
+  }
+  // measured stage times (max over the TP group's device times, float4
+  // loads) and the segment's exercised-link test, both issued here so their
+  // latency overlaps the copies; kept for the epilogue
+  float* s_meas = reinterpret_cast<float*>(smem_raw + p.w_rl + (size_t)p.ipb * 2 * P * 8);
+  bool link_bad = false;
+  if (DETECT && on && md >= 0) {
+    const float* dt = p.tr.device_time + (it * D + d) * P * (int64_t)T;
+    if (p.vec4 && T == 8) {
+#pragma unroll
+      for (int s = 0; s < P; ++s) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(dt + s * 8));
+        const float4 w = __ldg(reinterpret_cast<const float4*>(dt + s * 8 + 4));
+        s_meas[s * TW + tid] = fmaxf(fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)),
+                                     fmaxf(fmaxf(w.x, w.y), fmaxf(w.z, w.w)));
+      }
+    } else {
+#pragma unroll 4
+      for (int s = 0; s < P; ++s) {
+        float mx = 0.0f;
+        if (p.vec4) {
+          for (int q = 0; q < T; q += 4) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(dt + s * T + q));
+            mx = fmaxf(mx, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
+          }
+        } else {
+          for (int q = 0; q < T; ++q) mx = fmaxf(mx, __ldg(dt + s * T + q));
+        }
+        s_meas[s * TW + tid] = mx;
+      }
+    }
+  }
+  if (DETECT && on && p.sg.link_off) {  // exercised-link ratios, split over the replicas
+    const int32_t q0 = __ldg(p.sg.link_off + seg), q1 = __ldg(p.sg.link_off + seg + 1);
+    int32_t q = q0 + d;
+    for (; q + 3 * D < q1; q += 4 * D) {
+      const double a = __ldg(p.sg.link_ratio + q), b = __ldg(p.sg.link_ratio + q + D),
+                   c = __ldg(p.sg.link_ratio + q + 2 * D), e = __ldg(p.sg.link_ratio + q + 3 * D);
+      link_bad = link_bad || a > p.thr || b > p.thr || c > p.thr || e > p.thr;
+    }
+    for (; q < q1; q += D) link_bad = link_bad || __ldg(p.sg.link_ratio + q) > p.thr;
+  }
+  mbar_wait(&s_bar, 0);  // the bulk copies have landed
+  __syncthreads();       // ... and so have the threads' edge words
+  // ---- Q_j = sum l^2 and base costs alpha*N + beta*Q_j, one thread per replica
+  if (md > p.mmax) md = -1;
+  const int m = md > 0 ? md : 0;
+  double b_lo = CUDART_INF, b_hi = 0.0;  // base-cost range (non-zero minimum)
+  if (m > 0) {
+    const double lin = __dmul_rn(p.m.alpha, (double)p.sh.token_budget);
+    const int32_t* s_off = so.dst + li * M + m0;
+    for (int j = 0; j < m; ++j) {
+      const int32_t k0 = s_off[j] - d_lo, k1 = s_off[j + 1] - d_lo;
+      unsigned long long q = 0;
+      if (staged) {
+        for (int32_t k = k0; k < k1; ++k) {
+          const long long l = sd.dst[k];
+          q += (unsigned long long)(l * l);
+        }
+      } else {
+        for (int32_t k = k0; k < k1; ++k) {
+          const long long l = __ldg(p.tr.doc_len + d_lo + k);
+          q += (unsigned long long)(l * l);
+        }
+      }
+      const double b = __dadd_rn(lin, __dmul_rn(p.m.beta, (double)(long long)q));
+      base_t[j * TW + tid] = b;
+      b_hi = b > b_hi ? b : b_hi;
+      if (b > 0.0 && b < b_lo) b_lo = b;
+    }
+  }
+  __syncthreads();  // offsets and documents are dead: the region takes the hops
+#pragma unroll
+  for (int s = 0; s < P; ++s) {
+    s_hf[s * TW + tid] = hf[s];
+    s_hb[s * TW + tid] = hb[s];
+    // (every stage: a replica whose stage s runs at 1.0 still divides when
+    // another replica of its warp runs stage s slow -- by 1.0, exactly)
+    s_inv[s * TW + tid] = (slow & (1u << s)) ? recip_of(__ldg(gsp + s)) : 1.0;
+  }
+  if (m == 0) {  // nothing runs: no speeds, no costs
+    slow = 0;
+    stopped = false;
+    safe = true;
+  }
+  const double* rl = s_rl + li * 2 * P;
+  if (slow && m > 0) {  // exact hoisted-reciprocal division needs in-range operands
+    double r_lo = CUDART_INF, r_hi = 0.0;
+#pragma unroll
+    for (int s = 0; s < P; ++s) {
+      const double f = rl[s], bw = rl[P + s];
+      r_hi = f > r_hi ? f : r_hi;
+      r_hi = bw > r_hi ? bw : r_hi;
+      if (f > 0.0 && f < r_lo) r_lo = f;
+      if (bw > 0.0 && bw < r_lo) r_lo = bw;
+    }
+    safe = safe && div_range_ok(r_lo * b_lo, r_hi * b_hi);
+  }
+  const int mm = stopped ? 0 : m;
+  const bool over = p.sh.capacity > 0 && mm > 0 && __ldg(p.sched_peak + mm) > p.sh.capacity;
+  const unsigned wslow = __reduce_or_sync(0xffffffffu, mm > 0 ? slow : 0u);
+  __syncthreads();  // hops visible
+  double fin[P], ssum[P];
+#pragma unroll
+  for (int s = 0; s < P; ++s) fin[s] = ssum[s] = 0.0;
+  if (mm > 0) {
+    const uint32_t a_bt = smem_u32(base_t + tid), a_rl = smem_u32(rl),
+                   a_hf = smem_u32(s_hf + tid), a_hb = smem_u32(s_hb + tid),
+                   a_inv = smem_u32(s_inv + tid);
+    if (safe) {
+      WideWalk<P, TW, false> w{a_bt, a_rl, a_hf, a_hb, a_inv, gsp, wslow, {}, {}, {}};
+      w.walk(mm);
+#pragma unroll
+      for (int s = 0; s < P; ++s) fin[s] = w.fin[s], ssum[s] = w.ssum[s];
+    } else {  // operands outside the hoisted-reciprocal range
+      WideWalk<P, TW, true> w{a_bt, a_rl, a_hf, a_hb, a_inv, gsp, wslow, {}, {}, {}};
+      w.walk(mm);
+#pragma unroll
+      for (int s = 0; s < P; ++s) fin[s] = w.fin[s], ssum[s] = w.ssum[s];
+    }
+  }
+  // ---- replica makespan, validation, iteration reductions
+  unsigned bits = 0;
+  uint32_t flags = 0;  // bit s: stage s flagged
+  if (on) {
+    double g = 0.0;
+#pragma unroll
+    for (int s = 0; s < P; ++s) g = fmax(g, fin[s]);
+    if (md < 0) bits |= RH_IT_OVERFLOW;
+    if (stopped && m > 0) bits |= RH_IT_STOPPED;
+    if (over) bits |= RH_IT_CAPACITY;
+    if (p.sh.has_allreduce && D > 1) g = __dadd_rn(g, __ldg(p.sg.allreduce + (int64_t)seg * D + d));
+    atomic_max_nonneg(it_ms + li, g);
+    if (DETECT && md >= 0) {
+#pragma unroll
+      for (int s = 0; s < P; ++s) {
+        const double ms_d = (double)s_meas[s * TW + tid];
+        if (!(ssum[s] <= 0.0 || ms_d <= 0.0) && ms_d > __dmul_rn(p.thr, ssum[s])) {
+          flags |= 1u << s;
+          bits |= RH_IT_STAGE_FLAG;
+        }
+      }
+    }
+    if (link_bad) bits |= RH_IT_LINK_FLAG;
+    if (bits) atomicOr(it_st + li, bits);
+  }
+  __syncthreads();
+  if (!on) return;
+  const unsigned st_bits = it_st[li];
+  const bool dead = (st_bits & (RH_IT_STOPPED | RH_IT_OVERFLOW)) != 0;
+#pragma unroll
+  for (int s = 0; s < P; ++s) {
+    const int64_t o = (it * D + d) * P + s;
+    const bool f = !dead && ((flags >> s) & 1u);
+    if (p.out.stage_cost) p.out.stage_cost[o] = dead ? 0.0 : ssum[s];
+    if (DETECT) {
+      if (p.out.stage_flag) p.out.stage_flag[o] = f ? 1 : 0;
+      if (p.out.severity)
+        p.out.severity[o] = f ? (float)__ddiv_rn(ssum[s], (double)s_meas[s * TW + tid]) : 0.0f;
+    }
+  }
+  if (d == 0) {
+    unsigned st = st_bits;
+    double ms = dead ? 0.0 : it_ms[li];
+    if (dead) st &= (RH_IT_STOPPED | RH_IT_OVERFLOW);
+    if (DETECT && !dead) {
+      const double obs = __ldg(p.tr.observed + it);
+      if (ms <= 0.0 || obs > __dmul_rn(p.thr, ms)) st |= RH_IT_ESCALATE;
+    }
+    p.out.makespan[it] = ms;
+    p.out.status[it] = (uint8_t)st;
+  }
+}
+
+template <int DETECT>
+static void* wide_kernel_t(int P) {
+  switch (P) {
+#define RH_WIDE_CASE(n) \
+  case n:               \
+    return (void*)pass_wide_kernel<n, DETECT>;
+    RH_WIDE_CASE(5)
+    RH_WIDE_CASE(6)
+    RH_WIDE_CASE(7)
+    RH_WIDE_CASE(8)
+    RH_WIDE_CASE(9)
+    RH_WIDE_CASE(10)
+    RH_WIDE_CASE(11)
+    RH_WIDE_CASE(12)
+    RH_WIDE_CASE(13)
+    RH_WIDE_CASE(14)
+    RH_WIDE_CASE(15)
+    RH_WIDE_CASE(16)
+#undef RH_WIDE_CASE
+    default: return nullptr;
+  }
+}
+
+void* wide_kernel_ptr(int P, int zbh, int detect) {
+  if (zbh) return nullptr;  // ZBH long pipelines: the lane kernel
+  return detect ? wide_kernel_t<1>(P) : wide_kernel_t<0>(P);
+}
+
+}  // namespace rh

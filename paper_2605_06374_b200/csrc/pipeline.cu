@@ -29,39 +29,15 @@
 // intrinsics: no FMA contraction anywhere.
 #include <algorithm>
 #include <type_traits>
+#include <utility>
 
 #include <math_constants.h>
 
 #include "common.cuh"
 #include "wavefront.cuh"
+#include "walks.cuh"
 
 namespace rh {
-
-struct PassParams {
-  rh_pipe_shape sh;
-  rh_cost_model m;
-  rh_segments sg;
-  rh_trace tr;
-  rh_pass_out out;
-  double thr;
-  int pw, log_pw;  // lanes per pipeline
-  int lpi;         // lanes per iteration = D * pw
-  int ipb;         // iterations per CTA
-  int mmax;        // micro-batches per replica (smem row length)
-  int vec4;        // device_time rows are float4-aligned
-  // thread-per-replica kernel only
-  const unsigned long long* sched;  // level table (sched_table)
-  const int32_t* sched_off;         // [mmax+2] first level word of each micro-batch count
-  const int32_t* sched_peak;        // [mmax+1] peak in-flight forward chunks on any stage
-  int region_off;            // smem offset of the document / base-cost region
-  int doc_stage;             // documents that fit in that region
-  int pf_stride;             // resident CTA slots: CTA b prefetches CTA b + pf_stride (0: off)
-  int static_max;  // largest micro-batch count walked by the unrolled code
-  int steady;      // m >= P: the steady-state loop walk (walk_steady)
-  // lane kernel only: level table (lane_table), NULL = closed-form walk
-  const uint16_t* ltab;
-  const int32_t *ltab_off, *ltab_nlev, *ltab_peak;  // [mmax+1] each
-};
 
 // Lane walk driven by a host-built level table (lane_table): for the
 // replica's micro-batch count mm, codes[t * P + s] is stage s's chunk at DAG
@@ -305,401 +281,6 @@ constexpr int kSmallMinBlocks = RH_SMALL_MIN_BLOCKS;  // CTAs per SM the registe
 // the per-thread register budget of the wide kernel)
 constexpr int kSmallNarrow = kSmallThreads / 2;
 
-// ---- TMA bulk staging (cp.async.bulk + mbarrier, sm_90+ / sm_100a)
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
-               : "memory");
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // visible to the TMA unit
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
-  uint32_t done = 0;
-  while (!done)
-    asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
-        "selp.u32 %0, 1, 0, p; }"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(phase)
-        : "memory");
-}
-// L2 prefetch of [p, p + bytes), trimmed inward to 16-byte alignment (a hint:
-// nothing outside the range is touched)
-__device__ __forceinline__ void prefetch_l2(const void* p, size_t bytes) {
-  const uintptr_t a = (reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15);
-  const uintptr_t b = (reinterpret_cast<uintptr_t>(p) + bytes) & ~uintptr_t(15);
-  if (b > a)
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((unsigned)(b - a))
-                 : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
-                                         uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-          "r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-// Stage n ints at src into shared memory: the 16-byte-aligned interior by
-// one TMA bulk copy (issued by thread 0, completing on `bar`), the ragged
-// head / tail words by plain loads -- nothing outside [src, src+n) is read.
-// `dst_base` is 16-byte aligned with 16 spare bytes; the returned pointer is
-// dst_base shifted by src's misalignment so the interior lines up.  Returns
-// the bytes the TMA will deliver (for the barrier's expect_tx).
-struct StagePlan {
-  int32_t* dst;
-  int head, tail;      // words loaded by threads at the front / back
-  unsigned tx_bytes;   // bytes delivered by the bulk copy
-};
-__device__ __forceinline__ StagePlan stage_plan(unsigned char* dst_base, const int32_t* src,
-                                                int n) {
-  const uintptr_t a = reinterpret_cast<uintptr_t>(src);
-  StagePlan sp;
-  sp.dst = reinterpret_cast<int32_t*>(dst_base + (a & 15));
-  const uintptr_t a16 = (a + 15) & ~uintptr_t(15), b = a + 4 * (uintptr_t)n,
-                  b16 = b & ~uintptr_t(15);
-  if (b16 > a16) {
-    sp.head = (int)((a16 - a) / 4);
-    sp.tail = (int)((b - b16) / 4);
-    sp.tx_bytes = (unsigned)(b16 - a16);
-  } else {  // too short for a bulk copy: threads load everything
-    sp.head = n;
-    sp.tail = 0;
-    sp.tx_bytes = 0;
-  }
-  return sp;
-}
-__device__ __forceinline__ void stage_issue(const StagePlan& sp, const int32_t* src,
-                                            uint64_t* bar) {
-  if (sp.tx_bytes) bulk_g2s(sp.dst + sp.head, src + sp.head, sp.tx_bytes, bar);
-}
-__device__ __forceinline__ void stage_edges(const StagePlan& sp, const int32_t* src, int n) {
-  for (int q = threadIdx.x; q < sp.head + sp.tail; q += blockDim.x) {
-    const int k = q < sp.head ? q : n - sp.tail + (q - sp.head);
-    sp.dst[k] = __ldg(src + k);
-  }
-}
-
-// sched_table entry: one 64-bit word per DAG level, 16 bits per stage:
-// 0 = idle, else kind (1 F, 2 B / BW, 3 W) | j << 2
-enum : unsigned { kOpF = 1, kOpB = 2, kOpW = 3 };
-
-// Register state of one replica's walk (references into the kernel's arrays).
-template <int P, int TW>
-struct WalkArgs {
-  static constexpr int kStride = TW;  // CTA width: base costs live [j][thread]
-  const double* bt;  // base costs of this thread: bt[j * kStride]
-  const double (&rlF)[P];
-  const double (&rlB)[P];
-  const double (&rlW)[P];
-  const double (&sp)[P];
-  const double (&inv)[P];  // recip_of(sp): exact division by div_recip
-  const double (&hf)[P];
-  const double (&hb)[P];
-  double (&fin)[P];
-  double (&ssum)[P];
-};
-
-// One chunk of stage s: c = (rl * base_j) [/ speed], start = max(chain
-// finish, dependency finish + hop), finish = start + c (pipeline.py:275-291).
-template <bool SAFE>
-__device__ __forceinline__ double chunk(double& fin, double& ssum, double rl, double b,
-                                        double sp, double inv, double dep) {
-  // (rl * b) / sp exactly as __ddiv_rn; SAFE: the walk's operand ranges were
-  // checked up front, otherwise every division is __ddiv_rn itself
-  const double a = __dmul_rn(rl, b);
-  const double c = SAFE ? div_fast(a, sp, inv) : __ddiv_rn(a, sp);
-  const double st = fin > dep ? fin : dep;
-  fin = __dadd_rn(st, c);
-  ssum = __dadd_rn(ssum, c);
-  return fin;
-}
-
-// Dynamic walk over the level table: one 64-bit word per level, 16 bits per
-// stage (0 idle, else kind | j << 2); stages in descending order.
-template <int P, int ZBH, bool SAFE, class WA>
-__device__ __forceinline__ void walk_table(const WA& a, const unsigned long long* lv,
-                                           const unsigned long long* lv_end) {
-  double lastF[P], lastB[P];
-#pragma unroll
-  for (int s = 0; s < P; ++s) lastF[s] = lastB[s] = 0.0;
-  for (; lv < lv_end; ++lv) {
-    const unsigned long long codes = __ldg(lv);
-#pragma unroll
-    for (int s = P - 1; s >= 0; --s) {
-      const unsigned code = (unsigned)(codes >> (16 * s)) & 0xffffu;
-      if (code == 0) continue;
-      const unsigned kind = code & 3u;
-      const bool isF = kind == kOpF, isB = kind == kOpB;
-      const double dF = s > 0 ? __dadd_rn(lastF[s > 0 ? s - 1 : 0], a.hf[s]) : 0.0;
-      const double dB = s < P - 1 ? __dadd_rn(lastB[s < P - 1 ? s + 1 : 0], a.hb[s]) : 0.0;
-      const double nf = chunk<SAFE>(a.fin[s], a.ssum[s],
-                                   isF ? a.rlF[s] : (isB || !ZBH ? a.rlB[s] : a.rlW[s]),
-                                   a.bt[(code >> 2) * WA::kStride], a.sp[s], a.inv[s],
-                                   isF ? dF : (isB ? dB : 0.0));
-      lastF[s] = isF ? nf : lastF[s];
-      lastB[s] = isB ? nf : lastB[s];
-    }
-  }
-}
-
-// The chunk of stage s at DAG level t for MM micro-batches (ChainLevels::at,
-// the inverse of the wavefront.cuh closed forms).  Evaluated on compile-time
-// constants inside walk_static, so it folds away.
-__host__ __device__ __forceinline__ int op_at(int P, int MM, int zbh, int t, int s, int& j) {
-  return ChainLevels{s, P, MM, (P - 1 - s) < MM ? (P - 1 - s) : MM}.at(t, zbh != 0, j);
-}
-
-// Upper bound on the DAG levels of an MM-micro-batch replica (levels past the
-// last chunk are idle and fold away).
-__host__ __device__ constexpr int n_levels(int P, int MM) { return 2 * P + 3 * MM + 2; }
-
-// Fully unrolled walk for a compile-time micro-batch count: every op, its
-// kind and j are constants, so a chunk is ~8 instructions with no dispatch.
-template <int P, int ZBH, int MM, class WA>
-__device__ __forceinline__ void walk_static(const WA& a) {
-  double lastF[P], lastB[P];
-#pragma unroll
-  for (int s = 0; s < P; ++s) lastF[s] = lastB[s] = 0.0;
-  constexpr int L = n_levels(P, MM);
-#pragma unroll
-  for (int t = 0; t < L; ++t) {
-#pragma unroll
-    for (int s = P - 1; s >= 0; --s) {
-      int j = 0;
-      const int kind = op_at(P, MM, ZBH, t, s, j);
-      if (kind == kOpF) {
-        const double dep = s > 0 ? __dadd_rn(lastF[s > 0 ? s - 1 : 0], a.hf[s]) : 0.0;
-        lastF[s] = chunk<true>(a.fin[s], a.ssum[s], a.rlF[s], a.bt[j * WA::kStride], a.sp[s],
-                         a.inv[s], dep);
-      } else if (kind == kOpB) {
-        const double dep = s < P - 1 ? __dadd_rn(lastB[s < P - 1 ? s + 1 : 0], a.hb[s]) : 0.0;
-        lastB[s] = chunk<true>(a.fin[s], a.ssum[s], a.rlB[s], a.bt[j * WA::kStride], a.sp[s],
-                         a.inv[s], dep);
-      } else if (kind == kOpW) {
-        chunk<true>(a.fin[s], a.ssum[s], a.rlW[s], a.bt[j * WA::kStride], a.sp[s], a.inv[s],
-                    0.0);
-      }
-    }
-  }
-}
-
-// Levels [T0, T1) of the MM-micro-batch walk, with the chain state passed in:
-// F / B chunks read micro-batch j at bt_fb[j * WA::kStride], W chunks (ZBH)
-// at bt_w[j * WA::kStride] (callers shift the pointers to re-base j); with
-// COOL the W chunks of the chain's tail (j >= P-1-s) are left to the caller.
-// Everything folds to constants as in walk_static.
-template <int P, int ZBH, int MM, int T0, int T1, bool COOL, class WA>
-__device__ __forceinline__ void walk_levels(const WA& a, const double* bt_fb,
-                                            const double* bt_w, double (&lastF)[P],
-                                            double (&lastB)[P]) {
-#pragma unroll
-  for (int t = T0; t < T1; ++t) {
-#pragma unroll
-    for (int s = P - 1; s >= 0; --s) {
-      int j = 0;
-      const int kind = op_at(P, MM, ZBH, t, s, j);
-      if (kind == kOpF) {
-        const double dep = s > 0 ? __dadd_rn(lastF[s > 0 ? s - 1 : 0], a.hf[s]) : 0.0;
-        lastF[s] = chunk<true>(a.fin[s], a.ssum[s], a.rlF[s], bt_fb[j * WA::kStride], a.sp[s],
-                               a.inv[s], dep);
-      } else if (kind == kOpB) {
-        const double dep = s < P - 1 ? __dadd_rn(lastB[s < P - 1 ? s + 1 : 0], a.hb[s]) : 0.0;
-        lastB[s] = chunk<true>(a.fin[s], a.ssum[s], a.rlB[s], bt_fb[j * WA::kStride], a.sp[s],
-                               a.inv[s], dep);
-      } else if (kind == kOpW && !(COOL && j >= P - 1 - s)) {
-        chunk<true>(a.fin[s], a.ssum[s], a.rlW[s], bt_w[j * WA::kStride], a.sp[s], a.inv[s],
-                    0.0);
-      }
-    }
-  }
-}
-
-// Walk for any m >= P micro-batches with a compact steady state.  The level
-// pattern of m >= P micro-batches is: levels [0, 2P-1) as for m = P
-// (warm-up: every j involved is < P); then m - P level pairs in which every
-// stage does one F and one B -- at level 2P-1+2k even stages do B_{k+s/2}
-// and odd stages F_{P+k-(s+1)/2}, at the next level even stages do
-// F_{P+k-s/2} and odd stages B_{k+(s+1)/2}; then the cool-down, the m = P
-// pattern from level 2P-1 on with every F / B j shifted by m - P.  ZBH: the
-// cool-down's W chunks with j < P-1-s keep their j, and each stage's chain
-// ends with W_j for j = P-1-s .. m-1, walked last (a W chunk feeds only its
-// own stage's chain, so only the per-stage chain order matters for it).
-// The F / B order (stages descending within a level) and every stage's chain
-// order equal the level-ordered walk's; checked against the closed-form
-// levels for P <= 8, m < 40 (1F1B) and m < 30 (ZBH).  The steady pair is a
-// loop whose body stays in the instruction cache; warm-up and cool-down are
-// unrolled.
-template <int P, int ZBH, class WA>
-__device__ __forceinline__ void walk_steady(const WA& a, int m) {
-  double lastF[P], lastB[P];
-#pragma unroll
-  for (int s = 0; s < P; ++s) lastF[s] = lastB[s] = 0.0;
-  walk_levels<P, ZBH, P, 0, 2 * P - 1, false>(a, a.bt, a.bt, lastF, lastB);
-  const double* bk = a.bt;
-  for (int k = 0; k < m - P; ++k, bk += WA::kStride) {
-#pragma unroll
-    for (int s = P - 1; s >= 0; --s) {  // level 2P-1+2k
-      if (s % 2 == 0) {
-        const double dep = s < P - 1 ? __dadd_rn(lastB[s < P - 1 ? s + 1 : 0], a.hb[s]) : 0.0;
-        lastB[s] = chunk<true>(a.fin[s], a.ssum[s], a.rlB[s], bk[(s / 2) * WA::kStride],
-                               a.sp[s], a.inv[s], dep);
-      } else {
-        const double dep = __dadd_rn(lastF[s > 0 ? s - 1 : 0], a.hf[s]);
-        lastF[s] = chunk<true>(a.fin[s], a.ssum[s], a.rlF[s],
-                               bk[(P - (s + 1) / 2) * WA::kStride], a.sp[s], a.inv[s], dep);
-      }
-    }
-#pragma unroll
-    for (int s = P - 1; s >= 0; --s) {  // level 2P+2k
-      if (s % 2 == 0) {
-        const double dep = s > 0 ? __dadd_rn(lastF[s > 0 ? s - 1 : 0], a.hf[s]) : 0.0;
-        lastF[s] = chunk<true>(a.fin[s], a.ssum[s], a.rlF[s], bk[(P - s / 2) * WA::kStride],
-                               a.sp[s], a.inv[s], dep);
-      } else {
-        const double dep = s < P - 1 ? __dadd_rn(lastB[s < P - 1 ? s + 1 : 0], a.hb[s]) : 0.0;
-        lastB[s] = chunk<true>(a.fin[s], a.ssum[s], a.rlB[s],
-                               bk[((s + 1) / 2) * WA::kStride], a.sp[s], a.inv[s], dep);
-      }
-    }
-  }
-  walk_levels<P, ZBH, P, 2 * P - 1, n_levels(P, P), true>(a, a.bt + (m - P) * WA::kStride,
-                                                          a.bt, lastF, lastB);
-  if (ZBH) {
-#pragma unroll
-    for (int s = P - 1; s >= 0; --s)
-      for (int j = P - 1 - s; j < m; ++j)
-        chunk<true>(a.fin[s], a.ssum[s], a.rlW[s], a.bt[j * WA::kStride], a.sp[s], a.inv[s],
-                    0.0);
-  }
-}
-
-constexpr int kStaticMaxMB = 12;  // RH_STATIC_MAX_MB-style cap on the unrolled walks (m < P in practice)
-
-// Replicas with m >= P take walk_steady, so the kernels carry unrolled walks
-// only for m < P (less code competing for the instruction cache); the level
-// table covers the rest.
-template <int P, int ZBH, int MM = 1, class WA>
-__device__ __forceinline__ bool walk_static_dispatch(const WA& a, int mm) {
-  if constexpr (MM > P - 1) {
-    return false;
-  } else {
-    if (mm == MM) {
-      walk_static<P, ZBH, MM>(a);
-      return true;
-    }
-    return walk_static_dispatch<P, ZBH, MM + 1>(a, mm);
-  }
-}
-
-// Shared-memory layout of the thread-per-replica kernels:
-//   [it_ms | it_st][q: ipb*M int64][off: 16 + 4*(ipb*M+1)][documents -> base costs]
-struct CtaStage {
-  double* it_ms;
-  unsigned* it_st;
-  unsigned long long* s_q;
-  double* base_t;
-  int n_it, n_mb;
-};
-
-__device__ __forceinline__ CtaStage cta_layout(const PassParams& p, unsigned char* smem_raw) {
-  CtaStage c;
-  const int M = p.sh.micro_batches;
-  c.it_ms = reinterpret_cast<double*>(smem_raw);
-  c.it_st = reinterpret_cast<unsigned*>(c.it_ms + p.ipb);
-  const int it_bytes = ((p.ipb * 12 + 15) / 16) * 16;
-  c.s_q = reinterpret_cast<unsigned long long*>(smem_raw + it_bytes);
-  c.base_t = reinterpret_cast<double*>(smem_raw + p.region_off);
-  const int64_t it0 = (int64_t)blockIdx.x * p.ipb;
-  c.n_it = (int)min((int64_t)p.ipb, p.tr.n_iter - it0);
-  c.n_mb = c.n_it * M;
-  return c;
-}
-
-// Phase A of the CTA staging: thread 0 arms the mbarrier and issues the TMA
-// bulk copies of the offsets and (when they fit) the documents; everybody
-// loads the ragged edges.  Per-thread loads issued between stage_begin and
-// stage_finish overlap the copies.
-struct StageState {
-  StagePlan so, sd;
-  const int32_t* g_off;
-  int32_t d_lo;
-  int n_doc;
-  bool staged;
-};
-
-__device__ __forceinline__ StageState stage_begin(const PassParams& p, unsigned char* smem_raw,
-                                                  const CtaStage& c, uint64_t* bar) {
-  const int M = p.sh.micro_batches;
-  const int it_bytes = ((p.ipb * 12 + 15) / 16) * 16;
-  int32_t* s_off_raw = reinterpret_cast<int32_t*>(
-      smem_raw + ((it_bytes + 8 * (size_t)p.ipb * M + 15) & ~size_t(15)));
-  StageState g;
-  const int64_t it0 = (int64_t)blockIdx.x * p.ipb;
-  g.g_off = p.tr.mb_off + it0 * M;
-  g.d_lo = __ldg(g.g_off);
-  g.n_doc = __ldg(g.g_off + c.n_mb) - g.d_lo;
-  g.staged = g.n_doc <= p.doc_stage;
-  g.so = stage_plan(reinterpret_cast<unsigned char*>(s_off_raw), g.g_off, c.n_mb + 1);
-  g.sd = g.staged ? stage_plan(reinterpret_cast<unsigned char*>(c.base_t), p.tr.doc_len + g.d_lo,
-                               g.n_doc)
-                  : StagePlan{nullptr, 0, 0, 0u};
-  if (threadIdx.x == 0) {
-    mbar_init(bar, 1);
-    mbar_arrive_expect_tx(bar, g.so.tx_bytes + g.sd.tx_bytes);
-    stage_issue(g.so, g.g_off, bar);
-    if (g.staged) stage_issue(g.sd, p.tr.doc_len + g.d_lo, bar);
-  }
-  // nobody may poll the barrier before thread 0 has initialised it (the word
-  // may still hold a previous CTA's state)
-  __syncthreads();
-  stage_edges(g.so, g.g_off, c.n_mb + 1);
-  if (g.staged) stage_edges(g.sd, p.tr.doc_len + g.d_lo, g.n_doc);
-  return g;
-}
-
-// Phase B: wait for the copies, then Q_j = sum l^2, one thread per
-// micro-batch, into s_q; the document buffer is dead afterwards.
-__device__ __forceinline__ void stage_finish(const PassParams& p, const CtaStage& c,
-                                             const StageState& g, uint64_t* bar) {
-  mbar_wait(bar, 0);  // the bulk copies have landed
-  __syncthreads();    // ... and so have the threads' edge words
-  const int32_t* s_off = g.so.dst;
-  const int32_t* s_doc = g.sd.dst;
-  for (int mb = threadIdx.x; mb < c.n_mb; mb += blockDim.x) {
-    const int32_t k0 = s_off[mb] - g.d_lo, k1 = s_off[mb + 1] - g.d_lo;
-    unsigned long long q = 0;
-    if (g.staged) {
-      // packed bins hold few documents (C2: 2.4 on average, at most 4): the
-      // first four are summed branch-free with predicated loads
-      const int32_t nd = k1 - k0;
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const long long l = t < nd ? s_doc[k0 + t] : 0;
-        q += (unsigned long long)(l * l);
-      }
-      for (int32_t k = k0 + 4; k < k1; ++k) {
-        const long long l = s_doc[k];
-        q += (unsigned long long)(l * l);
-      }
-    } else {  // too many documents to stage: straight from global memory
-      for (int32_t k = k0; k < k1; ++k) {
-        const long long l = __ldg(p.tr.doc_len + g.d_lo + k);
-        q += (unsigned long long)(l * l);
-      }
-    }
-    c.s_q[mb] = q;
-  }
-  __syncthreads();  // sums complete; the document buffer is dead from here
-}
-
 #ifdef RH_DETECT_TRACE
 // debug build only (tools/detect_trace.py): per CTA, warp 0's globaltimer at
 // the phase boundaries of pass_small_kernel, and the SM it ran on
@@ -942,13 +523,15 @@ __global__ void __launch_bounds__(TW, (ZBH ? 4 : kSmallMinBlocks) * (kSmallThrea
 }
 
 // Level table for (P, schedule, mmax): for every micro-batch count
-// mm = 0..mmax, one 64-bit word per DAG level holding each stage's chunk at
-// that level (wavefront.cuh closed forms; a chain has at most one chunk per
-// level).  Device layout [off: mmax+2 int32, padded to 8 B][levels: uint64].
+// mm = 0..mmax, kWords = ceil(P/4) 64-bit words per DAG level holding each
+// stage's chunk at that level, 16 bits per stage (wavefront.cuh closed forms;
+// a chain has at most one chunk per level).  Device layout [off: mmax+2
+// int32 (word offsets) | peak: mmax+1 int32, padded to 8 B][level words].
 // Built once per context.
 static int sched_table(rh_ctx* ctx, int P, int zbh, int mmax,
                        const unsigned long long** lv_out, const int32_t** off_out,
                        const int32_t** peak_out) {
+  const int W = (P + 3) / 4;
   // [off: mmax+2][peak: mmax+1] int32, padded to 8 B, then the level words
   const size_t off_words = ((size_t)(2 * mmax + 3) + 1) & ~size_t(1);
   auto view = [&](void* dev) {
@@ -970,8 +553,9 @@ static int sched_table(rh_ctx* ctx, int P, int zbh, int mmax,
     if (mm == 0) continue;
     const size_t base = v.size();
     auto put = [&](int level, int s, unsigned kind, int j) {
-      if ((size_t)level >= v.size() - base) v.resize(base + level + 1, 0ull);
-      v[base + level] |= (unsigned long long)(kind | ((unsigned)j << 2)) << (16 * s);
+      const size_t at = base + (size_t)level * W + s / 4;
+      if (at >= v.size()) v.resize(base + (size_t)(level + 1) * W, 0ull);
+      v[at] |= (unsigned long long)(kind | ((unsigned)j << 2)) << (16 * (s % 4));
     };
     for (int s = 0; s < P; ++s) {
       const ChainLevels lv{s, P, mm, std::min(P - 1 - s, mm)};
@@ -985,8 +569,8 @@ static int sched_table(rh_ctx* ctx, int P, int zbh, int mmax,
     int peak = 0;
     for (int s = 0; s < P; ++s) {
       int live = 0;
-      for (size_t t = base; t < v.size(); ++t) {
-        const unsigned kind = (unsigned)(v[t] >> (16 * s)) & 3u;
+      for (size_t t = base + s / 4; t < v.size(); t += W) {
+        const unsigned kind = (unsigned)(v[t] >> (16 * (s % 4))) & 3u;
         if (kind == kOpF) peak = std::max(peak, ++live);
         if (kind == kOpB) --live;
       }
@@ -1184,6 +768,41 @@ int launch_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
       RH_CUDA(cudaLaunchKernel(kern, dim3((unsigned)blocks), dim3(threads), args, smem, stream));
       RH_CHECK_LAUNCH(ctx);
       return RH_OK;
+    }
+  }
+  if (P >= 5 && P <= 16 && D <= kWideThreads && p.mmax < 16384 && !getenv("RH_FORCE_LANE_KERNEL")) {
+    const bool zbh = sh->schedule == RH_SCHED_ZBH;
+    void* kern = wide_kernel_ptr(P, zbh ? 1 : 0, detect);
+    if (kern) {
+      constexpr int tw = kWideThreads;
+      p.ipb = std::max(1, tw / D);
+      auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
+      const size_t it_bytes = al((size_t)p.ipb * 12);
+      p.w_base = (int)it_bytes;
+      p.w_rl = (int)al(p.w_base + (size_t)tw * p.mmax * 8);
+      // [rl: ipb][2][P] doubles, then the measured stage times [P][TW] float
+      p.w_union = (int)al(p.w_rl + (size_t)p.ipb * 2 * P * 8 + (size_t)P * tw * 4);
+      const size_t off_bytes = al(16 + 4 * ((size_t)p.ipb * M + 1));
+      p.w_docs = (int)(p.w_union + off_bytes);
+      const size_t hops = 3 * (size_t)P * tw * 8;  // hf, hb, inv
+      // documents: what the hop area leaves, at least ~3 per micro-batch
+      const size_t docs = std::max<size_t>(hops > off_bytes ? hops - off_bytes : 0,
+                                           16 + 12 * (size_t)p.ipb * M);
+      p.doc_stage = (int)((docs - 16) / 4);
+      const size_t smem = p.w_docs + docs;
+      if (smem <= ctx->smem_optin) {
+        if (int e = sched_table(ctx, P, zbh, p.mmax, &p.sched, &p.sched_off, &p.sched_peak))
+          return e;
+        const int64_t blocks = (tr->n_iter + p.ipb - 1) / p.ipb;
+        if (int e = ensure_smem(ctx, kern, smem)) return e;
+        int occ = 0;
+        RH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, tw, smem));
+        p.pf_stride = getenv("RH_NO_L2_PREFETCH") ? 0 : occ * ctx->num_sms;
+        void* args[] = {&p};
+        RH_CUDA(cudaLaunchKernel(kern, dim3((unsigned)blocks), dim3(tw), args, smem, stream));
+        RH_CHECK_LAUNCH(ctx);
+        return RH_OK;
+      }
     }
   }
   p.ipb = std::max(1, 256 / p.lpi);

@@ -79,18 +79,18 @@ __device__ __forceinline__ double recip_of(double b) {
 
 struct ChainLevels {
   int s, P, m, w;
-  __host__ __device__ __forceinline__ int F(int j) const {
+  __host__ __device__ __forceinline__ constexpr int F(int j) const {
     return j >= m ? INT_MAX : (j <= w ? s + j : 2 * j + s);
   }
-  __host__ __device__ __forceinline__ int B(int j) const { return j >= m ? INT_MAX : 2 * P - 1 - s + 2 * j; }
-  __host__ __device__ __forceinline__ int W(int j) const {
+  __host__ __device__ __forceinline__ constexpr int B(int j) const { return j >= m ? INT_MAX : 2 * P - 1 - s + 2 * j; }
+  __host__ __device__ __forceinline__ constexpr int W(int j) const {
     if (j >= m) return INT_MAX;
     if (j < w) return 2 * P - s + 2 * (m - w + j);
     return (w > 0 ? 2 * P - s + 2 * m - 2 : 2 * P - 1 - s + 2 * (m - 1)) + (j - w + 1);
   }
   // Inverse: the chunk of this chain at level t -- kind 1 F, 2 B/BW, 3 W (ZBH),
   // 0 none -- and its micro-batch j.  A chain holds at most one chunk per level.
-  __host__ __device__ __forceinline__ int at(int t, bool zbh, int& j) const {
+  __host__ __device__ __forceinline__ constexpr int at(int t, bool zbh, int& j) const {
     const int k = t - s;
     if (k >= 0 && k <= w && k < m) {
       j = k;
@@ -122,7 +122,7 @@ struct ChainLevels {
     return 0;
   }
   // one past the last level of the chain
-  __host__ __device__ __forceinline__ int end(bool zbh) const {
+  __host__ __device__ __forceinline__ constexpr int end(bool zbh) const {
     return m == 0 ? 0 : 1 + (zbh ? W(m - 1) : B(m - 1));
   }
 };
