@@ -90,6 +90,12 @@ int64_t orc_search_size(const orc_search* s);
  * capacity) + amortised reconfiguration surcharge; +inf when infeasible */
 double orc_search_score(orc_search* s, int64_t index);
 /* lexicographic (score, index) min over [begin, end) on n_threads */
+/* the same scores and (score, index) winner, with each replica pipeline's
+ * critical path computed once per (layout, partition, replica, first
+ * micro-batch, count) and reused across assignment variants (max is exact):
+ * full-space argmin at 10^6-10^7 candidates in seconds */
+int orc_search_eval_memo(orc_search* s, int64_t begin, int64_t end, int n_threads,
+                         double* best_score, int64_t* best_index, double* scores);
 int orc_search_eval(orc_search* s, int64_t begin, int64_t end, int n_threads,
                     double* best_score, int64_t* best_index, double* scores);
 int orc_search_decode(orc_search* s, int64_t index, rh_candidate* out, int32_t* groups,

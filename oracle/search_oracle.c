@@ -492,3 +492,183 @@ int orc_search_decode(orc_search* s, int64_t index, rh_candidate* out, int32_t* 
   if (counts) for (int q = 0; q < l->D; ++q) counts[q] = cnt[q];
   return 0;
 }
+
+/*
+ * Full-space argmin at the benchmarked sizes (10^6-10^7 candidates).  The
+ * canonical DAG of a candidate is D disconnected replica pipelines plus one
+ * terminal all-reduce vertex per replica (pipeline.py:242-254), so Kahn's
+ * relaxation gives makespan = max_d RN(fin_d + AR) with fin_d the replica's
+ * own critical path (AR >= 0; an empty replica contributes RN(0 + AR)), and
+ * the candidate is infeasible when any replica is (a stopped stage with
+ * work, or the activation check).  fin_d depends only on (layout, partition
+ * variant, replica, first micro-batch, count): it is computed ONCE per such
+ * key -- by the same literal build_dag + critical_path (dag_iteration on the
+ * replica alone, D = 1) -- and reused across the assignment variants, which
+ * only shift replica boundaries.  The max is exact, so scores equal
+ * score_with() bit for bit (tests/test_search_oracle.py checks it).
+ */
+typedef struct {
+  int32_t r, start, cnt, used;
+  double fin;
+  int bad;
+} memo_e;
+
+typedef struct {
+  memo_e* tab;
+  int cap;
+} memo_t;
+
+static memo_e* memo_get(memo_t* m, int r, int start, int cnt) {
+  uint32_t h = (uint32_t)r * 2654435761u ^ (uint32_t)start * 40503u ^ (uint32_t)cnt * 97u;
+  for (int k = 0;; ++k) {
+    memo_e* e = &m->tab[(h + (uint32_t)k) & (uint32_t)(m->cap - 1)];
+    if (!e->used) {
+      e->used = 1; e->r = r; e->start = start; e->cnt = cnt; e->bad = -1;
+      return e;
+    }
+    if (e->r == r && e->start == start && e->cnt == cnt) return e;
+  }
+}
+
+typedef struct {
+  orc_search* s;
+  int64_t begin, end;
+  int64_t* next_block; /* shared work counter over (layout, partition) blocks */
+  pthread_mutex_t* mu;
+  double best;
+  int64_t best_i;
+  double* scores;
+} mjob_t;
+
+static void memo_block(mjob_t* J, void* scr, memo_t* memo, int li, int v) {
+  orc_search* s = J->s;
+  const rh_search_desc* d = &s->d;
+  const layout_t* l = &s->L[li];
+  const int T = l->T, D = l->D, P = l->P, M = d->n_micro_batches;
+  const int64_t b0 = l->base + (int64_t)v * l->nu;
+  const int64_t lo = b0 > J->begin ? b0 : J->begin;
+  const int64_t hi = b0 + l->nu < J->end ? b0 + l->nu : J->end;
+  if (lo >= hi) return;
+  int part[64], cnt[64], li2;
+  /* the block's partition (decode of its first candidate; u only moves counts) */
+  int part_ok = decode(s, b0, &li2, part, cnt);
+  for (int q = 0; q < P; ++q) part_ok &= part[q] >= d->min_layers;
+  double ar_v = 0.0;
+  if (d->has_comm && D > 1)
+    for (int st = 0; st < P; ++st) {
+      double nbytes = (double)part[st] * d->layer_bytes;
+      double x = 2.0 * nbytes * (double)(D - 1) / ((double)D * l->ring[st]);
+      if (x > ar_v) ar_v = x;
+    }
+  const int use_ar = d->has_comm && D > 1;
+  /* surcharge (as in score_with) */
+  int changed = 0;
+  long long moved = 0;
+  if (P == d->cur_pp)
+    for (int q = 0; q < P; ++q) {
+      if (part[q] != s->cur_part[q]) changed = 1;
+      if (part[q] > s->cur_part[q]) moved += part[q] - s->cur_part[q];
+    }
+  double reshard = 0.0;
+  if (!l->same)
+    for (int r = 0; r < D; ++r)
+      for (int q = 0; q < P; ++q) reshard += (double)part[q] * d->layer_bytes;
+  double sur = 0.0;
+  if (!l->same || changed) {
+    double transfer = ((double)moved * d->layer_bytes + reshard) / s->worst_inter;
+    int am = d->amortize_iterations > 1 ? d->amortize_iterations : 1;
+    sur = (d->group_rebuild_s + transfer) / (double)am;
+  }
+  memset(memo->tab, 0, sizeof(memo_e) * (size_t)memo->cap);
+  rh_pipe_shape sh = {P, 1, T, d->schedule, M, d->token_budget, d->capacity, 0, 0};
+  for (int64_t idx = lo; idx < hi; ++idx) {
+    double score = INFINITY;
+    if (part_ok && decode(s, idx, &li2, part, cnt)) {
+      int start = 0, bad = 0;
+      double ms = 0.0;
+      for (int r = 0; r < D && !bad; ++r) {
+        memo_e* e = memo_get(memo, r, start, cnt[r]);
+        if (e->bad < 0) {
+          int mbs[2] = {start, start + cnt[r]};
+          rh_segments sg = {1, part, mbs, l->gspeed + (size_t)r * P, l->hop + (size_t)r * P,
+                            l->hop + (size_t)r * P, NULL, NULL, NULL};
+          double f = 0.0;
+          uint8_t stt = orc_dag_iteration((struct scratch_s*)scr, &sh, &d->model, &sg, 0, &f,
+                                          NULL);
+          e->bad = stt != 0;
+          e->fin = cnt[r] > 0 ? f : 0.0;
+        }
+        bad |= e->bad;
+        double c = use_ar ? e->fin + ar_v : e->fin;
+        if (c > ms) ms = c;
+        start += cnt[r];
+      }
+      if (!bad) score = ms + sur;
+    }
+    if (J->scores) J->scores[idx - J->begin] = score;
+    /* lexicographic (score, index) over feasible candidates */
+    if (score < INFINITY &&
+        (J->best_i < 0 || score < J->best || (score == J->best && idx < J->best_i))) {
+      J->best = score;
+      J->best_i = idx;
+    }
+  }
+}
+
+static void* mworker(void* arg) {
+  mjob_t* J = arg;
+  orc_search* s = J->s;
+  void* scr = new_scratch(s);
+  memcpy(orc_scratch_quad(scr), s->quad, sizeof(int64_t) * s->d.n_micro_batches);
+  memo_t memo;
+  memo.cap = 1;
+  while (memo.cap < 64 * (s->maxD > 0 ? s->maxD : 1)) memo.cap <<= 1;
+  memo.tab = malloc(sizeof(memo_e) * (size_t)memo.cap);
+  J->best = INFINITY;
+  J->best_i = -1;
+  /* blocks enumerated in index order: (layout, partition variant) */
+  int64_t nblocks = 0;
+  for (int li = 0; li < s->nl; ++li) nblocks += s->L[li].nv;
+  for (;;) {
+    pthread_mutex_lock(J->mu);
+    int64_t k = (*J->next_block)++;
+    pthread_mutex_unlock(J->mu);
+    if (k >= nblocks) break;
+    int li = 0;
+    int64_t kk = k;
+    while (kk >= s->L[li].nv) kk -= s->L[li++].nv;
+    memo_block(J, scr, &memo, li, (int)kk);
+  }
+  free(memo.tab);
+  orc_scratch_delete(scr);
+  return NULL;
+}
+
+int orc_search_eval_memo(orc_search* s, int64_t begin, int64_t end, int n_threads,
+                         double* best_score, int64_t* best_index, double* scores) {
+  if (n_threads <= 0) n_threads = (int)sysconf(_SC_NPROCESSORS_ONLN);
+  if (n_threads < 1) n_threads = 1;
+  pthread_t* th = malloc(sizeof(pthread_t) * n_threads);
+  mjob_t* jobs = malloc(sizeof(mjob_t) * n_threads);
+  int64_t next = 0;
+  pthread_mutex_t mu = PTHREAD_MUTEX_INITIALIZER;
+  for (int k = 0; k < n_threads; ++k) {
+    jobs[k] = (mjob_t){s, begin, end, &next, &mu, INFINITY, -1, scores};
+    if (n_threads == 1) mworker(&jobs[0]);
+    else pthread_create(&th[k], NULL, mworker, &jobs[k]);
+  }
+  if (n_threads > 1) for (int k = 0; k < n_threads; ++k) pthread_join(th[k], NULL);
+  double b = INFINITY;
+  int64_t bi = -1;
+  for (int k = 0; k < n_threads; ++k) {
+    if (jobs[k].best_i < 0) continue;
+    if (bi < 0 || jobs[k].best < b || (jobs[k].best == b && jobs[k].best_i < bi)) {
+      b = jobs[k].best;
+      bi = jobs[k].best_i;
+    }
+  }
+  *best_score = b;
+  *best_index = bi;
+  free(th); free(jobs);
+  return 0;
+}

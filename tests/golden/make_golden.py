@@ -454,6 +454,121 @@ def gen_search():
     dump("search", {"cases": out})
 
 
+# ------------------------------------------------ benchmarked search spaces
+_SB = {}  # (reference problem, oracle) of the space being scored (fork-shared)
+
+
+def _ref_state_of(st_m):
+    """This package's ClusterState -> the reference's (same fields)."""
+    return rc.ClusterState(
+        devices=[rc.Device(d.id, d.node_id, d.speed, d.status) for d in st_m.devices],
+        devices_per_node=st_m.devices_per_node, tp_groups=dict(st_m.tp_groups),
+        intra_bw=st_m.intra_bw, inter_bw=st_m.inter_bw, link_factors=dict(st_m.link_factors))
+
+
+def _ref_score(idx):
+    """The reference's evaluate_plan + reconfig_cost of candidate idx (decoded
+    by the oracle: placement groups, partition, counts) -> [idx, ms, extra]."""
+    st_r, cfg_r, mbs_r, model_r, comm_r, cap, srch = _SB["problem"]
+    c = srch.decode(idx)
+    if not c.feasible:
+        return [idx, None, "infeasible variant"]
+    st2 = st_r.copy()
+    st2.tp_groups = {(g // c.pp, g % c.pp): tuple(m) for g, m in enumerate(c.groups)}
+    members = {m for g in c.groups for m in g}
+    for dev in st2.devices:
+        if dev.status == rc.FAIL_STOP:
+            continue
+        dev.status = ((rc.FAIL_SLOW if dev.speed < 1.0 else rc.HEALTHY)
+                      if dev.id in members else rc.STANDBY)
+    # the config keeps the NOMINAL TP degree: a c.tp-wide group runs at
+    # slowest * c.tp / nominal (effective_stage_speed, cluster.py:155-169)
+    cfg2 = rc.ParallelismConfig(tp=cfg_r.tp, dp=c.dp, pp=c.pp, schedule=cfg_r.schedule,
+                                layer_partition=list(c.partition))
+    plan = rs.AdaptationPlan(dp_assignment=list(c.counts))
+    try:
+        ms = rs.evaluate_plan(plan, st2, cfg2, mbs_r, model_r, comm=comm_r, capacity=cap)
+    except rp.SimulationError as exc:
+        return [idx, None, str(exc)[:40]]
+    T, D, P = cfg_r.tp, cfg_r.dp, cfg_r.pp
+    same = (c.tp == T and c.dp == D and c.pp == P and
+            all(tuple(sorted(st_r.tp_groups[(g // P, g % P)])) == tuple(m)
+                for g, m in enumerate(c.groups)))
+    if same:  # the reference's own reconfig_cost
+        rplan = rs.AdaptationPlan(layer_partition=list(c.partition))
+        reconf = rs.reconfig_cost(rplan, st_r, cfg_r, layer_bytes=256.0 * 2**20)
+    else:      # DESIGN.md §5 extension: full reshard over the worst link
+        moved = (sum(max(0, a - b) for a, b in zip(c.partition, cfg_r.layer_partition))
+                 if c.pp == P else 0)
+        reshard = 0.0
+        for _d in range(c.dp):
+            for q in range(c.pp):
+                reshard += c.partition[q] * (256.0 * 2**20)
+        worst = st_r.inter_bw * min(st_r.link_factors.values(), default=1.0)
+        reconf = 2.0 + (moved * (256.0 * 2**20) + reshard) / worst
+    return [idx, ms, reconf / max(1, 25)]
+
+
+def gen_search_bench(per_config=1200):
+    """Reference-scored candidates of the BENCHMARKED re-plan spaces (bench.py's
+    C3 / C4 / C5, replan_scenarios.py): per config >= 10^3 indices -- every
+    layout's first and last candidate, the oracle's full-space winner and its
+    neighbourhood, stratified random picks per layout (proportional to its
+    size, at least 4 each) and uniform random picks -- each scored by the
+    reference's evaluate_plan + reconfig_cost on the decoded plan, in parallel
+    over the host cores (one process per candidate batch)."""
+    import multiprocessing as mp
+
+    from paper_2605_06374_b200.comm import CommSpec as MCS  # noqa: F401
+    from paper_2605_06374_b200.replan_scenarios import replan_problem
+    from tests.oracle_bind import Oracle
+
+    oracle = Oracle()
+    out = {}
+    for name in ("C3", "C4", "C5"):
+        st_m, cfg_m, mbs_m, inputs = replan_problem(name)
+        srch = oracle.search(inputs)
+        best, bi = srch.best_memo()
+        rng = random.Random(sum(map(ord, name)) * 7)
+        picks = {0, srch.size - 1, bi}
+        picks |= {min(srch.size - 1, max(0, bi + k)) for k in range(-24, 25)}
+        d = inputs.desc
+        # layouts: bases from decode of increasing indices (the oracle's order)
+        lay = {}
+        i = 0
+        while i < srch.size:  # walk the layouts: (layout, partition, count) blocks
+            c = srch.decode(i)
+            lay.setdefault(len(lay), [i, i])
+            # jump to the next layout: its size is nv * nu
+            nv = 2 + c.pp * (c.pp - 1)
+            nu = 2 + c.dp * (c.dp - 1)
+            j = i - (c.partition_variant * nu + c.count_variant) + nv * nu
+            lay[len(lay) - 1][1] = j - 1
+            i = j
+        for li, (a, b) in lay.items():
+            picks |= {a, b}
+            k = max(4, int(per_config * 0.6 * (b - a + 1) / srch.size))
+            picks |= {rng.randint(a, b) for _ in range(k)}
+        while len(picks) < per_config:
+            picks.add(rng.randrange(srch.size))
+        picks = sorted(picks)
+        st_r = _ref_state_of(st_m)
+        cfg_r = rc.ParallelismConfig(tp=cfg_m.tp, dp=cfg_m.dp, pp=cfg_m.pp, schedule=cfg_m.schedule,
+                                     layer_partition=list(cfg_m.layer_partition))
+        mbs_r = [rw.MicroBatch(id=mb.id, doc_lengths=tuple(mb.doc_lengths),
+                               token_budget=mb.token_budget) for mb in mbs_m]
+        model_r = rw.CostModel(alpha=2e-6, beta=5e-10)
+        _SB["problem"] = (st_r, cfg_r, mbs_r, model_r, CommSpec(), cfg_m.pp + 2, srch)
+        with mp.get_context("fork").Pool(os.cpu_count() or 1) as pool:
+            rows = pool.map(_ref_score, picks, chunksize=4)
+        n_ok = sum(r[1] is not None for r in rows)
+        out[name] = {"size": srch.size, "devices": d.n_devices, "layouts": len(lay),
+                     "oracle_best": [best, bi], "rows": rows}
+        print(name, "size", srch.size, "layouts", len(lay), "scored", len(rows), "finite", n_ok,
+              "best", best, bi, flush=True)
+    dump("search_bench", out)
+
+
 # ----------------------------------------------------------------- migration
 def gen_migration():
     """Reference plan_migration (scheduler.py:272-513) on random problems."""
@@ -577,6 +692,6 @@ def gen_policies():
 
 if __name__ == "__main__":
     which = sys.argv[1:] or ["workload", "pipeline", "detector", "scheduler", "search",
-                             "migration", "policies"]
+                             "search_bench", "migration", "policies"]
     for w in which:
         globals()[f"gen_{w}"]()

@@ -93,6 +93,7 @@ class Oracle:
         L.orc_search_score.restype = C.c_double
         L.orc_search_eval.argtypes = [p, C.c_int64, C.c_int64, C.c_int, C.POINTER(C.c_double),
                                       C.POINTER(C.c_int64), p]
+        L.orc_search_eval_memo.argtypes = L.orc_search_eval.argtypes
         L.orc_search_decode.argtypes = [p, C.c_int64, C.POINTER(Candidate), p, p, p]
 
     # ------------------------------------------------------------ search
@@ -237,6 +238,16 @@ class OracleSearch:
         sc = np.zeros(max(end - begin, 1)) if with_scores else None
         self.o.lib.orc_search_eval(self.h, begin, end, threads, C.byref(b), C.byref(i),
                                    None if sc is None else sc.ctypes.data)
+        return (b.value, i.value, sc[:end - begin]) if with_scores else (b.value, i.value)
+
+    def best_memo(self, begin=0, end=None, threads=0, with_scores=False):
+        """orc_search_eval_memo: the same scores / winner, replica pipelines
+        memoised across assignment variants (full-space scans at C3-C5)."""
+        end = self.size if end is None else end
+        b, i = C.c_double(), C.c_int64()
+        sc = np.zeros(max(end - begin, 1)) if with_scores else None
+        self.o.lib.orc_search_eval_memo(self.h, begin, end, threads, C.byref(b), C.byref(i),
+                                        None if sc is None else sc.ctypes.data)
         return (b.value, i.value, sc[:end - begin]) if with_scores else (b.value, i.value)
 
     def decode(self, index: int):

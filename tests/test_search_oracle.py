@@ -50,6 +50,67 @@ def test_oracle_best_is_lexicographic_min(oracle, k):
         assert got == (best, bi)
 
 
+# ------------------------------------------- the benchmarked spaces C3-C5
+@pytest.mark.parametrize("name", ["C3", "C4", "C5"])
+def test_oracle_pinned_at_benchmarked_spaces(oracle, name):
+    """>= 10^3 candidates per benchmarked re-plan space (bench.py's
+    C3 / C4 / C5), scored by the REFERENCE's evaluate_plan + reconfig_cost
+    (tests/golden/search_bench.json, make_golden.py gen_search_bench): the
+    oracle gives every one of them bit for bit -- layout firsts / lasts, the
+    full-space winner's neighbourhood, stratified and uniform picks."""
+    from paper_2605_06374_b200.replan_scenarios import replan_problem
+
+    case = load("search_bench")[name]
+    *_, inputs = replan_problem(name)
+    s = oracle.search(inputs)
+    assert s.size == case["size"]
+    assert len(case["rows"]) >= 1000
+    n_ok = 0
+    for idx, ms, extra in case["rows"]:
+        got = s.score(idx)
+        if ms is None:
+            assert math.isinf(got), (idx, extra)
+            continue
+        assert bits(got) == bits(ms + extra), (idx, got, ms + extra)
+        n_ok += 1
+    assert n_ok >= 1000
+
+
+@pytest.mark.parametrize("k", range(4))
+def test_memo_oracle_equals_plain_full_space(oracle, k):
+    """orc_search_eval_memo (replica pipelines computed once per (layout,
+    partition, replica, first micro-batch, count)) gives every score and the
+    winner of the plain per-candidate oracle, on whole spaces."""
+    case = load("search")["cases"][k]
+    *_, inputs = search_problem(case)
+    s = oracle.search(inputs)
+    b1, i1, c1 = s.best(with_scores=True)
+    b2, i2, c2 = s.best_memo(with_scores=True)
+    assert (b1, i1) == (b2, i2)
+    np.testing.assert_array_equal(bits(c1), bits(c2))
+
+
+@pytest.mark.parametrize("name", ["C3", "C4", "C5"])
+def test_memo_oracle_equals_plain_at_benchmarked_spaces(oracle, name):
+    """... and on ranges of the benchmarked spaces: around the full-space
+    winner, a whole (layout, partition) block and random windows; the
+    full-space memo winner is the one recorded with the reference goldens."""
+    from paper_2605_06374_b200.replan_scenarios import replan_problem
+
+    *_, inputs = replan_problem(name)
+    s = oracle.search(inputs)
+    best, bi = s.best_memo()
+    assert [best, bi] == load("search_bench")[name]["oracle_best"]
+    rng = np.random.default_rng(len(name))
+    ranges = [(max(0, bi - 600), min(s.size, bi + 600))]
+    ranges += [(int(a), int(a) + 300) for a in rng.integers(0, s.size - 300, 4)]
+    for a, b in ranges:
+        b1, i1, c1 = s.best(a, b, with_scores=True)
+        b2, i2, c2 = s.best_memo(a, b, with_scores=True)
+        np.testing.assert_array_equal(bits(c1), bits(c2))
+        assert (b1, i1) == (b2, i2)
+
+
 def test_current_layout_has_no_surcharge(oracle):
     """Same groups + same partition + any counts: reconfig_cost == 0."""
     case = load("search")["cases"][0]
