@@ -380,6 +380,7 @@ def tile_trace(tr, reps: int):
     out.doc_len = np.tile(tr.doc_len, reps)
     out.seg = np.tile(tr.seg, reps)
     out.reset = np.tile(tr.reset, reps)
+    out.reset[::n] = 1  # each tile is its own series (reset at the tile start)
     out.device_time = np.tile(tr.device_time, (reps, 1, 1, 1))
     out.observed = np.tile(tr.observed, reps)
     return out
@@ -439,16 +440,25 @@ def run_scheduler(args, world, rank, local, names=("C3", "C4", "C5")):
 
     Each rank scores its contiguous shard of the candidate index range; one
     NCCL all-gather of (score, index) pairs finishes the min-loc.  Latency =
-    wall clock from host inputs to the decoded best plan (create + per-layout
-    GPU prep + sharded scoring + collective + decode)."""
+    wall clock from the failure report (the scheduler's known cluster state
+    and the workload) to the decoded plan: descriptor (build_desc), search
+    create + per-layout GPU prep, sharded scoring, the collective, decode --
+    and for C5 (10^5 sequences) also the FFD packing of the sequences into
+    the 512 micro-batches, their quad loads and every packed sequence's
+    replica under the chosen assignment (replan_from_sequences)."""
     import torch
 
-    from paper_2605_06374_b200.replan_scenarios import replan_problem
-    from paper_2605_06374_b200.search import ReplanSearch, distributed_best
+    from paper_2605_06374_b200.comm import CommSpec
+    from paper_2605_06374_b200.replan_scenarios import (SPECS, replan_from_sequences,
+                                                        replan_problem, sequence_workload)
+    from paper_2605_06374_b200.search import ReplanSearch, build_desc, distributed_best
+    from paper_2605_06374_b200.workload import CostModel
 
     dev = torch.device("cuda", local)
+    group = torch.distributed.group.WORLD if world > 1 else None
     out = {}
     for name in names:
+        sp = SPECS[name]
         st, cfg, mbs, inputs = replan_problem(name)
         s = ReplanSearch(inputs, dev)
         a, b = s.shard(rank, world)
@@ -456,7 +466,7 @@ def run_scheduler(args, world, rank, local, names=("C3", "C4", "C5")):
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        best_t, idx_t = s.eval_async(a, b)
+        s.eval_async(a, b)
         e1.record()
         torch.cuda.synchronize()
         eval_ms = e0.elapsed_time(e1)
@@ -464,19 +474,34 @@ def run_scheduler(args, world, rank, local, names=("C3", "C4", "C5")):
             t = torch.tensor([eval_ms], dtype=torch.float64, device=dev)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             eval_ms = float(t.item())
-        # end-to-end re-plan latency (fresh search each time), median of 3
+        model, comm = CostModel(2e-6, 5e-10), CommSpec()
+        kw = dict(capacity=cfg.pp + 2, min_utilization=sp["min_utilization"],
+                  max_dp=sp["max_dp"])
+        seqs = None
+        if "n_sequences" in sp:
+            seqs, N = sequence_workload(sp["n_sequences"], sp["M"])
+
+        def replan():
+            if seqs is not None:
+                plan, score, idx, entry_rep, srch = replan_from_sequences(
+                    st, cfg, seqs, N, sp["M"], model, comm, device=dev, group=group, **kw)
+                return plan, score, idx, srch
+            inp = build_desc(st, cfg, mbs, model, comm, quad=inputs.arrays["quad"], **kw)
+            srch = ReplanSearch(inp, dev)
+            score, idx = distributed_best(srch, group)
+            return (srch.decode(idx) if idx >= 0 else None), score, idx, srch
+
+        replan()  # warm-up
         lat = []
-        for _ in range(3):
+        for _ in range(5):
             if world > 1:
                 torch.distributed.barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            s2 = ReplanSearch(inputs, dev)
-            score, idx = distributed_best(s2)
-            plan = s2.decode(idx) if idx >= 0 else None
+            plan, score, idx, srch = replan()
             torch.cuda.synchronize()
             lat.append((time.perf_counter() - t0) * 1e3)
-            del s2
+            del srch
         lat_ms = float(np.median(lat))
         if world > 1:
             t = torch.tensor([lat_ms], dtype=torch.float64, device=dev)
@@ -484,14 +509,24 @@ def run_scheduler(args, world, rank, local, names=("C3", "C4", "C5")):
             lat_ms = float(t.item())
         out[name] = {
             "devices": len(st.devices), "candidates": s.size, "layouts": s.layouts,
+            "micro_batches": sp["M"], "token_budget": int(mbs[0].token_budget),
             "candidates_per_s": s.size / (eval_ms * 1e-3), "eval_ms": eval_ms,
             "replan_latency_ms": lat_ms, "best_score_s": score, "best_index": idx,
             "best_plan": None if plan is None else {
                 "tp": plan.tp, "dp": plan.dp, "pp": plan.pp, "partition": plan.partition,
                 "counts": plan.counts},
         }
+        if seqs is not None:
+            out[name]["n_sequences"] = int(len(seqs))
+            out[name]["latency_includes"] = ("FFD pack of the sequences, quad loads, build_desc, "
+                                             "search create, sharded eval, collective, decode, "
+                                             "sequence -> replica map")
+        else:
+            out[name]["latency_includes"] = ("build_desc, search create, sharded eval, "
+                                             "collective, decode")
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
             out[name]["cpu_baseline"] = search_cpu_baseline(inputs, s.size)
+        del s
     return out
 
 

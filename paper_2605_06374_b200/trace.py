@@ -26,19 +26,19 @@ from .tables import Segment
 
 
 def pack_ffd(lengths: np.ndarray, budget: int, max_bins: int = -1):
-    """pack_sequences via the native rh_pack_sequences -> (mb_off, doc_len)."""
+    """pack_sequences via the native rh_pack_sequences -> (mb_off, doc_len),
+    one call (outputs sized for the worst case: a bin per document plus its
+    padding entry)."""
     lib = _lib.load_library()
     lengths = np.ascontiguousarray(lengths, dtype=np.int32)
+    n = len(lengths)
     nb, ne = C.c_int64(), C.c_int64()
-    _lib.check(lib.rh_pack_sequences(len(lengths), lengths.ctypes.data, int(budget),
-                                     int(max_bins), None, None, C.byref(nb), C.byref(ne)),
-               "rh_pack_sequences")
-    off = np.zeros(nb.value + 1, dtype=np.int32)
-    docs = np.zeros(max(ne.value, 1), dtype=np.int32)
-    _lib.check(lib.rh_pack_sequences(len(lengths), lengths.ctypes.data, int(budget),
-                                     int(max_bins), off.ctypes.data, docs.ctypes.data,
-                                     C.byref(nb), C.byref(ne)), "rh_pack_sequences")
-    return off, docs[:ne.value]
+    off = np.empty(n + 2, dtype=np.int32)
+    docs = np.empty(2 * n + 1, dtype=np.int32)
+    _lib.check(lib.rh_pack_sequences(n, lengths.ctypes.data, int(budget), int(max_bins),
+                                     off.ctypes.data, docs.ctypes.data, C.byref(nb),
+                                     C.byref(ne)), "rh_pack_sequences")
+    return off[:nb.value + 1], docs[:ne.value]
 
 
 def draw_documents(rng: np.random.Generator, target_tokens: int, budget: int, mean: float,
