@@ -70,6 +70,36 @@ class ProgressTable:
         return max(col) - min(col)
 
 
+def migration_decision(progress: ProgressTable, stage: int, dead: set, next_pending,
+                       memory_feasible, outstanding=None):
+    """scheduler.py:210-251 -- one stage's per-slot migration decision.
+
+    The API form of the rule the native co-simulation (rh_plan_migration,
+    csrc/migration.cu) applies per slot, for callers that drive their own
+    slots with Python callbacks: source = the stage's least-progressed replica
+    (fail-stop first, then index); destination = the most-progressed healthy
+    replica (least outstanding work, then index); migrate when the source is
+    fail-stop or the progress gap exceeds delta, it has a pending forward
+    chunk, and the destination has memory headroom -> (mb, source, executor)."""
+    counts = progress.counts
+    n = len(counts)
+    d_min = min(range(n), key=lambda d: (counts[d][stage], 0 if (d, stage) in dead else 1, d))
+    healthy = [d for d in range(n) if (d, stage) not in dead]
+    if not healthy:
+        return None
+    load = outstanding or (lambda d, s: 0)
+    top = max(counts[d][stage] for d in healthy)
+    d_max = min((d for d in healthy if counts[d][stage] == top), key=lambda d: (load(d, stage), d))
+    if d_max == d_min:
+        return None
+    if (d_min, stage) not in dead and counts[d_max][stage] - counts[d_min][stage] <= progress.delta:
+        return None
+    j = next_pending(d_min, stage)
+    if j is None or not memory_feasible(j, stage, d_max):
+        return None
+    return j, d_min, d_max
+
+
 @dataclass
 class MigrationPlanResult:
     migrations: list[Migration]

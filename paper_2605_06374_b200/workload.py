@@ -166,3 +166,10 @@ def predict_chunk_time(mb: MicroBatch, kind: str, model: CostModel, layers_on_st
     if device_speed <= 0:
         raise ValueError("cannot schedule onto a stopped device (speed <= 0)")
     return float(chunk_times(model, [mb], [kind], [layers_on_stage], [device_speed])[0])
+
+
+def fit_cost_model(samples, chunk_ratios=None):
+    """workload.py:101-125 -- offline calibration of (alpha, beta), outside
+    the hot path: not built, raises."""
+    raise NotImplementedError("fit_cost_model is offline calibration, outside the B200 hot path "
+                              "(DESIGN.md §9): calibrate with the reference implementation")
