@@ -530,6 +530,89 @@ def run_scheduler(args, world, rank, local, names=("C3", "C4", "C5")):
     return out
 
 
+# ------------------------------------------------- re-plan: drop-in vs reference
+REPLAN_CASES = {
+    # name: (T, D, P, layers, micro-batches, fail-slow device, severity)
+    "C1": (4, 4, 2, 32, 16, 5, 0.5),
+    "C3": (4, 4, 16, 80, 64, 37, 0.4),
+}
+
+
+def _replan_ctx(ns, case, docs):
+    """A ResiHPPolicy.plan context (policies.py:53-81) built with the modules
+    of `ns` (the reference's or this package's): a confirmed fail-slow device
+    with its severity known to the scheduler (SURVEY §8(d) re-plan)."""
+    T, D, P, L, M, dev, sev = case
+    cfg = ns.cluster.ParallelismConfig(tp=T, dp=D, pp=P, layer_partition=[L // P] * P)
+    st = ns.cluster.build_cluster(max(1, T * D * P // 8), 8, cfg, 300.0 * 2**30, 25.0 * 2**30)
+    st = ns.cluster.apply_failures(
+        st, [ns.cluster.FailureEvent(kind="fail_slow_compute", start=0.0, device=dev,
+                                     severity=sev)], 0.0)
+    key = next(k for k, g in st.tp_groups.items() if dev in g)
+    mbs = ns.workload.pack_sequences([int(x) for x in docs], 4096)[:M]
+    conf = ns.detector.ValidationResult(confirmed=True, degraded_stages={key: sev},
+                                        degraded_links={}, cost_s=3.0)
+    return ns.policies.PlanningContext(
+        state=st, cfg=cfg, model=ns.workload.CostModel(alpha=2e-6, beta=5e-10), micro_batches=mbs,
+        comm=ns.comm.CommSpec(), known_speeds={dev: sev}, confirmed=conf, capacity=P + 2)
+
+
+def run_replan_compare():
+    """ResiHPPolicy.plan -- the reference's (baseline/_ref, Python, one host
+    core) against this package's drop-in (GPU subgroup / repartition /
+    proportional kernels, native plan_migration, GPU evaluate_plan) on the
+    same C1 and C3 contexts: wall time of one plan() and whether the two plans
+    agree (partition, assignment, subgroups, migrations, predicted makespan)."""
+    import importlib
+    import types
+
+    ref_dir = ROOT / "baseline" / "_ref"
+    if not (ref_dir / "resilsim").exists():
+        return {"unavailable": "baseline/_ref (pip install of /root/reference/pkg) is missing"}
+    sys.path.insert(0, str(ref_dir))
+    try:
+        ref = types.SimpleNamespace(**{m: importlib.import_module(f"resilsim.{m}") for m in
+                                       ("cluster", "comm", "workload", "detector", "policies")})
+    finally:
+        sys.path.remove(str(ref_dir))
+    import paper_2605_06374_b200 as pkg
+
+    ours = types.SimpleNamespace(**{m: importlib.import_module(f"paper_2605_06374_b200.{m}")
+                                    for m in ("cluster", "comm", "workload", "detector",
+                                              "policies")})
+    del pkg
+    out = {}
+    for name, case in REPLAN_CASES.items():
+        T, D, P, L, M, *_ = case
+        rng = np.random.default_rng([7, M])
+        docs = np.clip(np.rint(rng.lognormal(7.2, 0.8, M * 4096 // 1500 + 64)), 1, 4096)
+        rctx, octx = _replan_ctx(ref, case, docs), _replan_ctx(ours, case, docs)
+        t0 = time.perf_counter()
+        rplan = ref.policies.ResiHPPolicy().plan(rctx)
+        ref_ms = (time.perf_counter() - t0) * 1e3
+        ours.policies.ResiHPPolicy().plan(_replan_ctx(ours, case, docs))  # warm-up
+        times = []
+        for _ in range(3):
+            octx = _replan_ctx(ours, case, docs)
+            t0 = time.perf_counter()
+            oplan = ours.policies.ResiHPPolicy().plan(octx)
+            times.append((time.perf_counter() - t0) * 1e3)
+        ours_ms = float(np.median(times))
+        same = (rplan.layer_partition == oplan.layer_partition and
+                rplan.dp_assignment == oplan.dp_assignment and
+                sorted(rplan.tp_subgroups.items()) == sorted(oplan.tp_subgroups.items()) and
+                [(m.mb, m.stage, m.source, m.executor) for m in rplan.migrations] ==
+                [(m.mb, m.stage, m.source, m.executor) for m in oplan.migrations] and
+                np.float64(rplan.predicted_makespan_s).view(np.uint64) ==
+                np.float64(oplan.predicted_makespan_s).view(np.uint64))
+        out[name] = {"devices": T * D * P, "tp_dp_pp": [T, D, P], "micro_batches": M,
+                     "reference_ms": ref_ms, "ours_ms": ours_ms, "speedup": ref_ms / ours_ms,
+                     "plans_identical": bool(same), "migrations": len(oplan.migrations),
+                     "reference": "baseline/_ref resilsim ResiHPPolicy.plan (Python, 1 core)",
+                     "ours": "paper_2605_06374_b200 ResiHPPolicy.plan (drop-in, GPU + native)"}
+    return out
+
+
 def search_cpu_baseline(inputs, size, budget_s=4.0):
     """Oracle re-plan scoring on all host cores over a bounded contiguous sample."""
     from tests.oracle_bind import Oracle
@@ -558,6 +641,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-scheduler", action="store_true")
+    ap.add_argument("--no-replan", action="store_true",
+                    help="skip the drop-in vs reference ResiHPPolicy.plan comparison")
     ap.add_argument("--no-trace-r", action="store_true", help="skip the C5-shape trace R sample")
     ap.add_argument("--scheduler-only", default="", help="comma list of C3,C4,C5: only these")
     args = ap.parse_args()
@@ -582,6 +667,8 @@ def main():
         line["trace_R"] = run_trace_r(args, torch.device("cuda", local))
     if not args.no_scheduler:
         line["scheduler"] = run_scheduler(args, world, rank, local)
+    if rank == 0 and world == 1 and not args.no_replan:
+        line["replan"] = run_replan_compare()
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(tr)
