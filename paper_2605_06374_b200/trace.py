@@ -124,6 +124,25 @@ class DetectorTrace:
             "out_flag_severity": 5.0 * G,
         }
 
+    def slice(self, a: int, b: int) -> "DetectorTrace":
+        """Iterations [a, b) as a trace of their own (offsets rebased; the
+        segment tables are shared) -- one rank's shard (detect_shard.py)."""
+        import copy
+
+        M = self.M
+        out = copy.copy(self)
+        off = np.asarray(self.mb_off[a * M:b * M + 1], dtype=np.int64)
+        lo, hi = int(off[0]), int(off[-1])
+        out.mb_off = (off - lo).astype(np.int32)
+        out.doc_len = np.ascontiguousarray(self.doc_len[lo:hi])
+        out.seg = np.ascontiguousarray(self.seg[a:b])
+        out.reset = np.ascontiguousarray(self.reset[a:b])
+        if self.device_time is not None:
+            out.device_time = np.ascontiguousarray(self.device_time[a:b])
+        if self.observed is not None:
+            out.observed = np.ascontiguousarray(self.observed[a:b])
+        return out
+
     def packed(self) -> dict:
         """The packed wire form (rh_trace_packed): per-iteration document
         offsets (int32), documents per micro-batch (uint8) and document
