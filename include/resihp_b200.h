@@ -478,6 +478,23 @@ int rh_search_eval(rh_ctx* ctx, rh_search* search, int64_t begin, int64_t end,
 int rh_search_decode(rh_ctx* ctx, rh_search* search, int64_t index, rh_candidate* out,
                      int32_t* groups, int32_t* partition, int32_t* counts);
 
+/* ------------------------------------------- multi-GPU search collective */
+/*
+ * The one collective of the sharded re-plan search (search.py
+ * distributed_best), for callers without torch: every rank
+ * holds its shard's (score, index) winner on the device (rh_search_eval
+ * outputs); rh_minloc_allreduce all-gathers the 16-byte pairs over NCCL and
+ * reduces them on the device with the lexicographic (score, index) rule, in
+ * place, identically on every rank.  Asynchronous on `stream`.  NCCL is
+ * resolved at run time (the process's, else libnccl.so.2).
+ */
+int rh_nccl_unique_id(uint8_t* id_out /* 128 bytes */);
+int rh_nccl_comm_create(rh_ctx* ctx, int32_t world, int32_t rank, const uint8_t* id,
+                        void** comm_out);
+int rh_nccl_comm_destroy(void* comm);
+int rh_minloc_allreduce(rh_ctx* ctx, void* comm, int32_t world, double* score,
+                        int64_t* index, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -126,6 +126,10 @@ _SIGS = {
                    _p], C.c_int),
     "rh_screen_prepare": ([_p, C.POINTER(ScreenParams), C.c_int64, _p, C.c_int64, _p, _p, _p],
                           C.c_int),
+    "rh_nccl_unique_id": ([_p], C.c_int),
+    "rh_nccl_comm_create": ([_p, C.c_int32, C.c_int32, _p, C.POINTER(_p)], C.c_int),
+    "rh_nccl_comm_destroy": ([_p], C.c_int),
+    "rh_minloc_allreduce": ([_p, _p, C.c_int32, _p, _p, _p], C.c_int),
     "rh_dag_critical_path": ([_p, C.c_int32, _p, _p, _p, _p, C.c_int32, _p, _p, C.c_int32,
                               _p, _p, _p, _p, _p], C.c_int),
 }

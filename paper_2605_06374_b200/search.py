@@ -295,3 +295,43 @@ def distributed_best(search: ReplanSearch, group=None, begin: int = 0,
         vals = out.cpu().numpy().reshape(w, 2)
         return lexicographic_min((vals[k, 0].view(np.float64), vals[k, 1]) for k in range(w))
     return minloc_allreduce(float(best.item()), int(idx.item()), group)
+
+
+class NcclComm:
+    """An NCCL communicator made through the C ABI (rh_nccl_comm_create); the
+    unique id travels over the existing process group (or any channel)."""
+
+    def __init__(self, rank: int, world: int, device=None, group=None):
+        import torch
+        import torch.distributed as dist
+
+        self.lib = _lib.load_library()
+        self.world = world
+        self.dev = device or torch.device("cuda", torch.cuda.current_device())
+        self.ctx = _lib.context(self.dev.index)
+        uid = np.zeros(128, np.uint8)
+        if rank == 0:
+            _lib.check(self.lib.rh_nccl_unique_id(uid.ctypes.data), "rh_nccl_unique_id")
+        t = torch.from_numpy(uid)
+        if dist.get_backend(group) == "nccl":
+            t = t.to(self.dev)
+        dist.broadcast(t, src=0, group=group)
+        uid = t.cpu().numpy().astype(np.uint8)
+        h = C.c_void_p()
+        _lib.check(self.lib.rh_nccl_comm_create(self.ctx, world, rank, uid.ctypes.data,
+                                                C.byref(h)), "rh_nccl_comm_create")
+        self.handle = h.value
+
+    def minloc(self, best, idx, stream=None):
+        """In place: the (score, index) device scalars of this rank -> the
+        lexicographic minimum over all ranks (rh_minloc_allreduce)."""
+        _lib.check(self.lib.rh_minloc_allreduce(self.ctx, self.handle, self.world,
+                                                best.data_ptr(), idx.data_ptr(),
+                                                _lib.stream_handle(stream)),
+                   "rh_minloc_allreduce")
+        return best, idx
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.lib.rh_nccl_comm_destroy(self.handle)
+            self.handle = None
