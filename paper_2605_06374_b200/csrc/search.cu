@@ -27,6 +27,7 @@
 #include <cmath>
 #include <cstring>
 #include <limits>
+#include <utility>
 #include <vector>
 
 #include <math_constants.h>
@@ -635,6 +636,160 @@ __global__ void __launch_bounds__(kPipeThreads) pipe_kernel(SearchArgs a, const 
       res = over ? CUDART_INF : gm;
     }
     a.v.rtab[a.v.lrt[li] + (long long)vv * 8 * D + cs * D + d] = res;
+  }
+}
+
+// ---- phase 1 for 1F1B, P <= 32: register-resident replica walks ----------
+// One thread per replica pipeline, as in pipe_kernel, but the chain state
+// (each stage's last finish and last F finish) lives in registers and the
+// chunks are visited in the loop-form topological order of the Detector's
+// pass_wide_kernel (pass_wide.cu): a warm-up triangle (F_j on stages
+// ascending) and a main loop of (B_i, F_{P-s+i}) pairs on stages descending,
+// with the stage index unrolled at compile time.  Per chunk: one base-cost
+// load, a broadcast ratio * layers load, a coalesced hop load ([s][d] tables),
+// and the division only on stages some replica of the warp runs slow.  The
+// per-stage constants are reloaded per use (ld.global.nc through asm
+// volatile) instead of pinning 4P registers.
+__device__ __forceinline__ double ldg_nc(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
+template <int P, bool SAFE>
+struct SearchWalk {
+  const double* bs;   // base costs of the replica's first micro-batch on
+  const double* rl;   // [rlF: 32][rlB: 32] of the (layout, partition) pair
+  const double* sp;   // [s][d] tables at this replica: element s at s * D
+  const double* inv;
+  const double* hop;  // hop s -> s+1 at s * D
+  int D;
+  unsigned slow;      // warp-uniform: bit s = some replica of the warp runs stage s slow
+  double fin[P], lastF[P];
+
+  template <int S>
+  __device__ __forceinline__ double cost(double rl_, double b) const {
+    const double x = __dmul_rn(rl_, b);
+    if (slow & (1u << S)) {  // warp-uniform branch; x / 1.0 == x otherwise
+      const double v = __ldg(sp + S * D);
+      if (SAFE) return div_fast(x, v, __ldg(inv + S * D));
+      return v != 1.0 ? div_slow(x, v) : x;
+    }
+    return x;
+  }
+  template <int S>
+  __device__ __forceinline__ double step(double c, double dep) {
+    const double st = fin[S] > dep ? fin[S] : dep;
+    fin[S] = __dadd_rn(st, c);
+    return fin[S];
+  }
+  template <int S>
+  __device__ __forceinline__ void tri(int j, int m, double bj) {
+    if (j <= P - 1 - S && j < m) {
+      const double dep = S > 0 ? __dadd_rn(lastF[S > 0 ? S - 1 : 0], ldg_nc(hop + (S - 1) * D)) : 0.0;
+      lastF[S] = step<S>(cost<S>(ldg_nc(rl + S), bj), dep);
+    }
+  }
+  template <int S>
+  __device__ __forceinline__ void pair(int i, int m, double bi, double& nB) {
+    const double depB = S < P - 1 ? __dadd_rn(nB, ldg_nc(hop + S * D)) : 0.0;
+    nB = step<S>(cost<S>(ldg_nc(rl + 32 + S), bi), depB);
+    if (i < m - P + S) {
+      const double bF = __ldg(bs + (P - S + i));
+      const double dep = S > 0 ? __dadd_rn(lastF[S > 0 ? S - 1 : 0], ldg_nc(hop + (S - 1) * D)) : 0.0;
+      lastF[S] = step<S>(cost<S>(ldg_nc(rl + S), bF), dep);
+    }
+  }
+  template <int... I>
+  __device__ __forceinline__ void tri_all(int j, int m, double bj, std::integer_sequence<int, I...>) {
+    (tri<I>(j, m, bj), ...);
+  }
+  template <int... I>
+  __device__ __forceinline__ void pair_all(int i, int m, double bi, std::integer_sequence<int, I...>) {
+    double nB = 0.0;
+    (pair<P - 1 - I>(i, m, bi, nB), ...);
+  }
+  __device__ __forceinline__ double walk(int m) {
+#pragma unroll
+    for (int s = 0; s < P; ++s) fin[s] = lastF[s] = 0.0;
+#pragma unroll 1
+    for (int j = 0; j < P; ++j)
+      tri_all(j, m, __ldg(bs + (j < m ? j : 0)), std::make_integer_sequence<int, P>());
+#pragma unroll 1
+    for (int i = 0; i < m; ++i)
+      pair_all(i, m, __ldg(bs + i), std::make_integer_sequence<int, P>());
+    double g = 0.0;
+#pragma unroll
+    for (int s = 0; s < P; ++s) g = fin[s] > g ? fin[s] : g;
+    return g;
+  }
+};
+
+constexpr int search_reg_min_blocks(int P) { return P <= 12 ? 4 : (P <= 24 ? 3 : 2); }
+
+template <int P, bool SAFE>
+__global__ void __launch_bounds__(kPipeThreads, search_reg_min_blocks(P))
+    pipe_reg_kernel(SearchArgs a, const PipeTask* tk, int n_tk, long long n_pipes) {
+  const int nt = blockDim.x;
+  // every lane of a warp runs the same trip count (the slow mask is a warp vote)
+  const long long stride = (long long)gridDim.x * nt;
+  const long long g0 = (long long)blockIdx.x * nt + threadIdx.x;
+  const long long trips = (n_pipes + stride - 1 - ((long long)blockIdx.x * nt)) / stride + 1;
+  for (long long t = 0, g = g0; t < trips; ++t, g += stride) {
+    const bool live = g < n_pipes;
+    PipeId id{};
+    bool run = false;
+    const double *sp_d = nullptr, *inv_d = nullptr, *hop_d = nullptr;
+    unsigned slow = 0;
+    int md = 0;
+    bool over = false;
+    if (live) {
+      id = pipe_id(a, tk, n_tk, P, g, true);
+      md = id.md;
+      run = id.feas_v && id.valid && md > 0;
+      sp_d = a.v.tspeed + id.goff + id.d;
+      inv_d = a.v.tinv + id.goff + id.d;
+      hop_d = a.v.thop + id.goff + id.d;
+      if (id.feas_v && id.valid) {
+        const int slot = P * a.tab_stride + md;
+        over = a.cap > 0 && __ldg(a.v.tab_peak + slot) > a.cap;
+      }
+      if (run)
+#pragma unroll 4
+        for (int s = 0; s < P; ++s)
+          if (__ldg(sp_d + s * id.D) != 1.0) slow |= 1u << s;
+    }
+    const unsigned wslow = __reduce_or_sync(0xffffffffu, slow);
+    if (!live) continue;
+    double res = CUDART_INF;
+    if (id.feas_v && id.valid) {
+      double gm = 0.0;
+      if (run) {
+        SearchWalk<P, SAFE> w{a.v.base + id.start, a.v.rl + id.pair * 3LL * 32, sp_d, inv_d,
+                              hop_d, id.D, wslow, {}, {}};
+        gm = w.walk(md);
+      }
+      res = over ? CUDART_INF : gm;
+    }
+    a.v.rtab[a.v.lrt[id.li] + (long long)id.vv * 8 * id.D + id.cs * id.D + id.d] = res;
+  }
+}
+
+template <bool SAFE>
+static void* pipe_reg_kernel_for(int P) {
+  switch (P) {
+#define RH_REG_CASE(n) \
+  case n:              \
+    return (void*)pipe_reg_kernel<n, SAFE>;
+    RH_REG_CASE(1) RH_REG_CASE(2) RH_REG_CASE(3) RH_REG_CASE(4) RH_REG_CASE(5) RH_REG_CASE(6)
+    RH_REG_CASE(7) RH_REG_CASE(8) RH_REG_CASE(9) RH_REG_CASE(10) RH_REG_CASE(11)
+    RH_REG_CASE(12) RH_REG_CASE(13) RH_REG_CASE(14) RH_REG_CASE(15) RH_REG_CASE(16)
+    RH_REG_CASE(17) RH_REG_CASE(18) RH_REG_CASE(19) RH_REG_CASE(20) RH_REG_CASE(21)
+    RH_REG_CASE(22) RH_REG_CASE(23) RH_REG_CASE(24) RH_REG_CASE(25) RH_REG_CASE(26)
+    RH_REG_CASE(27) RH_REG_CASE(28) RH_REG_CASE(29) RH_REG_CASE(30) RH_REG_CASE(31)
+    RH_REG_CASE(32)
+#undef RH_REG_CASE
+    default: return nullptr;
   }
 }
 
@@ -1315,8 +1470,20 @@ int rh_search_eval(rh_ctx* ctx, rh_search* S, int64_t begin, int64_t end, double
     }
     long long n_pipes = g.n_pipes;
     int P = g.P;
-    void* args[] = {&a, &tp, &n_tk, &n_pipes, &P};
-    RH_CUDA(cudaLaunchKernel(kern, dim3(blocks), dim3(kPipeThreads), args, smem, gs));
+    void* reg = (!zbh && !getenv("RH_SEARCH_SMEM_WALK"))
+                    ? (S->div_safe ? pipe_reg_kernel_for<true>(P) : pipe_reg_kernel_for<false>(P))
+                    : nullptr;
+    if (reg) {  // register-resident walk (1F1B)
+      int rocc = 0;
+      RH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&rocc, reg, kPipeThreads, 0));
+      const int rblocks = (int)std::max<long long>(
+          1, std::min<long long>(want, (long long)ctx->num_sms * std::max(1, rocc) * 8));
+      void* rargs[] = {&a, &tp, &n_tk, &n_pipes};
+      RH_CUDA(cudaLaunchKernel(reg, dim3(rblocks), dim3(kPipeThreads), rargs, 0, gs));
+    } else {
+      void* args[] = {&a, &tp, &n_tk, &n_pipes, &P};
+      RH_CUDA(cudaLaunchKernel(kern, dim3(blocks), dim3(kPipeThreads), args, smem, gs));
+    }
     RH_CHECK_LAUNCH(ctx);
     // this group's candidates, layout by layout, right behind its table rows
     for (size_t q = g.first; q < g.first + g.count; ++q) {
