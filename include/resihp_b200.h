@@ -456,6 +456,15 @@ int rh_search_create(rh_ctx* ctx, const rh_search_desc* desc, rh_search** out, v
 /* Returns the search's device memory to the stream-ordered pool on the stream
  * of its latest create / eval call (so pending work on that stream finishes
  * first); that stream must still exist. */
+/*
+ * Deferred workload: rh_search_create accepts desc->quad == NULL (layouts,
+ * placement, repartition, proportional splits and op lists do not depend on
+ * the micro-batches' quad loads), and rh_search_set_workload supplies the
+ * quad loads (host, n_micro_batches int64) before the first eval -- so a
+ * re-plan can pack its sequences (rh_pack_sequences) on a host thread while
+ * the search is being created.  Synchronous on `stream`.
+ */
+int rh_search_set_workload(rh_ctx* ctx, rh_search* search, const int64_t* quad, void* stream);
 int rh_search_destroy(rh_search* search);
 /* total number of candidates / layouts */
 int64_t rh_search_size(const rh_search* search);

@@ -60,6 +60,9 @@ struct rh_search {
   // waits for it (the task list and block results are per search)
   cudaEvent_t done_ev = nullptr;
   int div_safe = 0;  // see SearchArgs::div_safe
+  bool div_dens = true;            // divisor range part of div_safe
+  double div_r_lo = 0.0, div_r_hi = 0.0;  // (ratio * L) range
+  bool workload_ready = false;     // quad loads uploaded and base costs built
   struct Dev {
     int32_t *lT, *lD, *lP, *lgoff, *lpoff, *ldoff, *lboff, *lnb;
     long long *lbase, *lnv, *lnu, *lpair, *lrt;
@@ -1057,13 +1060,30 @@ static int build_op_lists(rh_ctx* ctx, rh_search* S, cudaStream_t st) {
 
 }  // namespace rh
 
+namespace rh {
+// div_fast is exact for every chunk of the search when every numerator
+// (ratio * L) * base and every divisor (group speed) is in range
+static void set_div_safe(rh_search* S, const int64_t* quad) {
+  const rh_search_desc& d = S->d;
+  double q_lo = HUGE_VAL, q_hi = 0.0;
+  for (int j = 0; j < d.n_micro_batches; ++j) {
+    const double b = d.model.alpha * d.token_budget + d.model.beta * (double)quad[j];
+    q_hi = std::max(q_hi, b);
+    if (b > 0.0) q_lo = std::min(q_lo, b);
+  }
+  const double r_lo = S->div_r_lo, r_hi = S->div_r_hi;
+  const bool nums = q_hi * r_hi <= 0x1p890 && (q_hi * r_hi == 0.0 || q_lo * r_lo >= 0x1p-890);
+  S->div_safe = nums && S->div_dens ? 1 : 0;
+}
+}  // namespace rh
+
 using namespace rh;
 
 extern "C" {
 
 int rh_search_create(rh_ctx* ctx, const rh_search_desc* desc, rh_search** out, void* stream) {
   if (!ctx || !desc || !out || desc->n_devices <= 0 || desc->devices_per_node <= 0 ||
-      !desc->device_speed || desc->n_micro_batches <= 0 || !desc->quad ||
+      !desc->device_speed || desc->n_micro_batches <= 0 ||
       desc->total_layers <= 0 || desc->min_layers < 0 || desc->token_budget <= 0 ||
       (desc->schedule != RH_SCHED_1F1B && desc->schedule != RH_SCHED_ZBH) ||
       desc->intra_bw <= 0 || desc->inter_bw <= 0 || (desc->n_links && !desc->link_nodes)) {
@@ -1177,16 +1197,12 @@ int rh_search_create(rh_ctx* ctx, const rh_search_desc* desc, rh_search** out, v
   S->n_rep = doff;
   const int NL = (int)S->lT.size();
   if (NL == 0) {
+    S->workload_ready = true;  // nothing to score
     *out = S;
     return RH_OK;
   }
-  {  // ranges of every numerator ((ratio * L) * base) and divisor (group speed)
-    double q_lo = HUGE_VAL, q_hi = 0.0;
-    for (int j = 0; j < d.n_micro_batches; ++j) {
-      const double b = d.model.alpha * d.token_budget + d.model.beta * (double)desc->quad[j];
-      q_hi = std::max(q_hi, b);
-      if (b > 0.0) q_lo = std::min(q_lo, b);
-    }
+  {  // ranges of every numerator ((ratio * L) * base) and divisor (group speed);
+     // the base-cost part waits for the workload when it is deferred
     const double ratios[4] = {d.model.ratio_f, d.model.ratio_b, d.model.ratio_w,
                               d.model.ratio_b + d.model.ratio_w};
     double r_lo = HUGE_VAL, r_hi = 0.0;
@@ -1201,9 +1217,10 @@ int rh_search_create(rh_ctx* ctx, const rh_search_desc* desc, rh_search** out, v
       s_hi = std::max(s_hi, v * 32.0 / T0);
     }
     // margins of 2^10 absorb the rounding of these host estimates
-    const bool nums = q_hi * r_hi <= 0x1p890 && (q_hi * r_hi == 0.0 || q_lo * r_lo >= 0x1p-890);
-    const bool dens = S->blk_speed.empty() || (s_lo >= 0x1p-90 && s_hi <= 0x1p90);
-    S->div_safe = nums && dens ? 1 : 0;
+    S->div_dens = S->blk_speed.empty() || (s_lo >= 0x1p-90 && s_hi <= 0x1p90);
+    S->div_r_lo = r_lo;
+    S->div_r_hi = r_hi;
+    if (desc->quad) set_div_safe(S, desc->quad);
   }
   // ---- device memory
   int& max_blocks_per_sm = ctx->combine_occ;  // cached occupancy of the combine kernel
@@ -1282,7 +1299,7 @@ int rh_search_create(rh_ctx* ctx, const rh_search_desc* desc, rh_search** out, v
   {  // one host staging buffer, one copy
     std::vector<char> stage(up_bytes, 0);
     for (const Up& u : ups)
-      if (u.n) memcpy(stage.data() + u.off, u.src, u.n);
+      if (u.n && u.src) memcpy(stage.data() + u.off, u.src, u.n);
     RH_CUDA(cudaMemcpyAsync(B, stage.data(), up_bytes, cudaMemcpyHostToDevice, st));
     RH_CUDA(cudaStreamSynchronize(st));  // the staging buffer dies here
   }
@@ -1306,8 +1323,11 @@ int rh_search_create(rh_ctx* ctx, const rh_search_desc* desc, rh_search** out, v
   v.rspeed = Dp(o_rspeed); v.pstart = I(o_pstart); v.same = I(o_same); v.base = Dp(o_base);
   v.blk_best = Dp(o_bb); v.blk_idx = LL(o_bi);
   SearchArgs a = make_args(S);
-  base_kernel<<<(d.n_micro_batches + 255) / 256, 256, 0, st>>>(a);
-  RH_CHECK_LAUNCH(ctx);
+  if (desc->quad) {
+    base_kernel<<<(d.n_micro_batches + 255) / 256, 256, 0, st>>>(a);
+    RH_CHECK_LAUNCH(ctx);
+    S->workload_ready = true;
+  }
   prep_kernel<<<(NL * 32 + 127) / 128, 128, 0, st>>>(a);
   RH_CHECK_LAUNCH(ctx);
   if (int rc = build_op_lists(ctx, S, st)) {
@@ -1328,6 +1348,30 @@ int rh_search_destroy(rh_search* S) {
   if (S->dops) cudaFreeAsync(S->dops, S->last_stream);
   if (S->done_ev) cudaEventDestroy(S->done_ev);
   delete S;
+  return RH_OK;
+}
+
+int rh_search_set_workload(rh_ctx* ctx, rh_search* S, const int64_t* quad, void* stream) {
+  if (!ctx || !S || !quad) {
+    set_error("rh_search_set_workload: invalid arguments");
+    return RH_E_INVALID;
+  }
+  DeviceGuard guard(ctx);
+  std::lock_guard<std::mutex> lock(ctx->search_mu);
+  cudaStream_t st = as_stream(stream);
+  if (S->done_ev) RH_CUDA(cudaStreamWaitEvent(st, S->done_ev, 0));
+  set_div_safe(S, quad);
+  if (S->dmem && S->d.n_micro_batches > 0) {
+    RH_CUDA(cudaMemcpyAsync(S->dv.quad, quad, 8 * (size_t)S->d.n_micro_batches,
+                            cudaMemcpyHostToDevice, st));
+    SearchArgs a = make_args(S);
+    base_kernel<<<(S->d.n_micro_batches + 255) / 256, 256, 0, st>>>(a);
+    RH_CHECK_LAUNCH(ctx);
+    if (S->done_ev) RH_CUDA(cudaEventRecord(S->done_ev, st));
+    // the host copy source may be released when this returns
+    RH_CUDA(cudaStreamSynchronize(st));
+  }
+  S->workload_ready = true;
   return RH_OK;
 }
 
@@ -1387,6 +1431,10 @@ int rh_search_eval(rh_ctx* ctx, rh_search* S, int64_t begin, int64_t end, double
       end > S->total) {
     set_error("rh_search_eval: invalid range [%lld, %lld) of %lld", (long long)begin,
               (long long)end, (long long)(S ? S->total : 0));
+    return RH_E_INVALID;
+  }
+  if (!S->workload_ready) {
+    set_error("rh_search_eval: the workload (quad loads) was deferred and not yet set");
     return RH_E_INVALID;
   }
   cudaStream_t st = as_stream(stream);

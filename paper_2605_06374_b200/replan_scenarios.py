@@ -135,13 +135,33 @@ def replan_from_sequences(state, cfg, docs: np.ndarray, N: int, M: int, model, c
     decode, and the replica of every packed sequence under the chosen
     assignment.  Returns (plan, score, index, entry_replica[packed entries],
     search)."""
+    import threading
+
     from .search import ReplanSearch, distributed_best
 
-    off, packed, quad = pack_workload(docs, N, M)
+    # the FFD runs on a host thread (rh_pack_sequences releases the GIL)
+    # while the descriptor is built and the search is created: layouts,
+    # placement, repartition, splits and op lists do not depend on the quad
+    # loads, which are supplied afterwards (rh_search_set_workload)
+    packed_out = {}
+
+    def pack():
+        try:
+            packed_out["v"] = pack_workload(docs, N, M)
+        except Exception as exc:  # re-raised below
+            packed_out["e"] = exc
+
+    th = threading.Thread(target=pack)
+    th.start()
     mbs = [_Budget(N)] * M
-    inputs = build_desc(state, cfg, mbs, model, comm, capacity=capacity, quad=quad,
+    inputs = build_desc(state, cfg, mbs, model, comm, capacity=capacity, defer_quad=True,
                         min_utilization=min_utilization, max_dp=max_dp, max_pp=max_pp)
     search = ReplanSearch(inputs, device)
+    th.join()
+    if "e" in packed_out:
+        raise packed_out["e"]
+    off, packed, quad = packed_out["v"]
+    search.set_workload(quad)
     score, idx = distributed_best(search, group)
     plan = search.decode(idx) if idx >= 0 else None
     entry_replica = None

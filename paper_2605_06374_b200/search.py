@@ -50,6 +50,7 @@ _SIGS = {
     "rh_search_create": ([C.c_void_p, C.POINTER(SearchDesc), C.POINTER(C.c_void_p), C.c_void_p],
                          C.c_int),
     "rh_search_destroy": ([C.c_void_p], C.c_int),
+    "rh_search_set_workload": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "rh_search_size": ([C.c_void_p], C.c_int64),
     "rh_search_shard": ([C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_int64),
                          C.POINTER(C.c_int64)], C.c_int),
@@ -81,7 +82,7 @@ def build_desc(state: ClusterState, cfg: ParallelismConfig, micro_batches, model
                known_speeds: dict | None = None, capacity: int | None = None,
                min_layers: int = 1, max_tp: int | None = None, max_pp: int = 32,
                max_dp: int = 64, min_utilization: float = 0.9, group_rebuild_s: float = 2.0,
-               amortize_iterations: int = 25, quad=None) -> SearchInputs:
+               amortize_iterations: int = 25, quad=None, defer_quad: bool = False) -> SearchInputs:
     """Descriptor of a re-plan (PlanningContext fields, policies.py:53-81).
 
     Device speeds are the scheduler's KNOWN view (PlanningContext.known_state,
@@ -99,7 +100,8 @@ def build_desc(state: ClusterState, cfg: ParallelismConfig, micro_batches, model
     N = micro_batches[0].token_budget
     if any(mb.token_budget != N for mb in micro_batches):
         raise ValueError("micro-batches must share one token budget")
-    q = np.asarray(quad if quad is not None else quad_loads(micro_batches), dtype=np.int64)
+    q = (np.zeros(1, np.int64) if defer_quad else
+         np.asarray(quad if quad is not None else quad_loads(micro_batches), dtype=np.int64))
     T0, D0, P0 = cfg.tp, cfg.dp, cfg.pp
     groups = []
     full = True
@@ -117,7 +119,8 @@ def build_desc(state: ClusterState, cfg: ParallelismConfig, micro_batches, model
     desc = SearchDesc(
         n, state.devices_per_node, ptr(speed), float(state.intra_bw), float(state.inter_bw),
         len(links), ptr(link_nodes), ptr(link_factor), cost_model_c(model),
-        SCHED_CODE[cfg.schedule], N, len(micro_batches), ptr(q), int(sum(cfg.layer_partition)),
+        SCHED_CODE[cfg.schedule], N, len(micro_batches), None if defer_quad else ptr(q),
+        int(sum(cfg.layer_partition)),
         int(min_layers), int(capacity or 0), 1 if comm is not None else 0,
         float(comm.hidden_bytes_per_token) if comm is not None else 0.0,
         float(comm.layer_bytes) if comm is not None else 256.0 * 2**20,
@@ -191,6 +194,17 @@ class ReplanSearch:
                 self.handle = None
         except Exception:
             pass
+
+    def set_workload(self, quad) -> None:
+        """Quad loads of a search created with build_desc(defer_quad=True)
+        (rh_search_set_workload)."""
+        import torch
+
+        q = np.ascontiguousarray(quad, dtype=np.int64)
+        with torch.cuda.device(self.dev):
+            _lib.check(self.lib.rh_search_set_workload(self.ctx, self.handle, q.ctypes.data,
+                                                       _lib.stream_handle()),
+                       "rh_search_set_workload")
 
     def shard(self, rank: int, world: int) -> tuple[int, int]:
         """Cost-balanced contiguous shard of the candidate range for `rank`

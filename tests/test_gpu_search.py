@@ -226,3 +226,42 @@ def test_extreme_cost_model_exact_division(alpha, beta, oracle, cuda_device):
     assert fin.any()
     np.testing.assert_array_equal(bits(g[fin]), bits(c[fin]))
     assert gpu.best(0, b) == cpu.best(0, b)
+
+
+@pytest.mark.parametrize("name", ["C4", "C5"])
+def test_deferred_workload_and_sequence_replan(name, oracle, cuda_device):
+    """rh_search_create without quad loads + rh_search_set_workload gives the
+    same scores and winner as the one-shot create; for C5 the whole
+    replan_from_sequences path (FFD on a host thread overlapping the search
+    create) returns the oracle's full-space winner and maps every packed
+    sequence to the replica that owns its micro-batch."""
+    import numpy as np
+
+    from paper_2605_06374_b200.comm import CommSpec
+    from paper_2605_06374_b200.replan_scenarios import (SPECS, _Budget, replan_from_sequences,
+                                                        replan_problem, sequence_workload)
+    from paper_2605_06374_b200.search import ReplanSearch, build_desc
+    from paper_2605_06374_b200.workload import CostModel
+
+    st, cfg, mbs, inputs = replan_problem(name)
+    sp = SPECS[name]
+    quad = inputs.arrays["quad"]
+    kw = dict(capacity=cfg.pp + 2, min_utilization=sp["min_utilization"], max_dp=sp["max_dp"])
+    lazy = build_desc(st, cfg, [_Budget(mbs[0].token_budget)] * len(mbs), CostModel(2e-6, 5e-10),
+                      CommSpec(), defer_quad=True, **kw)
+    g = ReplanSearch(lazy)
+    g.set_workload(quad)
+    ref = ReplanSearch(inputs)
+    assert g.best() == ref.best()
+    a = max(0, ref.best()[1] - 2000)
+    np.testing.assert_array_equal(bits(g.scores(a, a + 4000)), bits(ref.scores(a, a + 4000)))
+    if "n_sequences" in sp:
+        docs, N = sequence_workload(sp["n_sequences"], sp["M"])
+        plan, score, idx, entry_rep, _ = replan_from_sequences(
+            st, cfg, docs, N, sp["M"], CostModel(2e-6, 5e-10), CommSpec(), **kw)
+        assert [score, idx] == load("search_bench")[name]["oracle_best"]
+        start = np.cumsum([0] + list(plan.counts))
+        assert entry_rep.min() == 0 and entry_rep.max() == plan.dp - 1
+        assert np.all(np.diff(entry_rep) >= 0)  # contiguous ownership
+        assert len(entry_rep) >= sp["n_sequences"]
+        assert start[-1] == sp["M"]

@@ -36,3 +36,12 @@ for rep in range(4):
     d = np.diff(t) * 1e3
     print(f"pack {d[0]:.2f} ms  build_desc {d[1]:.2f}  create {d[2]:.2f}  eval+sync {d[3]:.2f}  "
           f"decode {d[4]:.2f}  total {sum(d):.2f}")
+from paper_2605_06374_b200.replan_scenarios import replan_from_sequences  # noqa: E402
+
+for rep in range(4):
+    t0 = time.perf_counter()
+    plan, score, idx, er, srch = replan_from_sequences(st, cfg, docs, N, sp["M"], model, comm,
+                                                        device=dev, **kw)
+    torch.cuda.synchronize()
+    print(f"replan_from_sequences (FFD overlapped with create): {(time.perf_counter() - t0) * 1e3:.2f} ms")
+    del srch
