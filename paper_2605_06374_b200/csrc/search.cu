@@ -876,6 +876,119 @@ __global__ void __launch_bounds__(kEvalThreads) combine_kernel(SearchArgs a, lon
   }
 }
 
+// ---- phase 2, one CTA per (layout, partition) pair: O(1) per candidate ----
+// A count variant u >= 2 moves one micro-batch src -> dst; the replicas
+// between them shift by one position.  Its makespan is the max of the
+// case-1 row outside [min, max], the two moved replicas' cases and the
+// case-3 (src < dst) or case-6 (dst < src) row strictly inside: prefix /
+// suffix maxima of the case-1 row and a sparse table (range max) of rows 3
+// and 6, built once per pair in shared memory, make every candidate O(1)
+// instead of O(D) (max is exact and order-free, so the value is unchanged).
+constexpr int kComb2Threads = 256;
+constexpr int kComb2MaxD = 64;
+constexpr int kComb2Levels = 7;  // 2^6 = 64
+
+__global__ void __launch_bounds__(kComb2Threads) combine2_kernel(SearchArgs a, int li,
+                                                                long long begin, long long end,
+                                                                long long sbegin, int v_lo,
+                                                                double* scores, double* out_best,
+                                                                long long* out_idx) {
+  __shared__ double rows[8][kComb2MaxD];
+  __shared__ double pre1[kComb2MaxD + 1], suf1[kComb2MaxD + 1];
+  __shared__ double sp3[kComb2Levels][kComb2MaxD], sp6[kComb2Levels][kComb2MaxD];
+  __shared__ double s_best[kComb2Threads / 32];
+  __shared__ long long s_idx[kComb2Threads / 32];
+  const int vv = v_lo + blockIdx.x;
+  const int D = a.v.lD[li];
+  const long long nu = a.v.lnu[li];
+  const long long pbase = a.v.lbase[li] + (long long)vv * nu;
+  const long long u_lo = max(0LL, begin - pbase), u_hi = min(nu, end - pbase);
+  const long long pair = a.v.lpair[li] + vv;
+  const double ar = a.v.pinfo[2 * pair], sur = a.v.pinfo[2 * pair + 1];
+  const double* Rp = a.v.rtab + a.v.lrt[li] + (long long)vv * 8 * D;
+  for (int k = threadIdx.x; k < 8 * D; k += blockDim.x) rows[k / D][k % D] = Rp[k];
+  __syncthreads();
+  if (threadIdx.x == 0) {  // D <= 64: one thread each
+    double m = 0.0;
+    pre1[0] = 0.0;
+    for (int d = 0; d < D; ++d) pre1[d + 1] = m = fmax(m, rows[1][d]);
+    m = 0.0;
+    suf1[D] = 0.0;
+    for (int d = D - 1; d >= 0; --d) suf1[d] = m = fmax(m, rows[1][d]);
+  }
+  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    sp3[0][d] = rows[3][d];
+    sp6[0][d] = rows[6][d];
+  }
+  __syncthreads();
+  for (int k = 1; k < kComb2Levels && (1 << k) <= D; ++k) {
+    for (int d = threadIdx.x; d + (1 << k) <= D; d += blockDim.x) {
+      sp3[k][d] = fmax(sp3[k - 1][d], sp3[k - 1][d + (1 << (k - 1))]);
+      sp6[k][d] = fmax(sp6[k - 1][d], sp6[k - 1][d + (1 << (k - 1))]);
+    }
+    __syncthreads();
+  }
+  const int32_t* pst = a.v.pstart + a.v.ldoff[li] + li;
+  double best = CUDART_INF;
+  long long best_i = -1;
+  for (long long u = u_lo + threadIdx.x; u < u_hi; u += blockDim.x) {
+    double ms = 0.0;
+    bool feasible = sur < CUDART_INF;
+    if (u <= 1) {
+      for (int d = 0; d < D; ++d) ms = fmax(ms, rows[u][d]);
+    } else {
+      const int m = (int)(u - 2), r = m % (D - 1);
+      const int src = m / (D - 1), dst = r < src ? r : r + 1;
+      if (pst[src + 1] - pst[src] == 0) feasible = false;
+      const int lo = min(src, dst), hi = max(src, dst);
+      ms = fmax(pre1[lo], suf1[hi + 1]);  // case-1 replicas outside [lo, hi]
+      if (src < dst) ms = fmax(ms, fmax(rows[2][src], rows[4][dst]));
+      else ms = fmax(ms, fmax(rows[5][dst], rows[7][src]));
+      if (hi - lo >= 2) {  // strictly inside: case 3 (src < dst) or 6
+        const int l = lo + 1, len = hi - lo - 1;
+        const int k = 31 - __clz(len);
+        const double(*sp)[kComb2MaxD] = src < dst ? sp3 : sp6;
+        ms = fmax(ms, fmax(sp[k][l], sp[k][hi - (1 << k)]));
+      }
+    }
+    double score = CUDART_INF;
+    if (feasible && ms < CUDART_INF) {
+      if (ar >= 0.0) ms = __dadd_rn(ms, ar);  // max_d(g_d + AR) == max_d(g_d) + AR
+      score = __dadd_rn(ms, sur);
+    }
+    const long long idx = pbase + u;
+    if (scores) scores[idx - sbegin] = score;
+    if (lex_less(score, idx, best, best_i)) {
+      best = score;
+      best_i = idx;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const long long oi = __shfl_xor_sync(0xffffffffu, best_i, o);
+    if (oi >= 0 && (best_i < 0 || lex_less(ob, oi, best, best_i))) {
+      best = ob;
+      best_i = oi;
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+    s_best[threadIdx.x >> 5] = best;
+    s_idx[threadIdx.x >> 5] = best_i;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = s_best[0];
+    long long bi = s_idx[0];
+    for (int q = 1; q < (int)(blockDim.x >> 5); ++q)
+      if (s_idx[q] >= 0 && (bi < 0 || lex_less(s_best[q], s_idx[q], b, bi))) {
+        b = s_best[q];
+        bi = s_idx[q];
+      }
+    out_best[blockIdx.x] = b;
+    out_idx[blockIdx.x] = bi;
+  }
+}
+
 __global__ void minloc_kernel(const double* sc, const long long* ix, int n, double* out_s,
                               int64_t* out_i) {
   __shared__ double sb[32];
@@ -1272,7 +1385,10 @@ int rh_search_create(rh_ctx* ctx, const rh_search_desc* desc, rh_search** out, v
                o_repart = take(4 * S->n_stage), o_rspeed = take(8 * S->n_rep),
                o_pstart = take(4 * (S->n_rep + NL)), o_same = take(4 * NL),
                o_base = take(8 * (size_t)d.n_micro_batches),
-               o_bb = take(8 * (size_t)S->eval_blocks * NL), o_bi = take(8 * (size_t)S->eval_blocks * NL),
+               // block results: the old combine's grid per layout, or one per
+               // (layout, partition) pair (combine2)
+               o_bb = take(8 * std::max<size_t>((size_t)S->eval_blocks * NL, S->n_pairs + NL)),
+               o_bi = take(8 * std::max<size_t>((size_t)S->eval_blocks * NL, S->n_pairs + NL)),
                o_rtab = take(8 * (size_t)S->n_rt), o_pinfo = take(16 * (size_t)S->n_pairs),
                o_rl = take(8 * 96 * (size_t)S->n_pairs),
                o_tasks = take(sizeof(PipeTask) * (size_t)NL);
@@ -1539,11 +1655,23 @@ int rh_search_eval(rh_ctx* ctx, rh_search* S, int64_t begin, int64_t end, double
       const long long lo = std::max<long long>(begin, S->lbase[li]);
       const long long hi = std::min<long long>(end, S->lbase[li] + S->lnv[li] * S->lnu[li]);
       if (lo >= hi) continue;
-      const int cb = (int)std::min<long long>(S->eval_blocks, (hi - lo + kEvalThreads - 1) / kEvalThreads);
-      combine_kernel<<<cb, kEvalThreads, 0, gs>>>(a, lo, hi, begin, scores, S->dv.blk_best + n_blk,
-                                                 S->dv.blk_idx + n_blk);
-      RH_CHECK_LAUNCH(ctx);
-      n_blk += cb;
+      if (S->lD[li] <= kComb2MaxD && !getenv("RH_SEARCH_OLD_COMBINE")) {
+        // one CTA per (layout, partition) pair overlapping [lo, hi)
+        const int vlo = (int)((lo - S->lbase[li]) / S->lnu[li]);
+        const int vhi = (int)((hi - 1 - S->lbase[li]) / S->lnu[li]);
+        const int cb = vhi - vlo + 1;
+        combine2_kernel<<<cb, kComb2Threads, 0, gs>>>(a, li, lo, hi, begin, vlo, scores,
+                                                     S->dv.blk_best + n_blk,
+                                                     S->dv.blk_idx + n_blk);
+        RH_CHECK_LAUNCH(ctx);
+        n_blk += cb;
+      } else {
+        const int cb = (int)std::min<long long>(S->eval_blocks, (hi - lo + kEvalThreads - 1) / kEvalThreads);
+        combine_kernel<<<cb, kEvalThreads, 0, gs>>>(a, lo, hi, begin, scores, S->dv.blk_best + n_blk,
+                                                   S->dv.blk_idx + n_blk);
+        RH_CHECK_LAUNCH(ctx);
+        n_blk += cb;
+      }
     }
   }
   for (int q = 0; q < n_used; ++q) {
