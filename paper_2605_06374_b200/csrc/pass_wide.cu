@@ -128,7 +128,11 @@ struct WideWalk {
 // CTAs per SM the register budget targets: the loop-carried chain state is
 // 3P doubles (finish, last F finish, cost sum per stage), so long pipelines
 // trade occupancy for registers (P = 16: 168 registers, 6 CTAs = 12 warps).
+#ifdef RH_WIDE_MINB
+constexpr int wide_min_blocks(int P) { return P <= 10 ? 8 : RH_WIDE_MINB; }  // A/B builds
+#else
 constexpr int wide_min_blocks(int P) { return P <= 10 ? 8 : (P <= 12 ? 7 : 6); }
+#endif
 
 template <int P, int DETECT>
 __global__ void __launch_bounds__(kWideThreads, wide_min_blocks(P)) pass_wide_kernel(const PassParams p) {

@@ -389,6 +389,101 @@ def _simulate_canonical(state, cfg, micro_batches, model, dp_counts, comm, itera
         link_ratio=used_link_ratios(state, cfg) if comm is not None else {}, migrations=0)
 
 
+def simulate_iteration_batch(items):
+    """simulate_iteration for many independent (state, cfg, micro_batches,
+    model, plan, comm, iteration, capacity) items: every canonical item (no
+    migrations) with the same pipeline shape, cost model and capacity shares
+    ONE rh_pipeline_batch launch (each item = two trace iterations: its
+    actual and healthy views); migration plans take the general-DAG path one
+    by one.  Returns a list of IterationRecord, or the exception an item
+    raises (SimulationError / ValueError) in its place."""
+    import torch
+
+    out = [None] * len(items)
+    groups = {}
+    for k, (state, cfg, mbs, model, plan, comm, iteration, capacity) in enumerate(items):
+        try:
+            bad = validate_cluster(state, cfg, check_capacity=False)
+            if bad:
+                raise SimulationError("invalid cluster: " + "; ".join(bad))
+            executors = {(m.mb, m.stage): m.executor
+                         for m in (getattr(plan, "migrations", None) or [])} if plan else {}
+            budgets = {mb.token_budget for mb in mbs}
+            if executors or len(budgets) != 1 or any(x < 0 for x in cfg.layer_partition) or \
+                    (capacity is not None and min(cfg.layer_partition, default=1) == 0):
+                out[k] = simulate_iteration(state, cfg, mbs, model, plan, comm=comm,
+                                            iteration=iteration, capacity=capacity)
+                continue
+            dp_counts = getattr(plan, "dp_assignment", None) if plan is not None else None
+            owned = split_micro_batches(mbs, cfg.dp, dp_counts)
+            owner = {mb.id: d for d, ms in enumerate(owned) for mb in ms}
+            speeds, _ = stage_speed_maps(state, cfg)
+            _completeness(state, cfg, mbs, owner, {}, speeds)
+            key = (cfg.pp, cfg.dp, cfg.tp, cfg.schedule, len(mbs), mbs[0].token_budget,
+                   model.alpha, model.beta, tuple(sorted(model.chunk_ratios.items())),
+                   comm is not None, capacity)
+            groups.setdefault(key, []).append(k)
+        except (SimulationError, ValueError) as exc:
+            out[k] = exc
+    dev = torch.device("cuda", torch.cuda.current_device())
+    lib = _lib.load_library()
+    for key, ks in groups.items():
+        segs, offs, docs, counts_l = [], [], [], []
+        base = 0
+        for k in ks:
+            state, cfg, mbs, model, plan, comm, iteration, capacity = items[k]
+            M, N = len(mbs), mbs[0].token_budget
+            counts = dp_counts_or_even(M, cfg.dp, getattr(plan, "dp_assignment", None)
+                                       if plan is not None else None)
+            counts_l.append(counts)
+            segs.append(segment_for_view(state, cfg, M, N, comm=comm, dp_counts=counts))
+            segs.append(segment_for_view(state, cfg, M, N, comm=comm, dp_counts=counts,
+                                         healthy=True, clean_links=True))
+            off, d = csr_of(mbs)
+            n_docs = int(off[-1])
+            offs += [off[:-1] + base, off[:-1] + base + n_docs]
+            docs += [d, d]
+            base += 2 * n_docs
+        offs.append(np.array([base]))
+        state, cfg, mbs, model, plan, comm, iteration, capacity = items[ks[0]]
+        M, N, G = len(mbs), mbs[0].token_budget, cfg.dp * cfg.pp
+        n = 2 * len(ks)
+        dsegs = DeviceSegments(segs, dev)
+        t_off = torch.from_numpy(np.concatenate(offs).astype(np.int32)).to(dev)
+        t_doc = torch.from_numpy(np.concatenate(docs).astype(np.int32)).to(dev)
+        t_seg = torch.arange(n, dtype=torch.int32, device=dev)
+        tr = _lib.Trace(n, t_seg.data_ptr(), t_off.data_ptr(), t_doc.data_ptr(), None, None)
+        ms = torch.empty(n, dtype=torch.float64, device=dev)
+        st = torch.empty(n, dtype=torch.uint8, device=dev)
+        sc = torch.empty(n * G, dtype=torch.float64, device=dev)
+        res = _lib.PassOut(ms.data_ptr(), st.data_ptr(), sc.data_ptr(), None, None)
+        shape = pipe_shape(cfg, M, N, capacity=capacity, has_allreduce=comm is not None,
+                           max_mb=dsegs.max_mb)
+        _lib.check(lib.rh_pipeline_batch(_lib.context(), _lib.C.byref(shape),
+                                         _lib.C.byref(cost_model_c(model)),
+                                         _lib.C.byref(dsegs.c), _lib.C.byref(tr),
+                                         _lib.C.byref(res), _lib.stream_handle()),
+                   "rh_pipeline_batch")
+        ms_h, st_h, sc_h = ms.cpu().numpy(), st.cpu().numpy(), sc.cpu().numpy().reshape(n, G)
+        for q, k in enumerate(ks):
+            state, cfg, mbs, model, plan, comm, iteration, capacity = items[k]
+            if st_h[2 * q] & _lib.RH_IT_STOPPED:
+                out[k] = SimulationError("execution completeness violated")
+                continue
+            if st_h[2 * q] & _lib.RH_IT_CAPACITY:
+                out[k] = SimulationError(f"activation footprint exceeds capacity {capacity}")
+                continue
+            observed, predicted = float(ms_h[2 * q]), float(ms_h[2 * q + 1])
+            stage_cost, stage_ref = _stage_dicts(cfg, counts_l[q], sc_h[2 * q], sc_h[2 * q + 1])
+            busy, idle = _busy_idle(state, stage_cost, observed)
+            out[k] = IterationRecord(
+                iteration=iteration, observed_time=observed, predicted_healthy_time=predicted,
+                per_device_busy=busy, per_device_idle=idle, stage_cost=stage_cost,
+                stage_cost_reference=stage_ref,
+                link_ratio=used_link_ratios(state, cfg) if comm is not None else {}, migrations=0)
+    return out
+
+
 def _simulate_general(state, cfg, micro_batches, model, executors, dp_counts, orders, owner,
                       speeds, healthy, comm, iteration, capacity):
     from .comm import LinkModel

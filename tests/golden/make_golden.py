@@ -569,6 +569,63 @@ def gen_search_bench(per_config=1200):
     dump("search_bench", out)
 
 
+# --------------------------------------------------- batched closed loop
+def closed_loop_mappings():
+    """Acceptance criterion 4's fail-slow scenarios (test_acceptance.py:193-223:
+    16 GPUs TP4 x DP2 x PP2, 24 micro-batches of lognormal(7.0, 0.25), one
+    fail-slow of random device / severity near iteration 25, resihp, 34
+    iterations; the same random.Random(99) draws), the first 16 trials, plus
+    mixed scenarios: a fail-stop with heartbeats, a slow link, two staggered
+    fail-slows on a wider pipeline."""
+    from resilsim.harness import run_scenario, scenario_from_mapping
+
+    def det(seed, iterations, policy, failures=()):
+        return {"name": "detect", "seed": seed, "iterations": iterations, "policy": policy,
+                "cluster": {"nodes": 2, "devices_per_node": 8},
+                "parallelism": {"tp": 4, "dp": 2, "pp": 2, "layers": 8},
+                "workload": {"token_budget": 4096, "micro_batches": 24,
+                             "doc_lengths": {"kind": "lognormal", "mean": 7.0,
+                                             "sigma": 0.25}},
+                "failures": list(failures)}
+
+    probe = det(0, 12, "none")
+    h = run_scenario(scenario_from_mapping(probe)).summary["avg_iteration_s"]
+    rng = random.Random(99)
+    out = []
+    for i in range(16):
+        severity = rng.uniform(0.3, 0.7)
+        device = rng.randrange(16)
+        out.append(det(1000 + i, 34, "resihp", [{"kind": "fail_slow_compute", "device": device,
+                                                 "start": h * 25.4, "severity": severity}]))
+    out.append(det(3001, 30, "resihp", [{"kind": "fail_stop", "device": 6, "start": h * 9.5}]))
+    out.append(det(3002, 30, "resihp", [{"kind": "fail_slow_comm", "link": [0, 1],
+                                         "start": h * 12.2, "severity": 0.4}]))
+    wide = det(3003, 40, "resihp", [
+        {"kind": "fail_slow_compute", "device": 3, "start": h * 8.3, "severity": 0.5},
+        {"kind": "fail_slow_compute", "device": 27, "start": h * 21.7, "severity": 0.6}])
+    wide["cluster"] = {"nodes": 4, "devices_per_node": 8}
+    wide["parallelism"] = {"tp": 4, "dp": 2, "pp": 4, "layers": 16}
+    out.append(wide)
+    out.append(det(3004, 20, "none", [{"kind": "fail_slow_compute", "device": 9,
+                                       "start": h * 5.0, "severity": 0.5}]))
+    return out
+
+
+def gen_closed_loop():
+    """The reference's run_scenario rows / plans / detections on the
+    closed-loop scenarios (harness.py:283-475)."""
+    from resilsim.harness import run_scenario, scenario_from_mapping
+
+    cases = []
+    for m in closed_loop_mappings():
+        res = run_scenario(scenario_from_mapping(m))
+        cases.append({"mapping": m, "rows": res.iteration_rows,
+                      "plans": [[k, p.reason] for k, p in res.plans],
+                      "aborted_at": res.summary["aborted_at"]})
+        print(m["seed"], len(res.iteration_rows), "plans", [k for k, _ in res.plans], flush=True)
+    dump("closed_loop", {"cases": cases})
+
+
 # ----------------------------------------------------------------- migration
 def gen_migration():
     """Reference plan_migration (scheduler.py:272-513) on random problems."""
@@ -692,6 +749,6 @@ def gen_policies():
 
 if __name__ == "__main__":
     which = sys.argv[1:] or ["workload", "pipeline", "detector", "scheduler", "search",
-                             "search_bench", "migration", "policies"]
+                             "search_bench", "migration", "policies", "closed_loop"]
     for w in which:
         globals()[f"gen_{w}"]()
