@@ -170,6 +170,52 @@ def cpu_baseline(tr, threads=None):
                       "+DetectorState.observe), pthreads over iterations"}
 
 
+def _py_ref_worker(args):
+    """One reference run_scenario (baseline/_ref) at the C2 shape -> (iterations, seconds)."""
+    ref_dir, seed, iters = args
+    sys.path.insert(0, ref_dir)
+    from resilsim.harness import run_scenario, scenario_from_mapping
+
+    m = {"name": "c2", "seed": seed, "iterations": iters, "policy": "resihp",
+         "cluster": {"nodes": 32, "devices_per_node": 8},
+         "parallelism": {"tp": 4, "dp": 16, "pp": 4, "layers": 40},
+         "workload": {"token_budget": 4096, "micro_batches": 128,
+                      "doc_lengths": {"kind": "lognormal", "mean": 7.2, "sigma": 0.8}},
+         "failures": []}
+    sc = scenario_from_mapping(m)
+    t0 = time.perf_counter()
+    res = run_scenario(sc)
+    return len(res.records), time.perf_counter() - t0
+
+
+def python_reference_baseline(budget_s=20.0):
+    """The reference's own Python Detector loop: resilsim
+    run_scenario at the C2 shape -- per iteration simulate_iteration (actual +
+    known view) and DetectorState.observe -- one scenario per process over
+    all host cores (the cli.py:86-92 ProcessPool pattern); device-samples/s =
+    iterations x 256 devices / wall time."""
+    from concurrent.futures import ProcessPoolExecutor
+
+    ref_dir = ROOT / "baseline" / "_ref"
+    if not (ref_dir / "resilsim").exists():
+        return {"unavailable": "baseline/_ref (pip install of /root/reference/pkg) is missing"}
+    cores = os.cpu_count() or 1
+    # size: one probe run on this core, then a pool round of ~budget_s
+    n0, t0 = _py_ref_worker((str(ref_dir), 0, 2))
+    per_iter = t0 / max(1, n0)
+    iters = max(2, int(budget_s / max(per_iter, 1e-3)))
+    wall0 = time.perf_counter()
+    with ProcessPoolExecutor(max_workers=cores) as ex:
+        res = list(ex.map(_py_ref_worker, [(str(ref_dir), 1 + k, iters) for k in range(cores)]))
+    wall = time.perf_counter() - wall0
+    n = sum(r[0] for r in res)
+    return {"value": n * 256 / wall, "unit": UNIT, "cores": cores, "kind": "reference",
+            "sample": f"{cores} x resilsim run_scenario (C2 shape: 256 GPUs TP4xDP16xPP4, 128 "
+                      f"micro-batches, resihp detector on, no re-plan), {iters} iterations each, "
+                      "one process per core (cli.py:86-92 pattern); includes scenario setup",
+            "per_iteration_ms_one_core": per_iter * 1e3}
+
+
 def run_reference(args, world, rank):
     """--impl reference: the reference algorithm's CPU restatement on all host cores."""
     if rank != 0:
@@ -672,6 +718,7 @@ def main():
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(tr)
+            line["cpu_baseline_python_reference"] = python_reference_baseline()
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
