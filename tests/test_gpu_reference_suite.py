@@ -45,7 +45,7 @@ def test_reference_unit_tests_pass_on_the_drop_in():
     cmd = [sys.executable, "-m", "pytest", str(SUITE), "-q", "-p", "no:cacheprovider",
            "-o", "addopts=", "--rootdir", str(SUITE), "-x"]
     for t in OUT_OF_SCOPE:
-        cmd += ["--deselect", f"{SUITE}/{t}"]
+        cmd += ["--deselect", t]
     r = subprocess.run(cmd, capture_output=True, text=True, cwd=SUITE, timeout=1800)
     tail = r.stdout[-4000:] + r.stderr[-2000:]
     assert r.returncode == 0, tail
