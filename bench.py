@@ -16,8 +16,9 @@ validation, and the median/MAD change-point state machine.
            wire form (H2D + kernels + D2H inside the timed region);
   roofline of the dominant kernel (pass_small_kernel<P=4,1F1B,detect>);
   cpu_baseline = the C oracle restatement of the reference on the host cores.
-Multi-GPU (torchrun): each rank processes its own trace (weak scaling, no
-data-path collective); the step time is the max over ranks.
+Multi-GPU (torchrun): one trace of N x 10^4 iterations in contiguous shards, one
+per rank, cut at series resets (adaptation boundaries: detect_shard.py), so no
+data-path collective (weak scaling); the step time is the max over ranks.
 """
 
 from __future__ import annotations
@@ -256,7 +257,10 @@ def config_of(tr):
             "iterations_per_step": tr.n_iter, "devices": c.tp * c.dp * c.pp,
             "micro_batches": tr.M, "token_budget": tr.N,
             "doc_lengths": "lognormal(7.2, 0.8) FFD-packed", "l2": "flushed (256 MiB write) "
-            "before every step; trace ~35 MB", "parallelism": "independent trace per rank"}
+            "before every step; trace ~35 MB per rank",
+            "parallelism": "one trace of n_gpus x 10^4 iterations, one contiguous shard per "
+                           "rank cut at series resets (detect_shard.py), no data-path "
+                           "collective"}
 
 
 def run_ours(args, world, rank, local):
@@ -268,6 +272,12 @@ def run_ours(args, world, rank, local):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     tr = build_trace(rank, N_ITER, use_oracle=False)
+    if world > 1 and rank > 0:
+        # rank r holds iterations [r*10^4, (r+1)*10^4) of ONE trace of world*10^4
+        # iterations; its shard starts at a series reset (an adaptation
+        # boundary), so its screen needs no state from rank r-1
+        # (detect_shard.shard_bounds): no data-path collective
+        tr.reset[0] = 1
     p = DetectorPass(tr, dev)
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(256 * 2**20, dtype=torch.uint8, device=dev)
