@@ -378,6 +378,19 @@ __global__ void __launch_bounds__(TW, (ZBH ? 4 : kSmallMinBlocks) * (kSmallThrea
       meas[s] = mx;
     }
   }
+  // the segment's exercised-link test, loads issued now (4 independent
+  // chains) so their latency overlaps the staging
+  bool link_bad = false;
+  if (DETECT && on && p.sg.link_off) {
+    const int32_t q0 = __ldg(p.sg.link_off + seg), q1 = __ldg(p.sg.link_off + seg + 1);
+    int32_t q = q0 + d;
+    for (; q + 3 * D < q1; q += 4 * D) {
+      const double a0 = __ldg(p.sg.link_ratio + q), a1 = __ldg(p.sg.link_ratio + q + D),
+                   a2 = __ldg(p.sg.link_ratio + q + 2 * D), a3 = __ldg(p.sg.link_ratio + q + 3 * D);
+      link_bad = link_bad || a0 > p.thr || a1 > p.thr || a2 > p.thr || a3 > p.thr;
+    }
+    for (; q < q1; q += D) link_bad = link_bad || __ldg(p.sg.link_ratio + q) > p.thr;
+  }
   RH_DMARK(1);
   if (pf) {
     prefetch_l2(p.tr.mb_off + pf_it * M, 4 * (size_t)(pf_nmb + 1));
@@ -403,9 +416,9 @@ __global__ void __launch_bounds__(TW, (ZBH ? 4 : kSmallMinBlocks) * (kSmallThrea
     for (int k = 0; k < md; ++k, j = j + 1 == md ? 0 : j + 1) {
       const double b = __dadd_rn(lin, __dmul_rn(p.m.beta, (double)(long long)q[j]));
       base_t[j * TW + tid] = b;
-      if (!all_unit) {
-        b_hi = fmax(b_hi, b);
-        if (b > 0.0) b_lo = fmin(b_lo, b);
+      if (!all_unit) {  // (finite, non-negative: plain compares)
+        b_hi = b > b_hi ? b : b_hi;
+        if (b > 0.0 && b < b_lo) b_lo = b;
       }
     }
   }
@@ -440,13 +453,20 @@ __global__ void __launch_bounds__(TW, (ZBH ? 4 : kSmallMinBlocks) * (kSmallThrea
       const double rs[3] = {rlF[s], rlB[s], ZBH ? rlW[s] : rlB[s]};
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
-        r_hi = fmax(r_hi, rs[k]);
-        if (rs[k] > 0.0) r_lo = fmin(r_lo, rs[k]);
+        r_hi = rs[k] > r_hi ? rs[k] : r_hi;
+        if (rs[k] > 0.0 && rs[k] < r_lo) r_lo = rs[k];
       }
     }
     safe = safe && div_range_ok(r_lo * b_lo, r_hi * b_hi);
   }
-  WalkArgs<P, TW> wa{bt, rlF, rlB, rlW, sp, inv, hf, hb, fin, ssum};
+  // warp-uniform: the stages any replica of the warp runs slow (only those
+  // divide; x / 1.0 == x exactly)
+  unsigned slow = 0;
+#pragma unroll
+  for (int s = 0; s < P; ++s)
+    if (mm > 0 && sp[s] != 1.0) slow |= 1u << s;
+  slow = __reduce_or_sync(0xffffffffu, slow);
+  WalkArgs<P, TW> wa{bt, rlF, rlB, rlW, sp, inv, hf, hb, fin, ssum, slow};
   RH_DMARK(3);
   if (mm > 0) {
     const unsigned long long* l0 = p.sched + __ldg(p.sched_off + mm);
@@ -488,11 +508,7 @@ __global__ void __launch_bounds__(TW, (ZBH ? 4 : kSmallMinBlocks) * (kSmallThrea
         }
       }
     }
-    if (DETECT && p.sg.link_off) {  // exercised-link ratios, split over the replicas
-      const int32_t q0 = __ldg(p.sg.link_off + seg), q1 = __ldg(p.sg.link_off + seg + 1);
-      for (int32_t q = q0 + d; q < q1; q += D)
-        if (__ldg(p.sg.link_ratio + q) > p.thr) bits |= RH_IT_LINK_FLAG;
-    }
+    if (link_bad) bits |= RH_IT_LINK_FLAG;
     if (bits) atomicOr(it_st + li, bits);
   }
   __syncthreads();
@@ -749,6 +765,7 @@ int launch_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
     p.static_max = kStaticMaxMB;
 #endif
     p.steady = getenv("RH_NO_STEADY_WALK") ? 0 : 1;
+    p.q32 = getenv("RH_NO_Q32") ? 0 : 1;
     p.ltab = nullptr;
     const size_t smem = p.region_off + region;
     if (smem <= ctx->smem_optin && smem <= 56 * 1024) {

@@ -38,6 +38,7 @@ struct PassParams {
   // layers [ipb][3][P] doubles, then a union of {offsets (ipb*M+1 int32,
   // 16 B slack) + documents (doc_stage int32)} and {hops [2][P][TW] doubles}
   int w_base, w_rl, w_union, w_docs;
+  int q32;         // micro-batch sum l^2 in 32-bit integers (exactness checked per micro-batch)
   int static_max;  // largest micro-batch count walked by the unrolled code
   int steady;      // m >= P: the steady-state loop walk (walk_steady)
   // lane kernel only: level table (lane_table), NULL = closed-form walk
@@ -149,10 +150,13 @@ __device__ __forceinline__ double lds_nc(const double* p) {
 // stay in registers.
 //
 // WalkArgs (pass_small_kernel, P <= 4): everything in registers.
+#ifndef RH_SMALL_SLOWMASK
+#define RH_SMALL_SLOWMASK 0  // A/B knob: measured slower for the P <= 4 walks (40.0 vs 37.5 us)
+#endif
 template <int P, int TW>
 struct WalkArgs {
   static constexpr int kStride = TW;  // CTA width: base costs live [j][thread]
-  static constexpr bool kSlowMask = false;
+  static constexpr bool kSlowMask = RH_SMALL_SLOWMASK != 0;
   const double* bt;  // base costs of this thread: bt[j * kStride]
   const double (&rlF_)[P];
   const double (&rlB_)[P];
@@ -163,6 +167,9 @@ struct WalkArgs {
   const double (&hb_)[P];
   double (&fin)[P];
   double (&ssum)[P];
+  // warp-uniform: bit s = some replica of the warp runs stage s slower than
+  // 1.0; the other stages skip the division (x / 1.0 == x exactly)
+  unsigned slow;
   __device__ __forceinline__ static double ld(const double* p) { return *p; }
   __device__ __forceinline__ double rlF(int s) const { return rlF_[s]; }
   __device__ __forceinline__ double rlB(int s) const { return rlB_[s]; }
@@ -171,6 +178,7 @@ struct WalkArgs {
   __device__ __forceinline__ double inv(int s) const { return inv_[s]; }
   __device__ __forceinline__ double hf(int s) const { return hf_[s]; }
   __device__ __forceinline__ double hb(int s) const { return hb_[s]; }
+  __device__ __forceinline__ bool is_slow(int s) const { return (slow >> s) & 1u; }
 };
 
 // One chunk of stage s: c = (rl * b) [/ speed], start = max(chain finish,
@@ -462,6 +470,36 @@ __device__ __forceinline__ void stage_finish(const PassParams& p, const CtaStage
   __syncthreads();    // ... and so have the threads' edge words
   const int32_t* s_off = g.so.dst;
   const int32_t* s_doc = g.sd.dst;
+  if (p.q32 && g.staged) {
+    // 32-bit integer sums: whenever sum l < 2^16, sum l^2 <= (sum l)^2 < 2^32
+    // is exact (a packed micro-batch holds N = token_budget tokens); a
+    // micro-batch above that is redone in 64-bit
+    for (int mb = threadIdx.x; mb < c.n_mb; mb += blockDim.x) {
+      const int32_t k0 = s_off[mb] - g.d_lo, k1 = s_off[mb + 1] - g.d_lo;
+      const int32_t nd = k1 - k0;
+      uint32_t q = 0, sl = 0;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const uint32_t l = t < nd ? (uint32_t)s_doc[k0 + t] : 0u;
+        q += l * l;
+        sl += l;
+      }
+      for (int32_t k = k0 + 4; k < k1; ++k) {
+        const uint32_t l = (uint32_t)s_doc[k];
+        q += l * l;
+        sl += l;
+      }
+      unsigned long long q64 = q;
+      if (sl >= 65536u || nd < 0) {
+        q64 = 0;
+        for (int32_t k = k0; k < k1; ++k) {
+          const long long l = s_doc[k];
+          q64 += (unsigned long long)(l * l);
+        }
+      }
+      c.s_q[mb] = q64;
+    }
+  } else {
   for (int mb = threadIdx.x; mb < c.n_mb; mb += blockDim.x) {
     const int32_t k0 = s_off[mb] - g.d_lo, k1 = s_off[mb + 1] - g.d_lo;
     unsigned long long q = 0;
@@ -485,6 +523,7 @@ __device__ __forceinline__ void stage_finish(const PassParams& p, const CtaStage
       }
     }
     c.s_q[mb] = q;
+  }
   }
   __syncthreads();  // sums complete; the document buffer is dead from here
 }
