@@ -250,6 +250,8 @@ int rh_ctx_destroy(rh_ctx* ctx) {
   }
   if (ctx->aux_fork) cudaEventDestroy(ctx->aux_fork);
   if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
+  if (ctx->host_stage) cudaFreeHost(ctx->host_stage);
+  for (void* p : ctx->host_stage_retired) cudaFreeHost(p);
   delete ctx;
   return RH_OK;
 }

@@ -43,6 +43,10 @@ struct rh_ctx {
   // host-buffer entry points: copy stream + per-chunk events (lazily made)
   static constexpr int kChunkEvents = 8;
   cudaStream_t copy_stream = nullptr;
+  // pinned staging of the host pass's small inputs (fill_small_stage)
+  void* host_stage = nullptr;
+  size_t host_stage_bytes = 0;
+  std::vector<void*> host_stage_retired;
   cudaEvent_t chunk_ev[kChunkEvents] = {};
   // side stream of the host pass (rh_screen_prepare while the trace streams in)
   cudaStream_t side_stream = nullptr;

@@ -915,7 +915,69 @@ struct Carver {
 // Chunks of the host pass: H2D of chunk k+1 overlaps the kernels of chunk k.
 // (each extra chunk costs a handful of DMA setups; 4 measured best on B200)
 static int host_chunks(int64_t n) {
-  return (int)std::max<int64_t>(1, std::min<int64_t>(4, n / 1024));
+  static const int force = getenv("RH_HOST_CHUNKS") ? atoi(getenv("RH_HOST_CHUNKS")) : 0;
+  // 2 measured best on B200 (fewer DMA setups; 1: no overlap, 4: 613 vs 572 us)
+  const int cap = force > 0 ? std::min(force, rh_ctx::kChunkEvents) : 2;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(cap, n / 1024));
+}
+
+// The host pass's small inputs -- segment tables and the screen history --
+// travel as ONE copy: they are gathered into a pinned staging buffer of the
+// context on every call (a few KB of host memcpy) and the pass (or its
+// captured graph) copies the staging buffer to the device.  Separate
+// cudaMemcpyAsync calls cost ~5 us of DMA setup each.
+struct SmallLayout {
+  size_t layers, mbs, speed, hf, hb, ar, loff, lr, hist, bytes;
+};
+static SmallLayout small_layout(const rh_pipe_shape* sh, const rh_segments* sg) {
+  const int64_t P = sh->pp, D = sh->dp, G = D * P, S = sg->n_seg;
+  const int64_t n_links = sg->link_off ? sg->link_off[S] : 0;
+  SmallLayout L;
+  Carver c{nullptr};
+  L.layers = (size_t)(uintptr_t)c.take<int32_t>(S * P);
+  L.mbs = (size_t)(uintptr_t)c.take<int32_t>(S * (D + 1));
+  L.speed = (size_t)(uintptr_t)c.take<double>(S * G);
+  L.hf = (size_t)(uintptr_t)c.take<double>(S * G);
+  L.hb = (size_t)(uintptr_t)c.take<double>(S * G);
+  L.ar = (size_t)(uintptr_t)c.take<double>(S * D);
+  L.loff = (size_t)(uintptr_t)c.take<int32_t>(S + 1);
+  L.lr = (size_t)(uintptr_t)c.take<double>(n_links + 1);
+  L.hist = (size_t)(uintptr_t)c.take<double>(64);
+  L.bytes = (c.off + 255) & ~size_t(255);
+  return L;
+}
+
+static int fill_small_stage(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_segments* sg,
+                            const rh_screen_params* screen, int64_t series_len,
+                            const double* hist) {
+  const SmallLayout L = small_layout(sh, sg);
+  if (L.bytes > ctx->host_stage_bytes) {
+    // a captured graph may still copy from the old buffer: retire it
+    if (ctx->host_stage) ctx->host_stage_retired.push_back(ctx->host_stage);
+    ctx->host_stage = nullptr;
+    ctx->host_stage_bytes = 0;
+    RH_CUDA(cudaMallocHost(&ctx->host_stage, L.bytes + L.bytes / 2 + 4096));
+    ctx->host_stage_bytes = L.bytes + L.bytes / 2 + 4096;
+    std::lock_guard<std::mutex> lock(ctx->ws_mu);
+    ++ctx->ws_epoch;
+  }
+  char* h = static_cast<char*>(ctx->host_stage);
+  const int64_t P = sh->pp, D = sh->dp, G = D * P, S = sg->n_seg;
+  const int64_t n_links = sg->link_off ? sg->link_off[S] : 0;
+  auto put = [&](size_t off, const void* src, size_t bytes) {
+    if (src && bytes) memcpy(h + off, src, bytes);
+  };
+  put(L.layers, sg->layers, 4 * S * P);
+  put(L.mbs, sg->mb_start, 4 * S * (D + 1));
+  put(L.speed, sg->speed, 8 * S * G);
+  put(L.hf, sg->hop_fwd, 8 * S * G);
+  put(L.hb, sg->hop_bwd, 8 * S * G);
+  put(L.ar, sg->allreduce, 8 * S * D);
+  put(L.loff, sg->link_off, 4 * (S + 1));
+  put(L.lr, sg->link_ratio, 8 * n_links);
+  const int64_t hcount = screen ? std::min<int64_t>(series_len, screen->window) : 0;
+  put(L.hist, hist, 8 * std::min<int64_t>(hcount, 64));
+  return RH_OK;
 }
 
 // Host-buffer Detector pass over an int32 trace (tr) or a packed one (pk):
@@ -956,18 +1018,12 @@ int enqueue_host_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model*
     c.take<int32_t>(n_docs);
     c.take<float>(n * G * T);
     c.take<double>(n);
-    c.take<int32_t>(S * P);
-    c.take<int32_t>(S * (D + 1));
-    c.take<double>(S * G * 3);
-    c.take<double>(S * D);
-    c.take<int32_t>(S + 1);
-    c.take<double>(n_links + 1);
+    c.take<char>(small_layout(sh, sg).bytes);
     c.take<double>(n);
     c.take<uint8_t>(n);
     c.take<double>(n * G);
     c.take<uint8_t>(n * G);
     c.take<float>(n * G);
-    c.take<double>(64);
     c.take<uint8_t>(n);
     c.take<uint8_t>(n);
     c.take<int64_t>(1);
@@ -990,21 +1046,23 @@ int enqueue_host_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model*
   float* d_dt = c.take<float>(n * G * T);
   double* d_obs = c.take<double>(n);
   rh_segments dsg = *sg;
-  int32_t* d_layers = c.take<int32_t>(S * P);
-  int32_t* d_mbs = c.take<int32_t>(S * (D + 1));
-  double* d_speed = c.take<double>(S * G);
-  double* d_hf = c.take<double>(S * G);
-  double* d_hb = c.take<double>(S * G);
-  double* d_ar = c.take<double>(S * D);
-  int32_t* d_loff = c.take<int32_t>(S + 1);
-  double* d_lr = c.take<double>(n_links + 1);
+  const SmallLayout SL = small_layout(sh, sg);
+  char* d_small = c.take<char>(SL.bytes);
+  int32_t* d_layers = reinterpret_cast<int32_t*>(d_small + SL.layers);
+  int32_t* d_mbs = reinterpret_cast<int32_t*>(d_small + SL.mbs);
+  double* d_speed = reinterpret_cast<double*>(d_small + SL.speed);
+  double* d_hf = reinterpret_cast<double*>(d_small + SL.hf);
+  double* d_hb = reinterpret_cast<double*>(d_small + SL.hb);
+  double* d_ar = reinterpret_cast<double*>(d_small + SL.ar);
+  int32_t* d_loff = reinterpret_cast<int32_t*>(d_small + SL.loff);
+  double* d_lr = reinterpret_cast<double*>(d_small + SL.lr);
+  double* d_hist = reinterpret_cast<double*>(d_small + SL.hist);
   rh_pass_out dout = {};
   dout.makespan = c.take<double>(n);
   dout.status = c.take<uint8_t>(n);
   dout.stage_cost = out->stage_cost ? c.take<double>(n * G) : nullptr;
   dout.stage_flag = out->stage_flag ? c.take<uint8_t>(n * G) : nullptr;
   dout.severity = out->severity ? c.take<float>(n * G) : nullptr;
-  double* d_hist = c.take<double>(64);
   uint8_t* d_reset = c.take<uint8_t>(n);
   uint8_t* d_outcome = c.take<uint8_t>(n);
   int64_t* d_len = c.take<int64_t>(1);
@@ -1019,16 +1077,9 @@ int enqueue_host_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model*
   };
   const auto H2D = cudaMemcpyHostToDevice;
   const auto D2H = cudaMemcpyDeviceToHost;
-  // segment tables + screen state on the compute stream
-  if ((rc = cp(d_layers, sg->layers, 4 * S * P, H2D, stream)) ||
-      (rc = cp(d_mbs, sg->mb_start, 4 * S * (D + 1), H2D, stream)) ||
-      (rc = cp(d_speed, sg->speed, 8 * S * G, H2D, stream)) ||
-      (rc = cp(d_hf, sg->hop_fwd, 8 * S * G, H2D, stream)) ||
-      (rc = cp(d_hb, sg->hop_bwd, 8 * S * G, H2D, stream)) ||
-      (rc = cp(d_ar, sg->allreduce, 8 * S * D, H2D, stream)) ||
-      (rc = cp(d_loff, sg->link_off, 4 * (S + 1), H2D, stream)) ||
-      (rc = cp(d_lr, sg->link_ratio, 8 * n_links, H2D, stream)))
-    return rc;
+  // segment tables + screen history: one copy of the staging buffer that
+  // detect_host filled for this call (fill_small_stage)
+  if ((rc = cp(d_small, ctx->host_stage, SL.bytes, H2D, stream))) return rc;
   dsg.layers = d_layers;
   dsg.mb_start = d_mbs;
   dsg.speed = d_speed;
@@ -1042,7 +1093,6 @@ int enqueue_host_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model*
     set_error("detector_pass_host: window > 64");
     return RH_E_INVALID;
   }
-  if ((rc = cp(d_hist, hist, 8 * h, H2D, stream))) return rc;
   if (screen && reset && (rc = cp(d_reset, reset, n, H2D, stream))) return rc;
   // the screen's inputs are tiny: copy them first and start its input-only
   // half (rh_screen_prepare) on the side stream while the trace streams in
@@ -1196,6 +1246,7 @@ int detect_host(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
   }
   if ((pk ? pk->n_iter : tr->n_iter) == 0) return RH_OK;
   DeviceGuard guard(ctx);
+  if (int rc = fill_small_stage(ctx, sh, sg, screen, series_len, hist)) return rc;
   auto& g = ctx->host_graph;
   std::vector<uint64_t> key = host_pass_key(sh, m, sg, tr, pk, thr, screen, series_len, hist,
                                             reset, out, outcome, series_len_out, stream);
