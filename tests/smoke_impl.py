@@ -28,4 +28,21 @@ def run_smoke() -> None:
     assert np.array_equal(r["status"], ost), "status"
     assert np.array_equal(r["stage_flag"], ofl), "flags"
     assert np.array_equal(r["outcome"], ooc) and r["series_len"] == oln, "screen"
-    print(f"smoke ok: {tr.n_iter} iterations bit-exact, {_lib.launches()} launches")
+    # a long pipeline (the trace-R / C3-C5 kernel, pass_wide_kernel) ...
+    tw = with_measurements(random_trace(11, n_iter=40, tp=8, dp=8, pp=16, M=136, comm=True,
+                                        schedule="1f1b"), oracle, noise=0.02)
+    pw = DetectorPass(tw)
+    pw.detect()
+    rw = pw.results()
+    wms, wst, *_ = oracle.detect(tw)
+    assert np.array_equal(rw["makespan"].view(np.uint64), wms.view(np.uint64)), "wide makespan"
+    assert np.array_equal(rw["status"], wst), "wide status"
+    # ... and one re-plan search (register walks, combine2, min-loc)
+    from paper_2605_06374_b200.search import ReplanSearch
+    from tests.golden_io import load, search_problem
+
+    case = load("search")["cases"][0]
+    *_, inputs = search_problem(case)
+    assert list(ReplanSearch(inputs).best()) == case["best"], "search winner"
+    print(f"smoke ok: {tr.n_iter} + {tw.n_iter} iterations bit-exact, search winner, "
+          f"{_lib.launches()} launches")
