@@ -237,6 +237,10 @@ int rh_ctx_destroy(rh_ctx* ctx) {
   for (void* p : ctx->ws_retired) cudaFree(p);
   for (cudaEvent_t e : ctx->chunk_ev)
     if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : ctx->done_ev)
+    if (e) cudaEventDestroy(e);
+  if (ctx->d2h_ev) cudaEventDestroy(ctx->d2h_ev);
+  if (ctx->d2h_stream) cudaStreamDestroy(ctx->d2h_stream);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->side_stream) cudaStreamDestroy(ctx->side_stream);
   if (ctx->side_ev) cudaEventDestroy(ctx->side_ev);

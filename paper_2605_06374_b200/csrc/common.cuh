@@ -48,6 +48,11 @@ struct rh_ctx {
   size_t host_stage_bytes = 0;
   std::vector<void*> host_stage_retired;
   cudaEvent_t chunk_ev[kChunkEvents] = {};
+  // read-back stream of the host pass: chunk k's results cross PCIe while
+  // later chunks (and the screen) run; done_ev[k] = chunk k's kernels finished
+  cudaStream_t d2h_stream = nullptr;
+  cudaEvent_t done_ev[kChunkEvents] = {};
+  cudaEvent_t d2h_ev = nullptr;
   // side stream of the host pass (rh_screen_prepare while the trace streams in)
   cudaStream_t side_stream = nullptr;
   cudaEvent_t side_ev = nullptr;

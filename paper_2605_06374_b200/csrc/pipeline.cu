@@ -913,12 +913,26 @@ struct Carver {
 }  // namespace
 
 // Chunks of the host pass: H2D of chunk k+1 overlaps the kernels of chunk k.
-// (each extra chunk costs a handful of DMA setups; 4 measured best on B200)
+// The first and last chunks are small (RH_HOST_EDGE of the iterations each,
+// default 12 %): compute starts early, and what remains after the last byte
+// has crossed PCIe -- that chunk's kernels and read-back, the screen -- is
+// short.  RH_HOST_CHUNKS forces a count of equal chunks (A/B runs).
 static int host_chunks(int64_t n) {
   static const int force = getenv("RH_HOST_CHUNKS") ? atoi(getenv("RH_HOST_CHUNKS")) : 0;
-  // 2 measured best on B200 (fewer DMA setups; 1: no overlap, 4: 613 vs 572 us)
-  const int cap = force > 0 ? std::min(force, rh_ctx::kChunkEvents) : 2;
+  const int cap = force > 0 ? std::min(force, rh_ctx::kChunkEvents) : 3;
   return (int)std::max<int64_t>(1, std::min<int64_t>(cap, n / 1024));
+}
+// first iteration of chunk c (c = n_chunks: n)
+static int64_t chunk_start(int64_t n, int c, int n_chunks) {
+  static const int force = getenv("RH_HOST_CHUNKS") ? atoi(getenv("RH_HOST_CHUNKS")) : 0;
+  static const double edge = getenv("RH_HOST_EDGE") ? atof(getenv("RH_HOST_EDGE")) : 0.12;
+  if (c <= 0) return 0;
+  if (c >= n_chunks) return n;
+  if (force > 0 || n_chunks < 3) return n * c / n_chunks;
+  // small first and last chunks, the middle ones equal
+  const int64_t e = (int64_t)(edge * (double)n);
+  if (c == n_chunks - 1) return n - e;
+  return e + (n - 2 * e) * (c - 1) / (n_chunks - 2);
 }
 
 // The host pass's small inputs -- segment tables and the screen history --
@@ -979,6 +993,32 @@ static int fill_small_stage(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_segme
   put(L.hist, hist, 8 * std::min<int64_t>(hcount, 64));
   return RH_OK;
 }
+
+// RH_HOST_TRACE=1 (with RH_NO_GRAPH=1; debug aid, tools/e2e_timeline.py):
+// timing events at the host pass's milestones, printed to stderr after the call
+struct HostTrace {
+  bool on = false;
+  std::vector<std::pair<const char*, cudaEvent_t>> ev;
+  cudaEvent_t mark(const char* what, cudaStream_t st) {
+    if (!on) return nullptr;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    ev.emplace_back(what, e);
+    return e;
+  }
+  void dump() {
+    if (!on || ev.empty()) return;
+    for (auto& x : ev) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[0].second, x.second);
+      fprintf(stderr, "rh_host_trace %-16s %9.1f us\n", x.first, 1e3 * ms);
+      cudaEventDestroy(x.second);
+    }
+    ev.clear();
+  }
+};
+static HostTrace g_htrace;
 
 // Host-buffer Detector pass over an int32 trace (tr) or a packed one (pk):
 // enqueues copies, kernels and read-backs on `stream` (+ the copy stream).
@@ -1110,30 +1150,39 @@ int enqueue_host_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model*
       return rc;
   }
   // chunked pipeline: chunk k+1 crosses PCIe on the copy stream while chunk k
-  // is processed (and its results copied back) on the caller's stream
+  // is processed on the caller's stream and chunk k-1's results come back on
+  // the read-back stream
   const int n_chunks = host_chunks(n);
-  for (int k = 0; k < n_chunks; ++k)
+  for (int k = 0; k < n_chunks; ++k) {
     if (!ctx->chunk_ev[k])
       RH_CUDA(cudaEventCreateWithFlags(&ctx->chunk_ev[k], cudaEventDisableTiming));
+    if (!ctx->done_ev[k])
+      RH_CUDA(cudaEventCreateWithFlags(&ctx->done_ev[k], cudaEventDisableTiming));
+  }
+  if (!ctx->d2h_stream)
+    RH_CUDA(cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking));
+  if (!ctx->d2h_ev) RH_CUDA(cudaEventCreateWithFlags(&ctx->d2h_ev, cudaEventDisableTiming));
   // the copy stream must not overwrite buffers earlier work on `stream` reads
   RH_CUDA(cudaEventRecord(ctx->chunk_ev[0], stream));
   RH_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->chunk_ev[0], 0));
-  cudaStream_t cs = ctx->copy_stream;
-  // the per-iteration index arrays (segment ids, micro-batch offsets or the
-  // packed counts) are small: one copy each up front; only the bulky
-  // device times and documents are chunked (fewer, larger DMA transfers)
-  if ((rc = cp(d_seg, tr->seg, 4 * n, H2D, cs))) return rc;
-  if (pk) {
-    if ((rc = cp(d_idoc, pk->iter_doc, 4 * (n + 1), H2D, cs)) ||
-        (rc = cp(d_cnt, pk->mb_docs, n * M, H2D, cs)))
-      return rc;
-  } else if ((rc = cp(d_off, tr->mb_off, 4 * (n * M + 1), H2D, cs))) {
-    return rc;
-  }
+  cudaStream_t cs = ctx->copy_stream, ds = ctx->d2h_stream;
+  g_htrace.mark("chunks start", cs);
   for (int k = 0; k < n_chunks; ++k) {
-    const int64_t i0 = n * k / n_chunks, i1 = n * (k + 1) / n_chunks, ni = i1 - i0;
+    const int64_t i0 = chunk_start(n, k, n_chunks), i1 = chunk_start(n, k + 1, n_chunks);
+    const int64_t ni = i1 - i0;
     const int64_t o0 = pk ? pk->iter_doc[i0] : tr->mb_off[i0 * M];
     const int64_t o1 = pk ? pk->iter_doc[i1] : tr->mb_off[i1 * M];
+    // this chunk's index arrays (segment ids, offsets or packed counts), then
+    // its bulky device times and documents
+    if ((rc = cp(d_seg ? d_seg + i0 : nullptr, tr->seg ? tr->seg + i0 : nullptr, 4 * ni, H2D, cs)))
+      return rc;
+    if (pk) {
+      if ((rc = cp(d_idoc + i0, pk->iter_doc + i0, 4 * (ni + 1), H2D, cs)) ||
+          (rc = cp(d_cnt + i0 * M, pk->mb_docs + i0 * M, ni * M, H2D, cs)))
+        return rc;
+    } else if ((rc = cp(d_off + i0 * M, tr->mb_off + i0 * M, 4 * (ni * M + 1), H2D, cs))) {
+      return rc;
+    }
     if ((rc = cp(d_dt + i0 * G * T, tr->device_time + i0 * G * T, 4 * ni * G * T, H2D, cs)))
       return rc;
     if (pk) {
@@ -1142,6 +1191,7 @@ int enqueue_host_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model*
       return rc;
     }
     RH_CUDA(cudaEventRecord(ctx->chunk_ev[k], cs));
+    g_htrace.mark("h2d chunk", cs);
     RH_CUDA(cudaStreamWaitEvent(stream, ctx->chunk_ev[k], 0));
     if (pk) {  // rebuild this chunk's int32 CSR
       expand_kernel<<<(unsigned)ni, kExpandThreads, 0, stream>>>(i0, n, M, d_idoc, d_cnt,
@@ -1163,12 +1213,16 @@ int enqueue_host_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model*
     if (co.severity) co.severity += i0 * G;
     rc = launch_pass(ctx, sh, m, &dsg, &ct, thr, 1, &co, stream);
     if (rc) return rc;
-    if ((rc = cp(out->makespan + i0, co.makespan, 8 * ni, D2H, stream)) ||
-        (rc = cp(out->status + i0, co.status, ni, D2H, stream)) ||
-        (out->stage_cost && (rc = cp(out->stage_cost + i0 * G, co.stage_cost, 8 * ni * G, D2H, stream))) ||
-        (out->stage_flag && (rc = cp(out->stage_flag + i0 * G, co.stage_flag, ni * G, D2H, stream))) ||
-        (out->severity && (rc = cp(out->severity + i0 * G, co.severity, 4 * ni * G, D2H, stream))))
+    RH_CUDA(cudaEventRecord(ctx->done_ev[k], stream));
+    g_htrace.mark("detect chunk", stream);
+    RH_CUDA(cudaStreamWaitEvent(ds, ctx->done_ev[k], 0));
+    if ((rc = cp(out->makespan + i0, co.makespan, 8 * ni, D2H, ds)) ||
+        (rc = cp(out->status + i0, co.status, ni, D2H, ds)) ||
+        (out->stage_cost && (rc = cp(out->stage_cost + i0 * G, co.stage_cost, 8 * ni * G, D2H, ds))) ||
+        (out->stage_flag && (rc = cp(out->stage_flag + i0 * G, co.stage_flag, ni * G, D2H, ds))) ||
+        (out->severity && (rc = cp(out->severity + i0 * G, co.severity, 4 * ni * G, D2H, ds))))
       return rc;
+    g_htrace.mark("d2h chunk", ds);
   }
   if (screen) {
     rc = rh_screen(ctx, screen, series_len, d_hist, n, d_obs, dout.status,
@@ -1178,7 +1232,11 @@ int enqueue_host_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model*
       RH_CUDA(cudaMemcpyAsync(outcome, d_outcome, n, D2H, stream));
     if (series_len_out)
       RH_CUDA(cudaMemcpyAsync(series_len_out, d_len, sizeof(int64_t), D2H, stream));
+    g_htrace.mark("screen+out", stream);
   }
+  // the caller's stream covers the read-backs
+  RH_CUDA(cudaEventRecord(ctx->d2h_ev, ds));
+  RH_CUDA(cudaStreamWaitEvent(stream, ctx->d2h_ev, 0));
   return RH_OK;
 }
 
@@ -1220,7 +1278,7 @@ static std::vector<uint64_t> host_pass_key(const rh_pipe_shape* sh, const rh_cos
   k.push_back(sg->link_off ? (uint64_t)sg->link_off[sg->n_seg] : 0);
   const int n_chunks = host_chunks(n);
   for (int c = 0; c <= n_chunks; ++c) {
-    const int64_t i = n * c / n_chunks;
+    const int64_t i = chunk_start(n, c, n_chunks);
     k.push_back((uint64_t)(pk ? pk->iter_doc[i] : tr->mb_off[i * M]));
   }
   return k;
@@ -1286,10 +1344,15 @@ int detect_host(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
     cudaGetLastError();  // clear a capture failure; run directly below
     g.failed = true;
   }
+  static const bool trace_on = getenv("RH_HOST_TRACE") != nullptr;
+  g_htrace.on = trace_on;
+  g_htrace.mark("call", stream);
   if (int rc = enqueue_host_pass(ctx, sh, m, sg, tr, pk, thr, screen, series_len, hist, reset,
                                  out, outcome, series_len_out, stream))
     return rc;
+  g_htrace.mark("end", stream);
   RH_CUDA(cudaStreamSynchronize(stream));
+  g_htrace.dump();
   return RH_OK;
 }
 
