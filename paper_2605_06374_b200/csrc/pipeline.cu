@@ -994,28 +994,32 @@ static int fill_small_stage(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_segme
   return RH_OK;
 }
 
-// RH_HOST_TRACE=1 (with RH_NO_GRAPH=1; debug aid, tools/e2e_timeline.py):
-// timing events at the host pass's milestones, printed to stderr after the call
+// RH_HOST_TRACE=1 (debug aid, tools/e2e_timeline.py): timing events at the
+// host pass's milestones, printed to stderr after every call.  The events are
+// pooled and reused, so a captured graph re-records the ones it baked in.
 struct HostTrace {
   bool on = false;
-  std::vector<std::pair<const char*, cudaEvent_t>> ev;
-  cudaEvent_t mark(const char* what, cudaStream_t st) {
-    if (!on) return nullptr;
-    cudaEvent_t e;
-    cudaEventCreate(&e);
-    cudaEventRecord(e, st);
-    ev.emplace_back(what, e);
-    return e;
+  std::vector<cudaEvent_t> pool;
+  std::vector<const char*> names;  // of the last enqueue (= the captured graph's)
+  void begin() { names.clear(); }
+  void mark(const char* what, cudaStream_t st) {
+    if (!on) return;
+    if (names.size() == pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      pool.push_back(e);
+    }
+    cudaEventRecord(pool[names.size()], st);
+    names.push_back(what);
   }
   void dump() {
-    if (!on || ev.empty()) return;
-    for (auto& x : ev) {
+    if (!on) return;
+    for (size_t k = 0; k < names.size(); ++k) {
       float ms = 0.f;
-      cudaEventElapsedTime(&ms, ev[0].second, x.second);
-      fprintf(stderr, "rh_host_trace %-16s %9.1f us\n", x.first, 1e3 * ms);
-      cudaEventDestroy(x.second);
+      const cudaError_t e = cudaEventElapsedTime(&ms, pool[0], pool[k]);
+      fprintf(stderr, "rh_host_trace %-16s %9.1f us %s\n", names[k], 1e3 * ms,
+              e == cudaSuccess ? "" : cudaGetErrorString(e));
     }
-    ev.clear();
   }
 };
 static HostTrace g_htrace;
@@ -1117,9 +1121,29 @@ int enqueue_host_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model*
   };
   const auto H2D = cudaMemcpyHostToDevice;
   const auto D2H = cudaMemcpyDeviceToHost;
+  if (!ctx->copy_stream)
+    RH_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+  if (!ctx->side_stream)
+    RH_CUDA(cudaStreamCreateWithFlags(&ctx->side_stream, cudaStreamNonBlocking));
+  if (!ctx->side_ev) RH_CUDA(cudaEventCreateWithFlags(&ctx->side_ev, cudaEventDisableTiming));
+  const int n_chunks = host_chunks(n);
+  for (int k = 0; k < n_chunks; ++k) {
+    if (!ctx->chunk_ev[k])
+      RH_CUDA(cudaEventCreateWithFlags(&ctx->chunk_ev[k], cudaEventDisableTiming));
+    if (!ctx->done_ev[k])
+      RH_CUDA(cudaEventCreateWithFlags(&ctx->done_ev[k], cudaEventDisableTiming));
+  }
+  if (!ctx->d2h_stream)
+    RH_CUDA(cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking));
+  if (!ctx->d2h_ev) RH_CUDA(cudaEventCreateWithFlags(&ctx->d2h_ev, cudaEventDisableTiming));
+  // every copy runs on the copy stream, which must not overwrite buffers
+  // earlier work on `stream` reads
+  RH_CUDA(cudaEventRecord(ctx->chunk_ev[0], stream));
+  RH_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->chunk_ev[0], 0));
+  cudaStream_t cs = ctx->copy_stream, ds = ctx->d2h_stream;
   // segment tables + screen history: one copy of the staging buffer that
   // detect_host filled for this call (fill_small_stage)
-  if ((rc = cp(d_small, ctx->host_stage, SL.bytes, H2D, stream))) return rc;
+  if ((rc = cp(d_small, ctx->host_stage, SL.bytes, H2D, cs))) return rc;
   dsg.layers = d_layers;
   dsg.mb_start = d_mbs;
   dsg.speed = d_speed;
@@ -1133,17 +1157,12 @@ int enqueue_host_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model*
     set_error("detector_pass_host: window > 64");
     return RH_E_INVALID;
   }
-  if (screen && reset && (rc = cp(d_reset, reset, n, H2D, stream))) return rc;
   // the screen's inputs are tiny: copy them first and start its input-only
   // half (rh_screen_prepare) on the side stream while the trace streams in
-  if ((rc = cp(d_obs, tr->observed, 8 * n, H2D, stream))) return rc;
-  if (!ctx->copy_stream)
-    RH_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
-  if (!ctx->side_stream)
-    RH_CUDA(cudaStreamCreateWithFlags(&ctx->side_stream, cudaStreamNonBlocking));
-  if (!ctx->side_ev) RH_CUDA(cudaEventCreateWithFlags(&ctx->side_ev, cudaEventDisableTiming));
+  if (screen && reset && (rc = cp(d_reset, reset, n, H2D, cs))) return rc;
+  if ((rc = cp(d_obs, tr->observed, 8 * n, H2D, cs))) return rc;
   if (screen) {
-    RH_CUDA(cudaEventRecord(ctx->side_ev, stream));
+    RH_CUDA(cudaEventRecord(ctx->side_ev, cs));
     RH_CUDA(cudaStreamWaitEvent(ctx->side_stream, ctx->side_ev, 0));
     if ((rc = rh_screen_prepare(ctx, screen, series_len, d_hist, n, d_obs,
                                 reset ? d_reset : nullptr, ctx->side_stream)))
@@ -1152,20 +1171,6 @@ int enqueue_host_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model*
   // chunked pipeline: chunk k+1 crosses PCIe on the copy stream while chunk k
   // is processed on the caller's stream and chunk k-1's results come back on
   // the read-back stream
-  const int n_chunks = host_chunks(n);
-  for (int k = 0; k < n_chunks; ++k) {
-    if (!ctx->chunk_ev[k])
-      RH_CUDA(cudaEventCreateWithFlags(&ctx->chunk_ev[k], cudaEventDisableTiming));
-    if (!ctx->done_ev[k])
-      RH_CUDA(cudaEventCreateWithFlags(&ctx->done_ev[k], cudaEventDisableTiming));
-  }
-  if (!ctx->d2h_stream)
-    RH_CUDA(cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking));
-  if (!ctx->d2h_ev) RH_CUDA(cudaEventCreateWithFlags(&ctx->d2h_ev, cudaEventDisableTiming));
-  // the copy stream must not overwrite buffers earlier work on `stream` reads
-  RH_CUDA(cudaEventRecord(ctx->chunk_ev[0], stream));
-  RH_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->chunk_ev[0], 0));
-  cudaStream_t cs = ctx->copy_stream, ds = ctx->d2h_stream;
   g_htrace.mark("chunks start", cs);
   for (int k = 0; k < n_chunks; ++k) {
     const int64_t i0 = chunk_start(n, k, n_chunks), i1 = chunk_start(n, k + 1, n_chunks);
@@ -1314,10 +1319,13 @@ int detect_host(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
     std::lock_guard<std::mutex> lock(ctx->ws_mu);
     key.push_back(ctx->ws_epoch);
   }
+  static const bool trace_on = getenv("RH_HOST_TRACE") != nullptr;
+  g_htrace.on = trace_on;
   const bool same = key == g.key;
   if (same && g.exec) {
     RH_CUDA(cudaGraphLaunch(g.exec, stream));
     RH_CUDA(cudaStreamSynchronize(stream));
+    g_htrace.dump();
     return RH_OK;
   }
   if (!same) {
@@ -1328,8 +1336,11 @@ int detect_host(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
   } else if (!g.failed && !getenv("RH_NO_GRAPH")) {
     cudaGraph_t graph = nullptr;
     if (cudaStreamBeginCapture(stream, cudaStreamCaptureModeRelaxed) == cudaSuccess) {
+      g_htrace.begin();
+      g_htrace.mark("call", stream);
       const int rc = enqueue_host_pass(ctx, sh, m, sg, tr, pk, thr, screen, series_len, hist,
                                        reset, out, outcome, series_len_out, stream);
+      g_htrace.mark("end", stream);
       const cudaError_t e = cudaStreamEndCapture(stream, &graph);
       if (rc == RH_OK && e == cudaSuccess && graph &&
           cudaGraphInstantiate(&g.exec, graph, 0) == cudaSuccess) {
@@ -1344,8 +1355,7 @@ int detect_host(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
     cudaGetLastError();  // clear a capture failure; run directly below
     g.failed = true;
   }
-  static const bool trace_on = getenv("RH_HOST_TRACE") != nullptr;
-  g_htrace.on = trace_on;
+  g_htrace.begin();
   g_htrace.mark("call", stream);
   if (int rc = enqueue_host_pass(ctx, sh, m, sg, tr, pk, thr, screen, series_len, hist, reset,
                                  out, outcome, series_len_out, stream))

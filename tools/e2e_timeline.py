@@ -1,6 +1,6 @@
 """Device timeline of one e2e host pass (C2): RH_HOST_TRACE milestones
 (copy / detect / read-back per chunk, screen) relative to the call's first
-event.  Debug aid: runs the pass without the CUDA graph."""
+event, from the replayed CUDA graph (RH_NO_GRAPH=1: direct enqueue).  Debug aid."""
 import os
 import subprocess
 import sys
@@ -16,11 +16,12 @@ tr = bench.build_trace(0, bench.N_ITER, use_oracle=False)
 p = DetectorPass(tr, dev); p.run(); torch.cuda.synchronize()
 class A: warmup = 3; steps = 3
 r = bench.run_e2e(tr, p, A, dev)
-print('%%.1f us per call (untimed-graph mode)' %% (r['step_s'] * 1e6))
+print('%%.1f us per call (with trace events)' %% (r['step_s'] * 1e6))
 """ % ROOT
-env = dict(os.environ, RH_HOST_TRACE="1", RH_NO_GRAPH="1")
+env = dict(os.environ, RH_HOST_TRACE="1")
 out = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True)
 lines = [l for l in out.stderr.splitlines() if l.startswith("rh_host_trace")]
 last = max((k for k, l in enumerate(lines) if " call " in l), default=None)
 print("\n".join(lines[last:] if last is not None else out.stderr.splitlines()[-20:]))
 print(out.stdout.strip())
+print("\n".join(l for l in out.stderr.splitlines()[-8:] if not l.startswith("rh_host_trace")))
