@@ -582,6 +582,8 @@ def run_scheduler(args, world, rank, local, names=("C3", "C4", "C5")):
                                              "collective, decode")
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
             out[name]["cpu_baseline"] = search_cpu_baseline(inputs, s.size)
+            out[name]["cpu_baseline_python_reference"] = search_python_reference_baseline(
+                st, cfg, mbs, s, k={"C5": 100}.get(name, 1000))
         del s
     return out
 
@@ -667,6 +669,95 @@ def run_replan_compare():
                      "reference": "baseline/_ref resilsim ResiHPPolicy.plan (Python, 1 core)",
                      "ours": "paper_2605_06374_b200 ResiHPPolicy.plan (drop-in, GPU + native)"}
     return out
+
+
+_PYSB = {}  # the re-plan problem the forked reference workers score
+
+
+def _py_search_worker(cands):
+    """Reference evaluate_plan + reconfig_cost (baseline/_ref) of decoded
+    candidates -> (scored, seconds).  Mirrors tests/golden/make_golden.py's
+    _ref_score: the plan's TP groups replace the state's, non-members stand
+    by, the config keeps the nominal TP degree."""
+    ref_dir, prob = _PYSB["ref"], _PYSB["problem"]
+    sys.path.insert(0, ref_dir)
+    from resilsim import cluster as rc
+    from resilsim import pipeline as rp
+    from resilsim import scheduler as rs
+    from resilsim import workload as rw
+    from resilsim.comm import CommSpec
+
+    devs, dpn, groups0, intra, inter, links, T, D, P, sched, part0, mbs, cap = prob
+    st = rc.ClusterState(devices=[rc.Device(i, nd, sp, stt) for i, nd, sp, stt in devs],
+                         devices_per_node=dpn, tp_groups=dict(groups0), intra_bw=intra,
+                         inter_bw=inter, link_factors=dict(links))
+    mbs_r = [rw.MicroBatch(id=j, doc_lengths=d, token_budget=n) for j, d, n in mbs]
+    model, comm = rw.CostModel(alpha=2e-6, beta=5e-10), CommSpec()
+    t0 = time.perf_counter()
+    done = 0
+    for tp, dp, pp, part, counts, groups in cands:
+        st2 = st.copy()
+        st2.tp_groups = {(g // pp, g % pp): tuple(m) for g, m in enumerate(groups)}
+        members = {m for g in groups for m in g}
+        for dev in st2.devices:
+            if dev.status != rc.FAIL_STOP:
+                dev.status = ((rc.FAIL_SLOW if dev.speed < 1.0 else rc.HEALTHY)
+                              if dev.id in members else rc.STANDBY)
+        cfg2 = rc.ParallelismConfig(tp=T, dp=dp, pp=pp, schedule=sched, layer_partition=list(part))
+        try:
+            rs.evaluate_plan(rs.AdaptationPlan(dp_assignment=list(counts)), st2, cfg2, mbs_r,
+                             model, comm=comm, capacity=cap)
+        except rp.SimulationError:
+            pass
+        if tp == T and dp == D and pp == P:
+            rs.reconfig_cost(rs.AdaptationPlan(layer_partition=list(part)), st, rc.ParallelismConfig(
+                tp=T, dp=D, pp=P, schedule=sched, layer_partition=list(part0)),
+                layer_bytes=256.0 * 2**20)
+        done += 1
+    return done, time.perf_counter() - t0
+
+
+def search_python_reference_baseline(st, cfg, mbs, search, k, budget_s=12.0):
+    """The reference's own candidate scoring (SURVEY §8(d) CPU baseline (2)):
+    resilsim evaluate_plan + reconfig_cost (baseline/_ref) on k uniformly
+    sampled feasible candidates of the benchmarked space, decoded by the
+    search, one process per host core (fork; the cli.py:86-92 pattern)."""
+    import multiprocessing as mp
+
+    ref_dir = ROOT / "baseline" / "_ref"
+    if not (ref_dir / "resilsim").exists():
+        return {"unavailable": "baseline/_ref (pip install of /root/reference/pkg) is missing"}
+    rng = np.random.default_rng(7)
+    cands = []
+    tries = 0
+    while len(cands) < k and tries < 50 * k:
+        tries += 1
+        c = search.decode(int(rng.integers(0, search.size)))
+        if c.feasible:
+            cands.append((c.tp, c.dp, c.pp, list(c.partition), list(c.counts),
+                          [tuple(g) for g in c.groups]))
+    _PYSB["ref"] = str(ref_dir)
+    _PYSB["problem"] = (
+        [(d.id, d.node_id, d.speed, d.status) for d in st.devices], st.devices_per_node,
+        dict(st.tp_groups), st.intra_bw, st.inter_bw, dict(st.link_factors), cfg.tp, cfg.dp,
+        cfg.pp, cfg.schedule, list(cfg.layer_partition),
+        [(mb.id, tuple(mb.doc_lengths), mb.token_budget) for mb in mbs], cfg.pp + 2)
+    cores = os.cpu_count() or 1
+    # size the sample: one candidate on this core first
+    n1, t1 = _py_search_worker(cands[:1])
+    k = max(cores, min(len(cands), int(budget_s * cores / max(t1, 1e-4))))
+    cands = cands[:k]
+    parts = [cands[i::cores] for i in range(cores)]
+    wall0 = time.perf_counter()
+    with mp.get_context("fork").Pool(cores) as pool:
+        res = pool.map(_py_search_worker, parts)
+    wall = time.perf_counter() - wall0
+    n = sum(r[0] for r in res)
+    return {"value": n / wall, "unit": "candidates/s", "cores": cores, "kind": "reference",
+            "sample": f"{n} uniformly sampled feasible candidates, resilsim evaluate_plan + "
+                      "reconfig_cost (baseline/_ref) per candidate, one process per core; "
+                      "includes worker start-up",
+            "per_candidate_ms_one_core": t1 * 1e3}
 
 
 def search_cpu_baseline(inputs, size, budget_s=4.0):
