@@ -160,6 +160,10 @@ int64_t rh_ctx_launches(const rh_ctx* ctx);
  * a safe range): counts the bit mismatches against __ddiv_rn over n seeded
  * random (a, b) pairs.  Synchronous; 0 is the only acceptable result. */
 int rh_selftest_division(rh_ctx* ctx, int64_t n, uint64_t seed, int64_t* mismatches);
+/* Measured FP64 pipe peak of the context's device (fp64 instructions per
+ * second, thread-level: independent DFMA chains on every SM).  The roofline
+ * denominator bench.py reports the re-plan search against. */
+int rh_fp64_peak(rh_ctx* ctx, double* instr_per_s);
 
 /* ------------------------------------------------------- cost model rows */
 /* quad_load (workload.py:83-85) for n micro-batches given a CSR of docs. */

@@ -197,6 +197,52 @@ int rh_selftest_division(rh_ctx* ctx, int64_t n, uint64_t seed, int64_t* mismatc
   return RH_OK;
 }
 
+// FP64 pipe peak: 8 independent DFMA chains per thread, 4 x 256-thread CTAs
+// per SM -- enough independent work to saturate the pipe.  The roofline
+// denominator of the search kernels (bench.py); one fp64 instruction (add,
+// mul, compare, fma) per slot.
+__global__ void __launch_bounds__(256) fp64_peak_kernel(int iters, double seed, double* sink) {
+  double a[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = seed + threadIdx.x * 1e-9 + k;
+  const double m = 0.999999, c = 1e-7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = __fma_rn(a[k], m, c);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += a[k];
+  if (s == 12345.678) *sink = s;  // keeps the chains live
+}
+
+int rh_fp64_peak(rh_ctx* ctx, double* instr_per_s) {
+  if (!ctx || !instr_per_s) {
+    set_error("rh_fp64_peak: invalid arguments");
+    return RH_E_INVALID;
+  }
+  DeviceGuard guard(ctx);
+  double* sink = nullptr;
+  RH_CUDA(cudaMalloc(&sink, sizeof(double)));
+  cudaEvent_t e0, e1;
+  RH_CUDA(cudaEventCreate(&e0));
+  RH_CUDA(cudaEventCreate(&e1));
+  const int blocks = ctx->num_sms * 4, iters = 1 << 14;
+  fp64_peak_kernel<<<blocks, 256>>>(iters / 8, 1.0, sink);  // warm-up
+  RH_CUDA(cudaEventRecord(e0));
+  fp64_peak_kernel<<<blocks, 256>>>(iters, 1.0, sink);
+  RH_CUDA(cudaEventRecord(e1));
+  cudaError_t e = cudaEventSynchronize(e1);
+  float ms = 0.f;
+  if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(sink);
+  if (e != cudaSuccess) return cuda_fail(e, "rh_fp64_peak");
+  *instr_per_s = (double)blocks * 256.0 * 8.0 * iters / (ms * 1e-3);
+  return RH_OK;
+}
+
 int rh_abi_version(void) { return RH_ABI_VERSION; }
 
 const char* rh_last_error(void) { return g_err; }
