@@ -616,6 +616,21 @@ def _replan_ctx(ns, case, docs):
         comm=ns.comm.CommSpec(), known_speeds={dev: sev}, confirmed=conf, capacity=P + 2)
 
 
+def run_percall(reps=30):
+    """Per-call latency of the drop-in API against the reference's Python on
+    the same C1-shaped inputs (tools/percall.py in a child process: quad_load,
+    predict_chunk_time, build_dag + critical_path, simulate_iteration,
+    DetectorState.observe, evaluate_plan)."""
+    import subprocess
+
+    r = subprocess.run([sys.executable, str(ROOT / "tools" / "percall.py"), str(reps)],
+                       capture_output=True, text=True, timeout=600)
+    try:
+        return json.loads(r.stdout)
+    except ValueError:
+        return {"unavailable": (r.stderr or r.stdout)[-300:]}
+
+
 def run_replan_compare():
     """ResiHPPolicy.plan -- the reference's (baseline/_ref, Python, one host
     core) against this package's drop-in (GPU subgroup / repartition /
@@ -865,6 +880,7 @@ def main():
         line["scheduler"] = run_scheduler(args, world, rank, local)
     if rank == 0 and world == 1 and not args.no_replan:
         line["replan"] = run_replan_compare()
+        line["percall"] = run_percall()
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(tr)

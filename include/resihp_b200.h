@@ -241,6 +241,28 @@ int rh_screen(rh_ctx* ctx, const rh_screen_params* params, int64_t series_len,
               const uint8_t* it_status, const uint8_t* reset, uint8_t* outcome,
               int64_t* series_len_out, void* stream);
 
+/* ------------------------------------------- per-call host entry points */
+/* Host-buffer twins of rh_quad_load, rh_chunk_time, rh_validate and rh_screen
+ * for the drop-in API's per-call functions (workload.quad_load /
+ * predict_chunk_time, detector.validate, one DetectorState.observe): every
+ * pointer is HOST memory (any, not necessarily pinned); the inputs are
+ * gathered into the context's pinned staging and cross PCIe in one copy,
+ * the outputs come back in one copy, and the call returns when they are in
+ * the caller's arrays.  Synchronous; calls on one context are serialised. */
+int rh_quad_load_host(rh_ctx* ctx, int64_t n_mb, const int32_t* mb_off,
+                      const int32_t* doc_len, int64_t* quad_out);
+int rh_chunk_time_host(rh_ctx* ctx, const rh_cost_model* model, int64_t n,
+                       const int64_t* quad, const int32_t* budget, const uint8_t* kind,
+                       const int32_t* layers, const double* speed, double* t_out,
+                       uint8_t* bad_out);
+int rh_validate_host(rh_ctx* ctx, int64_t n, const double* measured,
+                     const double* expected, double threshold, uint8_t* flag,
+                     double* severity);
+int rh_screen_host(rh_ctx* ctx, const rh_screen_params* params, int64_t series_len,
+                   const double* hist, int64_t n, const double* observed,
+                   const uint8_t* it_status, const uint8_t* reset, uint8_t* outcome,
+                   int64_t* series_len_out);
+
 /*
  * Optional early half of rh_screen: the parts that depend only on the inputs
  * (reset indices and the round-0 median/MAD verdicts, which read observed,

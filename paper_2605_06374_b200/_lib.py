@@ -97,6 +97,12 @@ _SIGS = {
     "rh_ctx_destroy": ([_p], C.c_int),
     "rh_ctx_launches": ([_p], C.c_int64),
     "rh_selftest_division": ([_p, C.c_int64, C.c_uint64, C.POINTER(C.c_int64)], C.c_int),
+    "rh_quad_load_host": ([_p, C.c_int64, _p, _p, _p], C.c_int),
+    "rh_chunk_time_host": ([_p, C.POINTER(CostModelC), C.c_int64, _p, _p, _p, _p, _p, _p, _p],
+                           C.c_int),
+    "rh_validate_host": ([_p, C.c_int64, _p, _p, C.c_double, _p, _p], C.c_int),
+    "rh_screen_host": ([_p, C.POINTER(ScreenParams), C.c_int64, _p, C.c_int64, _p, _p, _p, _p,
+                        _p], C.c_int),
     "rh_fp64_peak": ([_p, C.POINTER(C.c_double)], C.c_int),
     "rh_quad_load": ([_p, C.c_int64, _p, _p, _p, _p], C.c_int),
     "rh_chunk_time": ([_p, C.POINTER(CostModelC), C.c_int64, _p, _p, _p, _p, _p, _p, _p, _p],

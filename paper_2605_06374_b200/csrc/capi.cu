@@ -3,8 +3,11 @@
 // validate (detector.py:127-158).
 #include <stdarg.h>
 
+#include <algorithm>
+#include <cstring>
 #include <mutex>
 #include <unordered_map>
+#include <vector>
 
 #include "common.cuh"
 #include "wavefront.cuh"
@@ -287,6 +290,8 @@ int rh_ctx_destroy(rh_ctx* ctx) {
     if (e) cudaEventDestroy(e);
   if (ctx->d2h_ev) cudaEventDestroy(ctx->d2h_ev);
   if (ctx->d2h_stream) cudaStreamDestroy(ctx->d2h_stream);
+  if (ctx->call_stream) cudaStreamDestroy(ctx->call_stream);
+  if (ctx->call_stage) cudaFreeHost(ctx->call_stage);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->side_stream) cudaStreamDestroy(ctx->side_stream);
   if (ctx->side_ev) cudaEventDestroy(ctx->side_ev);
@@ -353,6 +358,182 @@ int rh_validate(rh_ctx* ctx, int64_t n, const double* measured, const double* ex
       n, measured, expected, threshold, flag, severity);
   RH_CHECK_LAUNCH(ctx);
   return RH_OK;
+}
+
+
+}  // extern "C"
+
+namespace rh {
+
+// The per-call host entry points (rh_*_host): the caller's host arrays are
+// gathered into the context's pinned staging buffer, cross PCIe in ONE copy,
+// the device entry point runs on the staged copies, and every output comes
+// back in ONE copy -- instead of a synchronous copy per array (the drop-in
+// API's scalar calls: quad_load, predict_chunk_time, validate, the screen of
+// one DetectorState.observe).
+struct HostCall {
+  struct In {
+    const void* src;
+    size_t bytes, off;
+  };
+  struct Out {
+    void* dst;
+    size_t bytes, off;
+  };
+  std::vector<In> ins;
+  std::vector<Out> outs;
+  size_t in_bytes = 0, out_bytes = 0;
+  static size_t up(size_t x) { return (x + 15) & ~size_t(15); }
+  size_t in(const void* p, size_t b) {
+    ins.push_back({p, b, in_bytes});
+    in_bytes = up(in_bytes + b);
+    return ins.back().off;
+  }
+  size_t out(void* p, size_t b) {
+    outs.push_back({p, b, out_bytes});
+    out_bytes = up(out_bytes + b);
+    return outs.back().off;
+  }
+  // stage, copy in, launch(dev_in, dev_out, stream), copy out, wait, scatter
+  template <class F>
+  int run(rh_ctx* ctx, F&& launch) {
+    std::lock_guard<std::mutex> lock(ctx->call_mu);
+    const size_t total = in_bytes + out_bytes + 16;
+    if (total > ctx->call_stage_bytes) {
+      if (ctx->call_stage) RH_CUDA(cudaFreeHost(ctx->call_stage));
+      ctx->call_stage = nullptr;
+      ctx->call_stage_bytes = 0;
+      const size_t want = total + total / 2 + 4096;
+      RH_CUDA(cudaMallocHost(&ctx->call_stage, want));
+      ctx->call_stage_bytes = want;
+    }
+    if (!ctx->call_stream)
+      RH_CUDA(cudaStreamCreateWithFlags(&ctx->call_stream, cudaStreamNonBlocking));
+    cudaStream_t st = ctx->call_stream;
+    void* dev = nullptr;
+    if (int rc = workspace(ctx, total, &dev, 5, st)) return rc;
+    char* h = static_cast<char*>(ctx->call_stage);
+    for (const In& a : ins)
+      if (a.src && a.bytes) memcpy(h + a.off, a.src, a.bytes);
+    char* d_in = static_cast<char*>(dev);
+    char* d_out = d_in + in_bytes;
+    if (in_bytes) RH_CUDA(cudaMemcpyAsync(d_in, h, in_bytes, cudaMemcpyHostToDevice, st));
+    if (int rc = launch(d_in, d_out, st)) return rc;
+    if (out_bytes)
+      RH_CUDA(cudaMemcpyAsync(h + in_bytes, d_out, out_bytes, cudaMemcpyDeviceToHost, st));
+    RH_CUDA(cudaStreamSynchronize(st));
+    for (const Out& o : outs)
+      if (o.dst && o.bytes) memcpy(o.dst, h + in_bytes + o.off, o.bytes);
+    return RH_OK;
+  }
+};
+
+}  // namespace rh
+
+extern "C" {
+
+int rh_quad_load_host(rh_ctx* ctx, int64_t n_mb, const int32_t* mb_off, const int32_t* doc_len,
+                      int64_t* quad_out) {
+  if (!ctx || n_mb < 0 || (n_mb && (!mb_off || !quad_out))) {
+    set_error("rh_quad_load_host: invalid arguments");
+    return RH_E_INVALID;
+  }
+  if (n_mb == 0) return RH_OK;
+  const int64_t n_doc = mb_off[n_mb];
+  if (n_doc < 0 || (n_doc && !doc_len)) {
+    set_error("rh_quad_load_host: invalid offsets / documents");
+    return RH_E_INVALID;
+  }
+  DeviceGuard guard(ctx);
+  HostCall c;
+  const size_t o_off = c.in(mb_off, 4 * (size_t)(n_mb + 1));
+  const size_t o_doc = c.in(doc_len, 4 * (size_t)n_doc);
+  const size_t o_q = c.out(quad_out, 8 * (size_t)n_mb);
+  return c.run(ctx, [&](char* din, char* dout, cudaStream_t st) {
+    return rh_quad_load(ctx, n_mb, reinterpret_cast<const int32_t*>(din + o_off),
+                        reinterpret_cast<const int32_t*>(din + o_doc),
+                        reinterpret_cast<int64_t*>(dout + o_q), st);
+  });
+}
+
+int rh_chunk_time_host(rh_ctx* ctx, const rh_cost_model* model, int64_t n, const int64_t* quad,
+                       const int32_t* budget, const uint8_t* kind, const int32_t* layers,
+                       const double* speed, double* t_out, uint8_t* bad_out) {
+  if (!ctx || !model || n < 0 ||
+      (n && (!quad || !budget || !kind || !layers || !speed || !t_out))) {
+    set_error("rh_chunk_time_host: invalid arguments");
+    return RH_E_INVALID;
+  }
+  if (n == 0) return RH_OK;
+  DeviceGuard guard(ctx);
+  HostCall c;
+  const size_t oq = c.in(quad, 8 * (size_t)n), ob = c.in(budget, 4 * (size_t)n),
+               ok = c.in(kind, (size_t)n), ol = c.in(layers, 4 * (size_t)n),
+               os = c.in(speed, 8 * (size_t)n);
+  const size_t ot = c.out(t_out, 8 * (size_t)n);
+  // bad flags start zero: they travel in with the inputs' zeroed tail
+  std::vector<uint8_t> zeros(bad_out ? (size_t)n : 0, 0);
+  const size_t oz = c.in(zeros.data(), zeros.size());
+  const size_t obad = c.out(bad_out, bad_out ? (size_t)n : 0);
+  return c.run(ctx, [&](char* din, char* dout, cudaStream_t st) {
+    uint8_t* bad = bad_out ? reinterpret_cast<uint8_t*>(dout + obad) : nullptr;
+    if (bad) RH_CUDA(cudaMemcpyAsync(bad, din + oz, (size_t)n, cudaMemcpyDeviceToDevice, st));
+    return rh_chunk_time(ctx, model, n, reinterpret_cast<const int64_t*>(din + oq),
+                         reinterpret_cast<const int32_t*>(din + ob),
+                         reinterpret_cast<const uint8_t*>(din + ok),
+                         reinterpret_cast<const int32_t*>(din + ol),
+                         reinterpret_cast<const double*>(din + os),
+                         reinterpret_cast<double*>(dout + ot), bad, st);
+  });
+}
+
+int rh_validate_host(rh_ctx* ctx, int64_t n, const double* measured, const double* expected,
+                     double threshold, uint8_t* flag, double* severity) {
+  if (!ctx || n < 0 || (n && (!measured || !flag || !severity))) {
+    set_error("rh_validate_host: invalid arguments");
+    return RH_E_INVALID;
+  }
+  if (n == 0) return RH_OK;
+  DeviceGuard guard(ctx);
+  HostCall c;
+  const size_t om = c.in(measured, 8 * (size_t)n);
+  const size_t oe = c.in(expected, expected ? 8 * (size_t)n : 0);
+  const size_t of = c.out(flag, (size_t)n), os = c.out(severity, 8 * (size_t)n);
+  return c.run(ctx, [&](char* din, char* dout, cudaStream_t st) {
+    return rh_validate(ctx, n, reinterpret_cast<const double*>(din + om),
+                       expected ? reinterpret_cast<const double*>(din + oe) : nullptr, threshold,
+                       reinterpret_cast<uint8_t*>(dout + of),
+                       reinterpret_cast<double*>(dout + os), st);
+  });
+}
+
+int rh_screen_host(rh_ctx* ctx, const rh_screen_params* params, int64_t series_len,
+                   const double* hist, int64_t n, const double* observed,
+                   const uint8_t* it_status, const uint8_t* reset, uint8_t* outcome,
+                   int64_t* series_len_out) {
+  if (!ctx || !params || n < 0 || series_len < 0 || (n && (!observed || !it_status || !outcome)) ||
+      (series_len > 0 && !hist)) {
+    set_error("rh_screen_host: invalid arguments");
+    return RH_E_INVALID;
+  }
+  DeviceGuard guard(ctx);
+  const int64_t h = std::min<int64_t>(series_len, params->window > 0 ? params->window : 0);
+  HostCall c;
+  // hist holds the last min(series_len, window) series values
+  const size_t oh = c.in(h ? hist : nullptr, 8 * (size_t)h);
+  const size_t oo = c.in(observed, 8 * (size_t)n), os = c.in(it_status, (size_t)n);
+  const size_t orr = c.in(reset, reset ? (size_t)n : 0);
+  const size_t ooc = c.out(outcome, (size_t)n);
+  const size_t olen = c.out(series_len_out, series_len_out ? 8 : 0);
+  return c.run(ctx, [&](char* din, char* dout, cudaStream_t st) {
+    const double* dh = reinterpret_cast<const double*>(din + oh);
+    return rh_screen(ctx, params, series_len, h ? dh : nullptr, n,
+                     reinterpret_cast<const double*>(din + oo),
+                     reinterpret_cast<const uint8_t*>(din + os),
+                     reset ? reinterpret_cast<const uint8_t*>(din + orr) : nullptr,
+                     reinterpret_cast<uint8_t*>(dout + ooc),
+                     series_len_out ? reinterpret_cast<int64_t*>(dout + olen) : nullptr, st);
+  });
 }
 
 }  // extern "C"

@@ -51,6 +51,12 @@ struct rh_ctx {
   // read-back stream of the host pass: chunk k's results cross PCIe while
   // later chunks (and the screen) run; done_ev[k] = chunk k's kernels finished
   cudaStream_t d2h_stream = nullptr;
+  // per-call host entry points (rh_*_host): pinned in / out staging and the
+  // stream they run on, one call at a time per context
+  std::mutex call_mu;
+  void* call_stage = nullptr;
+  size_t call_stage_bytes = 0;
+  cudaStream_t call_stream = nullptr;
   cudaEvent_t done_ev[kChunkEvents] = {};
   cudaEvent_t d2h_ev = nullptr;
   // side stream of the host pass (rh_screen_prepare while the trace streams in)

@@ -115,45 +115,38 @@ def _dev():
 
 def _screen(series_len: int, hist: list[float], observed, it_status, window: int, kappa: float,
             filter_enabled: bool, reset=None):
-    """rh_screen -> (outcome uint8[n], final series length)."""
-    import torch
-
-    dev = _dev()
+    """rh_screen (rh_screen_host: one copy in, one copy out) -> (outcome
+    uint8[n], final series length)."""
     n = len(observed)
     h = min(series_len, window)
-    t_hist = torch.tensor(list(hist[len(hist) - h:]) if h else [0.0], dtype=torch.float64,
-                          device=dev)
-    t_obs = torch.as_tensor(np.asarray(observed, dtype=np.float64)).to(dev)
-    t_st = torch.as_tensor(np.asarray(it_status, dtype=np.uint8)).to(dev)
-    t_rst = None if reset is None else torch.as_tensor(np.asarray(reset, np.uint8)).to(dev)
-    out = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
-    t_len = torch.empty(1, dtype=torch.int64, device=dev)
+    t_hist = np.asarray(list(hist[len(hist) - h:]) if h else [0.0], dtype=np.float64)
+    t_obs = np.ascontiguousarray(observed, dtype=np.float64)
+    t_st = np.ascontiguousarray(it_status, dtype=np.uint8)
+    t_rst = None if reset is None else np.ascontiguousarray(reset, dtype=np.uint8)
+    out = np.zeros(max(n, 1), dtype=np.uint8)
+    t_len = np.zeros(1, dtype=np.int64)
     params = _lib.ScreenParams(int(window), 1 if filter_enabled else 0, float(kappa))
     lib = _lib.load_library()
-    _lib.check(lib.rh_screen(_lib.context(), _lib.C.byref(params), int(series_len),
-                             t_hist.data_ptr(), n, t_obs.data_ptr(), t_st.data_ptr(),
-                             None if t_rst is None else t_rst.data_ptr(), out.data_ptr(),
-                             t_len.data_ptr(), _lib.stream_handle()), "rh_screen")
-    return out.cpu().numpy()[:n], int(t_len.item())
+    _lib.check(lib.rh_screen_host(_lib.context(), _lib.C.byref(params), int(series_len),
+                                  t_hist.ctypes.data, n, t_obs.ctypes.data, t_st.ctypes.data,
+                                  None if t_rst is None else t_rst.ctypes.data, out.ctypes.data,
+                                  t_len.ctypes.data), "rh_screen_host")
+    return out[:n], int(t_len[0])
 
 
 def _validate_arrays(measured, expected, threshold):
-    import torch
-
-    dev = _dev()
     n = len(measured)
     if n == 0:
         return np.zeros(0, bool), np.zeros(0)
-    m = torch.as_tensor(np.asarray(measured, dtype=np.float64)).to(dev)
-    e = None if expected is None else torch.as_tensor(np.asarray(expected, np.float64)).to(dev)
-    flag = torch.empty(n, dtype=torch.uint8, device=dev)
-    sev = torch.empty(n, dtype=torch.float64, device=dev)
+    m = np.ascontiguousarray(measured, dtype=np.float64)
+    e = None if expected is None else np.ascontiguousarray(expected, dtype=np.float64)
+    flag = np.empty(n, dtype=np.uint8)
+    sev = np.empty(n, dtype=np.float64)
     lib = _lib.load_library()
-    _lib.check(lib.rh_validate(_lib.context(), n, m.data_ptr(),
-                               None if e is None else e.data_ptr(), float(threshold),
-                               flag.data_ptr(), sev.data_ptr(), _lib.stream_handle()),
-               "rh_validate")
-    return flag.cpu().numpy().astype(bool), sev.cpu().numpy()
+    _lib.check(lib.rh_validate_host(_lib.context(), n, m.ctypes.data,
+                                    None if e is None else e.ctypes.data, float(threshold),
+                                    flag.ctypes.data, sev.ctypes.data), "rh_validate_host")
+    return flag.astype(bool), sev
 
 
 # ------------------------------------------------------------ reference API

@@ -95,23 +95,20 @@ def csr_of(micro_batches) -> tuple[np.ndarray, np.ndarray]:
 
 
 def quad_loads(micro_batches) -> np.ndarray:
-    """quad_load of every micro-batch, computed by rh_quad_load on the GPU."""
-    import torch
-
+    """quad_load of every micro-batch, computed by rh_quad_load on the GPU
+    (rh_quad_load_host: one copy in, one copy out)."""
     from . import _lib
 
     n = len(micro_batches)
     if n == 0:
         return np.zeros(0, dtype=np.int64)
     off, docs = csr_of(micro_batches)
-    dev = torch.device("cuda", torch.cuda.current_device())
-    t_off = torch.from_numpy(off).to(dev)
-    t_doc = torch.from_numpy(docs if docs.size else np.zeros(1, np.int32)).to(dev)
-    out = torch.empty(n, dtype=torch.int64, device=dev)
+    docs = docs if docs.size else np.zeros(1, np.int32)
+    out = np.empty(n, dtype=np.int64)
     lib = _lib.load_library()
-    _lib.check(lib.rh_quad_load(_lib.context(), n, t_off.data_ptr(), t_doc.data_ptr(),
-                                out.data_ptr(), _lib.stream_handle()), "rh_quad_load")
-    return out.cpu().numpy()
+    _lib.check(lib.rh_quad_load_host(_lib.context(), n, off.ctypes.data, docs.ctypes.data,
+                                     out.ctypes.data), "rh_quad_load_host")
+    return out
 
 
 def quad_load(mb: MicroBatch) -> int:
@@ -125,17 +122,14 @@ def chunk_times(model, micro_batches, kinds, layers, speeds) -> np.ndarray:
     ``micro_batches``, ``kinds``, ``layers`` and ``speeds`` are parallel
     sequences.  Raises ValueError like the reference when a speed is <= 0.
     """
-    import torch
-
     from . import _lib
 
     n = len(kinds)
     if n == 0:
         return np.zeros(0, dtype=np.float64)
-    sp = np.asarray(speeds, dtype=np.float64)
+    sp = np.ascontiguousarray(speeds, dtype=np.float64)
     if (sp <= 0).any():
         raise ValueError("cannot schedule onto a stopped device (speed <= 0)")
-    dev = torch.device("cuda", torch.cuda.current_device())
     uniq: dict[int, int] = {}
     mbs = []
     idx = np.empty(n, dtype=np.int64)
@@ -145,19 +139,18 @@ def chunk_times(model, micro_batches, kinds, layers, speeds) -> np.ndarray:
             uniq[k] = len(mbs)
             mbs.append(mb)
         idx[i] = uniq[k]
-    q = torch.from_numpy(quad_loads(mbs)[idx]).to(dev)
-    budget = torch.from_numpy(np.fromiter((mbs[j].token_budget for j in idx), np.int32, n)).to(dev)
-    kind = torch.from_numpy(np.fromiter((KIND_CODE[k] for k in kinds), np.uint8, n)).to(dev)
-    lay = torch.from_numpy(np.asarray(layers, dtype=np.int32)).to(dev)
-    spd = torch.from_numpy(sp).to(dev)
-    out = torch.empty(n, dtype=torch.float64, device=dev)
-    bad = torch.empty(n, dtype=torch.uint8, device=dev)
+    q = np.ascontiguousarray(quad_loads(mbs)[idx])
+    budget = np.fromiter((mbs[j].token_budget for j in idx), np.int32, n)
+    kind = np.fromiter((KIND_CODE[k] for k in kinds), np.uint8, n)
+    lay = np.ascontiguousarray(layers, dtype=np.int32)
+    out = np.empty(n, dtype=np.float64)
+    bad = np.zeros(n, dtype=np.uint8)
     lib = _lib.load_library()
-    _lib.check(lib.rh_chunk_time(_lib.context(), _lib.C.byref(cost_model_c(model)), n,
-                                 q.data_ptr(), budget.data_ptr(), kind.data_ptr(),
-                                 lay.data_ptr(), spd.data_ptr(), out.data_ptr(),
-                                 bad.data_ptr(), _lib.stream_handle()), "rh_chunk_time")
-    return out.cpu().numpy()
+    _lib.check(lib.rh_chunk_time_host(_lib.context(), _lib.C.byref(cost_model_c(model)), n,
+                                      q.ctypes.data, budget.ctypes.data, kind.ctypes.data,
+                                      lay.ctypes.data, sp.ctypes.data, out.ctypes.data,
+                                      bad.ctypes.data), "rh_chunk_time_host")
+    return out
 
 
 def predict_chunk_time(mb: MicroBatch, kind: str, model: CostModel, layers_on_stage: int,

@@ -26,8 +26,11 @@ for _ in range(5):
 torch.cuda.synchronize()
 n = 200
 ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(n)]
+import os
+noflush = bool(os.environ.get("AB_NOFLUSH"))
 for k in range(n):
-    fl.fill_(k & 255)
+    if not noflush:
+        fl.fill_(k & 255)
     ev[k][0].record(st); p.detect(); ev[k][1].record(st); p.screen(); ev[k][2].record(st)
 torch.cuda.synchronize()
 d = sorted(e[0].elapsed_time(e[1]) for e in ev)
