@@ -289,6 +289,11 @@ int rh_screen_prepare(rh_ctx* ctx, const rh_screen_params* params, int64_t serie
 int rh_pack_sequences(int64_t n_docs, const int32_t* lengths, int32_t budget,
                       int64_t max_bins, int32_t* mb_off, int32_t* doc_len,
                       int64_t* n_bins_out, int64_t* n_entries_out);
+/* rh_pack_sequences plus quad[b] = quad_load of kept bin b (int64, padding
+ * included; workload.py:83-85) -- what a re-plan needs of its workload. */
+int rh_pack_sequences_quad(int64_t n_docs, const int32_t* lengths, int32_t budget,
+                           int64_t max_bins, int32_t* mb_off, int32_t* doc_len, int64_t* quad,
+                           int64_t* n_bins_out, int64_t* n_entries_out);
 
 /* ------------------------------------------- end-to-end Detector pass */
 /*

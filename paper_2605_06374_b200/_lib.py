@@ -121,6 +121,8 @@ _SIGS = {
                                       C.POINTER(ScreenParams), C.c_int64, _p, _p,
                                       C.POINTER(PassOut), _p, C.POINTER(C.c_int64), _p],
                                      C.c_int),
+    "rh_pack_sequences_quad": ([C.c_int64, _p, C.c_int32, C.c_int64, _p, _p, _p,
+                                C.POINTER(C.c_int64), C.POINTER(C.c_int64)], C.c_int),
     "rh_pack_sequences": ([C.c_int64, _p, C.c_int32, C.c_int64, _p, _p, C.POINTER(C.c_int64),
                            C.POINTER(C.c_int64)], C.c_int),
     "rh_repartition_batch": ([_p, C.c_int32, _p, _p, _p, _p, _p, _p, _p], C.c_int),

@@ -11,9 +11,9 @@
 
 #include "common.cuh"
 
-extern "C" int rh_pack_sequences(int64_t n_docs, const int32_t* lengths, int32_t budget,
-                                 int64_t max_bins, int32_t* mb_off, int32_t* doc_len,
-                                 int64_t* n_bins_out, int64_t* n_entries_out) {
+static int pack_sequences(int64_t n_docs, const int32_t* lengths, int32_t budget,
+                          int64_t max_bins, int32_t* mb_off, int32_t* doc_len,
+                          int64_t* n_bins_out, int64_t* n_entries_out, int64_t* quad_out) {
   if (n_docs < 0 || budget <= 0 || !n_bins_out || !n_entries_out ||
       (n_docs && !lengths)) {
     rh::set_error("rh_pack_sequences: invalid arguments");
@@ -45,6 +45,12 @@ extern "C" int rh_pack_sequences(int64_t n_docs, const int32_t* lengths, int32_t
   // so a descent is log2(cap) levels.  Start from ~11/9 of the volume bound
   // (FFD <= 11/9 OPT + 6/9, OPT >= ceil(total / budget)); if the documents
   // need more bins than that (OPT above the volume bound), double and redo.
+  //
+  // Equal lengths are placed in bulk: the leftmost bin with room >= l takes
+  // floor(room / l) of them (one by one, first fit would put each of them
+  // there: no earlier bin gains room), so a run of equal documents costs one
+  // descent per bin it touches rather than one per document -- the same
+  // bins, in the same insertion order.
   int64_t total = 0;
   for (int32_t l : v) total += l;
   const int64_t vol = (total + budget - 1) / budget;
@@ -59,26 +65,32 @@ extern "C" int rh_pack_sequences(int64_t n_docs, const int32_t* lengths, int32_t
     bin_count.assign(cap + 1, 0);
     opened = 0;
     bool overflow = false;
-    for (int64_t i = 0; i < n_docs; ++i) {
+    for (int64_t i = 0; i < n_docs && !overflow;) {
       const int32_t l = v[i];
-      if (tree[1] < l) {  // no slot left with room: more bins than slots
-        overflow = true;
-        break;
-      }
-      // leftmost slot with residual >= l: first-fit over opened bins, else
-      // the next fresh slot (index == opened, residual == budget >= l)
-      int64_t node = 1;
-      while (node < cap) node = 2 * node + (tree[2 * node] < l);  // branch-free descent
-      const int64_t b = node - cap;
-      if (b == opened) ++opened;
-      bin_of[i] = b;
-      bin_count[b]++;
-      tree[node] -= l;
-      // propagate the new maximum upward while it changes
-      for (node >>= 1; node; node >>= 1) {
-        const int32_t m = std::max(tree[2 * node], tree[2 * node + 1]);
-        if (tree[node] == m) break;
-        tree[node] = m;
+      int64_t run = i + 1;
+      while (run < n_docs && v[run] == l) ++run;
+      while (i < run) {
+        if (tree[1] < l) {  // no slot left with room: more bins than slots
+          overflow = true;
+          break;
+        }
+        // leftmost slot with residual >= l: first-fit over opened bins, else
+        // the next fresh slot (index == opened, residual == budget >= l)
+        int64_t node = 1;
+        while (node < cap) node = 2 * node + (tree[2 * node] < l);  // branch-free descent
+        const int64_t b = node - cap;
+        if (b == opened) ++opened;
+        const int64_t k = std::min<int64_t>(run - i, tree[node] / l);
+        for (int64_t q = 0; q < k; ++q) bin_of[i + q] = b;
+        i += k;
+        bin_count[b] += k;
+        tree[node] -= (int32_t)(k * l);
+        // propagate the new maximum upward while it changes
+        for (node >>= 1; node; node >>= 1) {
+          const int32_t m = std::max(tree[2 * node], tree[2 * node + 1]);
+          if (tree[node] == m) break;
+          tree[node] = m;
+        }
       }
     }
     if (!overflow) break;
@@ -104,5 +116,27 @@ extern "C" int rh_pack_sequences(int64_t n_docs, const int32_t* lengths, int32_t
     mb_off[b] = (int32_t)start[b];
   }
   mb_off[keep] = (int32_t)start[keep];
+  if (quad_out) {  // quad_load of every kept bin, padding included (workload.py:83-85)
+    for (int64_t b = 0; b < keep; ++b) {
+      int64_t q = 0;
+      for (int64_t e = start[b]; e < start[b + 1]; ++e) q += (int64_t)doc_len[e] * doc_len[e];
+      quad_out[b] = q;
+    }
+  }
   return RH_OK;
+}
+
+extern "C" int rh_pack_sequences(int64_t n_docs, const int32_t* lengths, int32_t budget,
+                                 int64_t max_bins, int32_t* mb_off, int32_t* doc_len,
+                                 int64_t* n_bins_out, int64_t* n_entries_out) {
+  return pack_sequences(n_docs, lengths, budget, max_bins, mb_off, doc_len, n_bins_out,
+                        n_entries_out, nullptr);
+}
+
+extern "C" int rh_pack_sequences_quad(int64_t n_docs, const int32_t* lengths, int32_t budget,
+                                      int64_t max_bins, int32_t* mb_off, int32_t* doc_len,
+                                      int64_t* quad, int64_t* n_bins_out,
+                                      int64_t* n_entries_out) {
+  return pack_sequences(n_docs, lengths, budget, max_bins, mb_off, doc_len, n_bins_out,
+                        n_entries_out, quad);
 }

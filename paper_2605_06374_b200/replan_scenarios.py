@@ -82,12 +82,22 @@ def pack_workload(docs: np.ndarray, N: int, M: int):
     """FFD-pack sequences into the first M micro-batches of N tokens ->
     (mb_off[M+1], packed lengths incl. padding, quad loads[M], bin of every
     packed entry)."""
-    off, packed = pack_ffd(docs, N, M)
-    if len(off) - 1 < M:
-        raise ValueError(f"workload fills only {len(off) - 1} of {M} micro-batches")
-    sq = packed.astype(np.int64) ** 2
-    quad = np.add.reduceat(sq, off[:-1].astype(np.int64)) if len(sq) else np.zeros(M, np.int64)
-    return off, packed, quad
+    from . import _lib
+
+    lib = _lib.load_library()
+    lengths = np.ascontiguousarray(docs, dtype=np.int32)
+    n = len(lengths)
+    nb, ne = _lib.C.c_int64(), _lib.C.c_int64()
+    off = np.empty(n + 2, dtype=np.int32)
+    packed = np.empty(2 * n + 1, dtype=np.int32)
+    quad = np.empty(max(M, 1), dtype=np.int64)
+    _lib.check(lib.rh_pack_sequences_quad(n, lengths.ctypes.data, int(N), int(M), off.ctypes.data,
+                                          packed.ctypes.data, quad.ctypes.data,
+                                          _lib.C.byref(nb), _lib.C.byref(ne)),
+               "rh_pack_sequences_quad")
+    if nb.value < M:
+        raise ValueError(f"workload fills only {nb.value} of {M} micro-batches")
+    return off[:nb.value + 1], packed[:ne.value], quad[:M]
 
 
 def replan_problem(name: str, seed: int = 0, *, min_utilization: float | None = None,
