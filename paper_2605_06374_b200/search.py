@@ -89,11 +89,17 @@ def build_desc(state: ClusterState, cfg: ParallelismConfig, micro_batches, model
     policies.py:73-81); fail-stop devices are not executable."""
     n = len(state.devices)
     speed = np.zeros(n, dtype=np.float64)
-    for dev in state.devices:
-        if dev.status == FAIL_STOP:
-            continue
-        speed[dev.id] = min(1.0, (known_speeds or {}).get(dev.id, dev.speed if known_speeds is None
-                                                          else 1.0))
+    devs = state.devices
+    stopped = {dev.id for dev in devs if dev.status == FAIL_STOP}
+    if known_speeds is None:
+        ids = np.fromiter((dev.id for dev in devs), dtype=np.int64, count=n)
+        sp = np.fromiter((dev.speed for dev in devs), dtype=np.float64, count=n)
+        speed[ids] = np.minimum(1.0, sp)
+    else:
+        for dev in devs:
+            speed[dev.id] = min(1.0, known_speeds.get(dev.id, 1.0))
+    if stopped:
+        speed[np.fromiter(stopped, dtype=np.int64, count=len(stopped))] = 0.0
     links = sorted(state.link_factors.items())
     link_nodes = np.array([[a, b] for (a, b), _ in links] or [[0, 0]], dtype=np.int32)
     link_factor = np.array([f for _, f in links] or [1.0], dtype=np.float64)
@@ -105,10 +111,11 @@ def build_desc(state: ClusterState, cfg: ParallelismConfig, micro_batches, model
     T0, D0, P0 = cfg.tp, cfg.dp, cfg.pp
     groups = []
     full = True
+    tg = state.tp_groups
     for d in range(D0):
         for s in range(P0):
-            g = tuple(sorted(state.tp_groups.get((d, s), ())))
-            if len(g) != T0 or any(state.devices[m].status == FAIL_STOP for m in g):
+            g = tuple(sorted(tg.get((d, s), ())))
+            if len(g) != T0 or (stopped and not stopped.isdisjoint(g)):
                 full = False
             groups.append(g)
     cur_groups = np.array([m for g in groups for m in g] if full else [-1], dtype=np.int32)
