@@ -480,9 +480,11 @@ typedef struct rh_candidate {
   int32_t feasible;
 } rh_candidate;
 
-/* Enumerate layouts, upload inputs and run the per-layout preparation
+/* Enumerate layouts, upload inputs and queue the per-layout preparation
  * (placement, hop/ring tables, repartition_layers, proportional_split) on
- * the GPU.  Synchronises `stream`. */
+ * the GPU.  Returns once the inputs are on the device; the preparation
+ * kernels stay queued on `stream` (rh_search_set_workload, rh_search_eval
+ * and rh_search_decode order after them, on any stream). */
 int rh_search_create(rh_ctx* ctx, const rh_search_desc* desc, rh_search** out, void* stream);
 /* Returns the search's device memory to the stream-ordered pool on the stream
  * of its latest create / eval call (so pending work on that stream finishes

@@ -24,9 +24,11 @@
 // amortised reconfiguration surcharge and keeps a lexicographic (score,
 // index) min (combine_kernel, minloc_kernel).
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <limits>
+#include <mutex>
 #include <utility>
 #include <vector>
 
@@ -45,6 +47,8 @@ struct rh_search {
   std::vector<int32_t> cur_groups, cur_partition;
   // prep results read back once (rh_search_decode is then host-only)
   std::vector<int32_t> h_gblk, h_repart, h_pstart;
+  std::mutex host_mu;       // guards the lazy fetch of the three above
+  bool host_ready = false;
   // layouts
   std::vector<int32_t> lT, lD, lP, lgoff, lpoff, ldoff, lboff, lnb;
   std::vector<long long> lbase, lnv, lnu, lpair, lrt;
@@ -753,10 +757,9 @@ __global__ void __launch_bounds__(kPipeThreads, search_reg_min_blocks(P))
       sp_d = a.v.tspeed + id.goff + id.d;
       inv_d = a.v.tinv + id.goff + id.d;
       hop_d = a.v.thop + id.goff + id.d;
-      if (id.feas_v && id.valid) {
-        const int slot = P * a.tab_stride + md;
-        over = a.cap > 0 && __ldg(a.v.tab_peak + slot) > a.cap;
-      }
+      // 1F1B activation peak (the op lists' in-flight count): stage 0 holds
+      // min(P, md) forward chunks before its first backward
+      if (id.feas_v && id.valid) over = a.cap > 0 && min(P, md) > a.cap;
       if (run)
 #pragma unroll 4
         for (int s = 0; s < P; ++s)
@@ -1074,10 +1077,13 @@ namespace rh {
 // have: the even split (M/D, M/D+1) and the proportional counts +-1 of every
 // layout (read back after prep_kernel).  Entry order: DAG level ascending,
 // stage descending; peak = most forward chunks in flight on any stage.
-static int build_op_lists(rh_ctx* ctx, rh_search* S, cudaStream_t st) {
-  const int NL = (int)S->lT.size(), M = S->d.n_micro_batches;
-  const int stride = M + 2;
-  const bool zbh = S->d.schedule == RH_SCHED_ZBH;
+// The prep kernel's per-layout results the host needs (decode, op lists):
+// group blocks, repartitions, proportional splits.  Fetched once, after the
+// create's kernels (a sync on the search's last stream).
+static int fetch_host_tables(rh_search* S, cudaStream_t st) {
+  std::lock_guard<std::mutex> lock(S->host_mu);
+  if (S->host_ready) return RH_OK;
+  const int NL = (int)S->lT.size();
   std::vector<int32_t>& pst = S->h_pstart;
   pst.resize(S->n_rep + NL);
   S->h_gblk.resize(S->n_groups);
@@ -1088,6 +1094,25 @@ static int build_op_lists(rh_ctx* ctx, rh_search* S, cudaStream_t st) {
   RH_CUDA(cudaMemcpyAsync(S->h_repart.data(), S->dv.repart, 4 * S->n_stage,
                           cudaMemcpyDeviceToHost, st));
   RH_CUDA(cudaStreamSynchronize(st));
+  S->host_ready = true;
+  return RH_OK;
+}
+
+// Op lists and capacity peaks of the op-list pipe kernel (ZBH, P > 32, or
+// the RH_SEARCH_SMEM_WALK A/B build); the 1F1B register walk needs neither.
+static int build_op_lists(rh_ctx* ctx, rh_search* S, cudaStream_t st) {
+  const int NL = (int)S->lT.size(), M = S->d.n_micro_batches;
+  const int stride = M + 2;
+  const bool zbh = S->d.schedule == RH_SCHED_ZBH;
+  bool want_ops = zbh || getenv("RH_SEARCH_SMEM_WALK") != nullptr;
+  for (int li = 0; li < NL && !want_ops; ++li) want_ops = S->lP[li] > 32;
+  if (!want_ops) {
+    S->dv.tab_off = S->dv.tab_cnt = S->dv.tab_peak = nullptr;
+    S->dv.ops = nullptr;
+    return RH_OK;
+  }
+  if (int rc = fetch_host_tables(S, st)) return rc;
+  const std::vector<int32_t>& pst = S->h_pstart;
   std::vector<char> need(33 * (size_t)stride, 0);
   for (int li = 0; li < NL; ++li) {
     const int D = S->lD[li], P = S->lP[li];
@@ -1205,6 +1230,15 @@ int rh_search_create(rh_ctx* ctx, const rh_search_desc* desc, rh_search** out, v
   }
   cudaStream_t st = as_stream(stream);
   DeviceGuard guard(ctx);
+  // RH_SEARCH_TRACE=1: host wall time of the create's phases on stderr (debug aid)
+  static const bool trace = getenv("RH_SEARCH_TRACE") != nullptr;
+  const auto tc0 = std::chrono::steady_clock::now();
+  auto tmark = [&](const char* what) {
+    if (trace)
+      fprintf(stderr, "rh_search_create %-10s %8.1f us\n", what,
+              std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tc0)
+                  .count());
+  };
   rh_search* S = new rh_search();
   S->d = *desc;
   const rh_search_desc& d = *desc;
@@ -1304,6 +1338,7 @@ int rh_search_create(rh_ctx* ctx, const rh_search_desc* desc, rh_search** out, v
       }
     }
   }
+  tmark("layouts");
   S->total = base;
   S->n_groups = goff;
   S->n_stage = poff;
@@ -1419,6 +1454,7 @@ int rh_search_create(rh_ctx* ctx, const rh_search_desc* desc, rh_search** out, v
     RH_CUDA(cudaMemcpyAsync(B, stage.data(), up_bytes, cudaMemcpyHostToDevice, st));
     RH_CUDA(cudaStreamSynchronize(st));  // the staging buffer dies here
   }
+  tmark("upload");
   auto I = [&](size_t o) { return reinterpret_cast<int32_t*>(B + o); };
   auto Dp = [&](size_t o) { return reinterpret_cast<double*>(B + o); };
   auto LL = [&](size_t o) { return reinterpret_cast<long long*>(B + o); };
@@ -1450,9 +1486,12 @@ int rh_search_create(rh_ctx* ctx, const rh_search_desc* desc, rh_search** out, v
     rh_search_destroy(S);
     return rc;
   }
+  tmark("op lists");
+  // the preparation kernels stay queued: set_workload, eval and decode order
+  // after them (done_ev / the stream)
   RH_CUDA(cudaEventCreateWithFlags(&S->done_ev, cudaEventDisableTiming));
   RH_CUDA(cudaEventRecord(S->done_ev, st));
-  RH_CUDA(cudaStreamSynchronize(st));
+  tmark("done");
   *out = S;
   return RH_OK;
 }
@@ -1693,6 +1732,10 @@ int rh_search_decode(rh_ctx* ctx, rh_search* S, int64_t index, rh_candidate* out
     return RH_E_INVALID;
   }
   DeviceGuard guard(ctx);
+  if (!S->host_ready) {
+    if (S->done_ev) RH_CUDA(cudaEventSynchronize(S->done_ev));
+    if (int rc = fetch_host_tables(S, S->last_stream)) return rc;
+  }
   const int NL = (int)S->lT.size();
   int li = (int)(std::upper_bound(S->lbase.begin(), S->lbase.end(), (long long)index) -
                  S->lbase.begin()) - 1;
