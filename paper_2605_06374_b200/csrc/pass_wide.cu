@@ -74,9 +74,11 @@ struct WideWalk {
   }
   // start = max(chain finish, dependency finish + hop); finish = start + c;
   // cost sum in chain order (pipeline.py:275-291, 446-453)
-  template <int S>
+  // NODEP: no data dependency (dep == 0.0): start = chain finish (a finish
+  // is a sum of non-negative costs from +0.0; see walks.cuh chunk())
+  template <int S, bool NODEP = false>
   __device__ __forceinline__ double step(double c, double dep) {
-    const double st = fin[S] > dep ? fin[S] : dep;
+    const double st = (NODEP || fin[S] > dep) ? fin[S] : dep;
     fin[S] = __dadd_rn(st, c);
     ssum[S] = __dadd_rn(ssum[S], c);
     return fin[S];
@@ -86,18 +88,18 @@ struct WideWalk {
   __device__ __forceinline__ void tri(int j, int m, double bj) {
     if (j <= P - 1 - S && j < m) {
       const double dep = S > 0 ? __dadd_rn(lastF[S > 0 ? S - 1 : 0], lds_at<S * TW * 8>(hf)) : 0.0;
-      lastF[S] = step<S>(cost<S>(lds_at<S * 8>(rl), bj), dep);
+      lastF[S] = step<S, S == 0>(cost<S>(lds_at<S * 8>(rl), bj), dep);
     }
   }
   // main-loop slot (stages descending): B_i(S), then F_{P-S+i}(S) if it exists
   template <int S>
   __device__ __forceinline__ void pair(int i, int m, double bi, double& nB) {
     const double depB = S < P - 1 ? __dadd_rn(nB, lds_at<S * TW * 8>(hb)) : 0.0;
-    nB = step<S>(cost<S>(lds_at<(P + S) * 8>(rl), bi), depB);
+    nB = step<S, S == P - 1>(cost<S>(lds_at<(P + S) * 8>(rl), bi), depB);
     if (i < m - P + S) {
       const double bF = lds_rt(bt + (uint32_t)((P - S + i) * TW * 8));
       const double dep = S > 0 ? __dadd_rn(lastF[S > 0 ? S - 1 : 0], lds_at<S * TW * 8>(hf)) : 0.0;
-      lastF[S] = step<S>(cost<S>(lds_at<S * 8>(rl), bF), dep);
+      lastF[S] = step<S, S == 0>(cost<S>(lds_at<S * 8>(rl), bF), dep);
     }
   }
   template <int... I>

@@ -684,9 +684,11 @@ struct SearchWalk {
     }
     return x;
   }
-  template <int S>
+  // NODEP: no data dependency (dep == 0.0): start = chain finish (a finish
+  // is a sum of non-negative costs from +0.0; see walks.cuh chunk())
+  template <int S, bool NODEP = false>
   __device__ __forceinline__ double step(double c, double dep) {
-    const double st = fin[S] > dep ? fin[S] : dep;
+    const double st = (NODEP || fin[S] > dep) ? fin[S] : dep;
     fin[S] = __dadd_rn(st, c);
     return fin[S];
   }
@@ -694,17 +696,17 @@ struct SearchWalk {
   __device__ __forceinline__ void tri(int j, int m, double bj) {
     if (j <= P - 1 - S && j < m) {
       const double dep = S > 0 ? __dadd_rn(lastF[S > 0 ? S - 1 : 0], ldg_nc(hop + (S - 1) * D)) : 0.0;
-      lastF[S] = step<S>(cost<S>(ldg_nc(rl + S), bj), dep);
+      lastF[S] = step<S, S == 0>(cost<S>(ldg_nc(rl + S), bj), dep);
     }
   }
   template <int S>
   __device__ __forceinline__ void pair(int i, int m, double bi, double& nB) {
     const double depB = S < P - 1 ? __dadd_rn(nB, ldg_nc(hop + S * D)) : 0.0;
-    nB = step<S>(cost<S>(ldg_nc(rl + 32 + S), bi), depB);
+    nB = step<S, S == P - 1>(cost<S>(ldg_nc(rl + 32 + S), bi), depB);
     if (i < m - P + S) {
       const double bF = __ldg(bs + (P - S + i));
       const double dep = S > 0 ? __dadd_rn(lastF[S > 0 ? S - 1 : 0], ldg_nc(hop + (S - 1) * D)) : 0.0;
-      lastF[S] = step<S>(cost<S>(ldg_nc(rl + S), bF), dep);
+      lastF[S] = step<S, S == 0>(cost<S>(ldg_nc(rl + S), bF), dep);
     }
   }
   template <int... I>

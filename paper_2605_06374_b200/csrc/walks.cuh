@@ -185,8 +185,14 @@ struct WalkArgs {
 // dependency finish + hop), finish = start + c (pipeline.py:275-291).
 // (rl * b) / sp exactly as __ddiv_rn; SAFE: the walk's operand ranges were
 // checked up front (div_fast), otherwise every division is __ddiv_rn.
+// nodep: the chunk has no data dependency (stage 0's F, the last stage's B,
+// every W; dep == 0.0), so start = chain finish -- a finish is a sum of
+// non-negative costs from +0.0, never -0.0 or NaN, so max(fin, 0.0) == fin;
+// stated explicitly because the compiler must otherwise keep the NaN-aware
+// max (5 instructions instead of none).
 template <bool SAFE, class WA>
-__device__ __forceinline__ double chunk(const WA& a, int s, double rl, double b, double dep) {
+__device__ __forceinline__ double chunk(const WA& a, int s, double rl, double b, double dep,
+                                        bool nodep = false) {
   const double x = __dmul_rn(rl, b);
   double c = x;
   if constexpr (WA::kSlowMask) {
@@ -197,7 +203,7 @@ __device__ __forceinline__ double chunk(const WA& a, int s, double rl, double b,
   } else {
     c = SAFE ? div_fast(x, a.sp(s), a.inv(s)) : __ddiv_rn(x, a.sp(s));
   }
-  const double st = a.fin[s] > dep ? a.fin[s] : dep;
+  const double st = (nodep || a.fin[s] > dep) ? a.fin[s] : dep;
   a.fin[s] = __dadd_rn(st, c);
   a.ssum[s] = __dadd_rn(a.ssum[s], c);
   return a.fin[s];
@@ -272,12 +278,12 @@ __device__ __forceinline__ void walk_slot(const WA& a, const double* bt_fb, cons
     if (MASK && j >= mlim) return;  // (masked 1F1B walk: m < P)
     if constexpr (kind == kOpF) {
       const double dep = S > 0 ? __dadd_rn(lastF[S > 0 ? S - 1 : 0], a.hf(S)) : 0.0;
-      lastF[S] = chunk<true>(a, S, a.rlF(S), WA::ld(bt_fb + j * WA::kStride), dep);
+      lastF[S] = chunk<true>(a, S, a.rlF(S), WA::ld(bt_fb + j * WA::kStride), dep, S == 0);
     } else if constexpr (kind == kOpB) {
       const double dep = S < P - 1 ? __dadd_rn(lastB[S < P - 1 ? S + 1 : 0], a.hb(S)) : 0.0;
-      lastB[S] = chunk<true>(a, S, a.rlB(S), WA::ld(bt_fb + j * WA::kStride), dep);
+      lastB[S] = chunk<true>(a, S, a.rlB(S), WA::ld(bt_fb + j * WA::kStride), dep, S == P - 1);
     } else if constexpr (!(COOL && j >= P - 1 - S)) {
-      chunk<true>(a, S, a.rlW(S), WA::ld(bt_w + j * WA::kStride), 0.0);
+      chunk<true>(a, S, a.rlW(S), WA::ld(bt_w + j * WA::kStride), 0.0, true);
     }
   }
 }
@@ -352,7 +358,7 @@ __device__ __forceinline__ void walk_steady(const WA& a, int m) {
     for (int s = P - 1; s >= 0; --s) {  // level 2P-1+2k
       if (s % 2 == 0) {
         const double dep = s < P - 1 ? __dadd_rn(lastB[s < P - 1 ? s + 1 : 0], a.hb(s)) : 0.0;
-        lastB[s] = chunk<true>(a, s, a.rlB(s), WA::ld(bk + (s / 2) * WA::kStride), dep);
+        lastB[s] = chunk<true>(a, s, a.rlB(s), WA::ld(bk + (s / 2) * WA::kStride), dep, s == P - 1);
       } else {
         const double dep = __dadd_rn(lastF[s > 0 ? s - 1 : 0], a.hf(s));
         lastF[s] = chunk<true>(a, s, a.rlF(s), WA::ld(bk + (P - (s + 1) / 2) * WA::kStride), dep);
@@ -362,10 +368,11 @@ __device__ __forceinline__ void walk_steady(const WA& a, int m) {
     for (int s = P - 1; s >= 0; --s) {  // level 2P+2k
       if (s % 2 == 0) {
         const double dep = s > 0 ? __dadd_rn(lastF[s > 0 ? s - 1 : 0], a.hf(s)) : 0.0;
-        lastF[s] = chunk<true>(a, s, a.rlF(s), WA::ld(bk + (P - s / 2) * WA::kStride), dep);
+        lastF[s] = chunk<true>(a, s, a.rlF(s), WA::ld(bk + (P - s / 2) * WA::kStride), dep, s == 0);
       } else {
         const double dep = s < P - 1 ? __dadd_rn(lastB[s < P - 1 ? s + 1 : 0], a.hb(s)) : 0.0;
-        lastB[s] = chunk<true>(a, s, a.rlB(s), WA::ld(bk + ((s + 1) / 2) * WA::kStride), dep);
+        lastB[s] = chunk<true>(a, s, a.rlB(s), WA::ld(bk + ((s + 1) / 2) * WA::kStride), dep,
+                               s == P - 1);
       }
     }
   }
@@ -374,7 +381,8 @@ __device__ __forceinline__ void walk_steady(const WA& a, int m) {
   if (ZBH) {
 #pragma unroll
     for (int s = P - 1; s >= 0; --s)
-      for (int j = P - 1 - s; j < m; ++j) chunk<true>(a, s, a.rlW(s), WA::ld(a.bt + j * WA::kStride), 0.0);
+      for (int j = P - 1 - s; j < m; ++j)
+        chunk<true>(a, s, a.rlW(s), WA::ld(a.bt + j * WA::kStride), 0.0, true);
   }
 }
 
