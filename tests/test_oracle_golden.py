@@ -48,6 +48,32 @@ def test_native_ffd_pack_golden():
         assert got == bins
 
 
+def test_native_ffd_bulk_runs_match_oracle(oracle):
+    """The native FFD places runs of equal lengths in bulk (one tree descent per
+    bin a run touches); the packing must equal the oracle's literal first-fit
+    scan -- many duplicates, tiny and large budgets, truncation to max_bins --
+    and the fused quad loads (rh_pack_sequences_quad) must equal sum l^2."""
+    from paper_2605_06374_b200.replan_scenarios import pack_workload
+
+    rng = np.random.default_rng(5)
+    for t in range(120):
+        n = int(rng.integers(1, 2500))
+        budget = int(rng.integers(4, 6000))
+        if t % 3 == 0:  # heavy duplication
+            docs = rng.integers(1, min(budget, 9) + 1, n)
+        else:
+            docs = np.minimum(budget, np.maximum(1, rng.lognormal(np.log(budget / 4), 0.8, n)))
+        docs = np.rint(docs).astype(np.int32)
+        off, flat = pack_ffd(docs, budget)
+        o2, f2 = oracle.pack_sequences(docs, budget)
+        assert np.array_equal(off, o2) and np.array_equal(flat, f2), t
+        nb = len(off) - 1
+        m = max(1, nb // 2)
+        poff, packed, quad = pack_workload(docs, budget, m)
+        q = [int((flat[off[b]:off[b + 1]].astype(np.int64) ** 2).sum()) for b in range(m)]
+        assert quad.tolist() == q and np.array_equal(poff, off[:m + 1]), t
+
+
 def test_native_ffd_rejects_bad_lengths():
     with pytest.raises(ValueError):
         pack_ffd(np.array([5000]), 4096)
