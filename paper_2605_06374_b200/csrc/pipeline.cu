@@ -998,10 +998,12 @@ static int fill_small_stage(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_segme
 // host pass's milestones, printed to stderr after every call.  The events are
 // pooled and reused, so a captured graph re-records the ones it baked in.
 struct HostTrace {
-  bool on = false;
+  const bool on = getenv("RH_HOST_TRACE") != nullptr;  // fixed at load: no per-call writes
   std::vector<cudaEvent_t> pool;
   std::vector<const char*> names;  // of the last enqueue (= the captured graph's)
-  void begin() { names.clear(); }
+  void begin() {
+    if (on) names.clear();
+  }
   void mark(const char* what, cudaStream_t st) {
     if (!on) return;
     if (names.size() == pool.size()) {
@@ -1319,8 +1321,6 @@ int detect_host(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
     std::lock_guard<std::mutex> lock(ctx->ws_mu);
     key.push_back(ctx->ws_epoch);
   }
-  static const bool trace_on = getenv("RH_HOST_TRACE") != nullptr;
-  g_htrace.on = trace_on;
   const bool same = key == g.key;
   if (same && g.exec) {
     RH_CUDA(cudaGraphLaunch(g.exec, stream));
