@@ -377,6 +377,8 @@ def run_e2e(tr, p, args, dev):
     off = np.zeros(len(segs) + 1, np.int32)
     np.cumsum([len(s.link_ratio) for s in segs], out=off[1:])
     h["loff"] = pin(off, np.int32)
+    h["lmax"] = pin(np.array([float(np.max(s.link_ratio)) if len(s.link_ratio) else 0.0
+                              for s in segs]), np.float64)
     n, G = tr.n_iter, tr.cfg.dp * tr.cfg.pp
     o = {"ms": torch.empty(n, dtype=torch.float64).pin_memory(),
          "st": torch.empty(n, dtype=torch.uint8).pin_memory(),
@@ -385,7 +387,8 @@ def run_e2e(tr, p, args, dev):
          "oc": torch.empty(n, dtype=torch.uint8).pin_memory()}
     seg_c = _lib.Segments(len(segs), h["layers"].data_ptr(), h["mb_start"].data_ptr(),
                           h["speed"].data_ptr(), h["hf"].data_ptr(), h["hb"].data_ptr(),
-                          h["ar"].data_ptr(), h["loff"].data_ptr(), h["lr"].data_ptr())
+                          h["ar"].data_ptr(), h["loff"].data_ptr(), h["lr"].data_ptr(),
+                          h["lmax"].data_ptr())
     tr_c = _lib.TracePacked(n, h["seg"].data_ptr(), h["iter_doc"].data_ptr(),
                             h["mb_docs"].data_ptr(), h["doc_len"].data_ptr(),
                             h["dt"].data_ptr(), h["obs"].data_ptr())

@@ -116,6 +116,11 @@ typedef struct rh_segments {
   const double* allreduce;    /* [n_seg][D]; read iff has_allreduce */
   const int32_t* link_off;    /* [n_seg+1] or NULL (no links)  */
   const double* link_ratio;   /* [link_off[n_seg]]             */
+  /* Optional [n_seg]: the largest link_ratio of each segment (0 for none).
+   * When given, the exercised-link test of an iteration is one compare
+   * (any ratio > thr  <=>  max > thr) instead of a scan; it must match
+   * link_ratio.  NULL: the kernels scan link_ratio. */
+  const double* link_max;
 } rh_segments;
 
 /*

@@ -59,7 +59,7 @@ class PipeShape(C.Structure):
 class Segments(C.Structure):
     _fields_ = [("n_seg", C.c_int32), ("layers", _p), ("mb_start", _p), ("speed", _p),
                 ("hop_fwd", _p), ("hop_bwd", _p), ("allreduce", _p), ("link_off", _p),
-                ("link_ratio", _p)]
+                ("link_ratio", _p), ("link_max", _p)]
 
 
 class Trace(C.Structure):

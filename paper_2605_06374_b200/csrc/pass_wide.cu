@@ -252,7 +252,9 @@ __global__ void __launch_bounds__(kWideThreads, wide_min_blocks(P)) pass_wide_ke
       }
     }
   }
-  if (DETECT && on && p.sg.link_off) {  // exercised-link ratios, split over the replicas
+  if (DETECT && on && p.sg.link_off && p.sg.link_max) {  // one compare (segment maximum)
+    link_bad = __ldg(p.sg.link_max + seg) > p.thr;
+  } else if (DETECT && on && p.sg.link_off) {  // exercised-link ratios, split over the replicas
     const int32_t q0 = __ldg(p.sg.link_off + seg), q1 = __ldg(p.sg.link_off + seg + 1);
     int32_t q = q0 + d;
     for (; q + 3 * D < q1; q += 4 * D) {

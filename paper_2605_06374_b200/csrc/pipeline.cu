@@ -209,7 +209,9 @@ __global__ void __launch_bounds__(MAXT) pass_kernel(const PassParams p) {
       atomic_max_nonneg(it_ms + li, msd);
     }
     if (flag) bits |= RH_IT_STAGE_FLAG;
-    if (DETECT && p.sg.link_off) {  // exercised-link ratios, split over the lanes
+    if (DETECT && p.sg.link_off && p.sg.link_max) {  // one compare (segment maximum)
+      if (within == 0 && __ldg(p.sg.link_max + seg) > p.thr) bits |= RH_IT_LINK_FLAG;
+    } else if (DETECT && p.sg.link_off) {  // exercised-link ratios, split over the lanes
       const int32_t q0 = __ldg(p.sg.link_off + seg), q1 = __ldg(p.sg.link_off + seg + 1);
       for (int32_t q = q0 + within; q < q1; q += p.lpi)
         if (__ldg(p.sg.link_ratio + q) > p.thr) bits |= RH_IT_LINK_FLAG;
@@ -381,7 +383,9 @@ __global__ void __launch_bounds__(TW, (ZBH ? 4 : kSmallMinBlocks) * (kSmallThrea
   // the segment's exercised-link test, loads issued now (4 independent
   // chains) so their latency overlaps the staging
   bool link_bad = false;
-  if (DETECT && on && p.sg.link_off) {
+  if (DETECT && on && p.sg.link_off && p.sg.link_max) {
+    link_bad = __ldg(p.sg.link_max + seg) > p.thr;  // any ratio > thr <=> max > thr
+  } else if (DETECT && on && p.sg.link_off) {
     const int32_t q0 = __ldg(p.sg.link_off + seg), q1 = __ldg(p.sg.link_off + seg + 1);
     int32_t q = q0 + d;
     for (; q + 3 * D < q1; q += 4 * D) {
@@ -941,7 +945,7 @@ static int64_t chunk_start(int64_t n, int c, int n_chunks) {
 // captured graph) copies the staging buffer to the device.  Separate
 // cudaMemcpyAsync calls cost ~5 us of DMA setup each.
 struct SmallLayout {
-  size_t layers, mbs, speed, hf, hb, ar, loff, lr, hist, bytes;
+  size_t layers, mbs, speed, hf, hb, ar, loff, lr, lmax, hist, bytes;
 };
 static SmallLayout small_layout(const rh_pipe_shape* sh, const rh_segments* sg) {
   const int64_t P = sh->pp, D = sh->dp, G = D * P, S = sg->n_seg;
@@ -956,6 +960,7 @@ static SmallLayout small_layout(const rh_pipe_shape* sh, const rh_segments* sg) 
   L.ar = (size_t)(uintptr_t)c.take<double>(S * D);
   L.loff = (size_t)(uintptr_t)c.take<int32_t>(S + 1);
   L.lr = (size_t)(uintptr_t)c.take<double>(n_links + 1);
+  L.lmax = (size_t)(uintptr_t)c.take<double>(S + 1);
   L.hist = (size_t)(uintptr_t)c.take<double>(64);
   L.bytes = (c.off + 255) & ~size_t(255);
   return L;
@@ -989,6 +994,7 @@ static int fill_small_stage(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_segme
   put(L.ar, sg->allreduce, 8 * S * D);
   put(L.loff, sg->link_off, 4 * (S + 1));
   put(L.lr, sg->link_ratio, 8 * n_links);
+  put(L.lmax, sg->link_max, 8 * S);
   const int64_t hcount = screen ? std::min<int64_t>(series_len, screen->window) : 0;
   put(L.hist, hist, 8 * std::min<int64_t>(hcount, 64));
   return RH_OK;
@@ -1102,6 +1108,7 @@ int enqueue_host_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model*
   double* d_ar = reinterpret_cast<double*>(d_small + SL.ar);
   int32_t* d_loff = reinterpret_cast<int32_t*>(d_small + SL.loff);
   double* d_lr = reinterpret_cast<double*>(d_small + SL.lr);
+  double* d_lmax = reinterpret_cast<double*>(d_small + SL.lmax);
   double* d_hist = reinterpret_cast<double*>(d_small + SL.hist);
   rh_pass_out dout = {};
   dout.makespan = c.take<double>(n);
@@ -1154,6 +1161,7 @@ int enqueue_host_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model*
   dsg.allreduce = sg->allreduce ? d_ar : nullptr;
   dsg.link_off = sg->link_off ? d_loff : nullptr;
   dsg.link_ratio = sg->link_off ? d_lr : nullptr;
+  dsg.link_max = sg->link_off && sg->link_max ? d_lmax : nullptr;
   const int64_t h = screen ? std::min<int64_t>(series_len, screen->window) : 0;
   if (screen && h > 64) {
     set_error("detector_pass_host: window > 64");

@@ -155,12 +155,17 @@ class DeviceSegments:
         np.cumsum(n_links, out=off[1:])
         self.link_off = torch.from_numpy(off).to(device)
         self.link_ratio = cat("link_ratio", np.float64)
+        # per-segment maximum ratio: the kernels' link test is one compare
+        lmax = np.array([float(np.max(s.link_ratio)) if len(s.link_ratio) else 0.0
+                         for s in segments] or [0.0], dtype=np.float64)
+        self.link_max = torch.from_numpy(lmax).to(device)
         self.n_seg = len(segments)
         self.max_mb = int(max((np.diff(s.mb_start).max() for s in segments), default=0))
         self.c = _lib.Segments(self.n_seg, self.layers.data_ptr(), self.mb_start.data_ptr(),
                                self.speed.data_ptr(), self.hop_fwd.data_ptr(),
                                self.hop_bwd.data_ptr(), self.allreduce.data_ptr(),
-                               self.link_off.data_ptr(), self.link_ratio.data_ptr())
+                               self.link_off.data_ptr(), self.link_ratio.data_ptr(),
+                               self.link_max.data_ptr())
 
 
 def pipe_shape(cfg, n_micro_batches: int, token_budget: int, *, capacity=None,
