@@ -339,10 +339,14 @@ __global__ void __launch_bounds__(TW, (ZBH ? 4 : kSmallMinBlocks) * (kSmallThrea
     pf_lo = __ldg(p.tr.mb_off + pf_it * M);
     pf_hi = __ldg(p.tr.mb_off + pf_it * M + pf_nmb);
   }
-  const StageState sg_state = stage_begin(p, smem_raw, cs, &s_bar);
+  // the replica's segment tables and device-time rows: loads issued before
+  // the staging's barrier so their latency overlaps it (consumed after)
   int m0 = 0, md = 0;
   double rlF[P], rlB[P], rlW[P], sp[P], hf[P], hb[P], fin[P], ssum[P];
+  int32_t Ls[P];
   float meas[P];
+  float4 dtv[P];
+  const bool pre4 = DETECT && on && p.vec4 && T == 4;
   if (on) {
     const int32_t* ms = p.sg.mb_start + (int64_t)seg * (D + 1);
     m0 = __ldg(ms + d);
@@ -353,20 +357,35 @@ __global__ void __launch_bounds__(TW, (ZBH ? 4 : kSmallMinBlocks) * (kSmallThrea
     const int64_t gs = ((int64_t)seg * D + d) * P + s;
     sp[s] = 1.0;
     hf[s] = hb[s] = 0.0;
-    rlF[s] = rlB[s] = rlW[s] = 0.0;
+    Ls[s] = 0;
     if (on) {
       sp[s] = __ldg(p.sg.speed + gs);
-      const double L = (double)__ldg(p.sg.layers + (int64_t)seg * P + s);
+      Ls[s] = __ldg(p.sg.layers + (int64_t)seg * P + s);
+      if (s > 0) hf[s] = __ldg(p.sg.hop_fwd + gs - 1);
+      if (s < P - 1) hb[s] = __ldg(p.sg.hop_bwd + gs);
+    }
+    if (pre4)
+      dtv[s] = __ldg(reinterpret_cast<const float4*>(p.tr.device_time +
+                                                     ((it * D + d) * P + s) * (int64_t)4));
+  }
+  const bool use_lmax = DETECT && on && p.sg.link_off && p.sg.link_max;
+  const double lmax = use_lmax ? __ldg(p.sg.link_max + seg) : 0.0;
+  const StageState sg_state = stage_begin(p, smem_raw, cs, &s_bar);
+#pragma unroll
+  for (int s = 0; s < P; ++s) {
+    rlF[s] = rlB[s] = rlW[s] = 0.0;
+    if (on) {
+      const double L = (double)Ls[s];
       rlF[s] = __dmul_rn(p.m.ratio_f, L);
       rlB[s] = __dmul_rn(ZBH ? p.m.ratio_b : __dadd_rn(p.m.ratio_b, p.m.ratio_w), L);
       rlW[s] = __dmul_rn(p.m.ratio_w, L);
-      if (s > 0) hf[s] = __ldg(p.sg.hop_fwd + gs - 1);
-      if (s < P - 1) hb[s] = __ldg(p.sg.hop_bwd + gs);
     }
     fin[s] = ssum[s] = 0.0;
     // measured stage time: max over the TP group's device times
     meas[s] = 0.0f;
-    if (DETECT && on) {
+    if (pre4) {
+      meas[s] = fmaxf(0.0f, fmaxf(fmaxf(dtv[s].x, dtv[s].y), fmaxf(dtv[s].z, dtv[s].w)));
+    } else if (DETECT && on) {
       const float* dt = p.tr.device_time + ((it * D + d) * P + s) * (int64_t)T;
       float mx = 0.0f;
       if (p.vec4) {
@@ -380,11 +399,11 @@ __global__ void __launch_bounds__(TW, (ZBH ? 4 : kSmallMinBlocks) * (kSmallThrea
       meas[s] = mx;
     }
   }
-  // the segment's exercised-link test, loads issued now (4 independent
-  // chains) so their latency overlaps the staging
+  // the segment's exercised-link test: one compare against the segment's
+  // maximum ratio, else a scan (4 independent load chains)
   bool link_bad = false;
-  if (DETECT && on && p.sg.link_off && p.sg.link_max) {
-    link_bad = __ldg(p.sg.link_max + seg) > p.thr;  // any ratio > thr <=> max > thr
+  if (use_lmax) {
+    link_bad = lmax > p.thr;  // any ratio > thr <=> max > thr
   } else if (DETECT && on && p.sg.link_off) {
     const int32_t q0 = __ldg(p.sg.link_off + seg), q1 = __ldg(p.sg.link_off + seg + 1);
     int32_t q = q0 + d;
