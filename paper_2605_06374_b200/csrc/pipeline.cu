@@ -459,7 +459,8 @@ __global__ void __launch_bounds__(TW, (ZBH ? 4 : kSmallMinBlocks) * (kSmallThrea
   const int mm = stopped ? 0 : m;
   // activation capacity: the in-flight count along a chain is fixed by the
   // schedule, so its peak per micro-batch count is precomputed
-  const bool over = p.sh.capacity > 0 && mm > 0 && __ldg(p.sched_peak + mm) > p.sh.capacity;
+  // (the peak is compared in the epilogue: its load's latency hides behind the walk)
+  const int32_t peak = p.sh.capacity > 0 && mm > 0 ? __ldg(p.sched_peak + mm) : 0;
   const double* bt = base_t + tid;
   // exact division by a hoisted reciprocal when every numerator rl * b of the
   // walk and every divisor are in range (always, in practice); otherwise the
@@ -492,14 +493,14 @@ __global__ void __launch_bounds__(TW, (ZBH ? 4 : kSmallMinBlocks) * (kSmallThrea
   WalkArgs<P, TW> wa{bt, rlF, rlB, rlW, sp, inv, hf, hb, fin, ssum, slow};
   RH_DMARK(3);
   if (mm > 0) {
-    const unsigned long long* l0 = p.sched + __ldg(p.sched_off + mm);
-    const unsigned long long* l1 = p.sched + __ldg(p.sched_off + mm + 1);
+    // the level table is read only by the table walks
+    auto lv = [&](int k) { return p.sched + __ldg(p.sched_off + mm + k); };
     if (!safe)
-      walk_table<P, ZBH, false>(wa, l0, l1);
+      walk_table<P, ZBH, false>(wa, lv(0), lv(1));
     else if (mm >= P && p.steady)
       walk_steady<P, ZBH>(wa, mm);
     else if (mm > p.static_max || !walk_static_dispatch<P, ZBH>(wa, mm))
-      walk_table<P, ZBH, true>(wa, l0, l1);
+      walk_table<P, ZBH, true>(wa, lv(0), lv(1));
   }
   RH_DMARK(4);
   __syncthreads();  // iteration slots initialised before the reductions
@@ -514,7 +515,7 @@ __global__ void __launch_bounds__(TW, (ZBH ? 4 : kSmallMinBlocks) * (kSmallThrea
     for (int s = 0; s < P; ++s) g = fmax(g, fin[s]);
     if (md < 0) bits |= RH_IT_OVERFLOW;
     if (stopped && m > 0) bits |= RH_IT_STOPPED;
-    if (over) bits |= RH_IT_CAPACITY;
+    if (p.sh.capacity > 0 && mm > 0 && peak > p.sh.capacity) bits |= RH_IT_CAPACITY;
     if (p.sh.has_allreduce && D > 1)
       g = __dadd_rn(g, __ldg(p.sg.allreduce + (int64_t)seg * D + d));
     atomic_max_nonneg(it_ms + li, g);
