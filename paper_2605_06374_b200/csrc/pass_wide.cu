@@ -159,10 +159,34 @@ __global__ void __launch_bounds__(kWideThreads, wide_min_blocks(P)) pass_wide_ke
     it_ms[tid] = 0.0;
     it_st[tid] = 0u;
   }
+  // ---- the replica's segment tables: loads issued first, so their latency
+  // overlaps the staging below (consumed after its barrier)
+  const int seg = on && p.tr.seg ? __ldg(p.tr.seg + it) : 0;
   // ---- TMA staging of the CTA's micro-batch offsets and documents
   const int n_mb = n_it * M;
   const int32_t* g_off = p.tr.mb_off + it0 * M;
   const int32_t d_lo = __ldg(g_off), n_doc = __ldg(g_off + n_mb) - d_lo;
+  int m0 = 0, md = 0;
+  if (on) {
+    const int32_t* ms = p.sg.mb_start + (int64_t)seg * (D + 1);
+    m0 = __ldg(ms + d);
+    md = __ldg(ms + d + 1) - m0;
+  }
+  const double* gsp = p.sg.speed + ((int64_t)seg * D + d) * P;
+  double hf[P], hb[P], spv[P];
+#pragma unroll
+  for (int s = 0; s < P; ++s) {
+    const int64_t gs = ((int64_t)seg * D + d) * P + s;
+    spv[s] = 1.0;
+    hf[s] = hb[s] = 0.0;
+    if (on) {
+      spv[s] = __ldg(gsp + s);
+      if (s > 0) hf[s] = __ldg(p.sg.hop_fwd + gs - 1);
+      if (s < P - 1) hb[s] = __ldg(p.sg.hop_bwd + gs);
+    }
+  }
+  // this thread's first ratio * layers entry (stage d)
+  const int32_t L_d = on && d < P ? __ldg(p.sg.layers + (int64_t)seg * P + d) : 0;
   const bool staged = n_doc <= p.doc_stage;
   const StagePlan so = stage_plan(smem_raw + p.w_union, g_off, n_mb + 1);
   const StagePlan sd = staged ? stage_plan(smem_raw + p.w_docs, p.tr.doc_len + d_lo, n_doc)
@@ -188,33 +212,17 @@ __global__ void __launch_bounds__(kWideThreads, wide_min_blocks(P)) pass_wide_ke
   stage_edges(so, g_off, n_mb + 1);
   if (staged) stage_edges(sd, p.tr.doc_len + d_lo, n_doc);
   // ---- per-replica inputs (overlap the copies)
-  const int seg = on && p.tr.seg ? __ldg(p.tr.seg + it) : 0;
-  int m0 = 0, md = 0;
-  if (on) {
-    const int32_t* ms = p.sg.mb_start + (int64_t)seg * (D + 1);
-    m0 = __ldg(ms + d);
-    md = __ldg(ms + d + 1) - m0;
-  }
   if (on)  // the iteration's ratio * layers (the same for all its replicas)
     for (int s = d; s < P; s += D) {
-      const double L = (double)__ldg(p.sg.layers + (int64_t)seg * P + s);
+      const double L = (double)(s == d ? L_d : __ldg(p.sg.layers + (int64_t)seg * P + s));
       s_rl[li * 2 * P + s] = __dmul_rn(p.m.ratio_f, L);
       s_rl[li * 2 * P + P + s] = __dmul_rn(__dadd_rn(p.m.ratio_b, p.m.ratio_w), L);
     }
-  const double* gsp = p.sg.speed + ((int64_t)seg * D + d) * P;
-  double hf[P], hb[P];
   bool stopped = false, safe = true;
   unsigned slow = 0;
 #pragma unroll
   for (int s = 0; s < P; ++s) {
-    const int64_t gs = ((int64_t)seg * D + d) * P + s;
-    double sp = 1.0;
-    hf[s] = hb[s] = 0.0;
-    if (on) {
-      sp = __ldg(gsp + s);
-      if (s > 0) hf[s] = __ldg(p.sg.hop_fwd + gs - 1);
-      if (s < P - 1) hb[s] = __ldg(p.sg.hop_bwd + gs);
-    }
+    const double sp = spv[s];
     if (sp != 1.0) {
       slow |= 1u << s;
       safe = safe && sp >= 0x1p-100 && sp <= 0x1p100;  // recip_of(sp) != 0
