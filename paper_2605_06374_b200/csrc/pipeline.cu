@@ -421,6 +421,10 @@ __global__ void __launch_bounds__(TW, (ZBH ? 4 : kSmallMinBlocks) * (kSmallThrea
     if (DETECT)
       prefetch_l2(p.tr.device_time + pf_it * D * P * T, 4 * (size_t)(pf_nmb / M) * D * P * T);
   }
+#ifdef RH_DETECT_TRACE
+  mbar_wait(&s_bar, 0);  // (trace build: time the copies' wait apart from the sums)
+  RH_DMARK(5);
+#endif
   stage_finish(p, cs, sg_state, &s_bar);
   RH_DMARK(2);
   if (md > p.mmax) md = -1;
@@ -504,7 +508,6 @@ __global__ void __launch_bounds__(TW, (ZBH ? 4 : kSmallMinBlocks) * (kSmallThrea
   }
   RH_DMARK(4);
   __syncthreads();  // iteration slots initialised before the reductions
-  RH_DMARK(5);
   // ---- replica makespan, validation, iteration reductions
   uint8_t flag[P];
   float sev[P];

@@ -38,12 +38,13 @@ t0 = t[:, 0].min()
 start = t[:, 0] - t0
 end = t[:, 6] - t0
 print(f"CTAs {n_blk}  kernel span {end.max() / 1e3:.2f} us  (first start -> last end)")
-names = ["setup", "tma+sumsq", "base", "walk", "barrier", "epilogue"]
+names = ["setup", "tma-wait", "sumsq", "base", "walk", "epilogue"]  # (mark 5: after the TMA wait)
 first = start < 1000  # started within 1 us of the first CTA
 for label, sel in (("wave 1", first), ("later", ~first)):
     if not sel.any():
         continue
-    d = np.diff(t[sel][:, :7], axis=1) / 1e3
+    tt = t[sel][:, [0, 1, 5, 2, 3, 4, 6]]
+    d = np.diff(tt, axis=1) / 1e3
     med = np.median(d, axis=0)
     print(f"{label:7s} n={sel.sum():5d} start med {np.median(start[sel]) / 1e3:6.2f} us  life med "
           f"{np.median((end - start)[sel]) / 1e3:6.2f} us  " +
