@@ -364,6 +364,13 @@ int rh_dag_critical_path(rh_ctx* ctx, int32_t n_vertices, const double* cost,
                          const int32_t* chain_off, const uint8_t* kind,
                          int32_t capacity, double* starts, double* makespan,
                          double* chain_sum, int32_t* flags, void* stream);
+/* Host-buffer twin of rh_dag_critical_path (every pointer HOST memory; flags
+ * are zeroed by the call): one staged copy in, one copy out, synchronous. */
+int rh_dag_critical_path_host(rh_ctx* ctx, int32_t n_vertices, const double* cost,
+                              const int32_t* succ_off, const int32_t* succ_dst,
+                              const double* succ_w, int32_t n_chains, const int32_t* chain_off,
+                              const uint8_t* kind, int32_t capacity, double* starts,
+                              double* makespan, double* chain_sum, int32_t* flags);
 
 /* ------------------------------------------- batched scalar Scheduler rows */
 /* One thread per problem; problems are CSR slices off[i]..off[i+1] (device).

@@ -103,6 +103,8 @@ _SIGS = {
     "rh_validate_host": ([_p, C.c_int64, _p, _p, C.c_double, _p, _p], C.c_int),
     "rh_screen_host": ([_p, C.POINTER(ScreenParams), C.c_int64, _p, C.c_int64, _p, _p, _p, _p,
                         _p], C.c_int),
+    "rh_dag_critical_path_host": ([_p, C.c_int32, _p, _p, _p, _p, C.c_int32, _p, _p, C.c_int32,
+                                   _p, _p, _p, _p], C.c_int),
     "rh_fp64_peak": ([_p, C.POINTER(C.c_double)], C.c_int),
     "rh_quad_load": ([_p, C.c_int64, _p, _p, _p, _p], C.c_int),
     "rh_chunk_time": ([_p, C.POINTER(CostModelC), C.c_int64, _p, _p, _p, _p, _p, _p, _p, _p],

@@ -536,4 +536,42 @@ int rh_screen_host(rh_ctx* ctx, const rh_screen_params* params, int64_t series_l
   });
 }
 
+int rh_dag_critical_path_host(rh_ctx* ctx, int32_t n_vertices, const double* cost,
+                              const int32_t* succ_off, const int32_t* succ_dst,
+                              const double* succ_w, int32_t n_chains, const int32_t* chain_off,
+                              const uint8_t* kind, int32_t capacity, double* starts,
+                              double* makespan, double* chain_sum, int32_t* flags) {
+  if (!ctx || n_vertices < 0 || !makespan || !flags || !succ_off || n_chains < 0 ||
+      (n_vertices && (!cost || !starts)) || (n_chains && (!chain_off || !chain_sum))) {
+    set_error("rh_dag_critical_path_host: invalid arguments");
+    return RH_E_INVALID;
+  }
+  const int64_t ne = succ_off[n_vertices];
+  if (ne < 0 || (ne && (!succ_dst || !succ_w))) {
+    set_error("rh_dag_critical_path_host: invalid successor lists");
+    return RH_E_INVALID;
+  }
+  DeviceGuard guard(ctx);
+  HostCall c;
+  const size_t oc = c.in(cost, 8 * (size_t)n_vertices);
+  const size_t oo = c.in(succ_off, 4 * ((size_t)n_vertices + 1));
+  const size_t od = c.in(succ_dst, 4 * (size_t)ne), ow = c.in(succ_w, 8 * (size_t)ne);
+  const size_t och = c.in(chain_off, n_chains ? 4 * ((size_t)n_chains + 1) : 0);
+  const size_t ok = c.in(kind, kind ? (size_t)n_vertices : 0);
+  const size_t os = c.out(starts, 8 * (size_t)n_vertices), om = c.out(makespan, 8);
+  const size_t osum = c.out(chain_sum, 8 * (size_t)n_chains), of = c.out(flags, 8);
+  return c.run(ctx, [&](char* din, char* dout, cudaStream_t st) {
+    RH_CUDA(cudaMemsetAsync(dout + of, 0, 8, st));
+    return rh_dag_critical_path(
+        ctx, n_vertices, reinterpret_cast<const double*>(din + oc),
+        reinterpret_cast<const int32_t*>(din + oo), reinterpret_cast<const int32_t*>(din + od),
+        reinterpret_cast<const double*>(din + ow), n_chains,
+        n_chains ? reinterpret_cast<const int32_t*>(din + och) : nullptr,
+        kind ? reinterpret_cast<const uint8_t*>(din + ok) : nullptr, capacity,
+        reinterpret_cast<double*>(dout + os), reinterpret_cast<double*>(dout + om),
+        n_chains ? reinterpret_cast<double*>(dout + osum) : nullptr,
+        reinterpret_cast<int32_t*>(dout + of), st);
+  });
+}
+
 }  // extern "C"

@@ -207,10 +207,7 @@ def _find_cycle(dag: ChunkDag, blocked: set[int]) -> str:
 
 def _run_dag(dag: ChunkDag, chain_keys=None, capacity=None):
     """rh_dag_critical_path on a ChunkDag -> (starts, makespan, chain sums, flags)."""
-    import torch
-
     nv = len(dag.vertices)
-    dev = torch.device("cuda", torch.cuda.current_device())
     src = np.fromiter((e.src for e in dag.edges), np.int64, len(dag.edges))
     dst = np.fromiter((e.dst for e in dag.edges), np.int64, len(dag.edges))
     w = np.fromiter((e.weight for e in dag.edges), np.float64, len(dag.edges))
@@ -229,26 +226,26 @@ def _run_dag(dag: ChunkDag, chain_keys=None, capacity=None):
             bounds.append(bounds[-1] + len(ch))
         chain_off = np.asarray(bounds, dtype=np.int32)
 
-    def t(a, dtype):
+    # host arrays through rh_dag_critical_path_host: one copy in, one copy out
+    def h(a, dtype):
         a = np.ascontiguousarray(a, dtype=dtype)
-        return torch.from_numpy(a if a.size else np.zeros(1, dtype)).to(dev)
+        return a if a.size else np.zeros(1, dtype)
 
-    d_cost, d_off = t(cost, np.float64), t(off, np.int32)
-    d_dst, d_w = t(dst[order], np.int32), t(w[order], np.float64)
-    d_kind, d_chain = t(kinds, np.uint8), t(chain_off, np.int32)
-    starts = torch.empty(max(nv, 1), dtype=torch.float64, device=dev)
-    ms = torch.empty(1, dtype=torch.float64, device=dev)
+    h_cost, h_off = h(cost, np.float64), h(off, np.int32)
+    h_dst, h_w = h(dst[order], np.int32), h(w[order], np.float64)
+    h_kind, h_chain = h(kinds, np.uint8), h(chain_off, np.int32)
     n_chains = len(chain_keys) if chain_keys else 0
-    sums = torch.empty(max(n_chains, 1), dtype=torch.float64, device=dev)
-    flags = torch.zeros(2, dtype=torch.int32, device=dev)
+    starts = np.zeros(max(nv, 1), dtype=np.float64)
+    ms = np.zeros(1, dtype=np.float64)
+    sums = np.zeros(max(n_chains, 1), dtype=np.float64)
+    flags = np.zeros(2, dtype=np.int32)
     lib = _lib.load_library()
-    _lib.check(lib.rh_dag_critical_path(
-        _lib.context(), nv, d_cost.data_ptr(), d_off.data_ptr(), d_dst.data_ptr(),
-        d_w.data_ptr(), n_chains, d_chain.data_ptr(), d_kind.data_ptr(), int(capacity or 0),
-        starts.data_ptr(), ms.data_ptr(), sums.data_ptr(), flags.data_ptr(),
-        _lib.stream_handle()), "rh_dag_critical_path")
-    return (starts.cpu().numpy()[:nv], float(ms.item()), sums.cpu().numpy()[:n_chains],
-            flags.cpu().numpy())
+    _lib.check(lib.rh_dag_critical_path_host(
+        _lib.context(), nv, h_cost.ctypes.data, h_off.ctypes.data, h_dst.ctypes.data,
+        h_w.ctypes.data, n_chains, h_chain.ctypes.data, h_kind.ctypes.data, int(capacity or 0),
+        starts.ctypes.data, ms.ctypes.data, sums.ctypes.data, flags.ctypes.data),
+        "rh_dag_critical_path_host")
+    return starts[:nv], float(ms[0]), sums[:n_chains], flags
 
 
 def critical_path(dag: ChunkDag) -> tuple[list[float], float]:
