@@ -197,6 +197,12 @@ int rh_pipeline_batch(rh_ctx* ctx, const rh_pipe_shape* shape,
                       const rh_cost_model* model, const rh_segments* segs,
                       const rh_trace* trace, const rh_pass_out* out,
                       void* stream);
+/* Host-buffer twin of rh_pipeline_batch (segments, trace and outputs in
+ * HOST memory): one staged copy in, one copy out, synchronous -- the drop-in
+ * simulate_iteration's per-call path. */
+int rh_pipeline_batch_host(rh_ctx* ctx, const rh_pipe_shape* shape, const rh_cost_model* model,
+                           const rh_segments* segs, const rh_trace* trace,
+                           const rh_pass_out* out);
 
 /*
  * Fused Detector pass: rh_pipeline_batch on the KNOWN view (the predictor,

@@ -574,4 +574,60 @@ int rh_dag_critical_path_host(rh_ctx* ctx, int32_t n_vertices, const double* cos
   });
 }
 
+int rh_pipeline_batch_host(rh_ctx* ctx, const rh_pipe_shape* shape, const rh_cost_model* model,
+                           const rh_segments* segs, const rh_trace* trace,
+                           const rh_pass_out* out) {
+  if (!ctx || !shape || !model || !segs || !trace || !out || !out->makespan || !out->status ||
+      !trace->mb_off || segs->n_seg < 1 || trace->n_iter < 0) {
+    set_error("rh_pipeline_batch_host: invalid arguments");
+    return RH_E_INVALID;
+  }
+  const int64_t n = trace->n_iter, S = segs->n_seg;
+  if (n == 0) return RH_OK;
+  const int64_t P = shape->pp, D = shape->dp, M = shape->micro_batches, G = D * P;
+  if (P < 1 || D < 1 || M < 1) {
+    set_error("rh_pipeline_batch_host: invalid shape");
+    return RH_E_INVALID;
+  }
+  const int64_t n_docs = trace->mb_off[n * M];
+  const int64_t n_links = segs->link_off ? segs->link_off[S] : 0;
+  DeviceGuard guard(ctx);
+  HostCall c;
+  const size_t o_lay = c.in(segs->layers, 4 * S * P), o_mbs = c.in(segs->mb_start, 4 * S * (D + 1)),
+               o_sp = c.in(segs->speed, 8 * S * G), o_hf = c.in(segs->hop_fwd, 8 * S * G),
+               o_hb = c.in(segs->hop_bwd, 8 * S * G),
+               o_ar = c.in(segs->allreduce, segs->allreduce ? 8 * S * D : 0),
+               o_lo = c.in(segs->link_off, segs->link_off ? 4 * (S + 1) : 0),
+               o_lr = c.in(segs->link_ratio, segs->link_off ? 8 * n_links : 0),
+               o_lm = c.in(segs->link_max, segs->link_off && segs->link_max ? 8 * S : 0);
+  const size_t o_seg = c.in(trace->seg, trace->seg ? 4 * n : 0),
+               o_off = c.in(trace->mb_off, 4 * (n * M + 1)), o_doc = c.in(trace->doc_len, 4 * n_docs);
+  const size_t o_ms = c.out(out->makespan, 8 * n), o_st = c.out(out->status, n),
+               o_sc = c.out(out->stage_cost, out->stage_cost ? 8 * n * G : 0);
+  return c.run(ctx, [&](char* din, char* dout, cudaStream_t st) {
+    rh_segments ds = *segs;
+    ds.layers = reinterpret_cast<const int32_t*>(din + o_lay);
+    ds.mb_start = reinterpret_cast<const int32_t*>(din + o_mbs);
+    ds.speed = reinterpret_cast<const double*>(din + o_sp);
+    ds.hop_fwd = reinterpret_cast<const double*>(din + o_hf);
+    ds.hop_bwd = reinterpret_cast<const double*>(din + o_hb);
+    ds.allreduce = segs->allreduce ? reinterpret_cast<const double*>(din + o_ar) : nullptr;
+    ds.link_off = segs->link_off ? reinterpret_cast<const int32_t*>(din + o_lo) : nullptr;
+    ds.link_ratio = segs->link_off ? reinterpret_cast<const double*>(din + o_lr) : nullptr;
+    ds.link_max = segs->link_off && segs->link_max ? reinterpret_cast<const double*>(din + o_lm)
+                                                   : nullptr;
+    rh_trace dt = *trace;
+    dt.seg = trace->seg ? reinterpret_cast<const int32_t*>(din + o_seg) : nullptr;
+    dt.mb_off = reinterpret_cast<const int32_t*>(din + o_off);
+    dt.doc_len = reinterpret_cast<const int32_t*>(din + o_doc);
+    dt.device_time = nullptr;
+    dt.observed = nullptr;
+    rh_pass_out dout_ = {};
+    dout_.makespan = reinterpret_cast<double*>(dout + o_ms);
+    dout_.status = reinterpret_cast<uint8_t*>(dout + o_st);
+    dout_.stage_cost = out->stage_cost ? reinterpret_cast<double*>(dout + o_sc) : nullptr;
+    return rh_pipeline_batch(ctx, shape, model, &ds, &dt, &dout_, st);
+  });
+}
+
 }  // extern "C"

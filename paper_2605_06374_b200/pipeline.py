@@ -16,7 +16,7 @@ import numpy as np
 from . import _lib
 from .cluster import (FAIL_STOP, SCHEDULE_1F1B, SCHEDULE_ZBH, IterationRecord,
                       dp_counts_or_even, split_micro_batches, validate_cluster)
-from .tables import (DeviceSegments, allreduce_map, edge_cost_fn, pipe_shape,
+from .tables import (DeviceSegments, HostSegments, allreduce_map, edge_cost_fn, pipe_shape,
                      segment_for_view, stage_speed_maps, used_link_ratios)
 from .workload import (CHUNK_ALLREDUCE, CHUNK_B, CHUNK_BW, CHUNK_F, CHUNK_W, KIND_CODE,
                        chunk_times, cost_model_c, csr_of)
@@ -341,36 +341,33 @@ def _stage_dicts(cfg, counts, sc_actual, sc_ref):
 
 
 def _simulate_canonical(state, cfg, micro_batches, model, dp_counts, comm, iteration, capacity):
-    import torch
-
     M = len(micro_batches)
     N = micro_batches[0].token_budget
     counts = dp_counts_or_even(M, cfg.dp, dp_counts)
     seg_a = segment_for_view(state, cfg, M, N, comm=comm, dp_counts=counts)
     seg_h = segment_for_view(state, cfg, M, N, comm=comm, dp_counts=counts, healthy=True,
                              clean_links=True)
-    dev = torch.device("cuda", torch.cuda.current_device())
-    segs = DeviceSegments([seg_a, seg_h], dev)
+    # the two views as a 2-iteration trace, host arrays through
+    # rh_pipeline_batch_host (one copy in, one copy out)
+    segs = HostSegments([seg_a, seg_h])
     off, docs = csr_of(micro_batches)
     n_docs = int(off[-1])
-    off2 = np.concatenate([off, off[1:] + n_docs]).astype(np.int32)
-    docs2 = np.concatenate([docs, docs]).astype(np.int32)
-    t_off = torch.from_numpy(off2).to(dev)
-    t_doc = torch.from_numpy(docs2).to(dev)
-    t_seg = torch.tensor([0, 1], dtype=torch.int32, device=dev)
-    tr = _lib.Trace(2, t_seg.data_ptr(), t_off.data_ptr(), t_doc.data_ptr(), None, None)
-    ms = torch.empty(2, dtype=torch.float64, device=dev)
-    st = torch.empty(2, dtype=torch.uint8, device=dev)
-    sc = torch.empty(2 * cfg.dp * cfg.pp, dtype=torch.float64, device=dev)
-    out = _lib.PassOut(ms.data_ptr(), st.data_ptr(), sc.data_ptr(), None, None)
+    off2 = np.ascontiguousarray(np.concatenate([off, off[1:] + n_docs]), dtype=np.int32)
+    docs2 = np.ascontiguousarray(np.concatenate([docs, docs]) if n_docs else np.zeros(1),
+                                 dtype=np.int32)
+    seg2 = np.array([0, 1], dtype=np.int32)
+    tr = _lib.Trace(2, seg2.ctypes.data, off2.ctypes.data, docs2.ctypes.data, None, None)
+    ms_h = np.zeros(2, dtype=np.float64)
+    st_h = np.zeros(2, dtype=np.uint8)
+    sc_h = np.zeros(2 * cfg.dp * cfg.pp, dtype=np.float64)
+    out = _lib.PassOut(ms_h.ctypes.data, st_h.ctypes.data, sc_h.ctypes.data, None, None)
     shape = pipe_shape(cfg, M, N, capacity=capacity, has_allreduce=comm is not None,
                        max_mb=segs.max_mb)
     lib = _lib.load_library()
-    _lib.check(lib.rh_pipeline_batch(_lib.context(), _lib.C.byref(shape),
-                                     _lib.C.byref(cost_model_c(model)), _lib.C.byref(segs.c),
-                                     _lib.C.byref(tr), _lib.C.byref(out), _lib.stream_handle()),
-               "rh_pipeline_batch")
-    ms_h, st_h, sc_h = ms.cpu().numpy(), st.cpu().numpy(), sc.cpu().numpy()
+    _lib.check(lib.rh_pipeline_batch_host(_lib.context(), _lib.C.byref(shape),
+                                          _lib.C.byref(cost_model_c(model)),
+                                          _lib.C.byref(segs.c), _lib.C.byref(tr),
+                                          _lib.C.byref(out)), "rh_pipeline_batch_host")
     if st_h[0] & _lib.RH_IT_STOPPED:
         raise SimulationError("execution completeness violated")
     if st_h[0] & _lib.RH_IT_CAPACITY:

@@ -168,6 +168,38 @@ class DeviceSegments:
                                self.link_max.data_ptr())
 
 
+class HostSegments:
+    """Segment tables stacked in host memory, C-ABI layout (the per-call
+    rh_pipeline_batch_host path; keeps the arrays alive)."""
+
+    def __init__(self, segments: list[Segment]):
+        from . import _lib
+
+        def cat(name, dtype):
+            arrs = [getattr(s, name) for s in segments]
+            a = np.concatenate(arrs).astype(dtype) if arrs else np.zeros(0, dtype)
+            return np.ascontiguousarray(a if a.size else np.zeros(1, dtype))
+
+        self.layers = cat("layers", np.int32)
+        self.mb_start = cat("mb_start", np.int32)
+        self.speed = cat("speed", np.float64)
+        self.hop_fwd = cat("hop_fwd", np.float64)
+        self.hop_bwd = cat("hop_bwd", np.float64)
+        self.allreduce = cat("allreduce", np.float64)
+        off = np.zeros(len(segments) + 1, dtype=np.int32)
+        np.cumsum([len(s.link_ratio) for s in segments], out=off[1:])
+        self.link_off = off
+        self.link_ratio = cat("link_ratio", np.float64)
+        self.link_max = np.array([float(np.max(s.link_ratio)) if len(s.link_ratio) else 0.0
+                                  for s in segments] or [0.0], dtype=np.float64)
+        self.n_seg = len(segments)
+        self.max_mb = int(max((np.diff(s.mb_start).max() for s in segments), default=0))
+        p = lambda a: a.ctypes.data
+        self.c = _lib.Segments(self.n_seg, p(self.layers), p(self.mb_start), p(self.speed),
+                               p(self.hop_fwd), p(self.hop_bwd), p(self.allreduce),
+                               p(self.link_off), p(self.link_ratio), p(self.link_max))
+
+
 def pipe_shape(cfg, n_micro_batches: int, token_budget: int, *, capacity=None,
                has_allreduce: bool = False, max_mb: int = 0):
     from . import _lib
