@@ -266,6 +266,14 @@ int rh_chunk_time_host(rh_ctx* ctx, const rh_cost_model* model, int64_t n,
                        const int64_t* quad, const int32_t* budget, const uint8_t* kind,
                        const int32_t* layers, const double* speed, double* t_out,
                        uint8_t* bad_out);
+/* predict_chunk_time from the documents in one round trip: quad loads of the
+ * n_mb micro-batches (CSR mb_off / doc_len), then t[i] for chunk i of
+ * micro-batch mb_idx[i] (host arrays; bad_out required). */
+int rh_chunk_time_docs_host(rh_ctx* ctx, const rh_cost_model* model, int64_t n_mb,
+                            const int32_t* mb_off, const int32_t* doc_len, int64_t n,
+                            const int64_t* mb_idx, const int32_t* budget, const uint8_t* kind,
+                            const int32_t* layers, const double* speed, double* t_out,
+                            uint8_t* bad_out);
 int rh_validate_host(rh_ctx* ctx, int64_t n, const double* measured,
                      const double* expected, double threshold, uint8_t* flag,
                      double* severity);

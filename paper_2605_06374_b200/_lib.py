@@ -107,6 +107,8 @@ _SIGS = {
                                    _p, _p, _p, _p], C.c_int),
     "rh_pipeline_batch_host": ([_p, C.POINTER(PipeShape), C.POINTER(CostModelC),
                                 C.POINTER(Segments), C.POINTER(Trace), C.POINTER(PassOut)], C.c_int),
+    "rh_chunk_time_docs_host": ([_p, C.POINTER(CostModelC), C.c_int64, _p, _p, C.c_int64, _p, _p,
+                                 _p, _p, _p, _p, _p], C.c_int),
     "rh_fp64_peak": ([_p, C.POINTER(C.c_double)], C.c_int),
     "rh_quad_load": ([_p, C.c_int64, _p, _p, _p, _p], C.c_int),
     "rh_chunk_time": ([_p, C.POINTER(CostModelC), C.c_int64, _p, _p, _p, _p, _p, _p, _p, _p],

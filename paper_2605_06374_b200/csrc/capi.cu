@@ -93,6 +93,7 @@ __global__ void quad_load_kernel(int64_t n, const int32_t* __restrict__ off,
 
 __global__ void chunk_time_kernel(rh_cost_model m, int64_t n,
                                   const int64_t* __restrict__ quad,
+                                  const int64_t* __restrict__ mb_idx,  // nullable: quad[mb_idx[i]]
                                   const int32_t* __restrict__ budget,
                                   const uint8_t* __restrict__ kind,
                                   const int32_t* __restrict__ layers,
@@ -110,8 +111,8 @@ __global__ void chunk_time_kernel(rh_cost_model m, int64_t n,
   double ratio = k == 0 ? m.ratio_f : k == 1 ? m.ratio_b : k == 2 ? m.ratio_w
                                                           : m.ratio_b + m.ratio_w;
   // ((ratio * L) * (alpha*N + beta*Q)) / speed, two roundings per a*b+c
-  double base = __dadd_rn(__dmul_rn(m.alpha, (double)budget[i]),
-                          __dmul_rn(m.beta, (double)quad[i]));
+  const int64_t q = mb_idx ? quad[mb_idx[i]] : quad[i];
+  double base = __dadd_rn(__dmul_rn(m.alpha, (double)budget[i]), __dmul_rn(m.beta, (double)q));
   double num = __dmul_rn(__dmul_rn(ratio, (double)layers[i]), base);
   t[i] = sp == 1.0 ? num : __ddiv_rn(num, sp);
   if (bad) bad[i] = 0;
@@ -340,7 +341,7 @@ int rh_chunk_time(rh_ctx* ctx, const rh_cost_model* model, int64_t n,
   DeviceGuard guard(ctx);
   int th = 256;
   chunk_time_kernel<<<(unsigned)((n + th - 1) / th), th, 0, as_stream(stream)>>>(
-      *model, n, quad, budget, kind, layers, speed, t_out, bad_out);
+      *model, n, quad, nullptr, budget, kind, layers, speed, t_out, bad_out);
   RH_CHECK_LAUNCH(ctx);
   return RH_OK;
 }
@@ -627,6 +628,51 @@ int rh_pipeline_batch_host(rh_ctx* ctx, const rh_pipe_shape* shape, const rh_cos
     dout_.status = reinterpret_cast<uint8_t*>(dout + o_st);
     dout_.stage_cost = out->stage_cost ? reinterpret_cast<double*>(dout + o_sc) : nullptr;
     return rh_pipeline_batch(ctx, shape, model, &ds, &dt, &dout_, st);
+  });
+}
+
+int rh_chunk_time_docs_host(rh_ctx* ctx, const rh_cost_model* model, int64_t n_mb,
+                            const int32_t* mb_off, const int32_t* doc_len, int64_t n,
+                            const int64_t* mb_idx, const int32_t* budget, const uint8_t* kind,
+                            const int32_t* layers, const double* speed, double* t_out,
+                            uint8_t* bad_out) {
+  if (!ctx || !model || n_mb < 1 || n < 0 || !mb_off ||
+      (n && (!mb_idx || !budget || !kind || !layers || !speed || !t_out || !bad_out))) {
+    set_error("rh_chunk_time_docs_host: invalid arguments");
+    return RH_E_INVALID;
+  }
+  if (n == 0) return RH_OK;
+  const int64_t n_doc = mb_off[n_mb];
+  if (n_doc < 0 || (n_doc && !doc_len)) {
+    set_error("rh_chunk_time_docs_host: invalid offsets / documents");
+    return RH_E_INVALID;
+  }
+  for (int64_t i = 0; i < n; ++i)
+    if (mb_idx[i] < 0 || mb_idx[i] >= n_mb) {
+      set_error("rh_chunk_time_docs_host: micro-batch index out of range");
+      return RH_E_INVALID;
+    }
+  DeviceGuard guard(ctx);
+  HostCall c;
+  const size_t o_off = c.in(mb_off, 4 * (size_t)(n_mb + 1)), o_doc = c.in(doc_len, 4 * (size_t)n_doc),
+               o_idx = c.in(mb_idx, 8 * (size_t)n), o_b = c.in(budget, 4 * (size_t)n),
+               o_k = c.in(kind, (size_t)n), o_l = c.in(layers, 4 * (size_t)n),
+               o_s = c.in(speed, 8 * (size_t)n);
+  const size_t o_t = c.out(t_out, 8 * (size_t)n), o_bad = c.out(bad_out, (size_t)n);
+  const size_t o_q = c.out(nullptr, 8 * (size_t)n_mb);  // device scratch: the quad loads
+  return c.run(ctx, [&](char* din, char* dout, cudaStream_t st) -> int {
+    int64_t* q = reinterpret_cast<int64_t*>(dout + o_q);
+    if (int rc = rh_quad_load(ctx, n_mb, reinterpret_cast<const int32_t*>(din + o_off),
+                              reinterpret_cast<const int32_t*>(din + o_doc), q, st))
+      return rc;
+    const int th = 256;
+    chunk_time_kernel<<<(unsigned)((n + th - 1) / th), th, 0, st>>>(
+        *model, n, q, reinterpret_cast<const int64_t*>(din + o_idx),
+        reinterpret_cast<const int32_t*>(din + o_b), reinterpret_cast<const uint8_t*>(din + o_k),
+        reinterpret_cast<const int32_t*>(din + o_l), reinterpret_cast<const double*>(din + o_s),
+        reinterpret_cast<double*>(dout + o_t), reinterpret_cast<uint8_t*>(dout + o_bad));
+    RH_CHECK_LAUNCH(ctx);
+    return RH_OK;
   });
 }
 

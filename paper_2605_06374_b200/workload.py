@@ -139,17 +139,20 @@ def chunk_times(model, micro_batches, kinds, layers, speeds) -> np.ndarray:
             uniq[k] = len(mbs)
             mbs.append(mb)
         idx[i] = uniq[k]
-    q = np.ascontiguousarray(quad_loads(mbs)[idx])
+    off, docs = csr_of(mbs)
+    docs = docs if docs.size else np.zeros(1, np.int32)
     budget = np.fromiter((mbs[j].token_budget for j in idx), np.int32, n)
     kind = np.fromiter((KIND_CODE[k] for k in kinds), np.uint8, n)
     lay = np.ascontiguousarray(layers, dtype=np.int32)
     out = np.empty(n, dtype=np.float64)
     bad = np.zeros(n, dtype=np.uint8)
     lib = _lib.load_library()
-    _lib.check(lib.rh_chunk_time_host(_lib.context(), _lib.C.byref(cost_model_c(model)), n,
-                                      q.ctypes.data, budget.ctypes.data, kind.ctypes.data,
-                                      lay.ctypes.data, sp.ctypes.data, out.ctypes.data,
-                                      bad.ctypes.data), "rh_chunk_time_host")
+    # quad loads + chunk times in one round trip (rh_chunk_time_docs_host)
+    _lib.check(lib.rh_chunk_time_docs_host(_lib.context(), _lib.C.byref(cost_model_c(model)),
+                                           len(mbs), off.ctypes.data, docs.ctypes.data, n,
+                                           idx.ctypes.data, budget.ctypes.data, kind.ctypes.data,
+                                           lay.ctypes.data, sp.ctypes.data, out.ctypes.data,
+                                           bad.ctypes.data), "rh_chunk_time_docs_host")
     return out
 
 
