@@ -253,6 +253,20 @@ int rh_screen(rh_ctx* ctx, const rh_screen_params* params, int64_t series_len,
               int64_t* series_len_out, void* stream);
 
 /* ------------------------------------------- per-call host entry points */
+/* One DetectorState.observe (detector.py:198-271) in one round trip: when
+ * do_validate, validate the n_stage (measured, expected) pairs and the n_link
+ * exercised-link ratios (detector.py:127-158) into the flag / severity arrays;
+ * fold the flags and `escalate` (the host's filter verdict) into the status
+ * bits; screen `observed` against the carried series (series_len, hist = its
+ * last min(series_len, window) values) -> outcome (RH_SC_* bits) and the new
+ * series length.  Host pointers, synchronous. */
+int rh_observe_host(rh_ctx* ctx, const rh_screen_params* params, int64_t series_len,
+                    const double* hist, double observed, int32_t escalate, int32_t do_validate,
+                    int32_t n_stage, const double* measured, const double* expected,
+                    int32_t n_link, const double* link_ratio, double threshold,
+                    uint8_t* stage_flag, double* stage_sev, uint8_t* link_flag, double* link_sev,
+                    uint8_t* outcome, int64_t* series_len_out);
+
 /* Host-buffer twins of rh_quad_load, rh_chunk_time, rh_validate and rh_screen
  * for the drop-in API's per-call functions (workload.quad_load /
  * predict_chunk_time, detector.validate, one DetectorState.observe): every

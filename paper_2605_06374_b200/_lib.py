@@ -109,6 +109,9 @@ _SIGS = {
                                 C.POINTER(Segments), C.POINTER(Trace), C.POINTER(PassOut)], C.c_int),
     "rh_chunk_time_docs_host": ([_p, C.POINTER(CostModelC), C.c_int64, _p, _p, C.c_int64, _p, _p,
                                  _p, _p, _p, _p, _p], C.c_int),
+    "rh_observe_host": ([_p, C.POINTER(ScreenParams), C.c_int64, _p, C.c_double, C.c_int32,
+                         C.c_int32, C.c_int32, _p, _p, C.c_int32, _p, C.c_double, _p, _p, _p, _p,
+                         _p, _p], C.c_int),
     "rh_fp64_peak": ([_p, C.POINTER(C.c_double)], C.c_int),
     "rh_quad_load": ([_p, C.c_int64, _p, _p, _p, _p], C.c_int),
     "rh_chunk_time": ([_p, C.POINTER(CostModelC), C.c_int64, _p, _p, _p, _p, _p, _p, _p, _p],

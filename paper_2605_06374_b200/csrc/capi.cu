@@ -364,73 +364,6 @@ int rh_validate(rh_ctx* ctx, int64_t n, const double* measured, const double* ex
 
 }  // extern "C"
 
-namespace rh {
-
-// The per-call host entry points (rh_*_host): the caller's host arrays are
-// gathered into the context's pinned staging buffer, cross PCIe in ONE copy,
-// the device entry point runs on the staged copies, and every output comes
-// back in ONE copy -- instead of a synchronous copy per array (the drop-in
-// API's scalar calls: quad_load, predict_chunk_time, validate, the screen of
-// one DetectorState.observe).
-struct HostCall {
-  struct In {
-    const void* src;
-    size_t bytes, off;
-  };
-  struct Out {
-    void* dst;
-    size_t bytes, off;
-  };
-  std::vector<In> ins;
-  std::vector<Out> outs;
-  size_t in_bytes = 0, out_bytes = 0;
-  static size_t up(size_t x) { return (x + 15) & ~size_t(15); }
-  size_t in(const void* p, size_t b) {
-    ins.push_back({p, b, in_bytes});
-    in_bytes = up(in_bytes + b);
-    return ins.back().off;
-  }
-  size_t out(void* p, size_t b) {
-    outs.push_back({p, b, out_bytes});
-    out_bytes = up(out_bytes + b);
-    return outs.back().off;
-  }
-  // stage, copy in, launch(dev_in, dev_out, stream), copy out, wait, scatter
-  template <class F>
-  int run(rh_ctx* ctx, F&& launch) {
-    std::lock_guard<std::mutex> lock(ctx->call_mu);
-    const size_t total = in_bytes + out_bytes + 16;
-    if (total > ctx->call_stage_bytes) {
-      if (ctx->call_stage) RH_CUDA(cudaFreeHost(ctx->call_stage));
-      ctx->call_stage = nullptr;
-      ctx->call_stage_bytes = 0;
-      const size_t want = total + total / 2 + 4096;
-      RH_CUDA(cudaMallocHost(&ctx->call_stage, want));
-      ctx->call_stage_bytes = want;
-    }
-    if (!ctx->call_stream)
-      RH_CUDA(cudaStreamCreateWithFlags(&ctx->call_stream, cudaStreamNonBlocking));
-    cudaStream_t st = ctx->call_stream;
-    void* dev = nullptr;
-    if (int rc = workspace(ctx, total, &dev, 5, st)) return rc;
-    char* h = static_cast<char*>(ctx->call_stage);
-    for (const In& a : ins)
-      if (a.src && a.bytes) memcpy(h + a.off, a.src, a.bytes);
-    char* d_in = static_cast<char*>(dev);
-    char* d_out = d_in + in_bytes;
-    if (in_bytes) RH_CUDA(cudaMemcpyAsync(d_in, h, in_bytes, cudaMemcpyHostToDevice, st));
-    if (int rc = launch(d_in, d_out, st)) return rc;
-    if (out_bytes)
-      RH_CUDA(cudaMemcpyAsync(h + in_bytes, d_out, out_bytes, cudaMemcpyDeviceToHost, st));
-    RH_CUDA(cudaStreamSynchronize(st));
-    for (const Out& o : outs)
-      if (o.dst && o.bytes) memcpy(o.dst, h + in_bytes + o.off, o.bytes);
-    return RH_OK;
-  }
-};
-
-}  // namespace rh
-
 extern "C" {
 
 int rh_quad_load_host(rh_ctx* ctx, int64_t n_mb, const int32_t* mb_off, const int32_t* doc_len,

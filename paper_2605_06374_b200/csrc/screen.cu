@@ -288,6 +288,63 @@ __device__ __forceinline__ unsigned outcome_of(bool cand, bool refill_len, unsig
   return pop ? 1u : 0u;
 }
 
+// One DetectorState.observe (detector.py:198-271) in one launch: validate
+// the (replica, stage) times and the exercised-link ratios when asked
+// (detector.py:127-158: flag = measured > thr * expected, severity =
+// expected / measured; links: ratio > thr, severity 1 / ratio), fold the
+// flags into the iteration's status, then warp 0 screens the new observation
+// against the carried series (the window test of window_test with no
+// earlier iteration in the batch: the window is the history itself).
+constexpr int kObserveThreads = 256;
+__global__ void __launch_bounds__(kObserveThreads) observe_kernel(
+    int w, int fe, double kappa, int64_t series_len, const double* __restrict__ hist, int h,
+    double x, unsigned escalate, int do_validate, int n_stage, const double* __restrict__ meas,
+    const double* __restrict__ expd, int n_link, const double* __restrict__ lr, double thr,
+    uint8_t* __restrict__ s_flag, double* __restrict__ s_sev, uint8_t* __restrict__ l_flag,
+    double* __restrict__ l_sev, uint8_t* __restrict__ outcome, int64_t* __restrict__ len_out) {
+  __shared__ WarpScratch ws;
+  int stage_hit = 0, link_hit = 0;
+  if (do_validate) {
+    for (int i = threadIdx.x; i < n_stage; i += blockDim.x) {
+      const double m = meas[i], e = expd[i];
+      const bool f = !(e <= 0.0 || m <= 0.0) && m > __dmul_rn(thr, e);
+      s_flag[i] = f ? 1 : 0;
+      s_sev[i] = f ? __ddiv_rn(e, m) : 0.0;
+      stage_hit |= f;
+    }
+    for (int i = threadIdx.x; i < n_link; i += blockDim.x) {
+      const double r = lr[i];
+      const bool f = r > thr;
+      l_flag[i] = f ? 1 : 0;
+      l_sev[i] = f ? __ddiv_rn(1.0, r) : 0.0;
+      link_hit |= f;
+    }
+  }
+  stage_hit = __syncthreads_or(stage_hit);
+  link_hit = __syncthreads_or(link_hit);
+  if (threadIdx.x >= 32) return;
+  const unsigned stb = (escalate ? RH_IT_ESCALATE : 0u) | (stage_hit ? RH_IT_STAGE_FLAG : 0u) |
+                       (link_hit ? RH_IT_LINK_FLAG : 0u);
+  const int lane = threadIdx.x;
+  const int64_t len = series_len + 1;  // the series after appending x
+  bool cand = false;
+  if (len >= w + 1) {  // detect_change_point: the previous w values
+    for (int q = lane; q < w; q += 32) ws.win[q] = hist[h - w + q];
+    __syncwarp();
+    const double med = warp_median(ws.win, w, ws.sel);
+    for (int q = lane; q < w; q += 32) ws.dev[q] = fabs(__dsub_rn(ws.win[q], med));
+    __syncwarp();
+    const double mad = warp_median(ws.dev, w, ws.sel);
+    cand = fabs(__dsub_rn(x, med)) > __dmul_rn(kappa, mad);
+  }
+  uint8_t oc;
+  const unsigned pop = outcome_of(cand, len <= w, stb, fe, oc);
+  if (lane == 0) {
+    *outcome = oc;
+    *len_out = len - (int64_t)pop;
+  }
+}
+
 // Round 0 (kept = all) of every iteration, one warp each over the whole GPU:
 // folds the reset index and runs the window test, which in this round only
 // depends on the inputs.  c0 = cand | refill_len << 1.
@@ -687,4 +744,46 @@ extern "C" int rh_screen(rh_ctx* ctx, const rh_screen_params* params, int64_t se
   RH_CUDA(cudaEventRecord(ctx->prep.consumed, st));
   ctx->prep.consumed_recorded = true;
   return RH_OK;
+}
+
+extern "C" int rh_observe_host(rh_ctx* ctx, const rh_screen_params* params, int64_t series_len,
+                               const double* hist, double observed, int32_t escalate,
+                               int32_t do_validate, int32_t n_stage, const double* measured,
+                               const double* expected, int32_t n_link, const double* link_ratio,
+                               double threshold, uint8_t* stage_flag, double* stage_sev,
+                               uint8_t* link_flag, double* link_sev, uint8_t* outcome,
+                               int64_t* series_len_out) {
+  if (!ctx || !params || series_len < 0 || params->window < 1 || params->window > kMaxWindow ||
+      (series_len > 0 && !hist) || !outcome || !series_len_out || n_stage < 0 || n_link < 0 ||
+      (do_validate && ((n_stage && (!measured || !expected || !stage_flag || !stage_sev)) ||
+                       (n_link && (!link_ratio || !link_flag || !link_sev))))) {
+    set_error("rh_observe_host: invalid arguments");
+    return RH_E_INVALID;
+  }
+  DeviceGuard guard(ctx);
+  const int h = (int)std::min<int64_t>(series_len, params->window);
+  const bool v = do_validate != 0;
+  HostCall c;
+  const size_t oh = c.in(h ? hist : nullptr, 8 * (size_t)h);
+  const size_t om = c.in(v ? measured : nullptr, v ? 8 * (size_t)n_stage : 0),
+               oe = c.in(v ? expected : nullptr, v ? 8 * (size_t)n_stage : 0),
+               ol = c.in(v ? link_ratio : nullptr, v ? 8 * (size_t)n_link : 0);
+  const size_t osf = c.out(v ? stage_flag : nullptr, v ? (size_t)n_stage : 0),
+               oss = c.out(v ? stage_sev : nullptr, v ? 8 * (size_t)n_stage : 0),
+               olf = c.out(v ? link_flag : nullptr, v ? (size_t)n_link : 0),
+               ols = c.out(v ? link_sev : nullptr, v ? 8 * (size_t)n_link : 0),
+               ooc = c.out(outcome, 1), olen = c.out(series_len_out, 8);
+  return c.run(ctx, [&](char* din, char* dout, cudaStream_t st) -> int {
+    observe_kernel<<<1, kObserveThreads, 0, st>>>(
+        params->window, params->filter_enabled != 0, params->kappa, series_len,
+        reinterpret_cast<const double*>(din + oh), h, observed, escalate ? 1u : 0u, v ? 1 : 0,
+        n_stage, reinterpret_cast<const double*>(din + om),
+        reinterpret_cast<const double*>(din + oe), n_link,
+        reinterpret_cast<const double*>(din + ol), threshold,
+        reinterpret_cast<uint8_t*>(dout + osf), reinterpret_cast<double*>(dout + oss),
+        reinterpret_cast<uint8_t*>(dout + olf), reinterpret_cast<double*>(dout + ols),
+        reinterpret_cast<uint8_t*>(dout + ooc), reinterpret_cast<int64_t*>(dout + olen));
+    RH_CHECK_LAUNCH(ctx);
+    return RH_OK;
+  });
 }

@@ -199,21 +199,37 @@ class DetectorState:
         out = DetectorOutcome()
         reference = reference_stage_cost or record.stage_cost_reference
         keys = sorted(record.stage_cost)
-        # validation inputs are evaluated lazily by the GPU only if escalated;
-        # the verdict bit feeds the screen's state machine
+        # the filter verdict is a host scalar rule; validation (when escalated,
+        # or with the filter disabled) and the screen of the new observation
+        # run in ONE device call (rh_observe_host: one copy in, one copy out)
         verdict = filter_candidate(record.observed_time, predicted, self.escalation_factor)
+        do_val = verdict == ESCALATE or not self.filter_enabled
+        lkeys = sorted(record.link_ratio or {})
+        ns, nl = len(keys), len(lkeys)
+        meas = np.ascontiguousarray([record.stage_cost[k] for k in keys] or [0.0], np.float64)
+        expd = np.ascontiguousarray([reference.get(k, 0.0) for k in keys] or [0.0], np.float64)
+        lr = np.ascontiguousarray([record.link_ratio[k] for k in lkeys] or [0.0], np.float64)
+        sf, ss = np.zeros(max(ns, 1), np.uint8), np.zeros(max(ns, 1))
+        lf, ls = np.zeros(max(nl, 1), np.uint8), np.zeros(max(nl, 1))
+        h = min(len(self.series), self.window)
+        hist = np.ascontiguousarray(self.series[len(self.series) - h:] if h else [0.0], np.float64)
+        oc = np.zeros(1, np.uint8)
+        new_len = np.zeros(1, np.int64)
+        params = _lib.ScreenParams(int(self.window), 1 if self.filter_enabled else 0,
+                                   float(self.kappa))
+        lib = _lib.load_library()
+        _lib.check(lib.rh_observe_host(
+            _lib.context(), _lib.C.byref(params), len(self.series), hist.ctypes.data,
+            float(record.observed_time), 1 if verdict == ESCALATE else 0, 1 if do_val else 0,
+            ns, meas.ctypes.data, expd.ctypes.data, nl, lr.ctypes.data,
+            float(self.escalation_factor), sf.ctypes.data, ss.ctypes.data, lf.ctypes.data,
+            ls.ctypes.data, oc.ctypes.data, new_len.ctypes.data), "rh_observe_host")
         result = None
-        status = _lib.RH_IT_ESCALATE if verdict == ESCALATE else 0
-        if verdict == ESCALATE or not self.filter_enabled:
-            result = validate({k: (record.stage_cost[k], reference.get(k, 0.0)) for k in keys},
-                              record.link_ratio, threshold=self.escalation_factor,
-                              cost_s=self.validation_cost_s)
-            if result.degraded_stages:
-                status |= _lib.RH_IT_STAGE_FLAG
-            if result.degraded_links:
-                status |= _lib.RH_IT_LINK_FLAG
-        oc, new_len = _screen(len(self.series), self.series, [record.observed_time], [status],
-                              self.window, self.kappa, self.filter_enabled)
+        if do_val:
+            stages = {k: float(v) for k, f, v in zip(keys, sf, ss) if f}
+            links = {k: float(v) for k, f, v in zip(lkeys, lf, ls) if f}
+            result = ValidationResult(bool(stages or links), stages, links,
+                                      self.validation_cost_s)
         return self._apply(int(oc[0]), record.observed_time, verdict, result, out)
 
     def _apply(self, oc: int, observed: float, verdict: str, result, out: DetectorOutcome):
