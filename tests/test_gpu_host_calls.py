@@ -107,3 +107,52 @@ def test_host_calls_reject_bad_arguments(cuda_device):
     # a non-empty series without its history
     assert lib.rh_screen_host(ctx, C.byref(params), 5, None, 4, x.ctypes.data, None, None, None,
                               None) == L.RH_E_INVALID
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_observe_host_sequence_matches_oracle_screen(seed, oracle, cuda_device):
+    """rh_observe_host called once per observation (the drop-in's
+    DetectorState.observe) equals the oracle's batch screen of the whole
+    sequence, with the validation flags folded into each status."""
+    L, lib, ctx = _lib()
+    rng = np.random.default_rng(40 + seed)
+    n, w, fe = 400, 20, seed % 2
+    obs = 1.0 + 0.01 * rng.standard_normal(n)
+    obs[rng.random(n) < 0.06] *= 1.5
+    esc = rng.random(n) < 0.3
+    params = L.ScreenParams(w, fe, 3.0)
+    series = []
+    st_all = np.zeros(n, np.uint8)
+    oc_all = np.zeros(n, np.uint8)
+    for i in range(n):
+        ns, nl = 6, 2
+        meas = rng.uniform(0.5, 1.6, ns)
+        exp = np.ones(ns)
+        lr = rng.uniform(0.8, 1.3, nl)
+        do_val = bool(esc[i] or not fe)
+        sf, ss = np.zeros(ns, np.uint8), np.zeros(ns)
+        lf, ls = np.zeros(nl, np.uint8), np.zeros(nl)
+        h = min(len(series), w)
+        hist = np.asarray(series[len(series) - h:] if h else [0.0], np.float64)
+        oc, ln = np.zeros(1, np.uint8), np.zeros(1, np.int64)
+        assert lib.rh_observe_host(ctx, C.byref(params), len(series), hist.ctypes.data,
+                                   float(obs[i]), int(esc[i]), int(do_val), ns, meas.ctypes.data,
+                                   exp.ctypes.data, nl, lr.ctypes.data, 1.25, sf.ctypes.data,
+                                   ss.ctypes.data, lf.ctypes.data, ls.ctypes.data, oc.ctypes.data,
+                                   ln.ctypes.data) == 0
+        st = L.RH_IT_ESCALATE if esc[i] else 0
+        if do_val:
+            want_sf = (meas > 1.25 * exp)
+            assert np.array_equal(sf.astype(bool), want_sf)
+            assert np.array_equal(lf.astype(bool), lr > 1.25)
+            if want_sf.any():
+                st |= L.RH_IT_STAGE_FLAG
+            if (lr > 1.25).any():
+                st |= L.RH_IT_LINK_FLAG
+        st_all[i], oc_all[i] = st, oc[0]
+        series.append(float(obs[i]))
+        if oc[0] & L.RH_SC_POPPED:
+            series.pop()
+        assert int(ln[0]) == len(series)
+    woc, wln = oracle.screen(obs, st_all, w, 3.0, bool(fe))
+    assert np.array_equal(oc_all, woc) and wln == len(series)
