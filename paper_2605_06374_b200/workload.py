@@ -165,7 +165,27 @@ def predict_chunk_time(mb: MicroBatch, kind: str, model: CostModel, layers_on_st
 
 
 def fit_cost_model(samples, chunk_ratios=None):
-    """workload.py:101-125 -- offline calibration of (alpha, beta), outside
-    the hot path: not built, raises."""
-    raise NotImplementedError("fit_cost_model is offline calibration, outside the B200 hot path "
-                              "(DESIGN.md §9): calibrate with the reference implementation")
+    """workload.py:101-125 -- offline calibration of (alpha, beta) from
+    (micro-batch, measured F time) pairs: least squares on the columns
+    (token budget N, quad load Q) -- the quad loads of all samples in one GPU
+    batch (quad_loads), the 2-column solve on the host (numpy lstsq, as the
+    reference) -- a negative coefficient is clamped to 0 and the other refit
+    alone; returns (CostModel, in-sample MAPE)."""
+    if len(samples) < 2:
+        raise ValueError("need at least two samples to fit the cost model")
+    mbs = [mb for mb, _ in samples]
+    times = np.array([float(t) for _, t in samples], dtype=np.float64)
+    budgets = np.array([float(mb.token_budget) for mb in mbs], dtype=np.float64)
+    quads = quad_loads(mbs).astype(np.float64)
+    if np.ptp(quads) == 0 and np.ptp(budgets) == 0:
+        raise ValueError("unidentifiable beta: all samples share the same quad load")
+    sol = np.linalg.lstsq(np.column_stack([budgets, quads]), times, rcond=None)[0]
+    alpha, beta = float(sol[0]), float(sol[1])
+    if alpha < 0:  # noise pushed one coefficient below zero: refit the other alone
+        alpha, beta = 0.0, float(np.dot(quads, times) / np.dot(quads, quads))
+    elif beta < 0:
+        alpha, beta = float(np.dot(budgets, times) / np.dot(budgets, budgets)), 0.0
+    fit = alpha * budgets + beta * quads
+    mape = float(np.mean(np.abs(fit - times) / times))
+    return CostModel(alpha=alpha, beta=beta,
+                     chunk_ratios=dict(chunk_ratios or DEFAULT_CHUNK_RATIOS)), mape
