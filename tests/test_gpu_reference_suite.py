@@ -14,19 +14,8 @@ pytestmark = pytest.mark.gpu
 
 SUITE = Path(__file__).resolve().parent / "reference_suite"
 
-# test id -> why it is not run against the drop-in: the paper's comparison
-# baselines are outside the hot path; the drop-in
-# raises NotImplementedError for them
-_BASELINE = "recycle / greyhound comparison baselines: out of scope"
-OUT_OF_SCOPE = {
-    "test_policies.py::TestRecycle::test_whole_group_excluded_on_single_failure": _BASELINE,
-    "test_policies.py::TestRecycle::test_dead_stage_chunks_rerouted_to_peer": _BASELINE,
-    "test_policies.py::TestRecycle::test_no_failures_empty_plan": _BASELINE,
-    "test_policies.py::TestRecycle::test_all_replicas_failed_aborts": _BASELINE,
-    "test_policies.py::TestGreyhound::test_half_speed_replica_gets_third_of_batch": _BASELINE,
-    "test_policies.py::TestGreyhound::test_equal_speeds_equal_split": _BASELINE,
-    "test_policies.py::TestGreyhound::test_intra_replica_bubble_persists": _BASELINE,
-}
+# test id -> why it is not run against the drop-in (none left)
+OUT_OF_SCOPE: dict[str, str] = {}
 
 
 def test_suite_files_are_the_reference_tests():
@@ -46,4 +35,4 @@ def test_reference_unit_tests_pass_on_the_drop_in():
     assert r.returncode == 0, tail
     assert " passed" in r.stdout and " failed" not in r.stdout, tail
     n_pass = int(r.stdout.strip().splitlines()[-1].split(" passed")[0].split()[-1])
-    assert n_pass >= 114, tail  # every in-scope reference test (119 of 126)
+    assert n_pass >= 126, tail  # all 126 reference unit tests
