@@ -3,8 +3,8 @@
 // shapes -- where a lane per stage (pass_kernel) idles half its DAG levels
 // and pays ~45 instructions of level bookkeeping per lane per level.
 //
-// One THREAD walks one replica pipeline: the chain state (last finish, last
-// F finish and cost sum of every stage) lives in registers, and the chunks
+// One THREAD walks one replica pipeline: the chain state (finish and cost
+// sum of every stage) lives in registers, and the chunks
 // are visited in a topological order that is a pair of short loops with the
 // stage index unrolled at compile time:
 //
@@ -24,11 +24,12 @@
 // few hundred instructions (the unrolled 512-chunk walk streamed 480 KB of
 // SASS through a 32 KB instruction cache).
 //
-// Shared memory per CTA (~26 KB for C5: 8 CTAs / SM): base costs [j][thread],
-// the iteration's ratio * layers, and one region that first holds the TMA-
-// staged offsets + documents and then the hop weights [stage][thread].
-// Speeds are read from global memory only on the stages some replica of the
-// warp runs slow (a warp-uniform branch; x / 1.0 == x exactly otherwise).
+// Shared memory per CTA (~27 KB for trace R: 8 CTAs / SM): base costs
+// [j][thread], the iteration's ratio * layers and the TMA-staged offsets +
+// documents.  Hop weights and stage speeds come from a per-launch transposed
+// copy of the segment tables (wide_prep_kernel) that L1 holds for every CTA
+// of the SM; speeds are read only on the stages some replica of the warp runs
+// slow (a warp-uniform branch; x / 1.0 == x exactly otherwise).
 #include "walks.cuh"
 
 namespace rh {
@@ -48,29 +49,57 @@ __device__ __forceinline__ double lds_rt(uint32_t a) {
   asm volatile("ld.volatile.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
   return v;
 }
+// the same for the L1-resident segment table (read-only global memory)
+template <int OFF>
+__device__ __forceinline__ double ldg_at(const double* a) {
+  double v;
+  asm volatile("ld.global.nc.f64 %0, [%1+%2];" : "=d"(v) : "l"(a), "n"(OFF));
+  return v;
+}
 
-// One replica's walk state: shared addresses of its base costs [j][TW], its
-// iteration's ratio * layers [rlF: P][rlB: P], its hop weights and speed
-// reciprocals [s][TW]; the chain state in registers.
+// Per-launch transposed segment table (wide_prep_kernel):
+//   tab[seg][k][s][kWideTabW], k = 0 hop into stage s on the forward path
+//   (hop_fwd[s-1], 0 for s = 0), 1 hop into s on the backward path
+//   (hop_bwd[s], 0 for s = P-1), 2 stage speed.
+// Replica d of a warp reads column d: every walk load is coalesced, and the
+// table of a segment (the same for all its iterations) stays in L1 for every
+// CTA of the SM -- shared memory keeps only the per-replica base costs.
+constexpr int kWideTabW = 64;
+__device__ __forceinline__ size_t wide_tab_index(int seg, int k, int s, int d, int P) {
+  return (((size_t)seg * 4 + k) * P + s) * kWideTabW + d;
+}
+
+__global__ void wide_prep_kernel(const rh_segments sg, int D, int P, double* tab) {
+  const int64_t n = (int64_t)sg.n_seg * D * P;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int s = (int)(i % P), d = (int)((i / P) % D), seg = (int)(i / ((int64_t)P * D));
+    const int64_t g = ((int64_t)seg * D + d) * P + s;  // [seg][d][s]
+    const double sp = sg.speed[g];
+    tab[wide_tab_index(seg, 0, s, d, P)] = s > 0 ? sg.hop_fwd[g - 1] : 0.0;
+    tab[wide_tab_index(seg, 1, s, d, P)] = s < P - 1 ? sg.hop_bwd[g] : 0.0;
+    tab[wide_tab_index(seg, 2, s, d, P)] = sp;
+    tab[wide_tab_index(seg, 3, s, d, P)] = recip_of(sp);
+  }
+}
+
+// One replica's walk: shared addresses of its base costs [j][TW] and its
+// iteration's ratio * layers [rlF: P][rlB: P]; its column of the segment
+// table; the chain state (finish and cost sum of every stage) in registers.
+// A stage's last F finish is never kept apart from its chain finish: when
+// F(S) reads stage S-1's last F, that F is stage S-1's latest chunk (warm-up:
+// just walked, stages ascending; main loop: the previous step's, S-1 not yet
+// visited this step), so fin[S-1] is that finish -- 2P doubles of state.
 template <int P, int TW, bool EXACT>
 struct WideWalk {
-  uint32_t bt, rl, hf, hb, inv;  // shared addresses (this thread's column)
-  const double* gsp;             // this (segment, replica)'s stage speeds
+  uint32_t bt, rl;  // shared addresses (this thread's column / iteration row)
+  const double* tb;  // this replica's column of the segment table
   unsigned slow;  // warp-uniform: bit s = some replica of the warp runs stage s slow
-  double fin[P], lastF[P], ssum[P];
+  double fin[P], ssum[P];
 
-  // c = (rl * b) / speed exactly as __ddiv_rn (the hoisted-reciprocal form
-  // after the kernel's operand-range check; EXACT: out-of-range operands,
-  // __ddiv_rn out of line), skipped on unit-speed stages (x / 1.0 == x)
-  template <int S>
-  __device__ __forceinline__ double cost(double rl_, double b_) const {
-    const double x = __dmul_rn(rl_, b_);
-    if (slow & (1u << S)) {  // warp-uniform branch
-      const double sp = __ldg(gsp + S);
-      if (EXACT) return div_slow(x, sp);
-      return div_fast(x, sp, lds_at<S * TW * 8>(inv));
-    }
-    return x;
+  template <int K, int S>
+  __device__ __forceinline__ double tab() const {
+    return ldg_at<(K * P + S) * kWideTabW * 8>(tb);
   }
   // start = max(chain finish, dependency finish + hop); finish = start + c;
   // cost sum in chain order (pipeline.py:275-291, 446-453)
@@ -83,23 +112,41 @@ struct WideWalk {
     ssum[S] = __dadd_rn(ssum[S], c);
     return fin[S];
   }
+  // one chunk of cost c = (rl * b) / speed, exactly as __ddiv_rn (the
+  // hoisted-reciprocal form after the kernel's operand-range check; EXACT:
+  // out-of-range operands, __ddiv_rn out of line), skipped on unit-speed
+  // stages (x / 1.0 == x).  ptxas predicates the division (no branch): a
+  // branch per chunk -- warp-uniform, or around an IEEE division -- splits
+  // the walk into basic blocks it cannot interleave, and measured slower
+  // (trace R 376 -> 442-480 us per 10^4 iterations).
+  template <int S, bool NODEP = false>
+  __device__ __forceinline__ double chunk(double rl_, double b_, double dep) {
+    double c = __dmul_rn(rl_, b_);
+    if (slow & (1u << S)) {  // warp-uniform
+      const double sp = tab<2, S>();
+      c = EXACT ? div_slow(c, sp) : div_fast(c, sp, tab<3, S>());
+    }
+    return step<S, NODEP>(c, dep);
+  }
   // warm-up triangle slot: F_j(S) if j <= P-1-S and j < m (stages ascending)
   template <int S>
   __device__ __forceinline__ void tri(int j, int m, double bj) {
     if (j <= P - 1 - S && j < m) {
-      const double dep = S > 0 ? __dadd_rn(lastF[S > 0 ? S - 1 : 0], lds_at<S * TW * 8>(hf)) : 0.0;
-      lastF[S] = step<S, S == 0>(cost<S>(lds_at<S * 8>(rl), bj), dep);
+      const double dep = S > 0 ? __dadd_rn(fin[S > 0 ? S - 1 : 0], tab<0, S>()) : 0.0;
+      chunk<S, S == 0>(lds_at<S * 8>(rl), bj, dep);
     }
   }
   // main-loop slot (stages descending): B_i(S), then F_{P-S+i}(S) if it exists
+  // (tried branch-free, a missing F costing +0.0 from a predicated load:
+  // 423 -> 459 us per 10^4 trace-R iterations)
   template <int S>
   __device__ __forceinline__ void pair(int i, int m, double bi, double& nB) {
-    const double depB = S < P - 1 ? __dadd_rn(nB, lds_at<S * TW * 8>(hb)) : 0.0;
-    nB = step<S, S == P - 1>(cost<S>(lds_at<(P + S) * 8>(rl), bi), depB);
+    const double depB = S < P - 1 ? __dadd_rn(nB, tab<1, S>()) : 0.0;
+    nB = chunk<S, S == P - 1>(lds_at<(P + S) * 8>(rl), bi, depB);
     if (i < m - P + S) {
       const double bF = lds_rt(bt + (uint32_t)((P - S + i) * TW * 8));
-      const double dep = S > 0 ? __dadd_rn(lastF[S > 0 ? S - 1 : 0], lds_at<S * TW * 8>(hf)) : 0.0;
-      lastF[S] = step<S, S == 0>(cost<S>(lds_at<S * 8>(rl), bF), dep);
+      const double dep = S > 0 ? __dadd_rn(fin[S > 0 ? S - 1 : 0], tab<0, S>()) : 0.0;
+      chunk<S, S == 0>(lds_at<S * 8>(rl), bF, dep);
     }
   }
   template <int... I>
@@ -115,8 +162,12 @@ struct WideWalk {
   // (Tried: K groups of stages skewed by one loop step each, so a step holds
   // K independent dependency chains -- bit-exact, but the per-group validity
   // and slow-stage branches kept the compiler from interleaving them: trace R
-  // 463 -> 520 us per 10^4 iterations; branch-free division on top: 624 us.)
+  // 463 -> 520 us per 10^4 iterations; branch-free division on top: 624 us.
+  // A level-ordered walk -- the P chunks of a DAG level are independent --
+  // issued more, not faster: tools/walkbench.cu, 1.57 -> 2.1 ms branch-free.)
   __device__ __forceinline__ void walk(int m) {
+#pragma unroll
+    for (int s = 0; s < P; ++s) fin[s] = ssum[s] = 0.0;
 #pragma unroll 1
     for (int j = 0; j < P; ++j)
       tri_all(j, m, lds_rt(bt + (uint32_t)((j < m ? j : 0) * TW * 8)),
@@ -127,17 +178,23 @@ struct WideWalk {
   }
 };
 
-// CTAs per SM the register budget targets: the loop-carried chain state is
-// 3P doubles (finish, last F finish, cost sum per stage), so long pipelines
-// trade occupancy for registers (P = 16: 168 registers, 6 CTAs = 12 warps).
+// CTAs per SM the register budget targets: with the hop / speed tables in L1
+// and the chain state at 2P doubles, 8 CTAs (16 warps) fit every P <= 16 in
+// 128 registers; shared memory (base costs + staging, ~27 KB for trace R)
+// allows the same.  (tools/walkbench.cu: 10 -> 16 warps per SM took the
+// trace-R walk from 1.57 to 1.03 ms; more warps than that did not help.)
+#ifndef RH_WIDE_DT_UNROLL
+#define RH_WIDE_DT_UNROLL 8
+#endif
+constexpr int kWideDtUnroll = RH_WIDE_DT_UNROLL;  // device-time rows in flight per thread
 #ifdef RH_WIDE_MINB
-constexpr int wide_min_blocks(int P) { return P <= 10 ? 8 : RH_WIDE_MINB; }  // A/B builds
+constexpr int kWideMinBlocks = RH_WIDE_MINB;  // A/B builds
 #else
-constexpr int wide_min_blocks(int P) { return P <= 10 ? 8 : (P <= 12 ? 7 : 6); }
+constexpr int kWideMinBlocks = 8;
 #endif
 
 template <int P, int DETECT>
-__global__ void __launch_bounds__(kWideThreads, wide_min_blocks(P)) pass_wide_kernel(const PassParams p) {
+__global__ void __launch_bounds__(kWideThreads, kWideMinBlocks) pass_wide_kernel(const PassParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int TW = kWideThreads;
   const int tid = threadIdx.x;
@@ -151,15 +208,12 @@ __global__ void __launch_bounds__(kWideThreads, wide_min_blocks(P)) pass_wide_ke
   unsigned* it_st = reinterpret_cast<unsigned*>(it_ms + p.ipb);
   double* base_t = reinterpret_cast<double*>(smem_raw + p.w_base);
   double* s_rl = reinterpret_cast<double*>(smem_raw + p.w_rl);
-  double* s_hf = reinterpret_cast<double*>(smem_raw + p.w_union);
-  double* s_hb = s_hf + P * TW;
-  double* s_inv = s_hb + P * TW;
   __shared__ uint64_t s_bar;
   if (tid < p.ipb) {
     it_ms[tid] = 0.0;
     it_st[tid] = 0u;
   }
-  // ---- the replica's segment tables: loads issued first, so their latency
+  // ---- the replica's segment: its loads are issued first, so their latency
   // overlaps the staging below (consumed after its barrier)
   const int seg = on && p.tr.seg ? __ldg(p.tr.seg + it) : 0;
   // ---- TMA staging of the CTA's micro-batch offsets and documents
@@ -172,19 +226,10 @@ __global__ void __launch_bounds__(kWideThreads, wide_min_blocks(P)) pass_wide_ke
     m0 = __ldg(ms + d);
     md = __ldg(ms + d + 1) - m0;
   }
-  const double* gsp = p.sg.speed + ((int64_t)seg * D + d) * P;
-  double hf[P], hb[P], spv[P];
+  const double* tb = p.wtab + wide_tab_index(seg, 0, 0, d, P);
+  double spv[P];
 #pragma unroll
-  for (int s = 0; s < P; ++s) {
-    const int64_t gs = ((int64_t)seg * D + d) * P + s;
-    spv[s] = 1.0;
-    hf[s] = hb[s] = 0.0;
-    if (on) {
-      spv[s] = __ldg(gsp + s);
-      if (s > 0) hf[s] = __ldg(p.sg.hop_fwd + gs - 1);
-      if (s < P - 1) hb[s] = __ldg(p.sg.hop_bwd + gs);
-    }
-  }
+  for (int s = 0; s < P; ++s) spv[s] = on ? __ldg(tb + (2 * P + s) * kWideTabW) : 1.0;
   // this thread's first ratio * layers entry (stage d)
   const int32_t L_d = on && d < P ? __ldg(p.sg.layers + (int64_t)seg * P + d) : 0;
   const bool staged = n_doc <= p.doc_stage;
@@ -229,37 +274,7 @@ __global__ void __launch_bounds__(kWideThreads, wide_min_blocks(P)) pass_wide_ke
     }
     stopped = stopped || sp <= 0.0;
   }
-  // measured stage times (max over the TP group's device times, float4
-  // loads) and the segment's exercised-link test, both issued here so their
-  // latency overlaps the copies; kept for the epilogue
-  float* s_meas = reinterpret_cast<float*>(smem_raw + p.w_rl + (size_t)p.ipb * 2 * P * 8);
-  bool link_bad = false;
-  if (DETECT && on && md >= 0) {
-    const float* dt = p.tr.device_time + (it * D + d) * P * (int64_t)T;
-    if (p.vec4 && T == 8) {
-#pragma unroll
-      for (int s = 0; s < P; ++s) {
-        const float4 v = __ldg(reinterpret_cast<const float4*>(dt + s * 8));
-        const float4 w = __ldg(reinterpret_cast<const float4*>(dt + s * 8 + 4));
-        s_meas[s * TW + tid] = fmaxf(fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)),
-                                     fmaxf(fmaxf(w.x, w.y), fmaxf(w.z, w.w)));
-      }
-    } else {
-#pragma unroll 4
-      for (int s = 0; s < P; ++s) {
-        float mx = 0.0f;
-        if (p.vec4) {
-          for (int q = 0; q < T; q += 4) {
-            const float4 v = __ldg(reinterpret_cast<const float4*>(dt + s * T + q));
-            mx = fmaxf(mx, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
-          }
-        } else {
-          for (int q = 0; q < T; ++q) mx = fmaxf(mx, __ldg(dt + s * T + q));
-        }
-        s_meas[s * TW + tid] = mx;
-      }
-    }
-  }
+  bool link_bad = false;  // the segment's exercised-link test, issued before the wait
   if (DETECT && on && p.sg.link_off && p.sg.link_max) {  // one compare (segment maximum)
     link_bad = __ldg(p.sg.link_max + seg) > p.thr;
   } else if (DETECT && on && p.sg.link_off) {  // exercised-link ratios, split over the replicas
@@ -301,21 +316,13 @@ __global__ void __launch_bounds__(kWideThreads, wide_min_blocks(P)) pass_wide_ke
       if (b > 0.0 && b < b_lo) b_lo = b;
     }
   }
-  __syncthreads();  // offsets and documents are dead: the region takes the hops
-#pragma unroll
-  for (int s = 0; s < P; ++s) {
-    s_hf[s * TW + tid] = hf[s];
-    s_hb[s * TW + tid] = hb[s];
-    // (every stage: a replica whose stage s runs at 1.0 still divides when
-    // another replica of its warp runs stage s slow -- by 1.0, exactly)
-    s_inv[s * TW + tid] = (slow & (1u << s)) ? recip_of(__ldg(gsp + s)) : 1.0;
-  }
   if (m == 0) {  // nothing runs: no speeds, no costs
     slow = 0;
     stopped = false;
     safe = true;
   }
   const double* rl = s_rl + li * 2 * P;
+  __syncthreads();  // ratio * layers visible
   if (slow && m > 0) {  // exact hoisted-reciprocal division needs in-range operands
     double r_lo = CUDART_INF, r_hi = 0.0;
 #pragma unroll
@@ -331,21 +338,25 @@ __global__ void __launch_bounds__(kWideThreads, wide_min_blocks(P)) pass_wide_ke
   const int mm = stopped ? 0 : m;
   const bool over = p.sh.capacity > 0 && mm > 0 && __ldg(p.sched_peak + mm) > p.sh.capacity;
   const unsigned wslow = __reduce_or_sync(0xffffffffu, mm > 0 ? slow : 0u);
-  __syncthreads();  // hops visible
   double fin[P], ssum[P];
 #pragma unroll
   for (int s = 0; s < P; ++s) fin[s] = ssum[s] = 0.0;
+  // (Tried: a warp whose replicas all walk the same micro-batch count taking
+  // that count from a warp reduction, so ptxas sees uniform loop bounds and
+  // validity tests -- no gain, 481 vs 481 us.)
+  const uint32_t a_bt = smem_u32(base_t + tid), a_rl = smem_u32(rl);
+#ifdef RH_WIDE_NOWALK
+  if (mm > 0 && p.thr < -1.0) {
+#else
   if (mm > 0) {
-    const uint32_t a_bt = smem_u32(base_t + tid), a_rl = smem_u32(rl),
-                   a_hf = smem_u32(s_hf + tid), a_hb = smem_u32(s_hb + tid),
-                   a_inv = smem_u32(s_inv + tid);
+#endif
     if (safe) {
-      WideWalk<P, TW, false> w{a_bt, a_rl, a_hf, a_hb, a_inv, gsp, wslow, {}, {}, {}};
+      WideWalk<P, TW, false> w{a_bt, a_rl, tb, wslow, {}, {}};
       w.walk(mm);
 #pragma unroll
       for (int s = 0; s < P; ++s) fin[s] = w.fin[s], ssum[s] = w.ssum[s];
     } else {  // operands outside the hoisted-reciprocal range
-      WideWalk<P, TW, true> w{a_bt, a_rl, a_hf, a_hb, a_inv, gsp, wslow, {}, {}, {}};
+      WideWalk<P, TW, true> w{a_bt, a_rl, tb, wslow, {}, {}};
       w.walk(mm);
 #pragma unroll
       for (int s = 0; s < P; ++s) fin[s] = w.fin[s], ssum[s] = w.ssum[s];
@@ -354,6 +365,9 @@ __global__ void __launch_bounds__(kWideThreads, wide_min_blocks(P)) pass_wide_ke
   // ---- replica makespan, validation, iteration reductions
   unsigned bits = 0;
   uint32_t flags = 0;  // bit s: stage s flagged
+  float meas[P];       // measured stage times: max over the TP group's device times
+#pragma unroll
+  for (int s = 0; s < P; ++s) meas[s] = 0.0f;
   if (on) {
     double g = 0.0;
 #pragma unroll
@@ -364,9 +378,33 @@ __global__ void __launch_bounds__(kWideThreads, wide_min_blocks(P)) pass_wide_ke
     if (p.sh.has_allreduce && D > 1) g = __dadd_rn(g, __ldg(p.sg.allreduce + (int64_t)seg * D + d));
     atomic_max_nonneg(it_ms + li, g);
     if (DETECT && md >= 0) {
+      const float* dt = p.tr.device_time + (it * D + d) * P * (int64_t)T;
+      if (p.vec4 && T == 8) {
+#pragma unroll kWideDtUnroll
+        for (int s = 0; s < P; ++s) {
+          const float4 v = __ldg(reinterpret_cast<const float4*>(dt + s * 8));
+          const float4 w = __ldg(reinterpret_cast<const float4*>(dt + s * 8 + 4));
+          meas[s] = fmaxf(fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)),
+                          fmaxf(fmaxf(w.x, w.y), fmaxf(w.z, w.w)));
+        }
+      } else {
+#pragma unroll 4
+        for (int s = 0; s < P; ++s) {
+          float mx = 0.0f;
+          if (p.vec4) {
+            for (int q = 0; q < T; q += 4) {
+              const float4 v = __ldg(reinterpret_cast<const float4*>(dt + s * T + q));
+              mx = fmaxf(mx, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
+            }
+          } else {
+            for (int q = 0; q < T; ++q) mx = fmaxf(mx, __ldg(dt + s * T + q));
+          }
+          meas[s] = mx;
+        }
+      }
 #pragma unroll
       for (int s = 0; s < P; ++s) {
-        const double ms_d = (double)s_meas[s * TW + tid];
+        const double ms_d = (double)meas[s];
         if (!(ssum[s] <= 0.0 || ms_d <= 0.0) && ms_d > __dmul_rn(p.thr, ssum[s])) {
           flags |= 1u << s;
           bits |= RH_IT_STAGE_FLAG;
@@ -388,7 +426,7 @@ __global__ void __launch_bounds__(kWideThreads, wide_min_blocks(P)) pass_wide_ke
     if (DETECT) {
       if (p.out.stage_flag) p.out.stage_flag[o] = f ? 1 : 0;
       if (p.out.severity)
-        p.out.severity[o] = f ? (float)__ddiv_rn(ssum[s], (double)s_meas[s * TW + tid]) : 0.0f;
+        p.out.severity[o] = f ? (float)__ddiv_rn(ssum[s], (double)meas[s]) : 0.0f;
     }
   }
   if (d == 0) {
@@ -430,6 +468,17 @@ static void* wide_kernel_t(int P) {
 void* wide_kernel_ptr(int P, int zbh, int detect) {
   if (zbh) return nullptr;  // ZBH long pipelines: the lane kernel
   return detect ? wide_kernel_t<1>(P) : wide_kernel_t<0>(P);
+}
+
+size_t wide_tab_bytes(int n_seg, int P) { return (size_t)n_seg * 4 * P * kWideTabW * 8; }
+
+int wide_prep(const rh_segments& sg, int D, int P, double* tab, cudaStream_t stream) {
+  const int64_t n = (int64_t)sg.n_seg * D * P;
+  if (n == 0) return RH_OK;
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, 1024);
+  wide_prep_kernel<<<blocks, 256, 0, stream>>>(sg, D, P, tab);
+  RH_CUDA(cudaGetLastError());
+  return RH_OK;
 }
 
 }  // namespace rh

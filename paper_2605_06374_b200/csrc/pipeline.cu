@@ -824,20 +824,25 @@ int launch_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
       const size_t it_bytes = al((size_t)p.ipb * 12);
       p.w_base = (int)it_bytes;
       p.w_rl = (int)al(p.w_base + (size_t)tw * p.mmax * 8);
-      // [rl: ipb][2][P] doubles, then the measured stage times [P][TW] float
-      p.w_union = (int)al(p.w_rl + (size_t)p.ipb * 2 * P * 8 + (size_t)P * tw * 4);
+      // [rl: ipb][2][P] doubles, then the staged offsets and documents (the
+      // hop / speed tables live in L1: wide_prep's transposed copy)
+      p.w_union = (int)al(p.w_rl + (size_t)p.ipb * 2 * P * 8);
       const size_t off_bytes = al(16 + 4 * ((size_t)p.ipb * M + 1));
       p.w_docs = (int)(p.w_union + off_bytes);
-      const size_t hops = 3 * (size_t)P * tw * 8;  // hf, hb, inv
-      // documents: what the hop area leaves, at least ~3 per micro-batch
-      const size_t docs = std::max<size_t>(hops > off_bytes ? hops - off_bytes : 0,
-                                           16 + 12 * (size_t)p.ipb * M);
+      // documents: ~3.5 per micro-batch (a CTA with more reads them from L2)
+      const size_t docs = al(16 + 14 * (size_t)p.ipb * M);
       p.doc_stage = (int)((docs - 16) / 4);
       const size_t smem = p.w_docs + docs;
       if (smem <= ctx->smem_optin) {
         if (int e = sched_table(ctx, P, zbh, p.mmax, &p.sched, &p.sched_off, &p.sched_peak))
           return e;
         const int64_t blocks = (tr->n_iter + p.ipb - 1) / p.ipb;
+        {
+          void* tab = nullptr;
+          if (int e = workspace(ctx, wide_tab_bytes(std::max(sg->n_seg, 1), P), &tab, 6, stream)) return e;
+          if (int e = wide_prep(*sg, D, P, static_cast<double*>(tab), stream)) return e;
+          p.wtab = static_cast<const double*>(tab);
+        }
         if (int e = ensure_smem(ctx, kern, smem)) return e;
         int occ = 0;
         RH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, tw, smem));

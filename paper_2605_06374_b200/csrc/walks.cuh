@@ -38,6 +38,7 @@ struct PassParams {
   // layers [ipb][3][P] doubles, then a union of {offsets (ipb*M+1 int32,
   // 16 B slack) + documents (doc_stage int32)} and {hops [2][P][TW] doubles}
   int w_base, w_rl, w_union, w_docs;
+  const double* wtab;  // wide kernel: per-launch transposed segment table (wide_prep)
   int q32;         // micro-batch sum l^2 in 32-bit integers (exactness checked per micro-batch)
   int static_max;  // largest micro-batch count walked by the unrolled code
   int steady;      // m >= P: the steady-state loop walk (walk_steady)
@@ -541,5 +542,7 @@ __device__ __forceinline__ void stage_finish(const PassParams& p, const CtaStage
 // detect), nullptr when P has no instantiation
 constexpr int kWideThreads = 64;
 void* wide_kernel_ptr(int P, int zbh, int detect);
+size_t wide_tab_bytes(int n_seg, int P);
+int wide_prep(const rh_segments& sg, int D, int P, double* tab, cudaStream_t stream);
 
 }  // namespace rh
