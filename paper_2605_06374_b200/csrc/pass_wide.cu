@@ -53,6 +53,8 @@ __device__ __forceinline__ double lds_rt(uint32_t a) {
 template <int OFF>
 __device__ __forceinline__ double ldg_at(const double* a) {
   double v;
+  // volatile: a plain load lets ptxas hoist every table read of the walk
+  // (1.5 KB of spills per thread, 2x slower)
   asm volatile("ld.global.nc.f64 %0, [%1+%2];" : "=d"(v) : "l"(a), "n"(OFF));
   return v;
 }
@@ -60,13 +62,25 @@ __device__ __forceinline__ double ldg_at(const double* a) {
 // Per-launch transposed segment table (wide_prep_kernel):
 //   tab[seg][k][s][kWideTabW], k = 0 hop into stage s on the forward path
 //   (hop_fwd[s-1], 0 for s = 0), 1 hop into s on the backward path
-//   (hop_bwd[s], 0 for s = P-1), 2 stage speed.
+//   (hop_bwd[s], 0 for s = P-1), 2 pow2_recip(speed), 3 speed,
+//   4 recip_of(speed).
 // Replica d of a warp reads column d: every walk load is coalesced, and the
 // table of a segment (the same for all its iterations) stays in L1 for every
 // CTA of the SM -- shared memory keeps only the per-replica base costs.
 constexpr int kWideTabW = 64;
+constexpr int kWideTabK = 5;
 __device__ __forceinline__ size_t wide_tab_index(int seg, int k, int s, int d, int P) {
-  return (((size_t)seg * 4 + k) * P + s) * kWideTabW + d;
+  return (((size_t)seg * kWideTabK + k) * P + s) * kWideTabW + d;
+}
+
+// 1/b when b is a power of two whose reciprocal is a normal double, else 0:
+// then x / b == x * (1/b) exactly for every x (both are the real x * 2^-e,
+// rounded once), so the division is one multiply.
+__device__ __forceinline__ double pow2_recip(double b) {
+  const unsigned long long u = __double_as_longlong(b);
+  const int e = (int)((u >> 52) & 0x7ff);
+  const bool pow2 = (u >> 63) == 0 && (u & 0xfffffffffffffull) == 0 && e >= 1 && e <= 2045;
+  return pow2 ? 1.0 / b : 0.0;
 }
 
 __global__ void wide_prep_kernel(const rh_segments sg, int D, int P, double* tab) {
@@ -78,8 +92,9 @@ __global__ void wide_prep_kernel(const rh_segments sg, int D, int P, double* tab
     const double sp = sg.speed[g];
     tab[wide_tab_index(seg, 0, s, d, P)] = s > 0 ? sg.hop_fwd[g - 1] : 0.0;
     tab[wide_tab_index(seg, 1, s, d, P)] = s < P - 1 ? sg.hop_bwd[g] : 0.0;
-    tab[wide_tab_index(seg, 2, s, d, P)] = sp;
-    tab[wide_tab_index(seg, 3, s, d, P)] = recip_of(sp);
+    tab[wide_tab_index(seg, 2, s, d, P)] = pow2_recip(sp);
+    tab[wide_tab_index(seg, 3, s, d, P)] = sp;
+    tab[wide_tab_index(seg, 4, s, d, P)] = recip_of(sp);
   }
 }
 
@@ -90,7 +105,12 @@ __global__ void wide_prep_kernel(const rh_segments sg, int D, int P, double* tab
 // F(S) reads stage S-1's last F, that F is stage S-1's latest chunk (warm-up:
 // just walked, stages ascending; main loop: the previous step's, S-1 not yet
 // visited this step), so fin[S-1] is that finish -- 2P doubles of state.
-template <int P, int TW, bool EXACT>
+// How a walk divides a chunk's cost by a slow stage's speed: kDivScale, every
+// slow speed of the warp is a power of two (one exact multiply); kDivFast, the
+// hoisted-reciprocal form (operands range-checked); kDivExact, __ddiv_rn.
+enum { kDivScale = 0, kDivFast = 1, kDivExact = 2 };
+
+template <int P, int TW, int MODE>
 struct WideWalk {
   uint32_t bt, rl;  // shared addresses (this thread's column / iteration row)
   const double* tb;  // this replica's column of the segment table
@@ -123,8 +143,12 @@ struct WideWalk {
   __device__ __forceinline__ double chunk(double rl_, double b_, double dep) {
     double c = __dmul_rn(rl_, b_);
     if (slow & (1u << S)) {  // warp-uniform
-      const double sp = tab<2, S>();
-      c = EXACT ? div_slow(c, sp) : div_fast(c, sp, tab<3, S>());
+      if (MODE == kDivScale) {
+        c = __dmul_rn(c, tab<2, S>());
+      } else {
+        const double sp = tab<3, S>();
+        c = MODE == kDivExact ? div_slow(c, sp) : div_fast(c, sp, tab<4, S>());
+      }
     }
     return step<S, NODEP>(c, dep);
   }
@@ -229,7 +253,7 @@ __global__ void __launch_bounds__(kWideThreads, kWideMinBlocks) pass_wide_kernel
   const double* tb = p.wtab + wide_tab_index(seg, 0, 0, d, P);
   double spv[P];
 #pragma unroll
-  for (int s = 0; s < P; ++s) spv[s] = on ? __ldg(tb + (2 * P + s) * kWideTabW) : 1.0;
+  for (int s = 0; s < P; ++s) spv[s] = on ? __ldg(tb + (3 * P + s) * kWideTabW) : 1.0;
   // this thread's first ratio * layers entry (stage d)
   const int32_t L_d = on && d < P ? __ldg(p.sg.layers + (int64_t)seg * P + d) : 0;
   const bool staged = n_doc <= p.doc_stage;
@@ -263,7 +287,7 @@ __global__ void __launch_bounds__(kWideThreads, kWideMinBlocks) pass_wide_kernel
       s_rl[li * 2 * P + s] = __dmul_rn(p.m.ratio_f, L);
       s_rl[li * 2 * P + P + s] = __dmul_rn(__dadd_rn(p.m.ratio_b, p.m.ratio_w), L);
     }
-  bool stopped = false, safe = true;
+  bool stopped = false, safe = true, pow2 = true;
   unsigned slow = 0;
 #pragma unroll
   for (int s = 0; s < P; ++s) {
@@ -271,6 +295,7 @@ __global__ void __launch_bounds__(kWideThreads, kWideMinBlocks) pass_wide_kernel
     if (sp != 1.0) {
       slow |= 1u << s;
       safe = safe && sp >= 0x1p-100 && sp <= 0x1p100;  // recip_of(sp) != 0
+      pow2 = pow2 && pow2_recip(sp) != 0.0;
     }
     stopped = stopped || sp <= 0.0;
   }
@@ -300,9 +325,29 @@ __global__ void __launch_bounds__(kWideThreads, kWideMinBlocks) pass_wide_kernel
       const int32_t k0 = s_off[j] - d_lo, k1 = s_off[j + 1] - d_lo;
       unsigned long long q = 0;
       if (staged) {
-        for (int32_t k = k0; k < k1; ++k) {
-          const long long l = sd.dst[k];
-          q += (unsigned long long)(l * l);
+        // 32-bit sums, the first 4 documents unrolled: whenever sum l < 2^16,
+        // sum l^2 <= (sum l)^2 < 2^32 is exact; a micro-batch above that
+        // (or with a negative length) is redone in 64-bit
+        const int32_t nd = k1 - k0;
+        uint32_t q32 = 0, sl = 0;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const uint32_t l = t < nd ? (uint32_t)sd.dst[k0 + t] : 0u;
+          q32 += l * l;
+          sl += l;
+        }
+        for (int32_t k = k0 + 4; k < k1; ++k) {
+          const uint32_t l = (uint32_t)sd.dst[k];
+          q32 += l * l;
+          sl += l;
+        }
+        q = q32;
+        if (sl >= 65536u || nd < 0) {
+          q = 0;
+          for (int32_t k = k0; k < k1; ++k) {
+            const long long l = sd.dst[k];
+            q += (unsigned long long)(l * l);
+          }
         }
       } else {
         for (int32_t k = k0; k < k1; ++k) {
@@ -345,18 +390,28 @@ __global__ void __launch_bounds__(kWideThreads, kWideMinBlocks) pass_wide_kernel
   // that count from a warp reduction, so ptxas sees uniform loop bounds and
   // validity tests -- no gain, 481 vs 481 us.)
   const uint32_t a_bt = smem_u32(base_t + tid), a_rl = smem_u32(rl);
+#ifdef RH_WIDE_NO_POW2
+  const bool wpow2 = false;
+#else
+  const bool wpow2 = __all_sync(0xffffffffu, pow2 || mm == 0);
+#endif
 #ifdef RH_WIDE_NOWALK
   if (mm > 0 && p.thr < -1.0) {
 #else
   if (mm > 0) {
 #endif
-    if (safe) {
-      WideWalk<P, TW, false> w{a_bt, a_rl, tb, wslow, {}, {}};
+    if (wpow2) {  // every slow speed of the warp a power of two (0.5, 0.25, ...)
+      WideWalk<P, TW, kDivScale> w{a_bt, a_rl, tb, wslow, {}, {}};
+      w.walk(mm);
+#pragma unroll
+      for (int s = 0; s < P; ++s) fin[s] = w.fin[s], ssum[s] = w.ssum[s];
+    } else if (safe) {
+      WideWalk<P, TW, kDivFast> w{a_bt, a_rl, tb, wslow, {}, {}};
       w.walk(mm);
 #pragma unroll
       for (int s = 0; s < P; ++s) fin[s] = w.fin[s], ssum[s] = w.ssum[s];
     } else {  // operands outside the hoisted-reciprocal range
-      WideWalk<P, TW, true> w{a_bt, a_rl, tb, wslow, {}, {}};
+      WideWalk<P, TW, kDivExact> w{a_bt, a_rl, tb, wslow, {}, {}};
       w.walk(mm);
 #pragma unroll
       for (int s = 0; s < P; ++s) fin[s] = w.fin[s], ssum[s] = w.ssum[s];
@@ -365,9 +420,10 @@ __global__ void __launch_bounds__(kWideThreads, kWideMinBlocks) pass_wide_kernel
   // ---- replica makespan, validation, iteration reductions
   unsigned bits = 0;
   uint32_t flags = 0;  // bit s: stage s flagged
-  float meas[P];       // measured stage times: max over the TP group's device times
-#pragma unroll
-  for (int s = 0; s < P; ++s) meas[s] = 0.0f;
+  // measured stage times (max over the TP group's device times, float4
+  // loads) land in the staging region, dead since the base costs: a register
+  // array indexed in a partially unrolled loop would live in local memory
+  float* s_meas = reinterpret_cast<float*>(smem_raw + p.w_union);
   if (on) {
     double g = 0.0;
 #pragma unroll
@@ -384,8 +440,8 @@ __global__ void __launch_bounds__(kWideThreads, kWideMinBlocks) pass_wide_kernel
         for (int s = 0; s < P; ++s) {
           const float4 v = __ldg(reinterpret_cast<const float4*>(dt + s * 8));
           const float4 w = __ldg(reinterpret_cast<const float4*>(dt + s * 8 + 4));
-          meas[s] = fmaxf(fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)),
-                          fmaxf(fmaxf(w.x, w.y), fmaxf(w.z, w.w)));
+          s_meas[s * TW + tid] = fmaxf(fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)),
+                                       fmaxf(fmaxf(w.x, w.y), fmaxf(w.z, w.w)));
         }
       } else {
 #pragma unroll 4
@@ -399,12 +455,12 @@ __global__ void __launch_bounds__(kWideThreads, kWideMinBlocks) pass_wide_kernel
           } else {
             for (int q = 0; q < T; ++q) mx = fmaxf(mx, __ldg(dt + s * T + q));
           }
-          meas[s] = mx;
+          s_meas[s * TW + tid] = mx;
         }
       }
 #pragma unroll
       for (int s = 0; s < P; ++s) {
-        const double ms_d = (double)meas[s];
+        const double ms_d = (double)s_meas[s * TW + tid];
         if (!(ssum[s] <= 0.0 || ms_d <= 0.0) && ms_d > __dmul_rn(p.thr, ssum[s])) {
           flags |= 1u << s;
           bits |= RH_IT_STAGE_FLAG;
@@ -426,7 +482,7 @@ __global__ void __launch_bounds__(kWideThreads, kWideMinBlocks) pass_wide_kernel
     if (DETECT) {
       if (p.out.stage_flag) p.out.stage_flag[o] = f ? 1 : 0;
       if (p.out.severity)
-        p.out.severity[o] = f ? (float)__ddiv_rn(ssum[s], (double)meas[s]) : 0.0f;
+        p.out.severity[o] = f ? (float)__ddiv_rn(ssum[s], (double)s_meas[s * TW + tid]) : 0.0f;
     }
   }
   if (d == 0) {
@@ -470,7 +526,7 @@ void* wide_kernel_ptr(int P, int zbh, int detect) {
   return detect ? wide_kernel_t<1>(P) : wide_kernel_t<0>(P);
 }
 
-size_t wide_tab_bytes(int n_seg, int P) { return (size_t)n_seg * 4 * P * kWideTabW * 8; }
+size_t wide_tab_bytes(int n_seg, int P) { return (size_t)n_seg * kWideTabK * P * kWideTabW * 8; }
 
 int wide_prep(const rh_segments& sg, int D, int P, double* tab, cudaStream_t stream) {
   const int64_t n = (int64_t)sg.n_seg * D * P;

@@ -830,7 +830,9 @@ int launch_pass(rh_ctx* ctx, const rh_pipe_shape* sh, const rh_cost_model* m,
       const size_t off_bytes = al(16 + 4 * ((size_t)p.ipb * M + 1));
       p.w_docs = (int)(p.w_union + off_bytes);
       // documents: ~3.5 per micro-batch (a CTA with more reads them from L2)
-      const size_t docs = al(16 + 14 * (size_t)p.ipb * M);
+      // (the region later holds the measured stage times [P][TW] floats)
+      const size_t docs = al(std::max<size_t>(16 + 14 * (size_t)p.ipb * M,
+                                              (size_t)P * tw * 4 > off_bytes ? (size_t)P * tw * 4 - off_bytes : 0));
       p.doc_stage = (int)((docs - 16) / 4);
       const size_t smem = p.w_docs + docs;
       if (smem <= ctx->smem_optin) {
