@@ -5,11 +5,12 @@
 //
 // One THREAD walks one replica pipeline: the chain state (finish and cost
 // sum of every stage) lives in registers, and the chunks
-// are visited in a topological order that is a pair of short loops with the
+// are visited in a topological order that is a few short loops with the
 // stage index unrolled at compile time:
 //
-//   warm-up triangle, for j = 0..P-1, stages ascending:
-//       F_j(s)                        if j <= P-1-s and j < m
+//   warm-up, by DAG level L = 0..P-1 (four loops over quarters of the
+//   levels, each holding only the stages it can touch), stages descending:
+//       F_{L-s}(s)                    if s <= L and L-s < m
 //   main loop, for i = 0..m-1, stages descending:
 //       B_i(s)                        (dependency B_i(s+1): same i, done)
 //       F_{P-s+i}(s)                  if P-s+i < m  (dependency
@@ -113,6 +114,7 @@ enum { kDivScale = 0, kDivFast = 1, kDivExact = 2 };
 template <int P, int TW, int MODE>
 struct WideWalk {
   uint32_t bt, rl;  // shared addresses (this thread's column / iteration row)
+
   const double* tb;  // this replica's column of the segment table
   unsigned slow;  // warp-uniform: bit s = some replica of the warp runs stage s slow
   double fin[P], ssum[P];
@@ -152,13 +154,31 @@ struct WideWalk {
     }
     return step<S, NODEP>(c, dep);
   }
-  // warm-up triangle slot: F_j(S) if j <= P-1-S and j < m (stages ascending)
+  // warm-up in DAG-level order: level L holds F_{L-S}(S) for every S <= L
+  // (j = L - S < m); they are independent (F_{L-S}(S) needs stage S-1's chunk
+  // of level L-1 and stage S's own), so a level is up to P-way ILP where the
+  // stage-ascending triangle is one serial chain per step.  Stages descend so
+  // fin[S-1] still holds level L-1's finish.
   template <int S>
-  __device__ __forceinline__ void tri(int j, int m, double bj) {
-    if (j <= P - 1 - S && j < m) {
+  __device__ __forceinline__ void warm(int L, int m, uint32_t brow) {
+    if (L >= S && L - S < m) {
       const double dep = S > 0 ? __dadd_rn(fin[S > 0 ? S - 1 : 0], tab<0, S>()) : 0.0;
-      chunk<S, S == 0>(lds_at<S * 8>(rl), bj, dep);
+      chunk<S, S == 0>(lds_at<S * 8>(rl), lds_at<-S * TW * 8>(brow), dep);
     }
+  }
+  template <int... I>
+  __device__ __forceinline__ void warm_all(int L, int m, uint32_t brow, std::integer_sequence<int, I...>) {
+    constexpr int NS = sizeof...(I);
+    (warm<NS - 1 - I>(L, m, brow), ...);  // S = NS-1, ..., 0
+  }
+  // levels [L0, L1) touch stages S <= L < L1 only: a quarter of the levels per
+  // loop, each loop's body holding just the stages it can touch
+  template <int Q>
+  __device__ __forceinline__ void warm_quarter(int m) {
+    constexpr int L0 = Q * P / 4, L1 = (Q + 1) * P / 4;
+#pragma unroll 1
+    for (int L = L0; L < L1; ++L)
+      warm_all(L, m, bt + (uint32_t)(L * TW * 8), std::make_integer_sequence<int, L1>());
   }
   // main-loop slot (stages descending): B_i(S), then F_{P-S+i}(S) if it exists
   // (tried branch-free, a missing F costing +0.0 from a predicated load:
@@ -174,15 +194,13 @@ struct WideWalk {
     }
   }
   template <int... I>
-  __device__ __forceinline__ void tri_all(int j, int m, double bj, std::integer_sequence<int, I...>) {
-    (tri<I>(j, m, bj), ...);  // S = 0, 1, ..., P-1
-  }
-  template <int... I>
   __device__ __forceinline__ void pair_all(int i, int m, double bi,
                                            std::integer_sequence<int, I...>) {
     double nB = 0.0;  // B_i of the stage above
     (pair<P - 1 - I>(i, m, bi, nB), ...);  // S = P-1, ..., 0
   }
+  // (Tried: the next stage's table / shared loads issued before this stage's
+  // chunk (software-pipelined operands): spills, 352 -> 362-388 us.)
   // (Tried: K groups of stages skewed by one loop step each, so a step holds
   // K independent dependency chains -- bit-exact, but the per-group validity
   // and slow-stage branches kept the compiler from interleaving them: trace R
@@ -192,10 +210,10 @@ struct WideWalk {
   __device__ __forceinline__ void walk(int m) {
 #pragma unroll
     for (int s = 0; s < P; ++s) fin[s] = ssum[s] = 0.0;
-#pragma unroll 1
-    for (int j = 0; j < P; ++j)
-      tri_all(j, m, lds_rt(bt + (uint32_t)((j < m ? j : 0) * TW * 8)),
-              std::make_integer_sequence<int, P>());
+    warm_quarter<0>(m);  // (the stage-ascending triangle per j: 350 -> 344 us)
+    warm_quarter<1>(m);
+    warm_quarter<2>(m);
+    warm_quarter<3>(m);
 #pragma unroll 1
     for (int i = 0; i < m; ++i)
       pair_all(i, m, lds_rt(bt + (uint32_t)(i * TW * 8)), std::make_integer_sequence<int, P>());
@@ -207,6 +225,9 @@ struct WideWalk {
 // 128 registers; shared memory (base costs + staging, ~27 KB for trace R)
 // allows the same.  (tools/walkbench.cu: 10 -> 16 warps per SM took the
 // trace-R walk from 1.57 to 1.03 ms; more warps than that did not help.)
+#ifndef RH_WIDE_DTPF
+#define RH_WIDE_DTPF 2  // device-time L2 prefetch: 0 CTA start, 1 none, 2 before the walk
+#endif
 #ifndef RH_WIDE_DT_UNROLL
 #define RH_WIDE_DT_UNROLL 8
 #endif
@@ -265,8 +286,10 @@ __global__ void __launch_bounds__(kWideThreads, kWideMinBlocks) pass_wide_kernel
     mbar_arrive_expect_tx(&s_bar, so.tx_bytes + sd.tx_bytes);
     stage_issue(so, g_off, &s_bar);
     if (staged) stage_issue(sd, p.tr.doc_len + d_lo, &s_bar);
+#if RH_WIDE_DTPF == 0
     if (DETECT)  // reduced after the walk: pull the rows into L2 now
       prefetch_l2(p.tr.device_time + it0 * D * P * T, 4 * (size_t)n_it * D * P * T);
+#endif
     const int64_t nb = (int64_t)blockIdx.x + p.pf_stride;
     if (p.pf_stride > 0 && nb < gridDim.x) {  // the next wave's inputs
       const int64_t pf_it = nb * p.ipb;
@@ -390,6 +413,13 @@ __global__ void __launch_bounds__(kWideThreads, kWideMinBlocks) pass_wide_kernel
   // that count from a warp reduction, so ptxas sees uniform loop bounds and
   // validity tests -- no gain, 481 vs 481 us.)
   const uint32_t a_bt = smem_u32(base_t + tid), a_rl = smem_u32(rl);
+#if RH_WIDE_DTPF == 2
+  // the rows the epilogue reduces: pulled into L2 as the walk starts (at the
+  // CTA's start they were partly evicted again by the time the walk ended:
+  // DRAM reads 1.4x the algorithmic bytes; trace R 3.00 -> 2.96 ms)
+  if (DETECT && tid == 0)
+    prefetch_l2(p.tr.device_time + it0 * D * P * T, 4 * (size_t)n_it * D * P * T);
+#endif
 #ifdef RH_WIDE_NO_POW2
   const bool wpow2 = false;
 #else
