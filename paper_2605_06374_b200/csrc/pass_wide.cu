@@ -504,15 +504,49 @@ __global__ void __launch_bounds__(kWideThreads, kWideMinBlocks) pass_wide_kernel
   if (!on) return;
   const unsigned st_bits = it_st[li];
   const bool dead = (st_bits & (RH_IT_STOPPED | RH_IT_OVERFLOW)) != 0;
+  // a replica's P outputs are contiguous: vector stores when P and the
+  // caller's pointer allow (4 flags per u32, float4 severities, double2 costs)
+  const int64_t o0 = (it * D + d) * P;
+  const auto al = [](const void* q, unsigned a) { return (reinterpret_cast<uintptr_t>(q) & (a - 1)) == 0; };
+  if (p.out.stage_cost) {
+    if (P % 2 == 0 && al(p.out.stage_cost, 16)) {
 #pragma unroll
-  for (int s = 0; s < P; ++s) {
-    const int64_t o = (it * D + d) * P + s;
-    const bool f = !dead && ((flags >> s) & 1u);
-    if (p.out.stage_cost) p.out.stage_cost[o] = dead ? 0.0 : ssum[s];
-    if (DETECT) {
-      if (p.out.stage_flag) p.out.stage_flag[o] = f ? 1 : 0;
-      if (p.out.severity)
-        p.out.severity[o] = f ? (float)__ddiv_rn(ssum[s], (double)s_meas[s * TW + tid]) : 0.0f;
+      for (int s = 0; s < P; s += 2)
+        *reinterpret_cast<double2*>(p.out.stage_cost + o0 + s) =
+            dead ? make_double2(0.0, 0.0) : make_double2(ssum[s], ssum[s + 1 < P ? s + 1 : s]);
+    } else {
+#pragma unroll
+      for (int s = 0; s < P; ++s) p.out.stage_cost[o0 + s] = dead ? 0.0 : ssum[s];
+    }
+  }
+  if (DETECT) {
+    const uint32_t fl = dead ? 0u : flags;
+    if (p.out.stage_flag) {
+      if (P % 4 == 0 && al(p.out.stage_flag, 4)) {
+#pragma unroll
+        for (int s = 0; s < P; s += 4)
+          *reinterpret_cast<uint32_t*>(p.out.stage_flag + o0 + s) =
+              ((fl >> s) & 1u) | (((fl >> (s + 1)) & 1u) << 8) | (((fl >> (s + 2)) & 1u) << 16) |
+              (((fl >> (s + 3)) & 1u) << 24);
+      } else {
+#pragma unroll
+        for (int s = 0; s < P; ++s) p.out.stage_flag[o0 + s] = (fl >> s) & 1u;
+      }
+    }
+    if (p.out.severity) {
+      float sev[P];
+#pragma unroll
+      for (int s = 0; s < P; ++s)
+        sev[s] = ((fl >> s) & 1u) ? (float)__ddiv_rn(ssum[s], (double)s_meas[s * TW + tid]) : 0.0f;
+      if (P % 4 == 0 && al(p.out.severity, 16)) {
+#pragma unroll
+        for (int s = 0; s < P; s += 4)
+          *reinterpret_cast<float4*>(p.out.severity + o0 + s) =
+              make_float4(sev[s], sev[(s + 1) % P], sev[(s + 2) % P], sev[(s + 3) % P]);
+      } else {
+#pragma unroll
+        for (int s = 0; s < P; ++s) p.out.severity[o0 + s] = sev[s];
+      }
     }
   }
   if (d == 0) {
