@@ -220,6 +220,22 @@ struct WideWalk {
   }
 };
 
+#ifdef RH_WIDE_TRACE
+// debug build only (tools/wide_trace.py): per CTA, thread 0's globaltimer at
+// the phase boundaries of pass_wide_kernel
+__device__ unsigned long long g_wtrace[4096 * 8];
+__device__ __forceinline__ void wmark(int k) {
+  if (threadIdx.x == 0 && blockIdx.x < 4096) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_wtrace[blockIdx.x * 8 + k] = t;
+  }
+}
+#define RH_WMARK(k) wmark(k)
+#else
+#define RH_WMARK(k) ((void)0)
+#endif
+
 // CTAs per SM the register budget targets: with the hop / speed tables in L1
 // and the chain state at 2P doubles, 8 CTAs (16 warps) fit every P <= 16 in
 // 128 registers; shared memory (base costs + staging, ~27 KB for trace R)
@@ -254,6 +270,7 @@ __global__ void __launch_bounds__(kWideThreads, kWideMinBlocks) pass_wide_kernel
   double* base_t = reinterpret_cast<double*>(smem_raw + p.w_base);
   double* s_rl = reinterpret_cast<double*>(smem_raw + p.w_rl);
   __shared__ uint64_t s_bar;
+  RH_WMARK(0);
   if (tid < p.ipb) {
     it_ms[tid] = 0.0;
     it_st[tid] = 0u;
@@ -335,8 +352,10 @@ __global__ void __launch_bounds__(kWideThreads, kWideMinBlocks) pass_wide_kernel
     }
     for (; q < q1; q += D) link_bad = link_bad || __ldg(p.sg.link_ratio + q) > p.thr;
   }
+  RH_WMARK(1);
   mbar_wait(&s_bar, 0);  // the bulk copies have landed
   __syncthreads();       // ... and so have the threads' edge words
+  RH_WMARK(2);
   // ---- Q_j = sum l^2 and base costs alpha*N + beta*Q_j, one thread per replica
   if (md > p.mmax) md = -1;
   const int m = md > 0 ? md : 0;
@@ -344,46 +363,68 @@ __global__ void __launch_bounds__(kWideThreads, kWideMinBlocks) pass_wide_kernel
   if (m > 0) {
     const double lin = __dmul_rn(p.m.alpha, (double)p.sh.token_budget);
     const int32_t* s_off = so.dst + li * M + m0;
-    for (int j = 0; j < m; ++j) {
-      const int32_t k0 = s_off[j] - d_lo, k1 = s_off[j + 1] - d_lo;
-      unsigned long long q = 0;
-      if (staged) {
-        // 32-bit sums, the first 4 documents unrolled: whenever sum l < 2^16,
-        // sum l^2 <= (sum l)^2 < 2^32 is exact; a micro-batch above that
-        // (or with a negative length) is redone in 64-bit
-        const int32_t nd = k1 - k0;
-        uint32_t q32 = 0, sl = 0;
+    const auto put = [&](int j, double q) {
+      const double b = __dadd_rn(lin, __dmul_rn(p.m.beta, q));
+      base_t[j * TW + tid] = b;
+      b_hi = b > b_hi ? b : b_hi;
+      if (b > 0.0 && b < b_lo) b_lo = b;
+    };
+    if (staged) {
+      // 32-bit sums, the first 4 documents of a micro-batch unrolled: whenever
+      // sum l < 2^16, sum l^2 <= (sum l)^2 < 2^32 is exact; a micro-batch above
+      // that (or with a negative length) is redone in 64-bit.  Two
+      // micro-batches per step, their heads side by side (independent chains)
+      const int32_t* doc = sd.dst;
+      const auto redo = [&](int32_t k0, int32_t k1) {
+        unsigned long long q = 0;
+        for (int32_t k = k0; k < k1; ++k) {
+          const long long l = doc[k];
+          q += (unsigned long long)(l * l);
+        }
+        return (double)(long long)q;
+      };
+      int32_t kb = s_off[0] - d_lo;
+      for (int j = 0; j < m; j += 2) {
+        const bool two = j + 1 < m;
+        const int32_t k0 = kb, k1 = s_off[j + 1] - d_lo, k2 = two ? s_off[j + 2] - d_lo : k1;
+        kb = k2;
+        const int32_t na = k1 - k0, nb = k2 - k1;
+        uint32_t qa = 0, sa = 0, qb = 0, sb = 0;
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
-          const uint32_t l = t < nd ? (uint32_t)sd.dst[k0 + t] : 0u;
-          q32 += l * l;
-          sl += l;
+          const uint32_t la = t < na ? (uint32_t)doc[k0 + t] : 0u;
+          const uint32_t lb = t < nb ? (uint32_t)doc[k1 + t] : 0u;
+          qa += la * la;
+          sa += la;
+          qb += lb * lb;
+          sb += lb;
         }
         for (int32_t k = k0 + 4; k < k1; ++k) {
-          const uint32_t l = (uint32_t)sd.dst[k];
-          q32 += l * l;
-          sl += l;
+          const uint32_t l = (uint32_t)doc[k];
+          qa += l * l;
+          sa += l;
         }
-        q = q32;
-        if (sl >= 65536u || nd < 0) {
-          q = 0;
-          for (int32_t k = k0; k < k1; ++k) {
-            const long long l = sd.dst[k];
-            q += (unsigned long long)(l * l);
-          }
+        for (int32_t k = k1 + 4; k < k2; ++k) {
+          const uint32_t l = (uint32_t)doc[k];
+          qb += l * l;
+          sb += l;
         }
-      } else {
+        put(j, sa >= 65536u || na < 0 ? redo(k0, k1) : (double)qa);
+        if (two) put(j + 1, sb >= 65536u || nb < 0 ? redo(k1, k2) : (double)qb);
+      }
+    } else {
+      for (int j = 0; j < m; ++j) {
+        const int32_t k0 = s_off[j] - d_lo, k1 = s_off[j + 1] - d_lo;
+        unsigned long long q = 0;
         for (int32_t k = k0; k < k1; ++k) {
           const long long l = __ldg(p.tr.doc_len + d_lo + k);
           q += (unsigned long long)(l * l);
         }
+        put(j, (double)(long long)q);
       }
-      const double b = __dadd_rn(lin, __dmul_rn(p.m.beta, (double)(long long)q));
-      base_t[j * TW + tid] = b;
-      b_hi = b > b_hi ? b : b_hi;
-      if (b > 0.0 && b < b_lo) b_lo = b;
     }
   }
+  RH_WMARK(7);
   if (m == 0) {  // nothing runs: no speeds, no costs
     slow = 0;
     stopped = false;
@@ -412,6 +453,7 @@ __global__ void __launch_bounds__(kWideThreads, kWideMinBlocks) pass_wide_kernel
   // (Tried: a warp whose replicas all walk the same micro-batch count taking
   // that count from a warp reduction, so ptxas sees uniform loop bounds and
   // validity tests -- no gain, 481 vs 481 us.)
+  RH_WMARK(3);
   const uint32_t a_bt = smem_u32(base_t + tid), a_rl = smem_u32(rl);
 #if RH_WIDE_DTPF == 2
   // the rows the epilogue reduces: pulled into L2 as the walk starts (at the
@@ -447,6 +489,7 @@ __global__ void __launch_bounds__(kWideThreads, kWideMinBlocks) pass_wide_kernel
       for (int s = 0; s < P; ++s) fin[s] = w.fin[s], ssum[s] = w.ssum[s];
     }
   }
+  RH_WMARK(4);
   // ---- replica makespan, validation, iteration reductions
   unsigned bits = 0;
   uint32_t flags = 0;  // bit s: stage s flagged
@@ -500,6 +543,7 @@ __global__ void __launch_bounds__(kWideThreads, kWideMinBlocks) pass_wide_kernel
     if (link_bad) bits |= RH_IT_LINK_FLAG;
     if (bits) atomicOr(it_st + li, bits);
   }
+  RH_WMARK(5);
   __syncthreads();
   if (!on) return;
   const unsigned st_bits = it_st[li];
@@ -560,6 +604,7 @@ __global__ void __launch_bounds__(kWideThreads, kWideMinBlocks) pass_wide_kernel
     p.out.makespan[it] = ms;
     p.out.status[it] = (uint8_t)st;
   }
+  RH_WMARK(6);
 }
 
 template <int DETECT>
@@ -589,6 +634,12 @@ void* wide_kernel_ptr(int P, int zbh, int detect) {
   if (zbh) return nullptr;  // ZBH long pipelines: the lane kernel
   return detect ? wide_kernel_t<1>(P) : wide_kernel_t<0>(P);
 }
+
+#ifdef RH_WIDE_TRACE
+extern "C" int rh_debug_wide_trace(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, g_wtrace, sizeof(g_wtrace)) == cudaSuccess ? 0 : 1;
+}
+#endif
 
 size_t wide_tab_bytes(int n_seg, int P) { return (size_t)n_seg * kWideTabK * P * kWideTabW * 8; }
 
