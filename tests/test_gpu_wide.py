@@ -105,3 +105,33 @@ def test_lane_kernel_1024_thread_instantiation(oracle, cuda_device):
         tr = with_measurements(random_trace(6101 + k, n_iter=30, pp=9, dp=64, M=64 * 10,
                                             schedule=sched), oracle, noise=0.02, seed=3)
         _check_detect(tr, oracle)
+
+
+@pytest.mark.parametrize("pp", [8, 12, 16])
+def test_wide_outputs_at_unaligned_addresses(pp, oracle, cuda_device):
+    """The wide kernel stores a replica's contiguous outputs as vectors (4 flags
+    per u32, float4 severities, double2 costs) only when the caller's pointers
+    are aligned for them; outputs at odd offsets take the scalar stores and
+    must be identical."""
+    import torch
+
+    from paper_2605_06374_b200.detect_pass import DetectorPass
+
+    tr = with_measurements(random_trace(6100 + pp, n_iter=40, pp=pp, dp=7, M=7 * pp + 3),
+                           oracle, noise=0.02, seed=pp)
+    p = DetectorPass(tr, keep_stage_cost=True)
+    n, G = tr.n_iter, tr.cfg.dp * tr.cfg.pp
+    dev = p.stage_flag.device
+    flag_buf = torch.zeros(n * G + 16, dtype=torch.uint8, device=dev)
+    sev_buf = torch.zeros(n * G + 8, dtype=torch.float32, device=dev)
+    cost_buf = torch.zeros(n * G + 4, dtype=torch.float64, device=dev)
+    p.stage_flag, p.severity, p.stage_cost = flag_buf[1:1 + n * G], sev_buf[1:1 + n * G], \
+        cost_buf[1:1 + n * G]
+    p.detect()
+    r = p.results()
+    oms, ost, osc, ofl, osv = oracle.detect(tr)
+    np.testing.assert_array_equal(r["status"], ost)
+    np.testing.assert_array_equal(_bits(r["stage_cost"]), _bits(osc))
+    np.testing.assert_array_equal(r["stage_flag"], ofl)
+    np.testing.assert_array_equal(r["severity"].view(np.uint32), osv.view(np.uint32))
+    assert int(flag_buf[0]) == 0 and int(flag_buf[1 + n * G]) == 0  # nothing outside
