@@ -488,7 +488,11 @@ def run_trace_r(args, dev, sample=10_000, reps=10):
            "detect_ms": det, "screen_ms": scr, "algorithmic_bytes": nbytes,
            "achieved_gbs": nbytes / (det * 1e-3) / 1e9,
            "frac_of_hbm": nbytes / (det * 1e-3) / 1e9 / peak,
-           "kernel": "pass_wide_kernel<P=16,detect> (thread per replica, loop-form 1F1B walk)"}
+           "kernel": "pass_wide_kernel<P=16,detect> (thread per replica, segment tables in L1, "
+                     "level-ordered warm-up + loop-form 1F1B walk)"}
+    prof = ROOT / "profiles" / "trace_r_kernel_ncu.json"
+    if prof.exists():  # DRAM bytes of one launch, from the committed ncu capture
+        res["traffic"] = json.loads(prof.read_text()).get("dram_bytes_per_launch")
     del p
     torch.cuda.empty_cache()
     return res
