@@ -16,6 +16,8 @@
 //       F_{P-s+i}(s)                  if P-s+i < m  (dependency
 //                                     F_{P-s+i}(s-1): previous i, not yet
 //                                     overwritten -- s-1 comes later)
+//   walked two steps at a time, step i+1 two stages behind step i, so the two
+//   B chains interleave (two_steps).
 //
 // Each stage's chunks come out in its 1F1B chain order (warm-up Fs, then
 // (B_i, F_{w+1+i}) pairs, then the B tail -- pipeline.py:92-126) and every
@@ -199,12 +201,47 @@ struct WideWalk {
     double nB = 0.0;  // B_i of the stage above
     (pair<P - 1 - I>(i, m, bi, nB), ...);  // S = P-1, ..., 0
   }
+  // Two main-loop steps at once, step i+1 two stages behind step i: at tick T
+  // step i does stage P-1-T and step i+1 stage P+1-T.  Every read still sees
+  // what the sequential order gives it (step i+1's B(s) follows step i's
+  // chunks of stage s, done two ticks before; its F(s) reads stage s-1 after
+  // step i, done the tick before and not yet touched by step i+1; step i reads
+  // stages step i+1 reaches only later), and the two B chains interleave:
+  // trace R 2.69 -> 2.58 ms.  (Three or four steps: register spills, 2.67 /
+  // 3.89 ms.)
+  template <int S>
+  __device__ __forceinline__ void half_b(double bi, double& nB) {
+    const double depB = S < P - 1 ? __dadd_rn(nB, tab<1, S>()) : 0.0;
+    nB = chunk<S, S == P - 1>(lds_at<(P + S) * 8>(rl), bi, depB);
+  }
+  template <int S>
+  __device__ __forceinline__ void half_f(int i, int m) {
+    if (i < m - P + S) {
+      const double bF = lds_rt(bt + (uint32_t)((P - S + i) * TW * 8));
+      const double dep = S > 0 ? __dadd_rn(fin[S > 0 ? S - 1 : 0], tab<0, S>()) : 0.0;
+      chunk<S, S == 0>(lds_at<S * 8>(rl), bF, dep);
+    }
+  }
+  template <int T>
+  __device__ __forceinline__ void tick(int i, int m, double b0, double b1, double& n0, double& n1) {
+    constexpr int SA = P - 1 - T, SB = P + 1 - T;
+    if constexpr (SA >= 0) half_b<SA>(b0, n0);
+    if constexpr (SB >= 0 && SB < P) half_b<SB>(b1, n1);
+    if constexpr (SA >= 0) half_f<SA>(i, m);
+    if constexpr (SB >= 0 && SB < P) half_f<SB>(i + 1, m);
+  }
+  template <int... T>
+  __device__ __forceinline__ void two_steps(int i, int m, double b0, double b1,
+                                            std::integer_sequence<int, T...>) {
+    double n0 = 0.0, n1 = 0.0;
+    (tick<T>(i, m, b0, b1, n0, n1), ...);
+  }
   // (Tried: the next stage's table / shared loads issued before this stage's
   // chunk (software-pipelined operands): spills, 352 -> 362-388 us.)
-  // (Tried: K groups of stages skewed by one loop step each, so a step holds
-  // K independent dependency chains -- bit-exact, but the per-group validity
-  // and slow-stage branches kept the compiler from interleaving them: trace R
-  // 463 -> 520 us per 10^4 iterations; branch-free division on top: 624 us.
+  // (Round 2 tried K groups of stages skewed by one loop step each: the
+  // per-group validity and slow-stage branches kept the compiler from
+  // interleaving them, 463 -> 520 us per 10^4 iterations; with the division
+  // predicated and the steps skewed two stages apart it pays, above.
   // A level-ordered walk -- the P chunks of a DAG level are independent --
   // issued more, not faster: tools/walkbench.cu, 1.57 -> 2.1 ms branch-free.)
   __device__ __forceinline__ void walk(int m) {
@@ -214,8 +251,12 @@ struct WideWalk {
     warm_quarter<1>(m);
     warm_quarter<2>(m);
     warm_quarter<3>(m);
+    int i = 0;
 #pragma unroll 1
-    for (int i = 0; i < m; ++i)
+    for (; i + 1 < m; i += 2)
+      two_steps(i, m, lds_rt(bt + (uint32_t)(i * TW * 8)), lds_rt(bt + (uint32_t)((i + 1) * TW * 8)),
+                std::make_integer_sequence<int, P + 2>());
+    if (i < m)  // odd m: the last step alone
       pair_all(i, m, lds_rt(bt + (uint32_t)(i * TW * 8)), std::make_integer_sequence<int, P>());
   }
 };
