@@ -648,7 +648,7 @@ __global__ void __launch_bounds__(kPipeThreads) pipe_kernel(SearchArgs a, const 
 
 // ---- phase 1 for 1F1B, P <= 32: register-resident replica walks ----------
 // One thread per replica pipeline, as in pipe_kernel, but the chain state
-// (each stage's last finish and last F finish) lives in registers and the
+// (each stage's last finish) lives in registers and the
 // chunks are visited in the loop-form topological order of the Detector's
 // pass_wide_kernel (pass_wide.cu): a warm-up triangle (F_j on stages
 // ascending) and a main loop of (B_i, F_{P-s+i}) pairs on stages descending,
@@ -672,7 +672,11 @@ struct SearchWalk {
   const double* hop;  // hop s -> s+1 at s * D
   int D;
   unsigned slow;      // warp-uniform: bit s = some replica of the warp runs stage s slow
-  double fin[P], lastF[P];
+  // A stage's last F finish is never kept apart from its chain finish: when
+  // F(s+1) reads it, that F is stage s's latest chunk (the warm-up walks
+  // stages ascending, the main loop descending; pass_wide.cu).  With P
+  // doubles of chain state instead of 2P, C5 eval 4.62 -> 3.88 ms.
+  double fin[P];
 
   template <int S>
   __device__ __forceinline__ double cost(double rl_, double b) const {
@@ -695,8 +699,8 @@ struct SearchWalk {
   template <int S>
   __device__ __forceinline__ void tri(int j, int m, double bj) {
     if (j <= P - 1 - S && j < m) {
-      const double dep = S > 0 ? __dadd_rn(lastF[S > 0 ? S - 1 : 0], ldg_nc(hop + (S - 1) * D)) : 0.0;
-      lastF[S] = step<S, S == 0>(cost<S>(ldg_nc(rl + S), bj), dep);
+      const double dep = S > 0 ? __dadd_rn(fin[S > 0 ? S - 1 : 0], ldg_nc(hop + (S - 1) * D)) : 0.0;
+      step<S, S == 0>(cost<S>(ldg_nc(rl + S), bj), dep);
     }
   }
   template <int S>
@@ -705,8 +709,8 @@ struct SearchWalk {
     nB = step<S, S == P - 1>(cost<S>(ldg_nc(rl + 32 + S), bi), depB);
     if (i < m - P + S) {
       const double bF = __ldg(bs + (P - S + i));
-      const double dep = S > 0 ? __dadd_rn(lastF[S > 0 ? S - 1 : 0], ldg_nc(hop + (S - 1) * D)) : 0.0;
-      lastF[S] = step<S, S == 0>(cost<S>(ldg_nc(rl + S), bF), dep);
+      const double dep = S > 0 ? __dadd_rn(fin[S > 0 ? S - 1 : 0], ldg_nc(hop + (S - 1) * D)) : 0.0;
+      step<S, S == 0>(cost<S>(ldg_nc(rl + S), bF), dep);
     }
   }
   template <int... I>
@@ -720,10 +724,12 @@ struct SearchWalk {
   }
   __device__ __forceinline__ double walk(int m) {
 #pragma unroll
-    for (int s = 0; s < P; ++s) fin[s] = lastF[s] = 0.0;
+    for (int s = 0; s < P; ++s) fin[s] = 0.0;
 #pragma unroll 1
     for (int j = 0; j < P; ++j)
       tri_all(j, m, __ldg(bs + (j < m ? j : 0)), std::make_integer_sequence<int, P>());
+    // (two steps at once, skewed as in pass_wide.cu: spills at these register
+    // budgets, C5 eval 3.88 -> 6.19 ms)
 #pragma unroll 1
     for (int i = 0; i < m; ++i)
       pair_all(i, m, __ldg(bs + i), std::make_integer_sequence<int, P>());
@@ -734,6 +740,8 @@ struct SearchWalk {
   }
 };
 
+// (one more CTA per SM at every length, spending the registers the last-F
+// array freed: spills, C5 eval 3.88 -> 4.34 ms)
 constexpr int search_reg_min_blocks(int P) { return P <= 12 ? 4 : (P <= 24 ? 3 : 2); }
 
 template <int P, bool SAFE>
@@ -774,7 +782,7 @@ __global__ void __launch_bounds__(kPipeThreads, search_reg_min_blocks(P))
       double gm = 0.0;
       if (run) {
         SearchWalk<P, SAFE> w{a.v.base + id.start, a.v.rl + id.pair * 3LL * 32, sp_d, inv_d,
-                              hop_d, id.D, wslow, {}, {}};
+                              hop_d, id.D, wslow, {}};
         gm = w.walk(md);
       }
       res = over ? CUDART_INF : gm;
