@@ -101,22 +101,21 @@ __global__ void wide_prep_kernel(const rh_segments sg, int D, int P, double* tab
   }
 }
 
-// One replica's walk: shared addresses of its base costs [j][TW] and its
-// iteration's ratio * layers [rlF: P][rlB: P]; its column of the segment
-// table; the chain state (finish and cost sum of every stage) in registers.
-// A stage's last F finish is never kept apart from its chain finish: when
-// F(S) reads stage S-1's last F, that F is stage S-1's latest chunk (warm-up:
-// just walked, stages ascending; main loop: the previous step's, S-1 not yet
-// visited this step), so fin[S-1] is that finish -- 2P doubles of state.
 // How a walk divides a chunk's cost by a slow stage's speed: kDivScale, every
 // slow speed of the warp is a power of two (one exact multiply); kDivFast, the
 // hoisted-reciprocal form (operands range-checked); kDivExact, __ddiv_rn.
 enum { kDivScale = 0, kDivFast = 1, kDivExact = 2 };
 
+// One replica's walk: shared addresses of its base costs [j][TW] and its
+// iteration's ratio * layers [rlF: P][rlB: P]; its column of the segment
+// table; the chain state (finish and cost sum of every stage) in registers.
+// A stage's last F finish is never kept apart from its chain finish: when
+// F(S) reads stage S-1's last F, that F is stage S-1's latest chunk (warm-up:
+// its chunk of the previous DAG level; main loop: the previous step's, S-1 not
+// yet visited this step), so fin[S-1] is that finish -- 2P doubles of state.
 template <int P, int TW, int MODE>
 struct WideWalk {
-  uint32_t bt, rl;  // shared addresses (this thread's column / iteration row)
-
+  uint32_t bt, rl;   // shared addresses (this thread's column / iteration row)
   const double* tb;  // this replica's column of the segment table
   unsigned slow;  // warp-uniform: bit s = some replica of the warp runs stage s slow
   double fin[P], ssum[P];
@@ -136,10 +135,11 @@ struct WideWalk {
     ssum[S] = __dadd_rn(ssum[S], c);
     return fin[S];
   }
-  // one chunk of cost c = (rl * b) / speed, exactly as __ddiv_rn (the
-  // hoisted-reciprocal form after the kernel's operand-range check; EXACT:
-  // out-of-range operands, __ddiv_rn out of line), skipped on unit-speed
-  // stages (x / 1.0 == x).  ptxas predicates the division (no branch): a
+  // one chunk of cost c = (rl * b) / speed, exactly as __ddiv_rn (MODE: one
+  // multiply by 1/speed for power-of-two speeds, the hoisted-reciprocal form
+  // after the kernel's operand-range check, or __ddiv_rn out of line),
+  // skipped on unit-speed stages (x / 1.0 == x).  ptxas predicates the
+  // division (no branch): a
   // branch per chunk -- warp-uniform, or around an IEEE division -- splits
   // the walk into basic blocks it cannot interleave, and measured slower
   // (trace R 376 -> 442-480 us per 10^4 iterations).
