@@ -86,7 +86,32 @@ __device__ __forceinline__ double pow2_recip(double b) {
   return pow2 ? 1.0 / b : 0.0;
 }
 
+// Per (segment, replica) summary of its stage speeds, one word (P <= 16):
+// bits 0-15 the stages not at 1.0, kSpRange every such speed in the
+// hoisted-reciprocal range, kSpPow2 every such speed a power of two, kSpStop
+// some speed <= 0 -- one load in the kernel instead of P.
+enum : uint32_t { kSpRange = 1u << 16, kSpPow2 = 1u << 17, kSpStop = 1u << 18 };
+
 __global__ void wide_prep_kernel(const rh_segments sg, int D, int P, double* tab) {
+  {
+    uint32_t* flags = reinterpret_cast<uint32_t*>(tab + (size_t)sg.n_seg * kWideTabK * P * kWideTabW);
+    const int64_t nr = (int64_t)sg.n_seg * D;
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nr;
+         r += (int64_t)gridDim.x * blockDim.x) {
+      const int d = (int)(r % D), seg = (int)(r / D);
+      uint32_t w = kSpRange | kSpPow2;
+      for (int s = 0; s < P; ++s) {
+        const double sp = sg.speed[r * P + s];
+        if (sp != 1.0) {
+          w |= 1u << s;
+          if (!(sp >= 0x1p-100 && sp <= 0x1p100)) w &= ~kSpRange;  // recip_of(sp) == 0
+          if (pow2_recip(sp) == 0.0) w &= ~kSpPow2;
+        }
+        if (sp <= 0.0) w |= kSpStop;
+      }
+      flags[(size_t)seg * kWideTabW + d] = w;
+    }
+  }
   const int64_t n = (int64_t)sg.n_seg * D * P;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -330,9 +355,10 @@ __global__ void __launch_bounds__(kWideThreads, kWideMinBlocks) pass_wide_kernel
     md = __ldg(ms + d + 1) - m0;
   }
   const double* tb = p.wtab + wide_tab_index(seg, 0, 0, d, P);
-  double spv[P];
-#pragma unroll
-  for (int s = 0; s < P; ++s) spv[s] = on ? __ldg(tb + (3 * P + s) * kWideTabW) : 1.0;
+  const uint32_t spw =
+      on ? __ldg(reinterpret_cast<const uint32_t*>(p.wtab + (size_t)p.sg.n_seg * kWideTabK * P * kWideTabW) +
+                 (size_t)seg * kWideTabW + d)
+         : kSpRange | kSpPow2;
   // this thread's first ratio * layers entry (stage d)
   const int32_t L_d = on && d < P ? __ldg(p.sg.layers + (int64_t)seg * P + d) : 0;
   const bool staged = n_doc <= p.doc_stage;
@@ -368,18 +394,11 @@ __global__ void __launch_bounds__(kWideThreads, kWideMinBlocks) pass_wide_kernel
       s_rl[li * 2 * P + s] = __dmul_rn(p.m.ratio_f, L);
       s_rl[li * 2 * P + P + s] = __dmul_rn(__dadd_rn(p.m.ratio_b, p.m.ratio_w), L);
     }
-  bool stopped = false, safe = true, pow2 = true;
-  unsigned slow = 0;
-#pragma unroll
-  for (int s = 0; s < P; ++s) {
-    const double sp = spv[s];
-    if (sp != 1.0) {
-      slow |= 1u << s;
-      safe = safe && sp >= 0x1p-100 && sp <= 0x1p100;  // recip_of(sp) != 0
-      pow2 = pow2 && pow2_recip(sp) != 0.0;
-    }
-    stopped = stopped || sp <= 0.0;
-  }
+  // the replica's speed summary (wide_prep_kernel): slow stages, divisor range,
+  // power-of-two slow speeds, a stopped stage
+  bool stopped = (spw & kSpStop) != 0, safe = (spw & kSpRange) != 0;
+  const bool pow2 = (spw & kSpPow2) != 0;
+  unsigned slow = spw & 0xffffu;
   bool link_bad = false;  // the segment's exercised-link test, issued before the wait
   if (DETECT && on && p.sg.link_off && p.sg.link_max) {  // one compare (segment maximum)
     link_bad = __ldg(p.sg.link_max + seg) > p.thr;
@@ -691,7 +710,9 @@ extern "C" int rh_debug_wide_trace(unsigned long long* out) {
 }
 #endif
 
-size_t wide_tab_bytes(int n_seg, int P) { return (size_t)n_seg * kWideTabK * P * kWideTabW * 8; }
+size_t wide_tab_bytes(int n_seg, int P) {
+  return (size_t)n_seg * kWideTabK * P * kWideTabW * 8 + (size_t)n_seg * kWideTabW * 4;
+}
 
 int wide_prep(const rh_segments& sg, int D, int P, double* tab, cudaStream_t stream) {
   const int64_t n = (int64_t)sg.n_seg * D * P;
